@@ -1,0 +1,354 @@
+/*
+ * oracle.c -- CPU ORACLE for portability tuning (arXiv 2507.15277).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.
+ * The product path (paper_2507_15277_b200/, libpt.so) never calls it and
+ * shares no code, header, table or helper with it.
+ *
+ * Plain, slow, obviously-correct definitions in fp64.  No blocking, no
+ * fusion, no reordering beyond what the definitions state.  Citations are
+ * PAPER.md line numbers (P:Ln) with the section they fall in.
+ *
+ * Data convention: T is the runtime matrix in milliseconds, env-major,
+ * T[e*ld + c] for environment e (= device x GEMM input) and
+ * parameter configuration c.  A non-finite entry (NaN, +inf)
+ * is a missing measurement.
+ *
+ * Parity status of each function: see DESIGN.md "Oracle pins".  All
+ * functions below are pinned (tests/test_oracle.py); none is
+ * "parity unpinned".
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_EINVAL -1
+#define OR_ENOMEM -2
+#define OR_EEMPTY -6
+#define OR_EDATA -7
+
+/*
+ * or_normalize -- the paper's post-processing pass (Sec. 5.3
+ * "relative to the best ... kernels for that device and input") and the
+ * Oracle of Sec. 5.5 ("best-known configuration ... for every
+ * ... device + input pair").
+ *
+ *   best[e]      = min_c T[e][c]
+ *   slowdown     = T[e][c] / best[e]                   (S/O)
+ *   penalty      = max over all measured cells of the slowdown
+ *                  (reading c4 in DESIGN.md: missing cell -> penalty x best)
+ *   logeff[e][c] = log(best[e] / T[e][c])  (<= 0; log of the relative
+ *                  performance P/best of north_star, reading c11)
+ *
+ * logeff is written env-major, logeff[e*C + c].
+ * Errors: OR_EDATA for a finite runtime <= 0, or an environment with no
+ * measured cell.
+ */
+int or_normalize(const float *T, int64_t E, int64_t C, int64_t ld,
+                 double *best, double *logeff, double *penalty_out)
+{
+    if (E <= 0 || C <= 0 || ld < C) return OR_EINVAL;
+    for (int64_t e = 0; e < E; e++) {
+        double b = INFINITY;
+        for (int64_t c = 0; c < C; c++) {
+            float t = T[e * ld + c];
+            if (!isfinite(t)) continue;
+            if (t <= 0.0f) return OR_EDATA;
+            if ((double)t < b) b = (double)t;
+        }
+        if (!isfinite(b)) return OR_EDATA;
+        best[e] = b;
+    }
+    double penalty = 1.0;
+    for (int64_t e = 0; e < E; e++)
+        for (int64_t c = 0; c < C; c++) {
+            float t = T[e * ld + c];
+            if (!isfinite(t)) continue;
+            double s = (double)t / best[e];
+            if (s > penalty) penalty = s;
+        }
+    for (int64_t e = 0; e < E; e++)
+        for (int64_t c = 0; c < C; c++) {
+            float t = T[e * ld + c];
+            double tt = isfinite(t) ? (double)t : penalty * best[e];
+            logeff[e * C + c] = log(best[e] / tt);
+        }
+    if (penalty_out) *penalty_out = penalty;
+    return OR_OK;
+}
+
+/* The environments in scope, ascending (mask == NULL: all). */
+static int64_t scope_list(const uint8_t *mask, int64_t E, int64_t *out)
+{
+    int64_t n = 0;
+    for (int64_t e = 0; e < E; e++)
+        if (!mask || mask[e]) out[n++] = e;
+    return n;
+}
+
+/*
+ * Sum over the scope, e ascending, of log(max_{c in S} eff[e][c]).
+ * Eq. 1 (Sec. 4.4.1) under the best-member reading c1:
+ * "the performance for each environment is that of the best-performing
+ * of the ... variants on that environment".
+ */
+static double logsum(const double *logeff, int64_t C, const int64_t *envs,
+                     int64_t ne, const int32_t *set, int k)
+{
+    double acc = 0.0;
+    for (int64_t q = 0; q < ne; q++) {
+        const double *row = logeff + envs[q] * C;
+        double m = row[set[0]];
+        for (int u = 1; u < k; u++)
+            if (row[set[u]] > m) m = row[set[u]];
+        acc += m;
+    }
+    return acc;
+}
+
+/*
+ * or_score -- Eq. 1 as a maximised efficiency (reading c2):
+ *   G(S) = exp( (1/|scope|) * sum_{e in scope} log max_{c in S} eff[e][c] )
+ * = 1 / geomean(Slowdown over Oracle).  Writes G and the log-sum L.
+ */
+int or_score(const double *logeff, int64_t E, int64_t C, const uint8_t *mask,
+             const int32_t *set, int k, double *G_out, double *L_out)
+{
+    if (k <= 0) return OR_EEMPTY;
+    for (int u = 0; u < k; u++)
+        if (set[u] < 0 || set[u] >= C) return OR_EINVAL;
+    int64_t *envs = malloc(sizeof(int64_t) * (size_t)E);
+    if (!envs) return OR_ENOMEM;
+    int64_t ne = scope_list(mask, E, envs);
+    if (ne == 0) { free(envs); return OR_EEMPTY; }
+    double L = logsum(logeff, C, envs, ne, set, k);
+    free(envs);
+    if (L_out) *L_out = L;
+    if (G_out) *G_out = exp(L / (double)ne);
+    return OR_OK;
+}
+
+/* ---- exhaustive k-subset search (Sec. 4.3.1) ---------------- */
+
+/* Total order of candidates: higher L first; ties -> lexicographically
+ * smaller sorted tuple first (reading c5). Returns 1 if (La,a) precedes (Lb,b). */
+static int precedes(double La, const int32_t *a, double Lb, const int32_t *b, int k)
+{
+    if (La > Lb) return 1;
+    if (La < Lb) return 0;
+    for (int u = 0; u < k; u++) {
+        if (a[u] < b[u]) return 1;
+        if (a[u] > b[u]) return 0;
+    }
+    return 0;
+}
+
+typedef struct {
+    double L1, L2;          /* best and runner-up log-sums */
+    int32_t s1[32], s2[32];   /* their tuples */
+    int have;               /* number of valid entries (0..2) */
+} top2;
+
+static void top2_offer(top2 *t, double L, const int32_t *s, int k)
+{
+    if (t->have == 0 || precedes(L, s, t->L1, t->s1, k)) {
+        if (t->have >= 1) { t->L2 = t->L1; memcpy(t->s2, t->s1, sizeof t->s1); }
+        t->L1 = L; memcpy(t->s1, s, sizeof(int32_t) * (size_t)k);
+        t->have = t->have < 2 ? t->have + 1 : 2;
+    } else if (t->have == 1 || precedes(L, s, t->L2, t->s2, k)) {
+        t->L2 = L; memcpy(t->s2, s, sizeof(int32_t) * (size_t)k);
+        t->have = 2;
+    }
+}
+
+typedef struct {
+    const double *logeff;
+    int64_t C;
+    const int64_t *envs;
+    int64_t ne;
+    int k;
+    int64_t lo, hi;     /* first-index range [lo, hi) */
+    int tid, nth;
+    top2 res;
+} exh_job;
+
+/* Enumerate every sorted k-tuple (a0 < a1 < ... < a_{k-1}) with
+ * a0 in {lo + tid, lo + tid + nth, ...} in lexicographic order and offer
+ * each to the thread-local top-2. */
+static void *exh_worker(void *arg)
+{
+    exh_job *j = (exh_job *)arg;
+    int k = j->k;
+    int32_t s[32];
+    memset(&j->res, 0, sizeof j->res);
+    for (int64_t a0 = j->lo + j->tid; a0 < j->hi; a0 += j->nth) {
+        if (a0 + k > j->C) break;
+        s[0] = (int32_t)a0;
+        for (int u = 1; u < k; u++) s[u] = s[u - 1] + 1;
+        for (;;) {
+            double L = logsum(j->logeff, j->C, j->envs, j->ne, s, k);
+            top2_offer(&j->res, L, s, k);
+            /* next combination with fixed s[0] (lexicographic) */
+            int u = k - 1;
+            while (u >= 1 && s[u] == (int32_t)(j->C - k + u)) u--;
+            if (u < 1) break;
+            s[u]++;
+            for (int v = u + 1; v < k; v++) s[v] = s[v - 1] + 1;
+        }
+    }
+    return NULL;
+}
+
+/*
+ * or_exhaustive -- "search through the space of variant combinations ...
+ * returns the variant combination with the highest ranking",
+ * restricted to distinct unordered subsets of size exactly k (reading c8).
+ * First indices restricted to [lo, hi) (pass 0, C for the full search;
+ * a sub-range is how bench.py takes a bounded CPU sample).
+ * Writes the best tuple + G and the runner-up (second in the total order)
+ * tuple + G; *n_found = number of candidates (0, 1 or 2 reported).
+ */
+int or_exhaustive(const double *logeff, int64_t E, int64_t C, const uint8_t *mask,
+                  int k, int64_t lo, int64_t hi, int nthreads,
+                  int32_t *best_set, double *G_best, int32_t *runner_set,
+                  double *G_runner, int *n_found)
+{
+    if (k <= 0 || k > 32) return OR_EINVAL;
+    if (k > C) return OR_EINVAL;
+    if (lo < 0) lo = 0;
+    if (hi > C) hi = C;
+    if (nthreads < 1) nthreads = 1;
+    int64_t *envs = malloc(sizeof(int64_t) * (size_t)E);
+    if (!envs) return OR_ENOMEM;
+    int64_t ne = scope_list(mask, E, envs);
+    if (ne == 0) { free(envs); return OR_EEMPTY; }
+    exh_job *jobs = calloc((size_t)nthreads, sizeof(exh_job));
+    pthread_t *th = calloc((size_t)nthreads, sizeof(pthread_t));
+    if (!jobs || !th) { free(envs); free(jobs); free(th); return OR_ENOMEM; }
+    for (int t = 0; t < nthreads; t++) {
+        jobs[t] = (exh_job){logeff, C, envs, ne, k, lo, hi, t, nthreads, {0}};
+        if (nthreads == 1) exh_worker(&jobs[t]);
+        else pthread_create(&th[t], NULL, exh_worker, &jobs[t]);
+    }
+    top2 all;
+    memset(&all, 0, sizeof all);
+    for (int t = 0; t < nthreads; t++) {
+        if (nthreads > 1) pthread_join(th[t], NULL);
+        if (jobs[t].res.have >= 1) top2_offer(&all, jobs[t].res.L1, jobs[t].res.s1, k);
+        if (jobs[t].res.have >= 2) top2_offer(&all, jobs[t].res.L2, jobs[t].res.s2, k);
+    }
+    if (n_found) *n_found = all.have;
+    if (all.have >= 1) {
+        memcpy(best_set, all.s1, sizeof(int32_t) * (size_t)k);
+        *G_best = exp(all.L1 / (double)ne);
+    }
+    if (all.have >= 2) {
+        memcpy(runner_set, all.s2, sizeof(int32_t) * (size_t)k);
+        *G_runner = exp(all.L2 / (double)ne);
+    }
+    free(envs); free(jobs); free(th);
+    return OR_OK;
+}
+
+/*
+ * or_greedy -- greedy forward selection (north_star; reading c12):
+ * S = init;  for t = 1..k:  score G(S u {c}) for every c not in S
+ * (ascending c), take the maximum, ties to the lowest c; record G and the
+ * top-two gap G_best - G_second of that step (reading c7).
+ * m[e] = max_{c in S} logeff[e][c] is kept between steps; it IS the
+ * per-environment maximum of the definition, not a reformulation.
+ * init may be NULL with n_init = 0.  Writes k indices (the picks after
+ * init), their G trace and gap trace (gap = +inf when only one candidate).
+ */
+int or_greedy(const double *logeff, int64_t E, int64_t C, const uint8_t *mask,
+              int k, const int32_t *init, int n_init,
+              int32_t *out_idx, double *G_trace, double *gap_trace)
+{
+    if (k <= 0 || k + n_init > C) return OR_EINVAL;
+    int64_t *envs = malloc(sizeof(int64_t) * (size_t)E);
+    double *m = malloc(sizeof(double) * (size_t)E);
+    uint8_t *in = calloc((size_t)C, 1);
+    if (!envs || !m || !in) { free(envs); free(m); free(in); return OR_ENOMEM; }
+    int64_t ne = scope_list(mask, E, envs);
+    if (ne == 0) { free(envs); free(m); free(in); return OR_EEMPTY; }
+    for (int64_t q = 0; q < ne; q++) m[q] = -INFINITY;   /* empty set */
+    for (int u = 0; u < n_init; u++) {
+        int32_t c = init[u];
+        if (c < 0 || c >= C || in[c]) { free(envs); free(m); free(in); return OR_EINVAL; }
+        in[c] = 1;
+        for (int64_t q = 0; q < ne; q++) {
+            double v = logeff[envs[q] * C + c];
+            if (v > m[q]) m[q] = v;
+        }
+    }
+    for (int t = 0; t < k; t++) {
+        double L1 = -INFINITY, L2 = -INFINITY;
+        int32_t c1 = -1;
+        for (int64_t c = 0; c < C; c++) {
+            if (in[c]) continue;
+            double L = 0.0;
+            for (int64_t q = 0; q < ne; q++) {
+                double v = logeff[envs[q] * C + c];
+                L += (v > m[q]) ? v : m[q];
+            }
+            if (c1 < 0 || L > L1) { L2 = L1; L1 = L; c1 = (int32_t)c; }
+            else if (L > L2 || L2 == -INFINITY) { L2 = L; }
+        }
+        out_idx[t] = c1;
+        in[c1] = 1;
+        for (int64_t q = 0; q < ne; q++) {
+            double v = logeff[envs[q] * C + c1];
+            if (v > m[q]) m[q] = v;
+        }
+        G_trace[t] = exp(L1 / (double)ne);
+        gap_trace[t] = (L2 == -INFINITY) ? INFINITY
+                       : exp(L1 / (double)ne) - exp(L2 / (double)ne);
+    }
+    free(envs); free(m); free(in);
+    return OR_OK;
+}
+
+/*
+ * or_holdout -- leave-one-device-out generalization, the analogue of the
+ * unseen-device experiment (Sec. 5.8; reading c13):
+ *   train scope = envs with device != d; test scope = envs with device == d
+ *   S_unseen = select(train, k)  (method 0 greedy, 1 exhaustive)
+ *   G_train  = G(S_unseen, train);  G_unseen = G(S_unseen, test)
+ *   S_known  = select(test, k);     G_known  = G(S_known, test)
+ * best[e] is each env's own Oracle over all configs (S:L400 reading).
+ */
+int or_holdout(const double *logeff, int64_t E, int64_t C, const int32_t *env_device,
+               int32_t d, int k, int method, int nthreads,
+               int32_t *out_idx, double *G_train, double *G_unseen, double *G_known,
+               int32_t *known_idx)
+{
+    uint8_t *tr = malloc((size_t)E), *te = malloc((size_t)E);
+    int32_t *tmp = malloc(sizeof(int32_t) * 32);
+    double *gt = malloc(sizeof(double) * (size_t)k), *gp = malloc(sizeof(double) * (size_t)k);
+    if (!tr || !te || !tmp || !gt || !gp) { free(tr); free(te); free(tmp); free(gt); free(gp); return OR_ENOMEM; }
+    int64_t ntr = 0, nte = 0;
+    for (int64_t e = 0; e < E; e++) {
+        tr[e] = env_device[e] != d; te[e] = env_device[e] == d;
+        ntr += tr[e]; nte += te[e];
+    }
+    int rc = OR_OK;
+    if (ntr == 0 || nte == 0) { rc = OR_EEMPTY; goto out; }
+    double g2; int nf;
+    for (int pass = 0; pass < 2; pass++) {
+        const uint8_t *sel_mask = pass == 0 ? tr : te;
+        int32_t *dst = pass == 0 ? out_idx : known_idx;
+        if (method == 0) rc = or_greedy(logeff, E, C, sel_mask, k, NULL, 0, dst, gt, gp);
+        else rc = or_exhaustive(logeff, E, C, sel_mask, k, 0, C, nthreads, dst, gt, tmp, &g2, &nf);
+        if (rc) goto out;
+    }
+    if ((rc = or_score(logeff, E, C, tr, out_idx, k, G_train, NULL))) goto out;
+    if ((rc = or_score(logeff, E, C, te, out_idx, k, G_unseen, NULL))) goto out;
+    rc = or_score(logeff, E, C, te, known_idx, k, G_known, NULL);
+out:
+    free(tr); free(te); free(tmp); free(gt); free(gp);
+    return rc;
+}
