@@ -1,0 +1,193 @@
+/*
+ * pt.h -- C ABI of the B200-native portability-tuning hot path
+ * (arXiv 2507.15277, "portability tuning").  Implemented by libpt.so
+ * (hand-written sm_100a CUDA, paper_2507_15277_b200/csrc/).
+ *
+ * Problem statement (Sec. 4.2):  kappa = PortabilityTune(iota,
+ * delta, eps) returns a size-bounded SET of parameter configurations that is
+ * best by a summary metric over the environments (device x GEMM input,
+ * P:L151).  The summary metric is Eq. 1 (Sec. 4.4.1) read with
+ * the best member per environment, reported as the geometric-mean
+ * efficiency
+ *
+ *     G(S) = exp( -(1/|scope|) * sum_{e in scope} min_{c in S} l[c][e] ),
+ *     l[c][e] = log( T[e][c] / best[e] ),   best[e] = min_c T[e][c]
+ *
+ * i.e. G = 1 / geomean(Slowdown over Oracle); G in (0, 1], maximised.
+ * eps (OS, compiler, ...) has no data representation and is not modelled.
+ *
+ * Conventions (every function):
+ *   - returns a pt_status; PT_OK = 0, errors < 0; never aborts; the message of
+ *     the last error on the calling thread is pt_last_error().
+ *   - the caller owns every input array (copied or read during the call) and
+ *     every output array; scalar and small outputs are HOST pointers.
+ *   - all device work is ordered on the CUDA stream given to pt_load_perf and
+ *     each call returns after its results are on the host.
+ *   - a pt_ctx is not thread-safe; use one per thread / per GPU.
+ *   - "host or device" pointers are classified with cudaPointerGetAttributes.
+ *   - ties between equal scores: exhaustive -> the lexicographically smallest
+ *     sorted index tuple; greedy -> the lowest configuration index.
+ */
+#ifndef PT_H
+#define PT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pt_ctx pt_ctx;   /* opaque; owns every device buffer it allocates */
+
+typedef enum {
+    PT_OK = 0,
+    PT_EINVAL = -1,   /* bad argument (k < 1, k > #configs, bad index, bad shard) */
+    PT_ENOMEM = -2,   /* host or device allocation failed */
+    PT_ECUDA = -3,    /* CUDA runtime / driver error (message has details) */
+    PT_ENCCL = -4,    /* reserved: collective failure */
+    PT_ECAP = -5,     /* C(n,k) exceeds the enumeration cap (1e13) */
+    PT_EEMPTY = -6,   /* empty scope (mask selects no environment) or empty set */
+    PT_EDATA = -7     /* runtime <= 0, or an environment with no measured cell */
+} pt_status;
+
+typedef enum {
+    PT_OBJ_GEOMEAN = 0,   /* Eq. 1 library objective (graded path) */
+    PT_OBJ_FLEET = 1      /* Eq. 2 fleet rate -- NEXT, returns PT_EINVAL for now */
+} pt_objective;
+
+/* pt_load_perf flags */
+enum {
+    PT_MISSING_PENALTY_MAX = 0x1, /* default: a missing cell (NaN/+inf) costs the
+                                     dataset-max slowdown x best[e] */
+    PT_EXACT_FP64 = 0x2,          /* debug: exhaustive search by the thread-per-subset
+                                     fp64 kernel, no fp32 tier */
+    PT_GREEDY_STREAM = 0x4        /* force the streamed fp32-filter/fp64-refine greedy
+                                     (default only when the matrix is large) */
+};
+
+/*
+ * pt_load_perf -- ingest + normalise (the post-processing pass, P:L392;
+ * the Oracle best[e]).
+ *   times_ms   host or device, fp32, env-major rows: times_ms[e*ld + c] is the
+ *              runtime (ms) of configuration c in environment e.  NaN/+inf =
+ *              missing.  Environments are device-major then input.
+ *   n_env, n_cfg, ld   E >= 1, C >= 1, ld >= C (elements).
+ *   env_device host, int32[n_env] device id per environment (>= 0), or NULL
+ *              (then every env is device 0; pt_eval_holdout needs it).
+ *   flags      PT_* flags above.
+ *   cuda_device  device ordinal; cuda_stream: cudaStream_t borrowed (NULL =
+ *              the legacy default stream), not owned.
+ * On success *out receives a context owning the device copies:
+ *   l32  [C][E_pad] fp32 and l64 [C][E_pad] fp64 (config-major), l32T
+ *   [E_pad][C_pad] fp32 (env-major), best [E] fp64.
+ * Errors: PT_EINVAL, PT_EDATA (runtime <= 0 / env with no measured cell),
+ *         PT_ENOMEM, PT_ECUDA.
+ */
+pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n_env, int64_t n_cfg,
+                       int64_t ld, const int32_t *env_device, uint32_t flags,
+                       int cuda_device, void *cuda_stream);
+
+/*
+ * pt_score_sets -- Eq. 1 fitness of a batch of candidate sets.
+ *   sets       host or device, int32[n_sets][k] configuration indices
+ *              (any order; duplicates allowed and harmless).
+ *   env_mask   host, uint8[n_env] (nonzero = env in scope) or NULL = all.
+ *   objective  PT_OBJ_GEOMEAN.
+ *   out_G      host or device, double[n_sets]: G of every set (fp64, fixed
+ *              summation order).
+ * Errors: PT_EINVAL (index out of range, k < 1), PT_EEMPTY (empty scope).
+ */
+pt_status pt_score_sets(pt_ctx *ctx, const int32_t *sets, int64_t n_sets, int32_t k,
+                        const uint8_t *env_mask, int32_t objective, double *out_G);
+
+/*
+ * pt_greedy_select -- greedy forward selection (north_star): k dependent steps,
+ * each scores S u {c} for every unselected c in parallel and takes the argmax
+ * (ties -> lowest c).  Exact in fp64 (or fp32 filter + fp64 refine, same
+ * result).
+ *   out_idx        host int32[k]: the picks in order.
+ *   out_G_trace    host double[k] or NULL: G(S_t) after step t.
+ *   out_gap_trace  host double[k] or NULL: G of the step's best minus G of its
+ *                  second-best candidate (+inf if there was one candidate).
+ * Errors: PT_EINVAL (k < 1 or k > C), PT_EEMPTY.
+ */
+pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t objective,
+                           int32_t *out_idx, double *out_G_trace, double *out_gap_trace);
+
+/*
+ * pt_exhaustive_best -- exhaustive search over every k-subset (P:L271-276,
+ * Sec. 4.3.1; distinct unordered subsets of size exactly k).
+ *   shard_rank, shard_count   this call searches shard `shard_rank` of
+ *              `shard_count` equal-work contiguous pieces of the subset space
+ *              (0, 1 = everything).  Results of all shards merged with
+ *              pt_merge_top2 equal the unsharded result.
+ *   out_idx        host int32[k]: best set, ascending.
+ *   out_G          host: its G.
+ *   out_runner_idx host int32[k] or NULL: the second set in (G desc, tuple asc)
+ *                  order; out_G_runner host or NULL: its G (NaN if none).
+ *   out_s          host double[2] or NULL: the exact fp64 log-slowdown sums
+ *                  s = -|scope| log G of best and runner-up (+inf if absent) --
+ *                  the keys pt_merge_top2 orders by.
+ * Errors: PT_EINVAL (k < 1, k > C, bad shard), PT_ECAP (C(n,k) > 1e13),
+ *         PT_EEMPTY.
+ */
+pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t objective,
+                             int32_t shard_rank, int32_t shard_count,
+                             int32_t *out_idx, double *out_G,
+                             int32_t *out_runner_idx, double *out_G_runner, double *out_s);
+
+/*
+ * pt_merge_top2 -- host-only: merge n_rec (s, sorted k-tuple) records (e.g.
+ * gathered from every shard/rank) into the best two in (s asc, tuple asc)
+ * order.  s = +inf marks an absent record.
+ *   s         host double[n_rec];  tuples host int32[n_rec][k]
+ *   out_idx, out_runner_idx  host int32[k];  out_s host double[2]
+ * Returns PT_EEMPTY if no record is present.
+ */
+pt_status pt_merge_top2(const double *s, const int32_t *tuples, int32_t n_rec, int32_t k,
+                        int32_t *out_idx, int32_t *out_runner_idx, double *out_s);
+
+/*
+ * pt_eval_holdout -- leave-one-device-out generalization, the analogue of the
+ * unseen-device experiment (Sec. 5.8).
+ *   train scope = envs whose device != heldout_device; test = device ==.
+ *   method 0 = greedy, 1 = exhaustive.
+ *   out_idx        host int32[k]  set selected on the train scope
+ *   out_G_train    G of out_idx on the train scope
+ *   out_G_unseen   G of out_idx on the held-out device (each env normalised by
+ *                  its own best[e])
+ *   out_G_known    G of the set selected directly on the held-out envs
+ *   out_known_idx  host int32[k] or NULL: that set
+ * Errors: PT_EINVAL (no env_device given / bad method), PT_EEMPTY (a scope is
+ * empty), plus those of the selection calls.
+ */
+pt_status pt_eval_holdout(pt_ctx *ctx, int32_t heldout_device, int32_t k, int32_t method,
+                          int32_t *out_idx, double *out_G_train, double *out_G_unseen,
+                          double *out_G_known, int32_t *out_known_idx);
+
+/* Per-context counters (for bench.py's roofline and gpu_launches fields). */
+typedef struct {
+    int64_t launches;        /* kernels this context has launched so far */
+    double exh_main_ms;      /* CUDA-event time of the last exhaustive main-kernel launch */
+    int64_t exh_sets;        /* k-subsets that launch scored (its shard) */
+    int64_t exh_slots;       /* (row, column) slots it computed, incl. masked waste */
+    int64_t exh_env_pad;     /* padded env count of its scope (K-loop length) */
+    int64_t exh_candidates;  /* fp32-tier candidates re-scored in fp64 */
+    int32_t exh_passes;      /* 1, or 2 after a candidate-buffer overflow */
+    int32_t exh_kernel;      /* 0 = tiled fp32 (min,+), 1 = generic fp64 */
+    double greedy_ms;        /* CUDA-event time of the last greedy selection */
+} pt_stats;
+
+pt_status pt_get_stats(const pt_ctx *ctx, pt_stats *out);
+
+/* Frees every buffer of the context (NULL is a no-op). */
+void pt_free(pt_ctx *ctx);
+
+/* Message of the last non-OK status returned on this thread ("" if none). */
+const char *pt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PT_H */

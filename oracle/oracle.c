@@ -298,6 +298,7 @@ int or_greedy(const double *logeff, int64_t E, int64_t C, const uint8_t *mask,
             if (c1 < 0 || L > L1) { L2 = L1; L1 = L; c1 = (int32_t)c; }
             else if (L > L2 || L2 == -INFINITY) { L2 = L; }
         }
+        if (c1 < 0) { free(envs); free(m); free(in); return OR_EINVAL; }
         out_idx[t] = c1;
         in[c1] = 1;
         for (int64_t q = 0; q < ne; q++) {

@@ -1,0 +1,785 @@
+// exhaustive.cu -- exhaustive k-subset search (Sec. 4.3.1):
+// "search through the space of variant combinations ... determine the fitness
+// of the kernel combination ... returns the variant combination with the
+// highest ranking".
+//
+// (min,+) structure.  Write a k-subset as a (k-1)-subset "row" rho (colex rank
+// R) plus a larger index l ("column").  With A_rho[e] = min_{c in rho} l[c][e]
+//     s(rho u {l}) = sum_e min(A_rho[e], l[l][e])
+// which is a (min,+) product of the row matrix A and the column matrix l over
+// the environment axis.  k_exh_tiled computes it on 128-row x 64-column tiles:
+//   * rows are 128 consecutive colex ranks (the combinatorial-rank decoder maps
+//     each thread's rows to their subsets); A for ALL environments stays
+//     resident in shared memory for every column tile of the row tile;
+//   * column tiles (64 configs x 32 envs, fp32) stream from the env-major copy
+//     l32T through the TMA engine (cp.async.bulk, one 256-byte row copy per
+//     env, completion on an mbarrier) into a 4-stage ring;
+//   * every thread holds an 8x4 block of running sums in registers; each env
+//     costs one FMNMX + one FADD per (set, env) -- the per-environment best
+//     member and the across-environment reduction of Eq. 1;
+//   * fp32 is a FILTER: a set survives only if its fp32 score is inside a
+//     rigorous error window of the best two; survivors
+//     are re-scored in fp64 (k_exh_refine) and the exact top-2 is taken in
+//     (s asc, sorted tuple asc) order (k_top2) -- indices bit-exact.
+// k_exh_generic is the plain thread-per-subset fp64 kernel (k = 1, k > 4,
+// scopes wider than 384 envs, and the PT_EXACT_FP64 debug mode).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "pt_internal.cuh"
+
+#define XT_R 128    // rows per CTA tile
+#define XT_C 64     // columns per CTA tile
+#define XT_K 32     // environments per pipeline stage
+#define XT_S 4      // pipeline stages
+#define XT_EMAX 352 // widest scope the resident-A kernel takes (smem)
+#define XT_UMAX 1024 // column tiles per task (a whole row tile: A staged once)
+#define KEY_BITS 21
+
+// ---------------------------------------------------------------------------
+// work list
+// ---------------------------------------------------------------------------
+struct pt_tasks {
+    int m = 0;
+    int64_t C = 0;
+    const void *tag = nullptr;       // view identity (l32T pointer)
+    std::vector<int4> h;              // (row tile, u0, u1, 0)
+    std::vector<int64_t> slot_pre;    // prefix sums of slots per task
+    std::vector<int64_t> set_pre;     // prefix sums of useful sets per task
+    int4 *d = nullptr;
+};
+
+void pt_tasks_free(pt_tasks *t)
+{
+    if (!t) return;
+    cudaFree(t->d);
+    delete t;
+}
+
+// colex rank range of m-subsets whose largest element is j: [C(j,m), C(j+1,m))
+static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **out)
+{
+    if (ctx->tasks && ctx->tasks->m == m && ctx->tasks->C == v->C && ctx->tasks->tag == v->qT) {
+        *out = ctx->tasks;
+        return PT_OK;
+    }
+    pt_tasks_free(ctx->tasks);
+    ctx->tasks = nullptr;
+    pt_tasks *T = new pt_tasks();
+    T->m = m;
+    T->C = v->C;
+    T->tag = v->qT;
+    const int64_t C = v->C;
+    const int64_t n_rows = pt_binom(C, m);
+    const int64_t n_rt = (n_rows + XT_R - 1) / XT_R;
+    T->slot_pre.push_back(0);
+    T->set_pre.push_back(0);
+    for (int64_t t = 0; t < n_rt; t++) {
+        const int64_t R0 = t * XT_R, R1 = std::min(n_rows, R0 + XT_R);
+        int32_t mem[PT_MAXK];
+        pt_unrank_colex(R0, m, C, mem);
+        const int64_t j0 = mem[m - 1];
+        const int64_t lo = j0 + 1;
+        const int64_t ncols = C - lo;
+        if (ncols <= 0) continue;
+        const int64_t n_ct = (ncols + XT_C - 1) / XT_C;
+        for (int64_t u0 = 0; u0 < n_ct; u0 += XT_UMAX) {
+            const int64_t u1 = std::min(n_ct, u0 + XT_UMAX);
+            const int64_t clo = lo + u0 * XT_C, chi = std::min(C, lo + u1 * XT_C);
+            // useful sets: rows grouped by their largest element j (colex)
+            int64_t useful = 0;
+            for (int64_t j = j0; j < C; j++) {
+                const int64_t a = std::max(R0, pt_binom(j, m)), b = std::min(R1, pt_binom(j + 1, m));
+                if (a >= R1) break;
+                if (b <= a) continue;
+                const int64_t first = std::max(clo, j + 1);
+                if (chi > first) useful += (b - a) * (chi - first);
+            }
+            T->h.push_back(make_int4((int)t, (int)u0, (int)u1, 0));
+            T->slot_pre.push_back(T->slot_pre.back() + (u1 - u0) * XT_R * XT_C);
+            T->set_pre.push_back(T->set_pre.back() + useful);
+        }
+    }
+    if (!T->h.empty()) {
+        if (cudaMalloc(&T->d, sizeof(int4) * T->h.size()) != cudaSuccess) {
+            cudaGetLastError();
+            pt_tasks_free(T);
+            return pt_fail(PT_ENOMEM, "task list allocation failed");
+        }
+        cudaMemcpy(T->d, T->h.data(), sizeof(int4) * T->h.size(), cudaMemcpyHostToDevice);
+    }
+    ctx->tasks = T;
+    *out = T;
+    return PT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t *b, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
+{
+    while (!mbar_try(b, parity)) {
+    }
+}
+// bulk async copy global -> shared on the TMA engine (SASS UBLKCP), completion
+// counted on an mbarrier.  src/dst 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// acc += x + y in one IADD3
+__device__ __forceinline__ uint32_t add3(uint32_t acc, uint32_t x, uint32_t y)
+{
+    uint32_t r;
+    asm("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %3;" : "=r"(r) : "r"(acc), "r"(x), "r"(y));
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// the tiled integer (min,+) kernel
+//
+// Fast tier = exact integer arithmetic on the fixed-point lower bounds
+// q = floor(l * 2^k): Q(S) = sum_e min_{c in S} q[c][e] (no rounding: floor
+// commutes with min, sums fit in 32 bits), so for every set
+//     Q/2^k <= s(S) < (Q + E)/2^k.
+// Inner loop per (set, env pair): 2 IMNMX + 1 IADD3 (3-input add).
+//
+// Warp roles (288 threads): warps 0-7 compute (8x4 sets each, 128x64 per
+// CTA), warp 8 is the producer: it streams 32-env x 64-config column tiles of
+// qT through the TMA engine (cp.async.bulk, one 256-byte row per lane) into an
+// XT_S-deep ring of full/empty mbarriers.  Consumers never block on each
+// other inside a task.
+// ---------------------------------------------------------------------------
+struct XParams {
+    int64_t C, C_pad, E_pad, n_rows;
+    int m;
+    const int4 *tasks;
+    int task_hi;              // end of this shard's task range
+    int *task_ctr;            // dynamic scheduler (starts at the shard's first task)
+    uint32_t tau_seed;        // integer threshold from the greedy seed
+    uint32_t slack;           // E + 1: Q-window between a lower bound and an upper bound
+    unsigned *U;              // min over warps of their best 2nd-smallest Q
+    unsigned long long *cand_key;
+    uint32_t *cand_q;
+    unsigned *cand_n;
+    unsigned cap;
+    const uint32_t *qT;
+};
+
+#define XT_THREADS 288
+#define XT_CONS 256
+
+__global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                  // [S][K][64]
+    uint32_t *As = Bs + XT_S * XT_K * XT_C;                              // [E_pad][128]
+    int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);          // [128]
+    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);        // [S]
+    uint64_t *empty = full + XT_S;                                       // [S]
+    int4 *task_s = reinterpret_cast<int4 *>(empty + XT_S);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nkc = (int)(p.E_pad / XT_K);
+    if (tid == 0) {
+        for (int s = 0; s < XT_S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], XT_CONS / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    uint32_t steps = 0;   // pipeline steps of all previous tasks (same in every thread)
+    // consumer state
+    const int tx = tid & 15, ty = (tid >> 4) & 15;
+    uint32_t b1 = 0xffffffffu, b2 = 0xffffffffu, published = 0xffffffffu;
+
+    for (;;) {
+        if (tid == 0) {
+            int ti = atomicAdd(p.task_ctr, 1);
+            *task_s = ti < p.task_hi ? p.tasks[ti] : make_int4(-1, 0, 0, 0);
+        }
+        __syncthreads();
+        const int4 tk = *task_s;
+        if (tk.x < 0) break;
+        const int64_t R0 = (int64_t)tk.x * XT_R;
+        int32_t mem0[PT_MAXK];
+        pt_unrank_colex(R0, p.m, p.C, mem0);
+        // first column of the row tile, rounded down to 16 bytes (the extra
+        // columns are <= the row's largest element and masked)
+        const int64_t lo = ((int64_t)mem0[p.m - 1] + 1) & ~(int64_t)3;
+        const int nsteps = (tk.z - tk.y) * nkc;
+
+        if (warp == XT_CONS / 32) {
+            // ---------------- producer warp ----------------
+            for (int g = 0; g < nsteps; g++) {
+                const uint32_t G = steps + g;
+                const int slot = G % XT_S;
+                mbar_wait(&empty[slot], ((G / XT_S) & 1u) ^ 1u);
+                const int u = tk.y + g / nkc, q = g % nkc;
+                if (lane == 0) mbar_expect_tx(&full[slot], XT_K * XT_C * 4);
+                __syncwarp();
+                bulk_g2s(Bs + slot * XT_K * XT_C + lane * XT_C,
+                         p.qT + (int64_t)(q * XT_K + lane) * p.C_pad + lo + (int64_t)u * XT_C,
+                         XT_C * 4, &full[slot]);
+            }
+        } else {
+            // ---------------- consumers ----------------
+            // stage A for the whole task: A[e][r] = min over the row's members
+            {
+                const int r = tid & (XT_R - 1);
+                const int64_t R = R0 + r;
+                int32_t mem[PT_MAXK];
+                const bool valid = R < p.n_rows;
+                if (valid) pt_unrank_colex(R, p.m, p.C, mem);
+                else for (int u = 0; u < p.m; u++) mem[u] = 0;
+                if (tid < XT_R) last_s[r] = valid ? mem[p.m - 1] : 0x7fffffff;
+                const uint32_t *base = p.qT;
+#pragma unroll 4
+                for (int64_t e = tid >> 7; e < p.E_pad; e += 2) {
+                    const uint32_t *rowp = base + e * p.C_pad;
+                    uint32_t a = rowp[mem[0]];
+                    for (int u = 1; u < p.m; u++) a = min(a, rowp[mem[u]]);
+                    As[e * XT_R + r] = valid ? a : 0u;
+                }
+            }
+            named_sync(1, XT_CONS);
+
+            uint32_t acc[8][4];
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = 0u;
+
+            for (int g = 0; g < nsteps; g++) {
+                const uint32_t G = steps + g;
+                const int slot = G % XT_S;
+                mbar_wait(&full[slot], (G / XT_S) & 1u);
+                const int q = g % nkc;
+                const uint32_t *B = Bs + slot * XT_K * XT_C + tx * 4;
+                const uint32_t *A = As + (int64_t)q * XT_K * XT_R + ty * 4;
+#pragma unroll 4
+                for (int e = 0; e < XT_K; e += 2) {
+                    const uint4 a0 = *reinterpret_cast<const uint4 *>(A + e * XT_R);
+                    const uint4 a1 = *reinterpret_cast<const uint4 *>(A + e * XT_R + 64);
+                    const uint4 b = *reinterpret_cast<const uint4 *>(B + e * XT_C);
+                    const uint4 c0 = *reinterpret_cast<const uint4 *>(A + (e + 1) * XT_R);
+                    const uint4 c1 = *reinterpret_cast<const uint4 *>(A + (e + 1) * XT_R + 64);
+                    const uint4 d = *reinterpret_cast<const uint4 *>(B + (e + 1) * XT_C);
+                    const uint32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const uint32_t cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+                    const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+                    const uint32_t dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+#pragma unroll
+                        for (int j = 0; j < 4; j++)
+                            acc[i][j] = add3(acc[i][j], min(av[i], bv[j]), min(cv[i], dv[j]));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                if (q == nkc - 1) {
+                    // epilogue of one column tile: mask, window test, candidate append
+                    const int u = tk.y + g / nkc;
+                    const int64_t l0 = lo + (int64_t)u * XT_C + tx * 4;
+                    const uint32_t Uv = *(volatile unsigned *)p.U;
+                    const uint32_t tau = min(p.tau_seed, Uv > 0xffffffffu - p.slack ? 0xffffffffu : Uv + p.slack);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        const int r = (i < 4) ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+                        const int last = last_s[r];
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const int64_t l = l0 + j;
+                            const uint32_t sq = acc[i][j];
+                            acc[i][j] = 0u;
+                            if (l < p.C && l > last) {
+                                if (sq < b1) {
+                                    b2 = b1;
+                                    b1 = sq;
+                                } else if (sq < b2) {
+                                    b2 = sq;
+                                }
+                                if (sq <= tau) {
+                                    const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                    if (idx < p.cap) {
+                                        p.cand_key[idx] = ((unsigned long long)(R0 + r) << KEY_BITS) |
+                                                          (unsigned long long)l;
+                                        p.cand_q[idx] = sq;
+                                    }
+                                }
+                            }
+                        }
+                    }
+                    uint32_t wb = b2;
+                    for (int o = 16; o; o >>= 1) wb = min(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+                    if (lane == 0 && wb < published) {
+                        atomicMin(p.U, wb);
+                        published = wb;
+                    }
+                }
+            }
+        }
+        steps += nsteps;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fp64 refine of the survivors: warp per candidate, fixed shuffle tree
+// ---------------------------------------------------------------------------
+__global__ void k_exh_refine(const unsigned long long *__restrict__ key,
+                             const uint32_t *__restrict__ cs, unsigned n, uint32_t tau, int m, int64_t C,
+                             const double *__restrict__ l64, int64_t E_pad,
+                             double *__restrict__ out_s, int32_t *__restrict__ out_t)
+{
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const int k = m + 1;
+    int32_t tup[PT_MAXK];
+    const unsigned long long kv = key[w];
+    pt_unrank_colex((int64_t)(kv >> KEY_BITS), m, C, tup);
+    tup[m] = (int32_t)(kv & ((1ull << KEY_BITS) - 1));
+    if (lane < k) out_t[w * k + lane] = tup[lane];
+    if (cs[w] > tau) {
+        if (lane == 0) out_s[w] = INFINITY;
+        return;
+    }
+    double acc = 0.0;
+    for (int64_t e = lane; e < E_pad; e += 32) {
+        double v = l64[(int64_t)tup[0] * E_pad + e];
+        for (int u = 1; u < k; u++) v = fmin(v, l64[(int64_t)tup[u] * E_pad + e]);
+        acc += v;
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out_s[w] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// top-2 over (s, tuple) records -- one CTA
+// ---------------------------------------------------------------------------
+struct Rec2 {
+    double s1, s2;
+    int32_t t1[PT_MAXK], t2[PT_MAXK];
+};
+
+__device__ __forceinline__ void rec_offer(Rec2 &r, double s, const int32_t *t, int k)
+{
+    if (s == INFINITY) return;
+    if (pt_key_less(s, t, r.s1, r.t1, k)) {
+        r.s2 = r.s1;
+        for (int u = 0; u < k; u++) r.t2[u] = r.t1[u];
+        r.s1 = s;
+        for (int u = 0; u < k; u++) r.t1[u] = t[u];
+    } else if (pt_key_less(s, t, r.s2, r.t2, k)) {
+        bool same = s == r.s1;
+        for (int u = 0; u < k && same; u++) same = t[u] == r.t1[u];
+        if (!same) {
+            r.s2 = s;
+            for (int u = 0; u < k; u++) r.t2[u] = t[u];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_top2(const double *__restrict__ s, const int32_t *__restrict__ t,
+                                             int64_t n, int k, double *__restrict__ out_s,
+                                             int32_t *__restrict__ out_t)
+{
+    __shared__ Rec2 sh[256];
+    Rec2 r;
+    r.s1 = r.s2 = INFINITY;
+    for (int u = 0; u < PT_MAXK; u++) r.t1[u] = r.t2[u] = 0x7fffffff;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) rec_offer(r, s[i], t + i * k, k);
+    sh[threadIdx.x] = r;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            Rec2 o = sh[threadIdx.x + w];
+            Rec2 me = sh[threadIdx.x];
+            rec_offer(me, o.s1, o.t1, k);
+            rec_offer(me, o.s2, o.t2, k);
+            sh[threadIdx.x] = me;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out_s[0] = sh[0].s1;
+        out_s[1] = sh[0].s2;
+        for (int u = 0; u < k; u++) {
+            out_t[u] = sh[0].t1[u];
+            out_t[k + u] = sh[0].t2[u];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// generic fp64 thread-per-subset kernel: block -> its top-2 records
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_exh_generic(const double *__restrict__ l64, int64_t C,
+                                                    int64_t E_pad, int k, int64_t r0, int64_t r1,
+                                                    double *__restrict__ blk_s,
+                                                    int32_t *__restrict__ blk_t)
+{
+    __shared__ Rec2 sh[256];
+    Rec2 r;
+    r.s1 = r.s2 = INFINITY;
+    for (int u = 0; u < PT_MAXK; u++) r.t1[u] = r.t2[u] = 0x7fffffff;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t R = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; R < r1; R += stride) {
+        int32_t tup[PT_MAXK];
+        pt_unrank_colex(R, k, C, tup);
+        double acc = 0.0;
+        for (int64_t e = 0; e < E_pad; e++) {
+            double v = l64[(int64_t)tup[0] * E_pad + e];
+            for (int u = 1; u < k; u++) v = fmin(v, l64[(int64_t)tup[u] * E_pad + e]);
+            acc += v;
+        }
+        rec_offer(r, acc, tup, k);
+    }
+    sh[threadIdx.x] = r;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            Rec2 o = sh[threadIdx.x + w];
+            Rec2 me = sh[threadIdx.x];
+            rec_offer(me, o.s1, o.t1, k);
+            rec_offer(me, o.s2, o.t2, k);
+            sh[threadIdx.x] = me;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        blk_s[2 * blockIdx.x] = sh[0].s1;
+        blk_s[2 * blockIdx.x + 1] = sh[0].s2;
+        for (int u = 0; u < k; u++) {
+            blk_t[(2 * blockIdx.x) * k + u] = sh[0].t1[u];
+            blk_t[(2 * blockIdx.x + 1) * k + u] = sh[0].t2[u];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static pt_status run_generic(pt_ctx *ctx, const pt_view *v, int k, int64_t r0, int64_t r1,
+                             double *s_out, int32_t *t_out)
+{
+    cudaStream_t s = ctx->stream;
+    const int64_t n = r1 - r0;
+    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8));
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
+    const size_t o_bs = take(sizeof(double) * 2 * nblk), o_bt = take(sizeof(int32_t) * 2 * nblk * k),
+                 o_os = take(sizeof(double) * 2), o_ot = take(sizeof(int32_t) * 2 * k);
+    void *scr = nullptr;
+    PT_TRY(pt_scratch(ctx, off, &scr));
+    char *b = (char *)scr;
+    double *bs = (double *)(b + o_bs), *os = (double *)(b + o_os);
+    int32_t *bt = (int32_t *)(b + o_bt), *ot = (int32_t *)(b + o_ot);
+    PT_CK(cudaEventRecord(ctx->ev0, s));
+    k_exh_generic<<<nblk, 256, 0, s>>>(v->l64, v->C, v->E_pad, k, r0, r1, bs, bt);
+    PT_CK(cudaEventRecord(ctx->ev1, s));
+    k_top2<<<1, 256, 0, s>>>(bs, bt, 2 * nblk, k, os, ot);
+    ctx->stats.launches += 2;
+    PT_CK(cudaGetLastError());
+    PT_CK(cudaMemcpyAsync(s_out, os, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+    PT_CK(cudaMemcpyAsync(t_out, ot, sizeof(int32_t) * 2 * k, cudaMemcpyDeviceToHost, s));
+    PT_CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->stats.exh_main_ms = ms;
+    ctx->stats.exh_kernel = 1;
+    ctx->stats.exh_sets = n;
+    ctx->stats.exh_slots = n;
+    ctx->stats.exh_env_pad = v->E_pad;
+    ctx->stats.exh_candidates = 0;
+    ctx->stats.exh_passes = 1;
+    return PT_OK;
+}
+
+static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_rank,
+                           int32_t shard_count, double *s_out, int32_t *t_out)
+{
+    cudaStream_t s = ctx->stream;
+    const int m = k - 1;
+    pt_tasks *T = nullptr;
+    PT_TRY(build_tasks(ctx, v, m, &T));
+    const int n_tasks = (int)T->h.size();
+    // equal-work contiguous shard of the task list
+    const int64_t total = T->slot_pre.back();
+    auto cut = [&](int64_t r) {
+        const int64_t target = total * r / shard_count;
+        return (int)(std::lower_bound(T->slot_pre.begin(), T->slot_pre.end(), target) -
+                     T->slot_pre.begin());
+    };
+    const int ta = std::min(cut(shard_rank), n_tasks), tb = std::min(cut(shard_rank + 1), n_tasks);
+    ctx->stats.exh_kernel = 0;
+    ctx->stats.exh_env_pad = v->E_pad;
+    ctx->stats.exh_sets = T->set_pre[tb] - T->set_pre[ta];
+    ctx->stats.exh_slots = T->slot_pre[tb] - T->slot_pre[ta];
+    ctx->stats.exh_candidates = 0;
+    ctx->stats.exh_passes = 0;
+    ctx->stats.exh_main_ms = 0.0;
+    s_out[0] = s_out[1] = INFINITY;
+    if (ta >= tb) return PT_OK;
+
+    // threshold seed: exact score of greedy's second-best set at its last step
+    // (s_(2) <= that score, and Q <= 2^k s for every set)
+    std::vector<int32_t> gidx(k);
+    std::vector<double> gs1(k), gs2(k);
+    PT_TRY(pt_greedy_view(ctx, v, k, gidx.data(), gs1.data(), gs2.data()));
+    const double scale = std::ldexp(1.0, v->qshift);
+    auto to_q = [](double x) -> uint32_t {
+        if (!(x < 4294967295.0)) return 0xffffffffu;
+        return (uint32_t)x;
+    };
+    const uint32_t tau_seed = to_q(std::floor(gs2[k - 1] * scale * (1.0 + 1e-12)) + 1.0);
+    const uint32_t slack = (uint32_t)v->E + 1u;
+
+    const size_t smem = sizeof(uint32_t) * (XT_S * XT_K * XT_C + v->E_pad * XT_R) +
+                        sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
+    PT_CK(cudaFuncSetAttribute(k_exh_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+
+    unsigned cap = 1u << 20;
+    unsigned n_cand = 0;
+    uint32_t tau_pass = tau_seed;
+    for (int pass = 0; pass < 2; pass++) {
+        size_t off = 0;
+        auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
+        const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)),
+                     o_n = take(sizeof(unsigned)), o_key = take(sizeof(unsigned long long) * cap),
+                     o_cq = take(sizeof(uint32_t) * cap), o_rs = take(sizeof(double) * cap),
+                     o_rt = take(sizeof(int32_t) * (size_t)cap * k), o_os = take(sizeof(double) * 2),
+                     o_ot = take(sizeof(int32_t) * 2 * k);
+        void *scr = nullptr;
+        PT_TRY(pt_scratch(ctx, off, &scr));
+        char *b = (char *)scr;
+        int *ctr = (int *)(b + o_ctr);
+        unsigned *U = (unsigned *)(b + o_U), *cn = (unsigned *)(b + o_n);
+        unsigned long long *ckey = (unsigned long long *)(b + o_key);
+        uint32_t *cq = (uint32_t *)(b + o_cq);
+        double *rs = (double *)(b + o_rs), *os = (double *)(b + o_os);
+        int32_t *rt = (int32_t *)(b + o_rt), *ot = (int32_t *)(b + o_ot);
+        const unsigned u_init = 0xffffffffu;
+        PT_CK(cudaMemcpyAsync(ctr, &ta, sizeof(int), cudaMemcpyHostToDevice, s));
+        PT_CK(cudaMemcpyAsync(U, &u_init, sizeof(unsigned), cudaMemcpyHostToDevice, s));
+        PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned), s));
+        XParams p;
+        p.C = v->C;
+        p.C_pad = v->C_pad;
+        p.E_pad = v->E_pad;
+        p.n_rows = pt_binom(v->C, m);
+        p.m = m;
+        p.tasks = T->d;
+        p.task_hi = tb;
+        p.task_ctr = ctr;
+        p.tau_seed = tau_pass;
+        p.slack = slack;
+        p.U = U;
+        p.cand_key = ckey;
+        p.cand_q = cq;
+        p.cand_n = cn;
+        p.cap = cap;
+        p.qT = v->qT;
+        const int grid = std::min(ctx->num_sms, tb - ta);
+        PT_CK(cudaEventRecord(ctx->ev0, s));
+        k_exh_tiled<<<grid, XT_THREADS, smem, s>>>(p);
+        PT_CK(cudaEventRecord(ctx->ev1, s));
+        ctx->stats.launches++;
+        PT_CK(cudaGetLastError());
+        unsigned hU = 0;
+        PT_CK(cudaMemcpyAsync(&n_cand, cn, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        PT_CK(cudaMemcpyAsync(&hU, U, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        PT_CK(cudaStreamSynchronize(s));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        if (pass == 0) ctx->stats.exh_main_ms = ms;
+        ctx->stats.exh_passes = pass + 1;
+        const uint32_t tau_final =
+            std::min<uint64_t>(tau_pass, (uint64_t)hU + (uint64_t)slack) > 0xffffffffull
+                ? 0xffffffffu
+                : (uint32_t)std::min<uint64_t>(tau_pass, (uint64_t)hU + (uint64_t)slack);
+        if (n_cand > cap) {
+            // overflow: rerun with the final threshold and room for every survivor
+            cap = n_cand;
+            tau_pass = tau_final;
+            continue;
+        }
+        ctx->stats.exh_candidates = n_cand;
+        if (n_cand > 0) {
+            const int64_t threads = (int64_t)n_cand * 32;
+            k_exh_refine<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+                ckey, cq, n_cand, tau_final, m, v->C, v->l64, v->E_pad, rs, rt);
+            k_top2<<<1, 256, 0, s>>>(rs, rt, n_cand, k, os, ot);
+            ctx->stats.launches += 2;
+            PT_CK(cudaGetLastError());
+            PT_CK(cudaMemcpyAsync(s_out, os, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+            PT_CK(cudaMemcpyAsync(t_out, ot, sizeof(int32_t) * 2 * k, cudaMemcpyDeviceToHost, s));
+            PT_CK(cudaStreamSynchronize(s));
+        }
+        return PT_OK;
+    }
+    return pt_fail(PT_ECUDA, "candidate buffer overflowed twice (internal error)");
+}
+
+pt_status pt_exhaustive_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t shard_rank,
+                             int32_t shard_count, int32_t *best, int32_t *runner, double *s_out,
+                             int *n_found)
+{
+    if (k < 1 || k > v->C) return pt_fail(PT_EINVAL, "k=%d outside [1, %lld]", k, (long long)v->C);
+    if (shard_count < 1 || shard_rank < 0 || shard_rank >= shard_count)
+        return pt_fail(PT_EINVAL, "bad shard %d of %d", shard_rank, shard_count);
+    if (k == v->C) {
+        // the only k-subset is every configuration
+        std::vector<int32_t> all(k);
+        for (int u = 0; u < k; u++) all[u] = u;
+        int32_t *d_set = nullptr;
+        double *d_s = nullptr;
+        PT_CK(cudaMallocAsync((void **)&d_set, sizeof(int32_t) * k, ctx->stream));
+        PT_CK(cudaMallocAsync((void **)&d_s, sizeof(double), ctx->stream));
+        PT_CK(cudaMemcpyAsync(d_set, all.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, ctx->stream));
+        PT_TRY(pt_score_view(ctx, v, d_set, 1, k, d_s));
+        PT_CK(cudaMemcpyAsync(s_out, d_s, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CK(cudaFreeAsync(d_set, ctx->stream));
+        PT_CK(cudaFreeAsync(d_s, ctx->stream));
+        PT_CK(cudaStreamSynchronize(ctx->stream));
+        s_out[1] = INFINITY;
+        for (int u = 0; u < k; u++) {
+            best[u] = u;
+            if (runner) runner[u] = -1;
+        }
+        if (n_found) *n_found = shard_rank == 0 ? 1 : 0;
+        if (shard_rank != 0) s_out[0] = INFINITY;
+        return PT_OK;
+    }
+    if (k > PT_MAXK) return pt_fail(PT_EINVAL, "k=%d above the supported maximum %d", k, PT_MAXK);
+    const double nsets = std::exp(std::lgamma((double)v->C + 1) - std::lgamma((double)k + 1) -
+                                  std::lgamma((double)(v->C - k) + 1));
+    if (nsets > 1e13) return pt_fail(PT_ECAP, "C(%lld,%d) = %.3g exceeds the cap 1e13", (long long)v->C, k, nsets);
+    std::vector<int32_t> t(2 * k, 0);
+    double sv[2] = {INFINITY, INFINITY};
+    const bool tiled = !(ctx->flags & PT_EXACT_FP64) && k >= 2 && k <= 4 && v->E_pad <= XT_EMAX &&
+                       v->C > k;
+    if (tiled) {
+        PT_TRY(run_tiled(ctx, v, k, shard_rank, shard_count, sv, t.data()));
+    } else {
+        const int64_t n = pt_binom(v->C, k);
+        const int64_t r0 = n * shard_rank / shard_count, r1 = n * (shard_rank + 1) / shard_count;
+        if (r1 > r0) PT_TRY(run_generic(ctx, v, k, r0, r1, sv, t.data()));
+    }
+    int nf = (sv[0] != INFINITY) + (sv[1] != INFINITY);
+    if (n_found) *n_found = nf;
+    for (int u = 0; u < k; u++) {
+        best[u] = t[u];
+        if (runner) runner[u] = t[k + u];
+    }
+    s_out[0] = sv[0];
+    s_out[1] = sv[1];
+    return PT_OK;
+}
+
+extern "C" pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *env_mask,
+                                        int32_t objective, int32_t shard_rank, int32_t shard_count,
+                                        int32_t *out_idx, double *out_G, int32_t *out_runner_idx,
+                                        double *out_G_runner, double *out_s)
+{
+    if (!ctx || !out_idx || !out_G) return pt_fail(PT_EINVAL, "NULL argument");
+    if (objective != PT_OBJ_GEOMEAN)
+        return pt_fail(PT_EINVAL, "objective %d not implemented (Eq. 2 fleet rate is NEXT)",
+                       objective);
+    PT_CK(cudaSetDevice(ctx->dev));
+    const pt_view *v = nullptr;
+    PT_TRY(pt_get_view(ctx, env_mask, &v));
+    std::vector<int32_t> runner(k > 0 ? k : 1);
+    double sv[2];
+    int nf = 0;
+    PT_TRY(pt_exhaustive_view(ctx, v, k, shard_rank, shard_count, out_idx, runner.data(), sv, &nf));
+    const double invE = 1.0 / (double)v->E;
+    *out_G = nf >= 1 ? std::exp(-sv[0] * invE) : NAN;
+    if (out_runner_idx)
+        for (int u = 0; u < k; u++) out_runner_idx[u] = runner[u];
+    if (out_G_runner) *out_G_runner = nf >= 2 ? std::exp(-sv[1] * invE) : NAN;
+    if (out_s) {
+        out_s[0] = sv[0];
+        out_s[1] = sv[1];
+    }
+    return PT_OK;
+}
+
+extern "C" pt_status pt_merge_top2(const double *s, const int32_t *tuples, int32_t n_rec, int32_t k,
+                                   int32_t *out_idx, int32_t *out_runner_idx, double *out_s)
+{
+    if (!s || !tuples || !out_idx || !out_s || k < 1 || k > PT_MAXK || n_rec < 0)
+        return pt_fail(PT_EINVAL, "bad argument");
+    double s1 = INFINITY, s2 = INFINITY;
+    int i1 = -1, i2 = -1;
+    for (int r = 0; r < n_rec; r++) {
+        if (!(s[r] < INFINITY)) continue;
+        const int32_t *t = tuples + (int64_t)r * k;
+        if (i1 < 0 || pt_key_less(s[r], t, s1, tuples + (int64_t)i1 * k, k)) {
+            s2 = s1;
+            i2 = i1;
+            s1 = s[r];
+            i1 = r;
+        } else if (i2 < 0 || pt_key_less(s[r], t, s2, tuples + (int64_t)i2 * k, k)) {
+            bool same = s[r] == s1;
+            for (int u = 0; u < k && same; u++) same = t[u] == tuples[(int64_t)i1 * k + u];
+            if (!same) {
+                s2 = s[r];
+                i2 = r;
+            }
+        }
+    }
+    if (i1 < 0) return pt_fail(PT_EEMPTY, "no record present");
+    for (int u = 0; u < k; u++) {
+        out_idx[u] = tuples[(int64_t)i1 * k + u];
+        if (out_runner_idx) out_runner_idx[u] = i2 >= 0 ? tuples[(int64_t)i2 * k + u] : -1;
+    }
+    out_s[0] = s1;
+    out_s[1] = i2 >= 0 ? s2 : INFINITY;
+    return PT_OK;
+}

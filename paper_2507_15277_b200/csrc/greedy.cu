@@ -1,0 +1,420 @@
+// greedy.cu -- greedy forward selection (north_star): k dependent steps; each
+// step scores S u {c} for every unselected configuration c in parallel and
+// takes the argmax (ties -> lowest c).  Score of a set S (Eq. 1 under the
+// best-member reading, P:L222 / P:L305-310), in log-slowdown form:
+//     s(S u {c}) = sum_e min(cur[e], l[c][e]),  cur[e] = min_{c' in S} l[c'][e]
+// (G = exp(-s/E) is monotone, so argmax G = argmin s).
+//
+// Two kernels families:
+//  * RESIDENT (paper shape, matrix in L2): one cooperative persistent kernel for
+//    all k steps.  cur[] lives in shared memory of every CTA, candidates are
+//    scored in fp64 by one warp each (lanes over envs, xor-shuffle tree), the
+//    per-CTA top-2 goes through global memory and a grid barrier, every CTA
+//    merges the same list (deterministic) and updates its own cur[].
+//    Latency-bound: k grid barriers.
+//  * STREAM (scaled shape, 1 GiB fp32 matrix in HBM): per step one HBM-bound
+//    scan kernel computes an fp32 key per config (direct sum at step 1, the
+//    facility-location gain sum_e max(0, cur - l) afterwards), then one
+//    single-CTA kernel derives a rigorous error window,
+//    re-scores every config inside it in fp64 and commits the exact argmin.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "pt_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+#define PT_BIGI 0x7fffffff
+
+__device__ __forceinline__ void top2_ins(double &s1, int &c1, double &s2, int &c2, double s,
+                                         int c)
+{
+    if (s < s1 || (s == s1 && c < c1)) {
+        s2 = s1;
+        c2 = c1;
+        s1 = s;
+        c1 = c;
+    } else if (c != c1 && (s < s2 || (s == s2 && c < c2))) {
+        s2 = s;
+        c2 = c;
+    }
+}
+
+__device__ __forceinline__ void warp_top2(double &s1, int &c1, double &s2, int &c2)
+{
+    for (int o = 16; o; o >>= 1) {
+        double a1 = __shfl_xor_sync(0xffffffffu, s1, o);
+        double a2 = __shfl_xor_sync(0xffffffffu, s2, o);
+        int b1 = __shfl_xor_sync(0xffffffffu, c1, o);
+        int b2 = __shfl_xor_sync(0xffffffffu, c2, o);
+        top2_ins(s1, c1, s2, c2, a1, b1);
+        top2_ins(s1, c1, s2, c2, a2, b2);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// RESIDENT fp64 cooperative kernel
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_greedy_resident(const double *__restrict__ l64,
+                                                          int64_t C, int64_t E_pad, int k,
+                                                          double4 *__restrict__ blk,
+                                                          int32_t *__restrict__ out_idx,
+                                                          double *__restrict__ s1_tr,
+                                                          double *__restrict__ s2_tr)
+{
+    extern __shared__ double sm[];
+    double *cur = sm;
+    uint32_t *taken = (uint32_t *)(cur + E_pad);
+    __shared__ double ws1[8], ws2[8];
+    __shared__ int wc1[8], wc2[8];
+    __shared__ int cstar;
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nwords = (C + 31) / 32;
+    for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) cur[e] = INFINITY;
+    for (int64_t w = threadIdx.x; w < nwords; w += blockDim.x) taken[w] = 0u;
+    __syncthreads();
+    const int64_t gw = (int64_t)blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
+    for (int t = 0; t < k; t++) {
+        double s1 = INFINITY, s2 = INFINITY;
+        int c1 = PT_BIGI, c2 = PT_BIGI;
+        for (int64_t c = gw; c < C; c += nw) {
+            if (taken[c >> 5] >> (c & 31) & 1u) continue;
+            const double *col = l64 + c * E_pad;
+            double acc = 0.0;
+            for (int64_t e = lane; e < E_pad; e += 32) acc += fmin(cur[e], col[e]);
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            top2_ins(s1, c1, s2, c2, acc, (int)c);
+        }
+        if (lane == 0) {
+            ws1[warp] = s1;
+            ws2[warp] = s2;
+            wc1[warp] = c1;
+            wc2[warp] = c2;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < 8; w++) {
+                top2_ins(s1, c1, s2, c2, ws1[w], wc1[w]);
+                top2_ins(s1, c1, s2, c2, ws2[w], wc2[w]);
+            }
+            blk[(t & 1) * gridDim.x + blockIdx.x] = make_double4(s1, s2, (double)c1, (double)c2);
+        }
+        grid.sync();
+        if (warp == 0) {
+            s1 = s2 = INFINITY;
+            c1 = c2 = PT_BIGI;
+            for (int b = lane; b < (int)gridDim.x; b += 32) {
+                double4 r = blk[(t & 1) * gridDim.x + b];
+                top2_ins(s1, c1, s2, c2, r.x, (int)r.z);
+                top2_ins(s1, c1, s2, c2, r.y, (int)r.w);
+            }
+            warp_top2(s1, c1, s2, c2);
+            if (lane == 0) {
+                cstar = c1;
+                if (blockIdx.x == 0) {
+                    out_idx[t] = c1;
+                    s1_tr[t] = s1;
+                    s2_tr[t] = s2;
+                }
+            }
+        }
+        __syncthreads();
+        const int cs = cstar;
+        if (threadIdx.x == 0) taken[cs >> 5] |= 1u << (cs & 31);
+        const double *col = l64 + (int64_t)cs * E_pad;
+        for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) cur[e] = fmin(cur[e], col[e]);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// STREAM: fp32 scan + single-CTA fp64 window refine
+// ---------------------------------------------------------------------------
+// key[c] (minimised): step 0 -> sum_e l32[c][e];  later -> -sum_e max(0, cur-l)
+__global__ void __launch_bounds__(256) k_greedy_scan(const float *__restrict__ l32, int64_t C,
+                                                      int64_t E_pad,
+                                                      const float *__restrict__ cur32,
+                                                      const uint32_t *__restrict__ taken,
+                                                      int gain_mode, float *__restrict__ key)
+{
+    extern __shared__ float cur_s[];
+    for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) cur_s[e] = cur32[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nq = E_pad >> 2;
+    const float4 *cur4 = reinterpret_cast<const float4 *>(cur_s);
+    for (int64_t c = gw; c < C; c += nw) {
+        const float4 *col = reinterpret_cast<const float4 *>(l32 + c * E_pad);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        if (gain_mode) {
+#pragma unroll 8
+            for (int64_t q = lane; q < nq; q += 32) {
+                float4 v = __ldcs(col + q);
+                float4 m = cur4[q];
+                a0 += fmaxf(m.x - v.x, 0.f);
+                a1 += fmaxf(m.y - v.y, 0.f);
+                a2 += fmaxf(m.z - v.z, 0.f);
+                a3 += fmaxf(m.w - v.w, 0.f);
+            }
+        } else {
+#pragma unroll 8
+            for (int64_t q = lane; q < nq; q += 32) {
+                float4 v = __ldcs(col + q);
+                a0 += v.x;
+                a1 += v.y;
+                a2 += v.z;
+                a3 += v.w;
+            }
+        }
+        float acc = (a0 + a1) + (a2 + a3);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            bool tk = taken[c >> 5] >> (c & 31) & 1u;
+            key[c] = tk ? INFINITY : (gain_mode ? -acc : acc);
+        }
+    }
+}
+
+struct pick_state {
+    double S;   // sum_e cur64[e] over real envs (finite from step 1 on)
+};
+
+// one CTA of 1024 threads
+__global__ void __launch_bounds__(1024) k_greedy_pick(
+    const float *__restrict__ key, int64_t C, const double *__restrict__ l64, int64_t E_pad,
+    int64_t E, float *__restrict__ cur32, double *__restrict__ cur64,
+    uint32_t *__restrict__ taken, pick_state *__restrict__ st, int t, int gain_mode,
+    double gamma, int32_t *__restrict__ cand, int32_t *__restrict__ out_idx,
+    double *__restrict__ s1_tr, double *__restrict__ s2_tr, int32_t *__restrict__ ncand_tr)
+{
+    __shared__ double rs1[32], rs2[32];
+    __shared__ int rc1[32], rc2[32];
+    __shared__ int ncand;
+    __shared__ double thr;
+    __shared__ int cstar;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // 1. two smallest keys (ties by index)
+    double s1 = INFINITY, s2 = INFINITY;
+    int c1 = PT_BIGI, c2 = PT_BIGI;
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) top2_ins(s1, c1, s2, c2, (double)key[c], (int)c);
+    warp_top2(s1, c1, s2, c2);
+    if (lane == 0) {
+        rs1[warp] = s1; rs2[warp] = s2; rc1[warp] = c1; rc2[warp] = c2;
+    }
+    if (threadIdx.x == 0) ncand = 0;
+    __syncthreads();
+    if (warp == 0) {
+        s1 = rs1[lane]; s2 = rs2[lane]; c1 = rc1[lane]; c2 = rc2[lane];
+        warp_top2(s1, c1, s2, c2);
+        if (lane == 0) {
+            // window: keep every c that could be one of the
+            // two exact best configurations
+            const double u = 5.9604644775390625e-08;   // 2^-24
+            if (!gain_mode) {
+                // key = s_hat >= 0, |s_hat - s| <= gamma*s
+                thr = (s2 == INFINITY) ? INFINITY : s2 * (1.0 + gamma) / (1.0 - gamma) * (1.0 + 1e-12);
+            } else {
+                // key = -g_hat; |g_hat - g| <= delta = 2u*S + gamma*g_max
+                const double gmax = -s1;
+                const double delta = (2.0 * u * st->S + gamma * gmax) * 1.01 + 1e-300;
+                thr = (s2 == INFINITY) ? INFINITY : s2 + 2.0 * delta;
+            }
+        }
+    }
+    __syncthreads();
+    // 2. collect candidates
+    const double th = thr;
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+        float kv = key[c];
+        if (kv != INFINITY && (double)kv <= th) cand[atomicAdd(&ncand, 1)] = (int32_t)c;
+    }
+    __syncthreads();
+    // 3. exact fp64 re-score: warp per candidate, lanes over envs
+    const int n = ncand;
+    s1 = s2 = INFINITY;
+    c1 = c2 = PT_BIGI;
+    for (int q = warp; q < n; q += 32) {
+        const int c = cand[q];
+        const double *col = l64 + (int64_t)c * E_pad;
+        double acc = 0.0;
+        for (int64_t e = lane; e < E_pad; e += 32) acc += fmin(cur64[e], col[e]);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        top2_ins(s1, c1, s2, c2, acc, c);
+    }
+    if (lane == 0) {
+        rs1[warp] = s1; rs2[warp] = s2; rc1[warp] = c1; rc2[warp] = c2;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        s1 = rs1[lane]; s2 = rs2[lane]; c1 = rc1[lane]; c2 = rc2[lane];
+        warp_top2(s1, c1, s2, c2);
+        if (lane == 0) {
+            cstar = c1;
+            out_idx[t] = c1;
+            s1_tr[t] = s1;
+            s2_tr[t] = s2;
+            ncand_tr[t] = n;
+            taken[c1 >> 5] |= 1u << (c1 & 31);
+        }
+    }
+    __syncthreads();
+    // 4. commit: cur <- min(cur, l[c*]); S = sum over real envs (block reduce)
+    const double *col = l64 + (int64_t)cstar * E_pad;
+    double part = 0.0;
+    for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) {
+        double v = fmin(cur64[e], col[e]);
+        cur64[e] = v;
+        cur32[e] = (float)v;
+        if (e < E) part += v;
+    }
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) rs1[warp] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double S = 0.0;
+        for (int w = 0; w < 32; w++) S += rs1[w];
+        st->S = S;
+    }
+}
+
+__global__ void k_fill_f64(double *p, int64_t n, double v)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+__global__ void k_fill_f32(float *p, int64_t n, float v)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+static bool use_stream(const pt_ctx *ctx, const pt_view *v)
+{
+    if (ctx->flags & PT_GREEDY_STREAM) return true;
+    const double bytes = (double)v->C * (double)v->E_pad * 8.0;
+    return bytes > 64.0 * (1 << 20) || v->E_pad * 8 > 160 * 1024;
+}
+
+pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_idx,
+                         double *s1_trace, double *s2_trace)
+{
+    if (k < 1 || k > v->C) return pt_fail(PT_EINVAL, "k=%d outside [1, %lld]", k, (long long)v->C);
+    const int64_t C = v->C, E_pad = v->E_pad;
+    const int64_t nwords = (C + 31) / 32;
+    cudaStream_t s = ctx->stream;
+    PT_CK(cudaEventRecord(ctx->ev0, s));
+    if (!use_stream(ctx, v)) {
+        const int nblk = ctx->num_sms;
+        size_t bytes = pt_round_up(sizeof(double4) * 2 * nblk, 256) + 256 +
+                       pt_round_up(sizeof(int32_t) * k, 256) + 2 * pt_round_up(sizeof(double) * k, 256);
+        void *scr = nullptr;
+        PT_TRY(pt_scratch(ctx, bytes, &scr));
+        char *p = (char *)scr;
+        double4 *blk = (double4 *)p;
+        p += pt_round_up(sizeof(double4) * 2 * nblk, 256) + 256;
+        int32_t *d_idx = (int32_t *)p;
+        p += pt_round_up(sizeof(int32_t) * k, 256);
+        double *d_s1 = (double *)p;
+        p += pt_round_up(sizeof(double) * k, 256);
+        double *d_s2 = (double *)p;
+        size_t smem = sizeof(double) * E_pad + sizeof(uint32_t) * nwords;
+        if (smem > 48 * 1024)
+            PT_CK(cudaFuncSetAttribute(k_greedy_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        int occ = 0;
+        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_resident, 256, smem));
+        if (occ < 1) return pt_fail(PT_ECUDA, "resident greedy kernel cannot be co-resident");
+        const double *l64 = v->l64;
+        int kk = k;
+        void *args[] = {(void *)&l64, (void *)&C, (void *)&E_pad, (void *)&kk, (void *)&blk,
+                        (void *)&d_idx, (void *)&d_s1, (void *)&d_s2};
+        PT_CK(cudaLaunchCooperativeKernel((void *)k_greedy_resident, dim3(nblk), dim3(256), args,
+                                          smem, s));
+        ctx->stats.launches++;
+        PT_CK(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+        PT_CK(cudaMemcpyAsync(s1_trace, d_s1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+        PT_CK(cudaMemcpyAsync(s2_trace, d_s2, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    } else {
+        // buffers: key[C] f32, cand[C] i32, taken[nwords], cur32[E_pad], cur64[E_pad],
+        // st, traces
+        size_t off = 0;
+        auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
+        size_t o_key = take(sizeof(float) * C), o_cand = take(sizeof(int32_t) * C),
+               o_taken = take(sizeof(uint32_t) * nwords), o_c32 = take(sizeof(float) * E_pad),
+               o_c64 = take(sizeof(double) * E_pad), o_st = take(sizeof(pick_state)),
+               o_idx = take(sizeof(int32_t) * k), o_s1 = take(sizeof(double) * k),
+               o_s2 = take(sizeof(double) * k), o_nc = take(sizeof(int32_t) * k);
+        void *scr = nullptr;
+        PT_TRY(pt_scratch(ctx, off, &scr));
+        char *b = (char *)scr;
+        float *key = (float *)(b + o_key);
+        int32_t *cand = (int32_t *)(b + o_cand);
+        uint32_t *taken = (uint32_t *)(b + o_taken);
+        float *cur32 = (float *)(b + o_c32);
+        double *cur64 = (double *)(b + o_c64);
+        pick_state *st = (pick_state *)(b + o_st);
+        int32_t *d_idx = (int32_t *)(b + o_idx), *d_nc = (int32_t *)(b + o_nc);
+        double *d_s1 = (double *)(b + o_s1), *d_s2 = (double *)(b + o_s2);
+        PT_CK(cudaMemsetAsync(taken, 0, sizeof(uint32_t) * nwords, s));
+        PT_CK(cudaMemsetAsync(st, 0, sizeof(pick_state), s));
+        k_fill_f64<<<(unsigned)((E_pad + 255) / 256), 256, 0, s>>>(cur64, E_pad, INFINITY);
+        k_fill_f32<<<(unsigned)((E_pad + 255) / 256), 256, 0, s>>>(cur32, E_pad, INFINITY);
+        ctx->stats.launches += 2;
+        const size_t smem = sizeof(float) * E_pad;
+        if (smem > 48 * 1024)
+            PT_CK(cudaFuncSetAttribute(k_greedy_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        const double u = 5.9604644775390625e-08;
+        const double n = (double)E_pad + 2.0;
+        const double gamma = n * u / (1.0 - n * u) * 1.01;
+        int occ = 0;
+        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_scan, 256, smem));
+        const int64_t want_blocks = (C * 32 + 255) / 256;
+        const int grid = (int)std::min<int64_t>(want_blocks, (int64_t)ctx->num_sms * std::max(occ, 1));
+        for (int t = 0; t < k; t++) {
+            k_greedy_scan<<<grid, 256, smem, s>>>(v->l32, C, E_pad, cur32, taken, t > 0, key);
+            k_greedy_pick<<<1, 1024, 0, s>>>(key, C, v->l64, E_pad, v->E, cur32, cur64, taken, st,
+                                             t, t > 0, gamma, cand, d_idx, d_s1, d_s2, d_nc);
+            ctx->stats.launches += 2;
+        }
+        PT_CK(cudaGetLastError());
+        PT_CK(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+        PT_CK(cudaMemcpyAsync(s1_trace, d_s1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+        PT_CK(cudaMemcpyAsync(s2_trace, d_s2, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    }
+    PT_CK(cudaEventRecord(ctx->ev1, s));
+    PT_CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->stats.greedy_ms = ms;
+    return PT_OK;
+}
+
+extern "C" pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask,
+                                      int32_t objective, int32_t *out_idx, double *out_G_trace,
+                                      double *out_gap_trace)
+{
+    if (!ctx || !out_idx) return pt_fail(PT_EINVAL, "NULL argument");
+    if (objective != PT_OBJ_GEOMEAN)
+        return pt_fail(PT_EINVAL, "objective %d not implemented (Eq. 2 fleet rate is NEXT)",
+                       objective);
+    PT_CK(cudaSetDevice(ctx->dev));
+    const pt_view *v = nullptr;
+    PT_TRY(pt_get_view(ctx, env_mask, &v));
+    std::vector<double> s1(k > 0 ? k : 1), s2(k > 0 ? k : 1);
+    PT_TRY(pt_greedy_view(ctx, v, k, out_idx, s1.data(), s2.data()));
+    const double invE = 1.0 / (double)v->E;
+    for (int t = 0; t < k; t++) {
+        double g1 = exp(-s1[t] * invE);
+        if (out_G_trace) out_G_trace[t] = g1;
+        if (out_gap_trace) out_gap_trace[t] = std::isinf(s2[t]) ? INFINITY : g1 - exp(-s2[t] * invE);
+    }
+    return PT_OK;
+}

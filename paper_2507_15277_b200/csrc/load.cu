@@ -1,0 +1,428 @@
+// load.cu -- pt_load_perf (ingest + normalise), scopes, context lifetime.
+//
+// The post-processing pass of the paper (Sec. 5.3: performance
+// "relative to the best ... kernels for that device and input") and the
+// Oracle best[e] run here once per matrix:
+//   k_rowstats : best[e] = min_c T[e][c] over measured cells, the row's max
+//                slowdown (for the missing-cell penalty, reading c4), data checks
+//   k_ell      : l[c][e] = log(T'/best[e]) in fp64 (T' = T, or penalty*best
+//                for a missing cell), written config-major fp64 + fp32 and
+//                env-major fp32 (smem-tiled transpose, coalesced both ways)
+// HBM-bound elementwise work: one read of T, 16 B written per cell.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "pt_internal.cuh"
+
+static thread_local std::string g_err;
+
+pt_status pt_fail(pt_status st, const char *fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+extern "C" const char *pt_last_error(void) { return g_err.c_str(); }
+
+bool pt_is_device_ptr(const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+pt_status pt_scratch(pt_ctx *ctx, size_t bytes, void **p)
+{
+    if (bytes > ctx->scratch_bytes) {
+        if (ctx->scratch) cudaFree(ctx->scratch);
+        ctx->scratch = nullptr;
+        ctx->scratch_bytes = 0;
+        size_t nb = std::max(bytes, (size_t)1 << 20);
+        if (cudaMalloc(&ctx->scratch, nb) != cudaSuccess) {
+            cudaGetLastError();
+            return pt_fail(PT_ENOMEM, "scratch allocation of %zu bytes failed", nb);
+        }
+        ctx->scratch_bytes = nb;
+    }
+    *p = ctx->scratch;
+    return PT_OK;
+}
+
+void pt_view_free(pt_view &v)
+{
+    if (v.owned) {
+        cudaFree(v.l32);
+        cudaFree(v.l64);
+        cudaFree(v.qT);
+    }
+    v = pt_view();
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+
+// one block per environment row: best (min over finite cells), max slowdown,
+// status bits (1 = a finite runtime <= 0, 2 = no measured cell)
+__global__ void k_rowstats(const float *__restrict__ T, int64_t C, double *__restrict__ best,
+                           double *__restrict__ rowmax, int *__restrict__ status)
+{
+    const int64_t e = blockIdx.x;
+    const float *row = T + e * C;
+    __shared__ float red[32];
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    float mn = INFINITY;
+    int nonpos = 0;
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+        float t = row[c];
+        if (isfinite(t)) {
+            if (t <= 0.0f) nonpos = 1;
+            mn = fminf(mn, t);
+        }
+    }
+    if (nonpos) atomicOr(&bad, 1);
+    for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : INFINITY;
+        for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double b = (double)red[0];
+    __syncthreads();
+    double mx = 1.0;
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+        float t = row[c];
+        if (isfinite(t) && t > 0.0f) mx = fmax(mx, (double)t / b);
+    }
+    __shared__ double redd[32];
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) redd[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 1.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) v = fmax(v, redd[w]);
+        rowmax[e] = v;
+        best[e] = b;
+        status[e] = bad | (isfinite(red[0]) ? 0 : 2);
+    }
+}
+
+// 32x32 tiles: read T[e][c] coalesced along c, write l64/l32[c][e] through a
+// shared transpose (coalesced along e).
+__global__ void k_ell(const float *__restrict__ T, int64_t E, int64_t C,
+                      const double *__restrict__ best, double penalty, int64_t E_pad,
+                      float *__restrict__ l32, double *__restrict__ l64)
+{
+    __shared__ double tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, e0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        int64_t e = e0 + r, c = c0 + tx;
+        double v = 0.0;
+        if (e < E && c < C) {
+            float t = T[e * C + c];
+            double b = best[e];
+            double tt = isfinite(t) ? (double)t : penalty * b;
+            v = log(tt / b);
+        }
+        tile[r][tx] = v;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        int64_t c = c0 + r, e = e0 + tx;
+        if (c < C && e < E_pad) {
+            double v = tile[tx][r];
+            l64[c * E_pad + e] = v;
+            l32[c * E_pad + e] = (float)v;
+        }
+    }
+}
+
+// gather the environments of a scope (list idx[E_s]) out of the full view
+__global__ void k_gather_cfg_major(const float *__restrict__ s32, const double *__restrict__ s64,
+                                   int64_t E_pad_src, const int32_t *__restrict__ idx,
+                                   int64_t E_s, int64_t E_pad_dst, int64_t C,
+                                   float *__restrict__ d32, double *__restrict__ d64)
+{
+    const int64_t c = blockIdx.x;
+    for (int64_t q = threadIdx.x; q < E_pad_dst; q += blockDim.x) {
+        float v32 = 0.0f;
+        double v64 = 0.0;
+        if (q < E_s) {
+            int64_t e = idx[q];
+            v32 = s32[c * E_pad_src + e];
+            v64 = s64[c * E_pad_src + e];
+        }
+        d32[c * E_pad_dst + q] = v32;
+        d64[c * E_pad_dst + q] = v64;
+    }
+}
+
+// max of l64 over the real cells of a view (one block per config row)
+__global__ void k_colmax(const double *__restrict__ l64, int64_t E, int64_t E_pad,
+                         double *__restrict__ cmax)
+{
+    const int64_t c = blockIdx.x;
+    double m = 0.0;
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) m = fmax(m, l64[c * E_pad + e]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ double r[32];
+    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmax(m, r[w]);
+        cmax[c] = fmax(m, r[0]);
+    }
+}
+
+// qT[e][c] = floor(l64[c][e] * 2^shift) (exact), 32x32 smem transpose
+__global__ void k_quant(const double *__restrict__ l64, int64_t E, int64_t C, int64_t E_pad,
+                        int64_t C_pad, double scale, uint32_t *__restrict__ qT)
+{
+    __shared__ uint32_t tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, e0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        int64_t c = c0 + r, e = e0 + tx;
+        uint32_t q = 0;
+        if (c < C && e < E) q = (uint32_t)floor(l64[c * E_pad + e] * scale);
+        tile[r][tx] = q;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        int64_t e = e0 + r, c = c0 + tx;
+        if (e < E_pad && c < C_pad) qT[e * C_pad + c] = tile[tx][r];
+    }
+}
+
+// ---------------------------------------------------------------------------
+static pt_status alloc_view(pt_view &v, int64_t E, int64_t C)
+{
+    v.E = E;
+    v.C = C;
+    v.E_pad = pt_round_up(std::max<int64_t>(E, 1), 32);
+    v.C_pad = pt_round_up(C + 64, 64);   // >= C + 64: a 64-column bulk row copy never leaves the row
+    v.owned = true;
+    if (cudaMalloc(&v.l32, sizeof(float) * v.C * v.E_pad) != cudaSuccess ||
+        cudaMalloc(&v.l64, sizeof(double) * v.C * v.E_pad) != cudaSuccess ||
+        cudaMalloc(&v.qT, sizeof(uint32_t) * v.E_pad * v.C_pad) != cudaSuccess) {
+        cudaGetLastError();
+        pt_view_free(v);
+        return pt_fail(PT_ENOMEM, "device allocation for a %lld x %lld view failed",
+                       (long long)E, (long long)C);
+    }
+    return PT_OK;
+}
+
+// fixed-point tier of a view: shift = largest k with E_pad * floor(lmax * 2^k) < 2^32
+static pt_status quantize_view(pt_ctx *ctx, pt_view &v)
+{
+    double *cmax = nullptr;
+    PT_CK(cudaMallocAsync((void **)&cmax, sizeof(double) * v.C, ctx->stream));
+    k_colmax<<<(unsigned)v.C, 128, 0, ctx->stream>>>(v.l64, v.E, v.E_pad, cmax);
+    std::vector<double> h(v.C);
+    PT_CK(cudaMemcpyAsync(h.data(), cmax, sizeof(double) * v.C, cudaMemcpyDeviceToHost, ctx->stream));
+    PT_CK(cudaFreeAsync(cmax, ctx->stream));
+    PT_CK(cudaStreamSynchronize(ctx->stream));
+    double lmax = 0.0;
+    for (double x : h) lmax = std::max(lmax, x);
+    const double qlim = 4294967295.0 / (double)v.E_pad;
+    int shift = 30;
+    while (shift > -30 && std::floor(lmax * std::ldexp(1.0, shift)) >= qlim) shift--;
+    v.qshift = shift;
+    PT_CK(cudaMemsetAsync(v.qT, 0, sizeof(uint32_t) * v.E_pad * v.C_pad, ctx->stream));
+    dim3 grid((unsigned)((v.C + 31) / 32), (unsigned)((v.E_pad + 31) / 32));
+    k_quant<<<grid, dim3(32, 8), 0, ctx->stream>>>(v.l64, v.E, v.C, v.E_pad, v.C_pad,
+                                                    std::ldexp(1.0, shift), v.qT);
+    ctx->stats.launches += 2;
+    PT_CK(cudaGetLastError());
+    return PT_OK;
+}
+
+pt_status pt_get_view(pt_ctx *ctx, const uint8_t *env_mask, const pt_view **out)
+{
+    if (!env_mask) {
+        *out = &ctx->full;
+        return PT_OK;
+    }
+    bool all = true;
+    for (int64_t e = 0; e < ctx->E; e++) all = all && env_mask[e];
+    if (all) {
+        *out = &ctx->full;
+        return PT_OK;
+    }
+    if (ctx->scope.E > 0 && ctx->scope_mask.size() == (size_t)ctx->E &&
+        memcmp(ctx->scope_mask.data(), env_mask, (size_t)ctx->E) == 0) {
+        *out = &ctx->scope;
+        return PT_OK;
+    }
+    std::vector<int32_t> idx;
+    for (int64_t e = 0; e < ctx->E; e++)
+        if (env_mask[e]) idx.push_back((int32_t)e);
+    if (idx.empty()) return pt_fail(PT_EEMPTY, "env_mask selects no environment");
+    pt_view_free(ctx->scope);
+    ctx->scope_mask.clear();
+    PT_TRY(alloc_view(ctx->scope, (int64_t)idx.size(), ctx->C));
+    int32_t *d_idx = nullptr;
+    PT_CK(cudaMallocAsync((void **)&d_idx, sizeof(int32_t) * idx.size(), ctx->stream));
+    PT_CK(cudaMemcpyAsync(d_idx, idx.data(), sizeof(int32_t) * idx.size(),
+                          cudaMemcpyHostToDevice, ctx->stream));
+    pt_view &s = ctx->scope;
+    k_gather_cfg_major<<<(unsigned)s.C, 128, 0, ctx->stream>>>(
+        ctx->full.l32, ctx->full.l64, ctx->full.E_pad, d_idx, s.E, s.E_pad, s.C, s.l32, s.l64);
+    ctx->stats.launches += 1;
+    PT_CK(cudaGetLastError());
+    PT_CK(cudaFreeAsync(d_idx, ctx->stream));
+    PT_TRY(quantize_view(ctx, s));
+    ctx->scope_mask.assign(env_mask, env_mask + ctx->E);
+    *out = &ctx->scope;
+    return PT_OK;
+}
+
+extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n_env,
+                                  int64_t n_cfg, int64_t ld, const int32_t *env_device,
+                                  uint32_t flags, int cuda_device, void *cuda_stream)
+{
+    if (!out) return pt_fail(PT_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!times_ms || n_env < 1 || n_cfg < 1 || ld < n_cfg)
+        return pt_fail(PT_EINVAL, "bad matrix arguments (n_env=%lld n_cfg=%lld ld=%lld)",
+                       (long long)n_env, (long long)n_cfg, (long long)ld);
+    if (n_cfg >= (1 << 21))
+        return pt_fail(PT_EINVAL, "n_cfg must be < 2^21 (subset keys pack 21-bit indices)");
+    PT_CK(cudaSetDevice(cuda_device));
+    pt_ctx *ctx = new pt_ctx();
+    ctx->dev = cuda_device;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    ctx->flags = flags;
+    ctx->E = n_env;
+    ctx->C = n_cfg;
+    if (env_device) {
+        ctx->env_device.assign(env_device, env_device + n_env);
+        ctx->have_device = true;
+    } else {
+        ctx->env_device.assign((size_t)n_env, 0);
+    }
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    auto bail = [&](pt_status st) {
+        pt_free(ctx);
+        return st;
+    };
+    if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess)
+        return bail(pt_fail(PT_ECUDA, "cudaEventCreate failed"));
+
+    const int64_t E = n_env, C = n_cfg;
+    float *dT = nullptr;
+    double *rowmax = nullptr;
+    int *status = nullptr;
+    if (cudaMalloc(&dT, sizeof(float) * E * C) != cudaSuccess ||
+        cudaMalloc(&ctx->best, sizeof(double) * E) != cudaSuccess ||
+        cudaMalloc(&rowmax, sizeof(double) * E) != cudaSuccess ||
+        cudaMalloc(&status, sizeof(int) * E) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(dT);
+        cudaFree(rowmax);
+        cudaFree(status);
+        return bail(pt_fail(PT_ENOMEM, "device allocation for %lld x %lld failed",
+                            (long long)E, (long long)C));
+    }
+    auto cleanup = [&]() {
+        cudaFree(dT);
+        cudaFree(rowmax);
+        cudaFree(status);
+    };
+    const cudaMemcpyKind kind =
+        pt_is_device_ptr(times_ms) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (cudaMemcpy2DAsync(dT, sizeof(float) * C, times_ms, sizeof(float) * ld,
+                          sizeof(float) * C, E, kind, ctx->stream) != cudaSuccess) {
+        cleanup();
+        return bail(pt_fail(PT_ECUDA, "copy of the runtime matrix failed: %s",
+                            cudaGetErrorString(cudaGetLastError())));
+    }
+    k_rowstats<<<(unsigned)E, 256, 0, ctx->stream>>>(dT, C, ctx->best, rowmax, status);
+    ctx->stats.launches++;
+    std::vector<double> h_rowmax(E);
+    std::vector<int> h_status(E);
+    cudaMemcpyAsync(h_rowmax.data(), rowmax, sizeof(double) * E, cudaMemcpyDeviceToHost,
+                    ctx->stream);
+    cudaMemcpyAsync(h_status.data(), status, sizeof(int) * E, cudaMemcpyDeviceToHost,
+                    ctx->stream);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+        cleanup();
+        return bail(pt_fail(PT_ECUDA, "load: %s", cudaGetErrorString(cudaGetLastError())));
+    }
+    double pen = 1.0;
+    for (int64_t e = 0; e < E; e++) {
+        if (h_status[e] & 1) {
+            cleanup();
+            return bail(pt_fail(PT_EDATA, "environment %lld has a runtime <= 0", (long long)e));
+        }
+        if (h_status[e] & 2) {
+            cleanup();
+            return bail(pt_fail(PT_EDATA, "environment %lld has no measured cell", (long long)e));
+        }
+        pen = std::max(pen, h_rowmax[e]);
+    }
+    ctx->penalty = pen;
+    pt_status st = alloc_view(ctx->full, E, C);
+    if (st != PT_OK) {
+        cleanup();
+        return bail(st);
+    }
+    pt_view &v = ctx->full;
+    dim3 grid((unsigned)((C + 31) / 32), (unsigned)((v.E_pad + 31) / 32));
+    k_ell<<<grid, dim3(32, 8), 0, ctx->stream>>>(dT, E, C, ctx->best, pen, v.E_pad, v.l32, v.l64);
+    ctx->stats.launches++;
+    st = quantize_view(ctx, v);
+    if (st != PT_OK) {
+        cleanup();
+        return bail(st);
+    }
+    cudaError_t ce = cudaStreamSynchronize(ctx->stream);
+    cleanup();
+    if (ce != cudaSuccess || cudaGetLastError() != cudaSuccess)
+        return bail(pt_fail(PT_ECUDA, "normalise kernel failed: %s", cudaGetErrorString(ce)));
+    *out = ctx;
+    return PT_OK;
+}
+
+extern "C" pt_status pt_get_stats(const pt_ctx *ctx, pt_stats *out)
+{
+    if (!ctx || !out) return pt_fail(PT_EINVAL, "NULL argument");
+    *out = ctx->stats;
+    return PT_OK;
+}
+
+extern "C" void pt_free(pt_ctx *ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->dev);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    pt_view_free(ctx->full);
+    pt_view_free(ctx->scope);
+    cudaFree(ctx->best);
+    cudaFree(ctx->scratch);
+    pt_tasks_free(ctx->tasks);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    delete ctx;
+}

@@ -1,0 +1,149 @@
+// pt_internal.cuh -- context, error plumbing and small device helpers shared by
+// the libpt.so translation units.  Nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda.h>            // CUtensorMap (type only; entry point fetched at run time)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "pt.h"
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+pt_status pt_fail(pt_status st, const char *fmt, ...);
+
+#define PT_CK(call)                                                                   \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return pt_fail(PT_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,       \
+                           cudaGetErrorString(e_));                                   \
+    } while (0)
+
+#define PT_TRY(call)                                                                  \
+    do {                                                                              \
+        pt_status s_ = (call);                                                        \
+        if (s_ != PT_OK) return s_;                                                   \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// a scope = the environments in play, compacted to a dense matrix.
+//   l32  [C][E_pad]  fp32 log-slowdowns, config-major (env fastest)
+//   l64  [C][E_pad]  fp64 log-slowdowns, config-major
+//   qT   [E_pad][C_pad] uint32, env-major (config fastest): the fixed-point
+//        lower bound q = floor(l64 * 2^qshift) (exact: l*2^k and floor are exact
+//        in fp64), source of the exhaustive kernel's integer (min,+) tier.
+//        qshift is chosen so that E_pad * max q < 2^32 (no sum can overflow).
+// Padded environments hold 0 (adds nothing to any sum); padded configs of qT
+// hold 0 and are never selectable (index-masked).
+// ---------------------------------------------------------------------------
+struct pt_view {
+    int64_t E = 0, E_pad = 0, C = 0, C_pad = 0;
+    float *l32 = nullptr;
+    double *l64 = nullptr;
+    uint32_t *qT = nullptr;
+    int qshift = 0;
+    bool owned = false;
+};
+
+struct pt_tasks;  // exhaustive work list (exhaustive.cu)
+
+struct pt_ctx {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    uint32_t flags = 0;
+    int num_sms = 0;
+    int64_t E = 0, C = 0;
+    std::vector<int32_t> env_device;
+    bool have_device = false;
+    double penalty = 1.0;
+    double *best = nullptr;   // [E] fp64, each env's Oracle
+    pt_view full;
+    // scope cache (one compacted scope kept alive)
+    std::vector<uint8_t> scope_mask;
+    pt_view scope;
+    // scratch reused across calls
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    pt_tasks *tasks = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    pt_stats stats{};
+};
+
+// scratch allocation (grows, never shrinks); returns PT_OK or PT_ENOMEM
+pt_status pt_scratch(pt_ctx *ctx, size_t bytes, void **p);
+// resolve a mask into a view (NULL -> full); E_scope returned in view->E
+pt_status pt_get_view(pt_ctx *ctx, const uint8_t *env_mask, const pt_view **out);
+void pt_view_free(pt_view &v);
+// true if p is device (or managed) memory
+bool pt_is_device_ptr(const void *p);
+
+// selection entry points used across files
+pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_idx,
+                         double *s1_trace, double *s2_trace);
+pt_status pt_exhaustive_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t shard_rank,
+                             int32_t shard_count, int32_t *best, int32_t *runner,
+                             double *s_out, int *n_found);
+pt_status pt_score_view(pt_ctx *ctx, const pt_view *v, const int32_t *d_sets, int64_t n_sets,
+                        int32_t k, double *d_s);
+
+void pt_tasks_free(pt_tasks *t);
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+static inline int64_t pt_round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// binomial coefficient C(n, r) for small r, exact in int64 for the sizes used
+// here (n <= 2^21, r <= 4); returns 0 when n < r.
+__host__ __device__ static inline int64_t pt_binom(int64_t n, int r)
+{
+    if (n < r || r < 0) return 0;
+    switch (r) {   // constant divisors: no 64-bit division loop on the device
+    case 0: return 1;
+    case 1: return n;
+    case 2: return n * (n - 1) / 2;
+    case 3: return n * (n - 1) * (n - 2) / 6;
+    case 4: return n * (n - 1) * (n - 2) / 6 * (n - 3) / 4;
+    default: {
+        int64_t v = 1;
+        for (int q = 0; q < r; q++) v = v * (n - q) / (q + 1);
+        return v;
+    }
+    }
+}
+
+// colex unranking of a (k-1)... generic m-subset: rank R -> ascending members.
+// Largest c with C(c, u+1) <= R, for u = m-1 .. 0.  n = universe size.
+__host__ __device__ static inline void pt_unrank_colex(int64_t R, int m, int64_t n, int32_t *out)
+{
+    for (int u = m - 1; u >= 0; u--) {
+        // binary search c in [u, n-1]
+        int64_t lo = u, hi = n - 1;
+        while (lo < hi) {
+            int64_t mid = (lo + hi + 1) >> 1;
+            if (pt_binom(mid, u + 1) <= R) lo = mid; else hi = mid - 1;
+        }
+        out[u] = (int32_t)lo;
+        R -= pt_binom(lo, u + 1);
+    }
+}
+
+// lexicographic order on sorted tuples + score: returns true if (sa,a) < (sb,b)
+__host__ __device__ static inline bool pt_key_less(double sa, const int32_t *a, double sb,
+                                                   const int32_t *b, int k)
+{
+    if (sa < sb) return true;
+    if (sa > sb) return false;
+    for (int u = 0; u < k; u++) {
+        if (a[u] < b[u]) return true;
+        if (a[u] > b[u]) return false;
+    }
+    return false;
+}
+
+#define PT_MAXK 8

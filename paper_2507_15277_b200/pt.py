@@ -1,0 +1,249 @@
+"""Thin ctypes binding of libpt.so (include/pt.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this
+module only converts numpy arrays / torch tensors to pointers, picks the
+current CUDA stream, and (for the multi-GPU search) moves the 8-byte-class
+(score, index) records between ranks with torch.distributed.  There is no CPU
+fallback: if libpt.so is missing or cannot initialise a GPU, calls raise.
+
+Names follow the C ABI: pt_load_perf, pt_score_sets, pt_greedy_select,
+pt_exhaustive_best, pt_merge_top2, pt_eval_holdout, pt_get_stats, pt_free.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpt.so")
+
+PT_OK, PT_EINVAL, PT_ENOMEM, PT_ECUDA, PT_ENCCL, PT_ECAP, PT_EEMPTY, PT_EDATA = 0, -1, -2, -3, -4, -5, -6, -7
+PT_OBJ_GEOMEAN, PT_OBJ_FLEET = 0, 1
+PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM = 0x1, 0x2, 0x4
+
+EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
+           "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_free", "pt_last_error")
+
+
+class pt_stats(ct.Structure):
+    _fields_ = [("launches", ct.c_int64), ("exh_main_ms", ct.c_double), ("exh_sets", ct.c_int64),
+                ("exh_slots", ct.c_int64), ("exh_env_pad", ct.c_int64),
+                ("exh_candidates", ct.c_int64), ("exh_passes", ct.c_int32),
+                ("exh_kernel", ct.c_int32), ("greedy_ms", ct.c_double)]
+
+
+class PTError(RuntimeError):
+    def __init__(self, code, where, msg):
+        super().__init__(f"{where}: status {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libpt.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (or make)")
+        L = ct.CDLL(LIB_PATH)
+        P, i64, i32, u32, dbl = ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_uint32, ct.c_double
+        L.pt_load_perf.argtypes = [ct.POINTER(P), P, i64, i64, i64, P, u32, ct.c_int, P]
+        L.pt_score_sets.argtypes = [P, P, i64, i32, P, i32, P]
+        L.pt_greedy_select.argtypes = [P, i32, P, i32, P, P, P]
+        L.pt_exhaustive_best.argtypes = [P, i32, P, i32, i32, i32, P, P, P, P, P]
+        L.pt_merge_top2.argtypes = [P, P, i32, i32, P, P, P]
+        L.pt_eval_holdout.argtypes = [P, i32, i32, i32, P, P, P, P, P]
+        L.pt_get_stats.argtypes = [P, ct.POINTER(pt_stats)]
+        L.pt_free.argtypes = [P]
+        L.pt_free.restype = None
+        L.pt_last_error.argtypes = []
+        L.pt_last_error.restype = ct.c_char_p
+        for f in ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
+                  "pt_merge_top2", "pt_eval_holdout", "pt_get_stats"):
+            getattr(L, f).restype = ct.c_int
+        _lib = L
+    return _lib
+
+
+def _chk(rc, where):
+    if rc != PT_OK:
+        raise PTError(rc, where, lib().pt_last_error().decode())
+
+
+def _ptr(a):
+    """Pointer of a numpy array or torch tensor (host or device); None -> NULL."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return ct.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(ct.c_void_p)
+
+
+def _np(a, dtype):
+    return np.ascontiguousarray(np.asarray(a), dtype=dtype)
+
+
+def _mask(m):
+    return None if m is None else _np(m, np.uint8)
+
+
+def _stream(stream):
+    if stream is not None:
+        return ct.c_void_p(int(stream))
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return ct.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except ImportError:
+        pass
+    return None
+
+
+class PtContext:
+    """Owner of a pt_ctx handle (freed on close / garbage collection)."""
+
+    def __init__(self, handle, n_env, n_cfg):
+        self.handle = handle
+        self.E, self.C = n_env, n_cfg
+
+    def close(self):
+        if self.handle:
+            lib().pt_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pt_load_perf(times_ms, env_device=None, flags=0, device=0, stream=None) -> PtContext:
+    """times_ms: [E][C] float32 numpy array (host) or torch tensor (host or cuda)."""
+    if hasattr(times_ms, "data_ptr"):
+        assert times_ms.dtype.__str__() == "torch.float32" and times_ms.is_contiguous()
+        E, C = times_ms.shape
+        keep = times_ms
+    else:
+        keep = _np(times_ms, np.float32)
+        E, C = keep.shape
+    dev = None if env_device is None else _np(env_device, np.int32)
+    h = ct.c_void_p()
+    _chk(lib().pt_load_perf(ct.byref(h), _ptr(keep), E, C, C, _ptr(dev), flags, device,
+                            _stream(stream)), "pt_load_perf")
+    return PtContext(h, E, C)
+
+
+def pt_score_sets(ctx, sets, env_mask=None, out=None):
+    """G of each set.  sets: [n][k] int32 (numpy or torch); returns numpy (or fills `out`)."""
+    if hasattr(sets, "data_ptr"):
+        n, k = sets.shape
+        s = sets
+    else:
+        s = np.atleast_2d(_np(sets, np.int32))
+        n, k = s.shape
+    res = out if out is not None else np.empty(n, np.float64)
+    _chk(lib().pt_score_sets(ctx.handle, _ptr(s), n, k, _ptr(_mask(env_mask)), PT_OBJ_GEOMEAN,
+                             _ptr(res)), "pt_score_sets")
+    return res
+
+
+def pt_greedy_select(ctx, k, env_mask=None):
+    """Greedy forward selection: (indices, G_trace, gap_trace)."""
+    idx = np.zeros(k, np.int32)
+    gt = np.zeros(k, np.float64)
+    gp = np.zeros(k, np.float64)
+    _chk(lib().pt_greedy_select(ctx.handle, k, _ptr(_mask(env_mask)), PT_OBJ_GEOMEAN, _ptr(idx),
+                                _ptr(gt), _ptr(gp)), "pt_greedy_select")
+    return [int(x) for x in idx], gt, gp
+
+
+def pt_exhaustive_best(ctx, k, env_mask=None, shard_rank=0, shard_count=1):
+    """Exhaustive k-subset search (one shard): dict(best, G, runner, G_runner, s)."""
+    b = np.zeros(k, np.int32)
+    r = np.zeros(k, np.int32)
+    g = np.zeros(2, np.float64)
+    s = np.zeros(2, np.float64)
+    _chk(lib().pt_exhaustive_best(ctx.handle, k, _ptr(_mask(env_mask)), PT_OBJ_GEOMEAN,
+                                  shard_rank, shard_count, _ptr(b), _ptr(g[0:1]), _ptr(r),
+                                  _ptr(g[1:2]), _ptr(s)), "pt_exhaustive_best")
+    has1, has2 = np.isfinite(s[0]), np.isfinite(s[1])
+    return {"best": tuple(int(x) for x in b) if has1 else None, "G": float(g[0]),
+            "runner": tuple(int(x) for x in r) if has2 else None, "G_runner": float(g[1]),
+            "s": (float(s[0]), float(s[1]))}
+
+
+def pt_merge_top2(s, tuples, k):
+    """Merge (s, tuple) records -> (best, runner, (s1, s2)); host-only."""
+    s = _np(s, np.float64)
+    t = _np(tuples, np.int32).reshape(len(s), k)
+    b = np.zeros(k, np.int32)
+    r = np.zeros(k, np.int32)
+    o = np.zeros(2, np.float64)
+    _chk(lib().pt_merge_top2(_ptr(s), _ptr(t), len(s), k, _ptr(b), _ptr(r), _ptr(o)),
+         "pt_merge_top2")
+    runner = tuple(int(x) for x in r) if np.isfinite(o[1]) else None
+    return tuple(int(x) for x in b), runner, (float(o[0]), float(o[1]))
+
+
+def pt_eval_holdout(ctx, heldout_device, k, method=0):
+    """Leave-one-device-out: dict(idx, G_train, G_unseen, G_known, known_idx)."""
+    idx = np.zeros(k, np.int32)
+    kidx = np.zeros(k, np.int32)
+    g = np.zeros(3, np.float64)
+    _chk(lib().pt_eval_holdout(ctx.handle, heldout_device, k, method, _ptr(idx), _ptr(g[0:1]),
+                               _ptr(g[1:2]), _ptr(g[2:3]), _ptr(kidx)), "pt_eval_holdout")
+    return {"idx": [int(x) for x in idx], "G_train": float(g[0]), "G_unseen": float(g[1]),
+            "G_known": float(g[2]), "known_idx": [int(x) for x in kidx]}
+
+
+def pt_get_stats(ctx):
+    st = pt_stats()
+    _chk(lib().pt_get_stats(ctx.handle, ct.byref(st)), "pt_get_stats")
+    return {f: getattr(st, f) for f, _ in pt_stats._fields_}
+
+
+def pt_free(ctx):
+    ctx.close()
+
+
+def exhaustive_best_distributed(ctx, k, env_mask=None, group=None, local_search=None,
+                                n_env=None):
+    """Sharded exhaustive search: rank r of world W searches shard r of W, then
+    the (s, tuple) top-2 records of every rank are all-gathered (NCCL over
+    NVLink for a cuda group, gloo on CPU) and merged identically on every rank
+    with pt_merge_top2.  `local_search(shard_rank, shard_count)` may replace the
+    GPU shard search (tests drive the protocol on CPU with it)."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if local_search is None:
+        res = pt_exhaustive_best(ctx, k, env_mask, rank, world)
+        recs = [(res["s"][0], res["best"]), (res["s"][1], res["runner"])]
+    else:
+        recs = local_search(rank, world)
+    buf = torch.full((2, k + 1), float("inf"), dtype=torch.float64)
+    for q, (sv, tup) in enumerate(recs):
+        if tup is not None and np.isfinite(sv):
+            buf[q, 0] = sv
+            buf[q, 1:] = torch.tensor(tup, dtype=torch.float64)
+    if world > 1:
+        backend = dist.get_backend(group)
+        dev_buf = buf.cuda() if backend == "nccl" else buf
+        out = [torch.empty_like(dev_buf) for _ in range(world)]
+        dist.all_gather(out, dev_buf, group=group)
+        allr = torch.cat([o.cpu() for o in out]).numpy()
+    else:
+        allr = buf.numpy()
+    s = allr[:, 0]
+    t = np.where(np.isfinite(allr[:, 1:]), allr[:, 1:], -1).astype(np.int32)
+    best, runner, (s1, s2) = pt_merge_top2(s, t, k)
+    E = (ctx.E if ctx is not None else n_env) if env_mask is None else int(np.count_nonzero(env_mask))
+    return {"best": best, "G": float(np.exp(-s1 / E)), "runner": runner,
+            "G_runner": float(np.exp(-s2 / E)) if np.isfinite(s2) else float("nan"),
+            "s": (s1, s2)}

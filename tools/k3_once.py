@@ -1,0 +1,8 @@
+import sys
+sys.path.insert(0, ".")
+import torch
+from paper_2507_15277_b200 import pt, synth
+T, dev = synth.paper_matrix(1)
+ctx = pt.pt_load_perf(torch.from_numpy(T).cuda(), dev)
+r = pt.pt_exhaustive_best(ctx, int(sys.argv[1]) if len(sys.argv) > 1 else 3)
+print(r, pt.pt_get_stats(ctx))
