@@ -34,7 +34,7 @@
 #define XT_C 64     // columns per CTA tile
 #define XT_K 32     // environments per pipeline stage
 #define XT_S 4      // pipeline stages
-#define XT_EMAX 352 // widest scope the resident-A kernel takes (smem)
+#define XT_EMAX 384 // widest scope the resident-A kernel takes (smem)
 #define XT_UMAX 1024 // column tiles per task (a whole row tile: A staged once)
 #define KEY_BITS 21
 
@@ -61,7 +61,7 @@ void pt_tasks_free(pt_tasks *t)
 // colex rank range of m-subsets whose largest element is j: [C(j,m), C(j+1,m))
 static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **out)
 {
-    if (ctx->tasks && ctx->tasks->m == m && ctx->tasks->C == v->C && ctx->tasks->tag == v->qT) {
+    if (ctx->tasks && ctx->tasks->m == m && ctx->tasks->C == v->C && ctx->tasks->tag == v->hT) {
         *out = ctx->tasks;
         return PT_OK;
     }
@@ -70,12 +70,22 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **ou
     pt_tasks *T = new pt_tasks();
     T->m = m;
     T->C = v->C;
-    T->tag = v->qT;
+    T->tag = v->hT;
     const int64_t C = v->C;
     const int64_t n_rows = pt_binom(C, m);
     const int64_t n_rt = (n_rows + XT_R - 1) / XT_R;
     T->slot_pre.push_back(0);
     T->set_pre.push_back(0);
+    // task granularity: whole row tiles (A staged once) unless that leaves too
+    // few tasks for the SMs (small problems, e.g. k=2)
+    int64_t total_ct = 0;
+    for (int64_t t = 0; t < n_rt; t++) {
+        int32_t mem[PT_MAXK];
+        pt_unrank_colex(t * XT_R, m, C, mem);
+        const int64_t ncols = C - (mem[m - 1] + 1);
+        if (ncols > 0) total_ct += (ncols + XT_C - 1) / XT_C;
+    }
+    const int64_t umax = std::max<int64_t>(1, std::min<int64_t>(XT_UMAX, total_ct / (8 * std::max(ctx->num_sms, 1))));
     for (int64_t t = 0; t < n_rt; t++) {
         const int64_t R0 = t * XT_R, R1 = std::min(n_rows, R0 + XT_R);
         int32_t mem[PT_MAXK];
@@ -85,8 +95,8 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **ou
         const int64_t ncols = C - lo;
         if (ncols <= 0) continue;
         const int64_t n_ct = (ncols + XT_C - 1) / XT_C;
-        for (int64_t u0 = 0; u0 < n_ct; u0 += XT_UMAX) {
-            const int64_t u1 = std::min(n_ct, u0 + XT_UMAX);
+        for (int64_t u0 = 0; u0 < n_ct; u0 += umax) {
+            const int64_t u1 = std::min(n_ct, u0 + umax);
             const int64_t clo = lo + u0 * XT_C, chi = std::min(C, lo + u1 * XT_C);
             // useful sets: rows grouped by their largest element j (colex)
             int64_t useful = 0;
@@ -170,28 +180,46 @@ __device__ __forceinline__ void named_sync(int id, int n)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-// acc += x + y in one IADD3
-__device__ __forceinline__ uint32_t add3(uint32_t acc, uint32_t x, uint32_t y)
+// packed-fp16 helpers (values are non-negative log-slowdowns)
+__device__ __forceinline__ uint32_t hmin2(uint32_t a, uint32_t b)
 {
     uint32_t r;
-    asm("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %3;" : "=r"(r) : "r"(acc), "r"(x), "r"(y));
+    asm("min.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
     return r;
+}
+__device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b)
+{
+    uint32_t r;
+    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+// (acc_lo, acc_hi) += (f32(p.lo), f32(p.hi)): two FHADD (fp32 += fp16)
+__device__ __forceinline__ void fhadd2(float &lo_acc, float &hi_acc, uint32_t p)
+{
+    unsigned short lo, hi;
+    asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(p));
+    asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(lo_acc) : "h"(lo));
+    asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(hi_acc) : "h"(hi));
 }
 
 // ---------------------------------------------------------------------------
-// the tiled integer (min,+) kernel
+// the tiled (min,+) kernel -- packed-fp16 filter tier
 //
-// Fast tier = exact integer arithmetic on the fixed-point lower bounds
-// q = floor(l * 2^k): Q(S) = sum_e min_{c in S} q[c][e] (no rounding: floor
-// commutes with min, sums fit in 32 bits), so for every set
-//     Q/2^k <= s(S) < (Q + E)/2^k.
-// Inner loop per (set, env pair): 2 IMNMX + 1 IADD3 (3-input add).
+// Fast score of a set = sum over env pairs of fp16(min(a,b)_e + min(a,b)_e+1)
+// accumulated in fp32: per (set, env pair) HMNMX2 (two mins for two columns)
+// is shared by two sets, one HADD2 adds the two envs of both sets, two FHADD
+// accumulate into fp32 -- 1.25 issue slots per (set, env) instead of 2 for
+// FMNMX+FADD, with the mins on the (half-rate) ALU pipe and the adds on the
+// FMA pipe.  Every error is bounded:
+//     |s_hat - s| <= eta_rel * s + eta_abs
+// so the filter keeps every set that could be one of the exact best two and
+// the fp64 refine decides.
 //
-// Warp roles (288 threads): warps 0-7 compute (8x4 sets each, 128x64 per
-// CTA), warp 8 is the producer: it streams 32-env x 64-config column tiles of
-// qT through the TMA engine (cp.async.bulk, one 256-byte row per lane) into an
-// XT_S-deep ring of full/empty mbarriers.  Consumers never block on each
-// other inside a task.
+// Warp roles (288 threads): warps 0-7 compute (8 rows x 4 columns each, 128x64
+// per CTA), warp 8 is the producer: it streams 32-env x 64-config fp16 column
+// tiles of hT through the TMA engine (cp.async.bulk, one 128-byte row per
+// lane) into an XT_S-deep ring of full/empty mbarriers.  Consumers never wait
+// for each other inside a task.
 // ---------------------------------------------------------------------------
 struct XParams {
     int64_t C, C_pad, E_pad, n_rows;
@@ -199,27 +227,29 @@ struct XParams {
     const int4 *tasks;
     int task_hi;              // end of this shard's task range
     int *task_ctr;            // dynamic scheduler (starts at the shard's first task)
-    uint32_t tau_seed;        // integer threshold from the greedy seed
-    uint32_t slack;           // E + 1: Q-window between a lower bound and an upper bound
-    unsigned *U;              // min over warps of their best 2nd-smallest Q
+    float tau_seed;           // threshold seeded by greedy's exact runner-up score
+    float kappa;              // tau(U) = U * kappa + beta (rounded up)
+    float beta;
+    unsigned *U;              // float bits: min over warps of their 2nd-smallest s_hat
     unsigned long long *cand_key;
-    uint32_t *cand_q;
+    float *cand_s;
     unsigned *cand_n;
     unsigned cap;
-    const uint32_t *qT;
+    const uint16_t *hT;
 };
 
 #define XT_THREADS 288
 #define XT_CONS 256
+#define XT_BROW (XT_C * 2)     // bytes of one env row of a column tile
 
 __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                  // [S][K][64]
-    uint32_t *As = Bs + XT_S * XT_K * XT_C;                              // [E_pad][128]
-    int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);          // [128]
-    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);        // [S]
-    uint64_t *empty = full + XT_S;                                       // [S]
+    uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2
+    uint32_t *As = Bs + XT_S * XT_K * (XT_C / 2);                              // [E_pad][128] (a,a)
+    int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);                // [128]
+    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);              // [S]
+    uint64_t *empty = full + XT_S;                                             // [S]
     int4 *task_s = reinterpret_cast<int4 *>(empty + XT_S);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -234,9 +264,8 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
     __syncthreads();
 
     uint32_t steps = 0;   // pipeline steps of all previous tasks (same in every thread)
-    // consumer state
     const int tx = tid & 15, ty = (tid >> 4) & 15;
-    uint32_t b1 = 0xffffffffu, b2 = 0xffffffffu, published = 0xffffffffu;
+    float b1 = INFINITY, b2 = INFINITY, published = INFINITY;
 
     for (;;) {
         if (tid == 0) {
@@ -249,9 +278,9 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
         const int64_t R0 = (int64_t)tk.x * XT_R;
         int32_t mem0[PT_MAXK];
         pt_unrank_colex(R0, p.m, p.C, mem0);
-        // first column of the row tile, rounded down to 16 bytes (the extra
-        // columns are <= the row's largest element and masked)
-        const int64_t lo = ((int64_t)mem0[p.m - 1] + 1) & ~(int64_t)3;
+        // first column of the row tile, rounded down to 16 bytes (8 configs);
+        // the extra columns are <= the row's largest element and masked
+        const int64_t lo = ((int64_t)mem0[p.m - 1] + 1) & ~(int64_t)7;
         const int nsteps = (tk.z - tk.y) * nkc;
 
         if (warp == XT_CONS / 32) {
@@ -261,15 +290,16 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
                 const int slot = G % XT_S;
                 mbar_wait(&empty[slot], ((G / XT_S) & 1u) ^ 1u);
                 const int u = tk.y + g / nkc, q = g % nkc;
-                if (lane == 0) mbar_expect_tx(&full[slot], XT_K * XT_C * 4);
+                if (lane == 0) mbar_expect_tx(&full[slot], XT_K * XT_BROW);
                 __syncwarp();
-                bulk_g2s(Bs + slot * XT_K * XT_C + lane * XT_C,
-                         p.qT + (int64_t)(q * XT_K + lane) * p.C_pad + lo + (int64_t)u * XT_C,
-                         XT_C * 4, &full[slot]);
+                bulk_g2s(Bs + slot * XT_K * (XT_C / 2) + lane * (XT_C / 2),
+                         p.hT + (int64_t)(q * XT_K + lane) * p.C_pad + lo + (int64_t)u * XT_C,
+                         XT_BROW, &full[slot]);
             }
         } else {
             // ---------------- consumers ----------------
-            // stage A for the whole task: A[e][r] = min over the row's members
+            // stage A for the whole task: A[e][r] = min over the row's members,
+            // replicated into both halves of a half2
             {
                 const int r = tid & (XT_R - 1);
                 const int64_t R = R0 + r;
@@ -278,47 +308,44 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
                 if (valid) pt_unrank_colex(R, p.m, p.C, mem);
                 else for (int u = 0; u < p.m; u++) mem[u] = 0;
                 if (tid < XT_R) last_s[r] = valid ? mem[p.m - 1] : 0x7fffffff;
-                const uint32_t *base = p.qT;
 #pragma unroll 4
                 for (int64_t e = tid >> 7; e < p.E_pad; e += 2) {
-                    const uint32_t *rowp = base + e * p.C_pad;
-                    uint32_t a = rowp[mem[0]];
-                    for (int u = 1; u < p.m; u++) a = min(a, rowp[mem[u]]);
-                    As[e * XT_R + r] = valid ? a : 0u;
+                    const uint16_t *rowp = p.hT + e * p.C_pad;
+                    uint32_t a = rowp[mem[0]];     // non-negative fp16: integer order
+                    for (int u = 1; u < p.m; u++) a = min(a, (uint32_t)rowp[mem[u]]);
+                    As[e * XT_R + r] = valid ? (a | (a << 16)) : 0u;
                 }
             }
             named_sync(1, XT_CONS);
 
-            uint32_t acc[8][4];
+            float acc[8][4];
 #pragma unroll
             for (int i = 0; i < 8; i++)
 #pragma unroll
-                for (int j = 0; j < 4; j++) acc[i][j] = 0u;
+                for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
 
             for (int g = 0; g < nsteps; g++) {
                 const uint32_t G = steps + g;
                 const int slot = G % XT_S;
                 mbar_wait(&full[slot], (G / XT_S) & 1u);
                 const int q = g % nkc;
-                const uint32_t *B = Bs + slot * XT_K * XT_C + tx * 4;
+                const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + tx * 2;
                 const uint32_t *A = As + (int64_t)q * XT_K * XT_R + ty * 4;
 #pragma unroll 4
                 for (int e = 0; e < XT_K; e += 2) {
                     const uint4 a0 = *reinterpret_cast<const uint4 *>(A + e * XT_R);
                     const uint4 a1 = *reinterpret_cast<const uint4 *>(A + e * XT_R + 64);
-                    const uint4 b = *reinterpret_cast<const uint4 *>(B + e * XT_C);
                     const uint4 c0 = *reinterpret_cast<const uint4 *>(A + (e + 1) * XT_R);
                     const uint4 c1 = *reinterpret_cast<const uint4 *>(A + (e + 1) * XT_R + 64);
-                    const uint4 d = *reinterpret_cast<const uint4 *>(B + (e + 1) * XT_C);
+                    const uint2 b = *reinterpret_cast<const uint2 *>(B + e * (XT_C / 2));
+                    const uint2 d = *reinterpret_cast<const uint2 *>(B + (e + 1) * (XT_C / 2));
                     const uint32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                     const uint32_t cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-                    const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
-                    const uint32_t dv[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-                    for (int i = 0; i < 8; i++)
-#pragma unroll
-                        for (int j = 0; j < 4; j++)
-                            acc[i][j] = add3(acc[i][j], min(av[i], bv[j]), min(cv[i], dv[j]));
+                    for (int i = 0; i < 8; i++) {
+                        fhadd2(acc[i][0], acc[i][1], hadd2(hmin2(av[i], b.x), hmin2(cv[i], d.x)));
+                        fhadd2(acc[i][2], acc[i][3], hadd2(hmin2(av[i], b.y), hmin2(cv[i], d.y)));
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
@@ -326,8 +353,8 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
                     // epilogue of one column tile: mask, window test, candidate append
                     const int u = tk.y + g / nkc;
                     const int64_t l0 = lo + (int64_t)u * XT_C + tx * 4;
-                    const uint32_t Uv = *(volatile unsigned *)p.U;
-                    const uint32_t tau = min(p.tau_seed, Uv > 0xffffffffu - p.slack ? 0xffffffffu : Uv + p.slack);
+                    const float Uv = __uint_as_float(*(volatile unsigned *)p.U);
+                    const float tau = fminf(p.tau_seed, fmaf(Uv, p.kappa, p.beta));
 #pragma unroll
                     for (int i = 0; i < 8; i++) {
                         const int r = (i < 4) ? ty * 4 + i : 64 + ty * 4 + (i - 4);
@@ -335,30 +362,30 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             const int64_t l = l0 + j;
-                            const uint32_t sq = acc[i][j];
-                            acc[i][j] = 0u;
+                            const float sh = acc[i][j];
+                            acc[i][j] = 0.0f;
                             if (l < p.C && l > last) {
-                                if (sq < b1) {
+                                if (sh < b1) {
                                     b2 = b1;
-                                    b1 = sq;
-                                } else if (sq < b2) {
-                                    b2 = sq;
+                                    b1 = sh;
+                                } else if (sh < b2) {
+                                    b2 = sh;
                                 }
-                                if (sq <= tau) {
+                                if (sh <= tau) {
                                     const unsigned idx = atomicAdd(p.cand_n, 1u);
                                     if (idx < p.cap) {
                                         p.cand_key[idx] = ((unsigned long long)(R0 + r) << KEY_BITS) |
                                                           (unsigned long long)l;
-                                        p.cand_q[idx] = sq;
+                                        p.cand_s[idx] = sh;
                                     }
                                 }
                             }
                         }
                     }
-                    uint32_t wb = b2;
-                    for (int o = 16; o; o >>= 1) wb = min(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+                    float wb = b2;
+                    for (int o = 16; o; o >>= 1) wb = fminf(wb, __shfl_xor_sync(0xffffffffu, wb, o));
                     if (lane == 0 && wb < published) {
-                        atomicMin(p.U, wb);
+                        atomicMin(p.U, __float_as_uint(wb));
                         published = wb;
                     }
                 }
@@ -372,7 +399,7 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
 // fp64 refine of the survivors: warp per candidate, fixed shuffle tree
 // ---------------------------------------------------------------------------
 __global__ void k_exh_refine(const unsigned long long *__restrict__ key,
-                             const uint32_t *__restrict__ cs, unsigned n, uint32_t tau, int m, int64_t C,
+                             const float *__restrict__ cs, unsigned n, float tau, int m, int64_t C,
                              const double *__restrict__ l64, int64_t E_pad,
                              double *__restrict__ out_s, int32_t *__restrict__ out_t)
 {
@@ -567,32 +594,42 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     s_out[0] = s_out[1] = INFINITY;
     if (ta >= tb) return PT_OK;
 
-    // threshold seed: exact score of greedy's second-best set at its last step
-    // (s_(2) <= that score, and Q <= 2^k s for every set)
+    // error model of the fp16 tier:
+    //   |s_hat - s| <= eta_rel * s + eta_abs
+    //   eta_rel: fp16 rounding of each term (2^-11) + fp16 pair add (2^-11) +
+    //            fp32 accumulation of E_pad/2 pair sums; eta_abs: fp16 subnormals
+    const double u16 = std::ldexp(1.0, -11), u32 = std::ldexp(1.0, -24);
+    const double npair = (double)v->E_pad / 2.0 + 2.0;
+    const double eta_rel = (2.0 * u16 + u16 * u16 + npair * u32 / (1.0 - npair * u32)) * 1.01;
+    const double eta_abs = 2.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
+    const double kap = (1.0 + eta_rel) / (1.0 - eta_rel) * (1.0 + 1e-6);
+    auto f_up = [](double x) -> float {
+        if (!(x < 3.0e38)) return INFINITY;
+        float f = (float)x;
+        if ((double)f < x) f = nextafterf(f, INFINITY);
+        return f;
+    };
+    // seed: exact score of greedy's runner-up set at its last step (>= s_(2))
     std::vector<int32_t> gidx(k);
     std::vector<double> gs1(k), gs2(k);
     PT_TRY(pt_greedy_view(ctx, v, k, gidx.data(), gs1.data(), gs2.data()));
-    const double scale = std::ldexp(1.0, v->qshift);
-    auto to_q = [](double x) -> uint32_t {
-        if (!(x < 4294967295.0)) return 0xffffffffu;
-        return (uint32_t)x;
-    };
-    const uint32_t tau_seed = to_q(std::floor(gs2[k - 1] * scale * (1.0 + 1e-12)) + 1.0);
-    const uint32_t slack = (uint32_t)v->E + 1u;
+    const float tau_seed = f_up((gs2[k - 1] * (1.0 + eta_rel) + eta_abs) * (1.0 + 1e-6));
+    const float kappa = f_up(kap);
+    const float beta = f_up(eta_abs * (kap + 1.0) * (1.0 + 1e-6));
 
-    const size_t smem = sizeof(uint32_t) * (XT_S * XT_K * XT_C + v->E_pad * XT_R) +
+    const size_t smem = sizeof(uint32_t) * (XT_S * XT_K * (XT_C / 2) + v->E_pad * XT_R) +
                         sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
     PT_CK(cudaFuncSetAttribute(k_exh_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
     unsigned cap = 1u << 20;
     unsigned n_cand = 0;
-    uint32_t tau_pass = tau_seed;
+    float tau_pass = tau_seed;
     for (int pass = 0; pass < 2; pass++) {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
         const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)),
                      o_n = take(sizeof(unsigned)), o_key = take(sizeof(unsigned long long) * cap),
-                     o_cq = take(sizeof(uint32_t) * cap), o_rs = take(sizeof(double) * cap),
+                     o_cq = take(sizeof(float) * cap), o_rs = take(sizeof(double) * cap),
                      o_rt = take(sizeof(int32_t) * (size_t)cap * k), o_os = take(sizeof(double) * 2),
                      o_ot = take(sizeof(int32_t) * 2 * k);
         void *scr = nullptr;
@@ -601,10 +638,10 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         int *ctr = (int *)(b + o_ctr);
         unsigned *U = (unsigned *)(b + o_U), *cn = (unsigned *)(b + o_n);
         unsigned long long *ckey = (unsigned long long *)(b + o_key);
-        uint32_t *cq = (uint32_t *)(b + o_cq);
+        float *cq = (float *)(b + o_cq);
         double *rs = (double *)(b + o_rs), *os = (double *)(b + o_os);
         int32_t *rt = (int32_t *)(b + o_rt), *ot = (int32_t *)(b + o_ot);
-        const unsigned u_init = 0xffffffffu;
+        const unsigned u_init = 0x7f800000u;   // +inf
         PT_CK(cudaMemcpyAsync(ctr, &ta, sizeof(int), cudaMemcpyHostToDevice, s));
         PT_CK(cudaMemcpyAsync(U, &u_init, sizeof(unsigned), cudaMemcpyHostToDevice, s));
         PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned), s));
@@ -618,13 +655,14 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.task_hi = tb;
         p.task_ctr = ctr;
         p.tau_seed = tau_pass;
-        p.slack = slack;
+        p.kappa = kappa;
+        p.beta = beta;
         p.U = U;
         p.cand_key = ckey;
-        p.cand_q = cq;
+        p.cand_s = cq;
         p.cand_n = cn;
         p.cap = cap;
-        p.qT = v->qT;
+        p.hT = v->hT;
         const int grid = std::min(ctx->num_sms, tb - ta);
         PT_CK(cudaEventRecord(ctx->ev0, s));
         k_exh_tiled<<<grid, XT_THREADS, smem, s>>>(p);
@@ -639,10 +677,9 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
         if (pass == 0) ctx->stats.exh_main_ms = ms;
         ctx->stats.exh_passes = pass + 1;
-        const uint32_t tau_final =
-            std::min<uint64_t>(tau_pass, (uint64_t)hU + (uint64_t)slack) > 0xffffffffull
-                ? 0xffffffffu
-                : (uint32_t)std::min<uint64_t>(tau_pass, (uint64_t)hU + (uint64_t)slack);
+        float Uf;
+        memcpy(&Uf, &hU, sizeof Uf);
+        const float tau_final = std::min(tau_pass, f_up((double)Uf * kap + eta_abs * (kap + 1.0)));
         if (n_cand > cap) {
             // overflow: rerun with the final threshold and room for every survivor
             cap = n_cand;

@@ -17,6 +17,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "pt_internal.cuh"
 
 static thread_local std::string g_err;
@@ -67,7 +69,7 @@ void pt_view_free(pt_view &v)
     if (v.owned) {
         cudaFree(v.l32);
         cudaFree(v.l64);
-        cudaFree(v.qT);
+        cudaFree(v.hT);
     }
     v = pt_view();
 }
@@ -177,40 +179,23 @@ __global__ void k_gather_cfg_major(const float *__restrict__ s32, const double *
     }
 }
 
-// max of l64 over the real cells of a view (one block per config row)
-__global__ void k_colmax(const double *__restrict__ l64, int64_t E, int64_t E_pad,
-                         double *__restrict__ cmax)
+// hT[e][c] = fp16(l64[c][e]) (round to nearest), 32x32 smem transpose
+__global__ void k_half(const double *__restrict__ l64, int64_t E, int64_t C, int64_t E_pad,
+                       int64_t C_pad, uint16_t *__restrict__ hT)
 {
-    const int64_t c = blockIdx.x;
-    double m = 0.0;
-    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) m = fmax(m, l64[c * E_pad + e]);
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    __shared__ double r[32];
-    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmax(m, r[w]);
-        cmax[c] = fmax(m, r[0]);
-    }
-}
-
-// qT[e][c] = floor(l64[c][e] * 2^shift) (exact), 32x32 smem transpose
-__global__ void k_quant(const double *__restrict__ l64, int64_t E, int64_t C, int64_t E_pad,
-                        int64_t C_pad, double scale, uint32_t *__restrict__ qT)
-{
-    __shared__ uint32_t tile[32][33];
+    __shared__ uint16_t tile[32][34];
     const int64_t c0 = (int64_t)blockIdx.x * 32, e0 = (int64_t)blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
     for (int r = ty; r < 32; r += 8) {
         int64_t c = c0 + r, e = e0 + tx;
-        uint32_t q = 0;
-        if (c < C && e < E) q = (uint32_t)floor(l64[c * E_pad + e] * scale);
-        tile[r][tx] = q;
+        uint16_t h = 0;
+        if (c < C && e < E) h = __half_as_ushort(__double2half(l64[c * E_pad + e]));
+        tile[r][tx] = h;
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
         int64_t e = e0 + r, c = c0 + tx;
-        if (e < E_pad && c < C_pad) qT[e * C_pad + c] = tile[tx][r];
+        if (e < E_pad && c < C_pad) hT[e * C_pad + c] = tile[tx][r];
     }
 }
 
@@ -224,7 +209,7 @@ static pt_status alloc_view(pt_view &v, int64_t E, int64_t C)
     v.owned = true;
     if (cudaMalloc(&v.l32, sizeof(float) * v.C * v.E_pad) != cudaSuccess ||
         cudaMalloc(&v.l64, sizeof(double) * v.C * v.E_pad) != cudaSuccess ||
-        cudaMalloc(&v.qT, sizeof(uint32_t) * v.E_pad * v.C_pad) != cudaSuccess) {
+        cudaMalloc(&v.hT, sizeof(uint16_t) * v.E_pad * v.C_pad) != cudaSuccess) {
         cudaGetLastError();
         pt_view_free(v);
         return pt_fail(PT_ENOMEM, "device allocation for a %lld x %lld view failed",
@@ -233,27 +218,13 @@ static pt_status alloc_view(pt_view &v, int64_t E, int64_t C)
     return PT_OK;
 }
 
-// fixed-point tier of a view: shift = largest k with E_pad * floor(lmax * 2^k) < 2^32
+// fp16 tier of a view (env-major copy of l64 rounded to nearest fp16)
 static pt_status quantize_view(pt_ctx *ctx, pt_view &v)
 {
-    double *cmax = nullptr;
-    PT_CK(cudaMallocAsync((void **)&cmax, sizeof(double) * v.C, ctx->stream));
-    k_colmax<<<(unsigned)v.C, 128, 0, ctx->stream>>>(v.l64, v.E, v.E_pad, cmax);
-    std::vector<double> h(v.C);
-    PT_CK(cudaMemcpyAsync(h.data(), cmax, sizeof(double) * v.C, cudaMemcpyDeviceToHost, ctx->stream));
-    PT_CK(cudaFreeAsync(cmax, ctx->stream));
-    PT_CK(cudaStreamSynchronize(ctx->stream));
-    double lmax = 0.0;
-    for (double x : h) lmax = std::max(lmax, x);
-    const double qlim = 4294967295.0 / (double)v.E_pad;
-    int shift = 30;
-    while (shift > -30 && std::floor(lmax * std::ldexp(1.0, shift)) >= qlim) shift--;
-    v.qshift = shift;
-    PT_CK(cudaMemsetAsync(v.qT, 0, sizeof(uint32_t) * v.E_pad * v.C_pad, ctx->stream));
+    PT_CK(cudaMemsetAsync(v.hT, 0, sizeof(uint16_t) * v.E_pad * v.C_pad, ctx->stream));
     dim3 grid((unsigned)((v.C + 31) / 32), (unsigned)((v.E_pad + 31) / 32));
-    k_quant<<<grid, dim3(32, 8), 0, ctx->stream>>>(v.l64, v.E, v.C, v.E_pad, v.C_pad,
-                                                    std::ldexp(1.0, shift), v.qT);
-    ctx->stats.launches += 2;
+    k_half<<<grid, dim3(32, 8), 0, ctx->stream>>>(v.l64, v.E, v.C, v.E_pad, v.C_pad, v.hT);
+    ctx->stats.launches += 1;
     PT_CK(cudaGetLastError());
     return PT_OK;
 }

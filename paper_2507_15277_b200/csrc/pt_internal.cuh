@@ -34,19 +34,17 @@ pt_status pt_fail(pt_status st, const char *fmt, ...);
 // a scope = the environments in play, compacted to a dense matrix.
 //   l32  [C][E_pad]  fp32 log-slowdowns, config-major (env fastest)
 //   l64  [C][E_pad]  fp64 log-slowdowns, config-major
-//   qT   [E_pad][C_pad] uint32, env-major (config fastest): the fixed-point
-//        lower bound q = floor(l64 * 2^qshift) (exact: l*2^k and floor are exact
-//        in fp64), source of the exhaustive kernel's integer (min,+) tier.
-//        qshift is chosen so that E_pad * max q < 2^32 (no sum can overflow).
-// Padded environments hold 0 (adds nothing to any sum); padded configs of qT
+//   hT   [E_pad][C_pad] fp16 (raw bits), env-major (config fastest): l64
+//        rounded to nearest fp16 -- the operand of the exhaustive kernel's
+//        packed-fp16 filter tier (error window in DESIGN.md "Numerics").
+// Padded environments hold 0 (adds nothing to any sum); padded configs of hT
 // hold 0 and are never selectable (index-masked).
 // ---------------------------------------------------------------------------
 struct pt_view {
     int64_t E = 0, E_pad = 0, C = 0, C_pad = 0;
     float *l32 = nullptr;
     double *l64 = nullptr;
-    uint32_t *qT = nullptr;
-    int qshift = 0;
+    uint16_t *hT = nullptr;
     bool owned = false;
 };
 
