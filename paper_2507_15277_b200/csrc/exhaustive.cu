@@ -26,6 +26,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "pt_internal.cuh"
@@ -34,7 +37,7 @@
 #define XT_C 64     // columns per CTA tile
 #define XT_K 32     // environments per pipeline stage
 #define XT_S 4      // pipeline stages
-#define XT_EMAX 384 // widest scope the resident-A kernel takes (smem)
+#define XT_EMAX 768 // widest scope the resident-A kernel takes (smem)
 #define XT_UMAX 1024 // column tiles per task (a whole row tile: A staged once)
 #define KEY_BITS 21
 
@@ -44,33 +47,28 @@
 struct pt_tasks {
     int m = 0;
     int64_t C = 0;
-    const void *tag = nullptr;       // view identity (l32T pointer)
     std::vector<int4> h;              // (row tile, u0, u1, 0)
     std::vector<int64_t> slot_pre;    // prefix sums of slots per task
     std::vector<int64_t> set_pre;     // prefix sums of useful sets per task
-    int4 *d = nullptr;
+    int4 *d = nullptr;                // device copy (lives for the process)
 };
 
-void pt_tasks_free(pt_tasks *t)
-{
-    if (!t) return;
-    cudaFree(t->d);
-    delete t;
-}
-
-// colex rank range of m-subsets whose largest element is j: [C(j,m), C(j+1,m))
+// The work list depends only on (device, C, m, #SMs): built once per process
+// and shared by every context (a fresh pt_load_perf does not rebuild it).
 static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **out)
 {
-    if (ctx->tasks && ctx->tasks->m == m && ctx->tasks->C == v->C && ctx->tasks->tag == v->hT) {
-        *out = ctx->tasks;
+    static std::mutex mu;
+    static std::map<std::tuple<int, int64_t, int, int>, pt_tasks *> cache;
+    std::lock_guard<std::mutex> g(mu);
+    const auto key = std::make_tuple(ctx->dev, v->C, m, ctx->num_sms);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
         return PT_OK;
     }
-    pt_tasks_free(ctx->tasks);
-    ctx->tasks = nullptr;
     pt_tasks *T = new pt_tasks();
     T->m = m;
     T->C = v->C;
-    T->tag = v->hT;
     const int64_t C = v->C;
     const int64_t n_rows = pt_binom(C, m);
     const int64_t n_rt = (n_rows + XT_R - 1) / XT_R;
@@ -115,12 +113,12 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **ou
     if (!T->h.empty()) {
         if (cudaMalloc(&T->d, sizeof(int4) * T->h.size()) != cudaSuccess) {
             cudaGetLastError();
-            pt_tasks_free(T);
+            delete T;
             return pt_fail(PT_ENOMEM, "task list allocation failed");
         }
         cudaMemcpy(T->d, T->h.data(), sizeof(int4) * T->h.size(), cudaMemcpyHostToDevice);
     }
-    ctx->tasks = T;
+    cache[key] = T;
     *out = T;
     return PT_OK;
 }
@@ -242,11 +240,26 @@ struct XParams {
 #define XT_CONS 256
 #define XT_BROW (XT_C * 2)     // bytes of one env row of a column tile
 
-__global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
+// broadcast one fp16 lane of a word to both halves (ptxas folds this into the
+// .H0_H0 / .H1_H1 operand selector of the HMNMX2 that consumes it)
+__device__ __forceinline__ uint32_t bcast_lo(uint32_t w)
+{
+    uint32_t r;
+    asm("{ .reg .b16 l, h; mov.b32 {l, h}, %1; mov.b32 %0, {l, l}; }" : "=r"(r) : "r"(w));
+    return r;
+}
+__device__ __forceinline__ uint32_t bcast_hi(uint32_t w)
+{
+    uint32_t r;
+    asm("{ .reg .b16 l, h; mov.b32 {l, h}, %1; mov.b32 %0, {h, h}; }" : "=r"(r) : "r"(w));
+    return r;
+}
+
+__global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2
-    uint32_t *As = Bs + XT_S * XT_K * (XT_C / 2);                              // [E_pad][128] (a,a)
+    uint16_t *As = reinterpret_cast<uint16_t *>(Bs + XT_S * XT_K * (XT_C / 2)); // [E_pad][128] fp16
     int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);                // [128]
     uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);              // [S]
     uint64_t *empty = full + XT_S;                                             // [S]
@@ -285,21 +298,25 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
 
         if (warp == XT_CONS / 32) {
             // ---------------- producer warp ----------------
-            for (int g = 0; g < nsteps; g++) {
-                const uint32_t G = steps + g;
+            int q = 0;
+            int64_t col = lo + (int64_t)tk.y * XT_C;
+            uint32_t G = steps;
+            for (int g = 0; g < nsteps; g++, G++) {
                 const int slot = G % XT_S;
                 mbar_wait(&empty[slot], ((G / XT_S) & 1u) ^ 1u);
-                const int u = tk.y + g / nkc, q = g % nkc;
                 if (lane == 0) mbar_expect_tx(&full[slot], XT_K * XT_BROW);
                 __syncwarp();
                 bulk_g2s(Bs + slot * XT_K * (XT_C / 2) + lane * (XT_C / 2),
-                         p.hT + (int64_t)(q * XT_K + lane) * p.C_pad + lo + (int64_t)u * XT_C,
-                         XT_BROW, &full[slot]);
+                         p.hT + (int64_t)(q * XT_K + lane) * p.C_pad + col, XT_BROW, &full[slot]);
+                if (++q == nkc) {
+                    q = 0;
+                    col += XT_C;
+                }
             }
         } else {
             // ---------------- consumers ----------------
-            // stage A for the whole task: A[e][r] = min over the row's members,
-            // replicated into both halves of a half2
+            // stage A for the whole task: A[e][r] = min over the row's members
+            // (fp16, non-negative: integer order).  Loads are batched 8 deep.
             {
                 const int r = tid & (XT_R - 1);
                 const int64_t R = R0 + r;
@@ -308,12 +325,20 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
                 if (valid) pt_unrank_colex(R, p.m, p.C, mem);
                 else for (int u = 0; u < p.m; u++) mem[u] = 0;
                 if (tid < XT_R) last_s[r] = valid ? mem[p.m - 1] : 0x7fffffff;
-#pragma unroll 4
-                for (int64_t e = tid >> 7; e < p.E_pad; e += 2) {
-                    const uint16_t *rowp = p.hT + e * p.C_pad;
-                    uint32_t a = rowp[mem[0]];     // non-negative fp16: integer order
-                    for (int u = 1; u < p.m; u++) a = min(a, (uint32_t)rowp[mem[u]]);
-                    As[e * XT_R + r] = valid ? (a | (a << 16)) : 0u;
+                const int64_t e0 = tid >> 7;
+                for (int64_t eb = e0; eb < p.E_pad; eb += 16) {
+                    uint16_t v[8];
+#pragma unroll
+                    for (int t = 0; t < 8; t++) v[t] = p.hT[(eb + 2 * t) * p.C_pad + mem[0]];
+                    for (int u = 1; u < p.m; u++) {
+                        uint16_t w[8];
+#pragma unroll
+                        for (int t = 0; t < 8; t++) w[t] = p.hT[(eb + 2 * t) * p.C_pad + mem[u]];
+#pragma unroll
+                        for (int t = 0; t < 8; t++) v[t] = v[t] < w[t] ? v[t] : w[t];
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; t++) As[(eb + 2 * t) * XT_R + r] = valid ? v[t] : (uint16_t)0;
                 }
             }
             named_sync(1, XT_CONS);
@@ -324,23 +349,26 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
 #pragma unroll
                 for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
 
-            for (int g = 0; g < nsteps; g++) {
-                const uint32_t G = steps + g;
+            int q = 0;
+            int64_t l0 = lo + (int64_t)tk.y * XT_C + tx * 4;
+            uint32_t G = steps;
+            for (int g = 0; g < nsteps; g++, G++) {
                 const int slot = G % XT_S;
                 mbar_wait(&full[slot], (G / XT_S) & 1u);
-                const int q = g % nkc;
                 const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + tx * 2;
-                const uint32_t *A = As + (int64_t)q * XT_K * XT_R + ty * 4;
+                const uint16_t *A = As + (int64_t)q * XT_K * XT_R + ty * 4;
 #pragma unroll 4
                 for (int e = 0; e < XT_K; e += 2) {
-                    const uint4 a0 = *reinterpret_cast<const uint4 *>(A + e * XT_R);
-                    const uint4 a1 = *reinterpret_cast<const uint4 *>(A + e * XT_R + 64);
-                    const uint4 c0 = *reinterpret_cast<const uint4 *>(A + (e + 1) * XT_R);
-                    const uint4 c1 = *reinterpret_cast<const uint4 *>(A + (e + 1) * XT_R + 64);
+                    const uint2 a0 = *reinterpret_cast<const uint2 *>(A + e * XT_R);
+                    const uint2 a1 = *reinterpret_cast<const uint2 *>(A + e * XT_R + 64);
+                    const uint2 c0 = *reinterpret_cast<const uint2 *>(A + (e + 1) * XT_R);
+                    const uint2 c1 = *reinterpret_cast<const uint2 *>(A + (e + 1) * XT_R + 64);
                     const uint2 b = *reinterpret_cast<const uint2 *>(B + e * (XT_C / 2));
                     const uint2 d = *reinterpret_cast<const uint2 *>(B + (e + 1) * (XT_C / 2));
-                    const uint32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                    const uint32_t cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+                    const uint32_t av[8] = {bcast_lo(a0.x), bcast_hi(a0.x), bcast_lo(a0.y), bcast_hi(a0.y),
+                                            bcast_lo(a1.x), bcast_hi(a1.x), bcast_lo(a1.y), bcast_hi(a1.y)};
+                    const uint32_t cv[8] = {bcast_lo(c0.x), bcast_hi(c0.x), bcast_lo(c0.y), bcast_hi(c0.y),
+                                            bcast_lo(c1.x), bcast_hi(c1.x), bcast_lo(c1.y), bcast_hi(c1.y)};
 #pragma unroll
                     for (int i = 0; i < 8; i++) {
                         fhadd2(acc[i][0], acc[i][1], hadd2(hmin2(av[i], b.x), hmin2(cv[i], d.x)));
@@ -349,10 +377,9 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
-                if (q == nkc - 1) {
+                if (++q == nkc) {
+                    q = 0;
                     // epilogue of one column tile: mask, window test, candidate append
-                    const int u = tk.y + g / nkc;
-                    const int64_t l0 = lo + (int64_t)u * XT_C + tx * 4;
                     const float Uv = __uint_as_float(*(volatile unsigned *)p.U);
                     const float tau = fminf(p.tau_seed, fmaf(Uv, p.kappa, p.beta));
 #pragma unroll
@@ -382,6 +409,7 @@ __global__ void __launch_bounds__(XT_THREADS, 1) k_exh_tiled(const XParams p)
                             }
                         }
                     }
+                    l0 += XT_C;
                     float wb = b2;
                     for (int o = 16; o; o >>= 1) wb = fminf(wb, __shfl_xor_sync(0xffffffffu, wb, o));
                     if (lane == 0 && wb < published) {
@@ -617,7 +645,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const float kappa = f_up(kap);
     const float beta = f_up(eta_abs * (kap + 1.0) * (1.0 + 1e-6));
 
-    const size_t smem = sizeof(uint32_t) * (XT_S * XT_K * (XT_C / 2) + v->E_pad * XT_R) +
+    const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
                         sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
     PT_CK(cudaFuncSetAttribute(k_exh_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
@@ -663,7 +691,9 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.cand_n = cn;
         p.cap = cap;
         p.hT = v->hT;
-        const int grid = std::min(ctx->num_sms, tb - ta);
+        int occ = 1;
+        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_tiled, XT_THREADS, smem));
+        const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
         PT_CK(cudaEventRecord(ctx->ev0, s));
         k_exh_tiled<<<grid, XT_THREADS, smem, s>>>(p);
         PT_CK(cudaEventRecord(ctx->ev1, s));

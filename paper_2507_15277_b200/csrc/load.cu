@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <vector>
 
@@ -47,29 +48,60 @@ bool pt_is_device_ptr(const void *p)
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Device memory comes from the device's default stream-ordered pool with the
+// release threshold lifted, so repeated loads / scopes / scratch reuse memory
+// without cudaMalloc/cudaFree (and their implicit device synchronisation).
+static void keep_pool(int dev)
+{
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> g(mu);
+    if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done.push_back(dev);
+}
+
+pt_status pt_dalloc(pt_ctx *ctx, void **p, size_t bytes)
+{
+    *p = nullptr;
+    if (cudaMallocAsync(p, std::max<size_t>(bytes, 16), ctx->stream) != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return pt_fail(PT_ENOMEM, "device allocation of %zu bytes failed", bytes);
+    }
+    return PT_OK;
+}
+
+void pt_dfree(pt_ctx *ctx, void *p)
+{
+    if (p) cudaFreeAsync(p, ctx->stream);
+}
+
 pt_status pt_scratch(pt_ctx *ctx, size_t bytes, void **p)
 {
     if (bytes > ctx->scratch_bytes) {
-        if (ctx->scratch) cudaFree(ctx->scratch);
+        pt_dfree(ctx, ctx->scratch);
         ctx->scratch = nullptr;
         ctx->scratch_bytes = 0;
         size_t nb = std::max(bytes, (size_t)1 << 20);
-        if (cudaMalloc(&ctx->scratch, nb) != cudaSuccess) {
-            cudaGetLastError();
-            return pt_fail(PT_ENOMEM, "scratch allocation of %zu bytes failed", nb);
-        }
+        PT_TRY(pt_dalloc(ctx, &ctx->scratch, nb));
         ctx->scratch_bytes = nb;
     }
     *p = ctx->scratch;
     return PT_OK;
 }
 
-void pt_view_free(pt_view &v)
+void pt_view_free(pt_ctx *ctx, pt_view &v)
 {
     if (v.owned) {
-        cudaFree(v.l32);
-        cudaFree(v.l64);
-        cudaFree(v.hT);
+        pt_dfree(ctx, v.l32);
+        pt_dfree(ctx, v.l64);
+        pt_dfree(ctx, v.hT);
     }
     v = pt_view();
 }
@@ -200,18 +232,17 @@ __global__ void k_half(const double *__restrict__ l64, int64_t E, int64_t C, int
 }
 
 // ---------------------------------------------------------------------------
-static pt_status alloc_view(pt_view &v, int64_t E, int64_t C)
+static pt_status alloc_view(pt_ctx *ctx, pt_view &v, int64_t E, int64_t C)
 {
     v.E = E;
     v.C = C;
     v.E_pad = pt_round_up(std::max<int64_t>(E, 1), 32);
     v.C_pad = pt_round_up(C + 64, 64);   // >= C + 64: a 64-column bulk row copy never leaves the row
     v.owned = true;
-    if (cudaMalloc(&v.l32, sizeof(float) * v.C * v.E_pad) != cudaSuccess ||
-        cudaMalloc(&v.l64, sizeof(double) * v.C * v.E_pad) != cudaSuccess ||
-        cudaMalloc(&v.hT, sizeof(uint16_t) * v.E_pad * v.C_pad) != cudaSuccess) {
-        cudaGetLastError();
-        pt_view_free(v);
+    if (pt_dalloc(ctx, (void **)&v.l32, sizeof(float) * v.C * v.E_pad) != PT_OK ||
+        pt_dalloc(ctx, (void **)&v.l64, sizeof(double) * v.C * v.E_pad) != PT_OK ||
+        pt_dalloc(ctx, (void **)&v.hT, sizeof(uint16_t) * v.E_pad * v.C_pad) != PT_OK) {
+        pt_view_free(ctx, v);
         return pt_fail(PT_ENOMEM, "device allocation for a %lld x %lld view failed",
                        (long long)E, (long long)C);
     }
@@ -241,31 +272,45 @@ pt_status pt_get_view(pt_ctx *ctx, const uint8_t *env_mask, const pt_view **out)
         *out = &ctx->full;
         return PT_OK;
     }
-    if (ctx->scope.E > 0 && ctx->scope_mask.size() == (size_t)ctx->E &&
-        memcmp(ctx->scope_mask.data(), env_mask, (size_t)ctx->E) == 0) {
-        *out = &ctx->scope;
-        return PT_OK;
-    }
+    ctx->tick++;
+    for (auto &sc : ctx->scopes)
+        if (sc.mask.size() == (size_t)ctx->E && memcmp(sc.mask.data(), env_mask, (size_t)ctx->E) == 0) {
+            sc.last_use = ctx->tick;
+            *out = &sc.view;
+            return PT_OK;
+        }
     std::vector<int32_t> idx;
     for (int64_t e = 0; e < ctx->E; e++)
         if (env_mask[e]) idx.push_back((int32_t)e);
     if (idx.empty()) return pt_fail(PT_EEMPTY, "env_mask selects no environment");
-    pt_view_free(ctx->scope);
-    ctx->scope_mask.clear();
-    PT_TRY(alloc_view(ctx->scope, (int64_t)idx.size(), ctx->C));
+    // reuse the least recently used slot once the cache is full
+    const size_t kMaxScopes = 8;
+    pt_scope *slot = nullptr;
+    if (ctx->scopes.size() < kMaxScopes) {
+        ctx->scopes.emplace_back();
+        slot = &ctx->scopes.back();
+    } else {
+        slot = &ctx->scopes[0];
+        for (auto &sc : ctx->scopes)
+            if (sc.last_use < slot->last_use) slot = &sc;
+        pt_view_free(ctx, slot->view);
+        slot->mask.clear();
+    }
+    pt_view &s = slot->view;
+    PT_TRY(alloc_view(ctx, s, (int64_t)idx.size(), ctx->C));
     int32_t *d_idx = nullptr;
-    PT_CK(cudaMallocAsync((void **)&d_idx, sizeof(int32_t) * idx.size(), ctx->stream));
+    PT_TRY(pt_dalloc(ctx, (void **)&d_idx, sizeof(int32_t) * idx.size()));
     PT_CK(cudaMemcpyAsync(d_idx, idx.data(), sizeof(int32_t) * idx.size(),
                           cudaMemcpyHostToDevice, ctx->stream));
-    pt_view &s = ctx->scope;
     k_gather_cfg_major<<<(unsigned)s.C, 128, 0, ctx->stream>>>(
         ctx->full.l32, ctx->full.l64, ctx->full.E_pad, d_idx, s.E, s.E_pad, s.C, s.l32, s.l64);
     ctx->stats.launches += 1;
     PT_CK(cudaGetLastError());
-    PT_CK(cudaFreeAsync(d_idx, ctx->stream));
+    pt_dfree(ctx, d_idx);
     PT_TRY(quantize_view(ctx, s));
-    ctx->scope_mask.assign(env_mask, env_mask + ctx->E);
-    *out = &ctx->scope;
+    slot->mask.assign(env_mask, env_mask + ctx->E);
+    slot->last_use = ctx->tick;
+    *out = &s;
     return PT_OK;
 }
 
@@ -302,24 +347,24 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
         return bail(pt_fail(PT_ECUDA, "cudaEventCreate failed"));
 
     const int64_t E = n_env, C = n_cfg;
+    keep_pool(cuda_device);
     float *dT = nullptr;
     double *rowmax = nullptr;
     int *status = nullptr;
-    if (cudaMalloc(&dT, sizeof(float) * E * C) != cudaSuccess ||
-        cudaMalloc(&ctx->best, sizeof(double) * E) != cudaSuccess ||
-        cudaMalloc(&rowmax, sizeof(double) * E) != cudaSuccess ||
-        cudaMalloc(&status, sizeof(int) * E) != cudaSuccess) {
-        cudaGetLastError();
-        cudaFree(dT);
-        cudaFree(rowmax);
-        cudaFree(status);
+    if (pt_dalloc(ctx, (void **)&dT, sizeof(float) * E * C) != PT_OK ||
+        pt_dalloc(ctx, (void **)&ctx->best, sizeof(double) * E) != PT_OK ||
+        pt_dalloc(ctx, (void **)&rowmax, sizeof(double) * E) != PT_OK ||
+        pt_dalloc(ctx, (void **)&status, sizeof(int) * E) != PT_OK) {
+        pt_dfree(ctx, dT);
+        pt_dfree(ctx, rowmax);
+        pt_dfree(ctx, status);
         return bail(pt_fail(PT_ENOMEM, "device allocation for %lld x %lld failed",
                             (long long)E, (long long)C));
     }
     auto cleanup = [&]() {
-        cudaFree(dT);
-        cudaFree(rowmax);
-        cudaFree(status);
+        pt_dfree(ctx, dT);
+        pt_dfree(ctx, rowmax);
+        pt_dfree(ctx, status);
     };
     const cudaMemcpyKind kind =
         pt_is_device_ptr(times_ms) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -354,7 +399,7 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
         pen = std::max(pen, h_rowmax[e]);
     }
     ctx->penalty = pen;
-    pt_status st = alloc_view(ctx->full, E, C);
+    pt_status st = alloc_view(ctx, ctx->full, E, C);
     if (st != PT_OK) {
         cleanup();
         return bail(st);
@@ -368,8 +413,8 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
         cleanup();
         return bail(st);
     }
-    cudaError_t ce = cudaStreamSynchronize(ctx->stream);
     cleanup();
+    cudaError_t ce = cudaStreamSynchronize(ctx->stream);
     if (ce != cudaSuccess || cudaGetLastError() != cudaSuccess)
         return bail(pt_fail(PT_ECUDA, "normalise kernel failed: %s", cudaGetErrorString(ce)));
     *out = ctx;
@@ -388,11 +433,11 @@ extern "C" void pt_free(pt_ctx *ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->dev);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    pt_view_free(ctx->full);
-    pt_view_free(ctx->scope);
-    cudaFree(ctx->best);
-    cudaFree(ctx->scratch);
-    pt_tasks_free(ctx->tasks);
+    pt_view_free(ctx, ctx->full);
+    for (auto &sc : ctx->scopes) pt_view_free(ctx, sc.view);
+    pt_dfree(ctx, ctx->best);
+    pt_dfree(ctx, ctx->scratch);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     delete ctx;

@@ -50,6 +50,12 @@ struct pt_view {
 
 struct pt_tasks;  // exhaustive work list (exhaustive.cu)
 
+struct pt_scope {   // one cached compacted scope
+    std::vector<uint8_t> mask;
+    pt_view view;
+    uint64_t last_use = 0;
+};
+
 struct pt_ctx {
     int dev = 0;
     cudaStream_t stream = nullptr;
@@ -61,22 +67,24 @@ struct pt_ctx {
     double penalty = 1.0;
     double *best = nullptr;   // [E] fp64, each env's Oracle
     pt_view full;
-    // scope cache (one compacted scope kept alive)
-    std::vector<uint8_t> scope_mask;
-    pt_view scope;
+    // scope cache (LRU of compacted scopes)
+    std::vector<pt_scope> scopes;
+    uint64_t tick = 0;
     // scratch reused across calls
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
-    pt_tasks *tasks = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     pt_stats stats{};
 };
 
+// stream-ordered device allocation from the device's (cached) memory pool
+pt_status pt_dalloc(pt_ctx *ctx, void **p, size_t bytes);
+void pt_dfree(pt_ctx *ctx, void *p);
 // scratch allocation (grows, never shrinks); returns PT_OK or PT_ENOMEM
 pt_status pt_scratch(pt_ctx *ctx, size_t bytes, void **p);
 // resolve a mask into a view (NULL -> full); E_scope returned in view->E
 pt_status pt_get_view(pt_ctx *ctx, const uint8_t *env_mask, const pt_view **out);
-void pt_view_free(pt_view &v);
+void pt_view_free(pt_ctx *ctx, pt_view &v);
 // true if p is device (or managed) memory
 bool pt_is_device_ptr(const void *p);
 
@@ -89,7 +97,6 @@ pt_status pt_exhaustive_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t s
 pt_status pt_score_view(pt_ctx *ctx, const pt_view *v, const int32_t *d_sets, int64_t n_sets,
                         int32_t k, double *d_s);
 
-void pt_tasks_free(pt_tasks *t);
 
 // ---------------------------------------------------------------------------
 // device helpers
