@@ -19,7 +19,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -56,25 +55,30 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled (NVML, in-process) during the timed region."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, gpu):
-        self.gpu, self.rows, self.stop = gpu, [], threading.Event()
+    def __init__(self, gpu, period=0.05):
+        self.gpu, self.period, self.rows, self.stop = gpu, period, [], threading.Event()
+        self.max_mhz = None
 
     def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return
         while not self.stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((sm, rs))
             except Exception:
                 pass
-            self.stop.wait(0.2)
+            self.stop.wait(self.period)
 
     def __enter__(self):
         self.t = threading.Thread(target=self._run, daemon=True)
@@ -87,14 +91,10 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 2 + i and "Active" in r[2 + i] and "Not" not in r[2 + i]})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        reasons = sorted({n for _, rs in self.rows for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML"}
 
 
 # --------------------------------------------------------------------------- oracle
@@ -195,6 +195,8 @@ def main():
     dT = torch.from_numpy(T).cuda()
     hT = torch.from_numpy(T).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    flush.fill_(0)                     # load the fill kernel's module before any timing
+    torch.cuda.synchronize()
     folds = [d for d in range(5) if d % world == rank]
 
     def step(src):
@@ -224,15 +226,19 @@ def main():
         torch.cuda.synchronize()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         with ClockSampler(local) as clk:
             ev0.record(stream)
-            for _ in range(steps):
+            for i in range(steps):
                 flush.fill_(1)                     # L2 flushed between steps
+                marks[i].record(stream)
                 res, d2h = step(src)
                 k3_ms.append(res["k3_ms"])
                 launches += res["launches"] + 1
+            marks[steps].record(stream)
             ev1.record(stream)
             torch.cuda.synchronize()
+        step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(steps)]
         if world > 1:
             dist.barrier()
         ms = ev0.elapsed_time(ev1)
@@ -240,10 +246,10 @@ def main():
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        return ms, k3_ms, launches, res, d2h, clk.summary()
+        return ms, k3_ms, launches, res, d2h, dict(clk.summary(), step_ms=[round(x, 3) for x in step_ms])
 
     ms, k3_ms, launches, res, d2h, clocks = timed(dT, args.steps, args.warmup)
-    ms_e2e, _, _, _, d2h_e2e, _ = timed(hT, args.steps, 1)
+    ms_e2e, _, _, _, d2h_e2e, clocks_e2e = timed(hT, args.steps, 1)
 
     if rank != 0:
         if world > 1:
@@ -253,12 +259,17 @@ def main():
     pk = peaks()
     sm_max = pk.get("sm_max_mhz", 1965.0)
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    # roofline of the dominant kernel (k_exh_tiled, k=3): one FP32-class min + one add
-    # per (set, env) at 128 lanes/clk/SM (issue bound of 1 warp-instr/clk/SMSP)
-    ops = 2.0 * E_PAPER * res["k3_sets"]
+    # roofline of the dominant kernel (k_exh_tiled, k=3).  Algorithmic work: one
+    # min + one add per (set, env), E = 320 envs per set.  Peak = the ALU-pipe
+    # ceiling for the mins (the only pipe with a min): 16 lanes/clk/SMSP x 4 SMSP
+    # x 2 mins per packed f16x2 HMNMX2 = 128 (set,env)/clk/SM (DESIGN.md
+    # "Roofline").  The FP32 roofline of the north star (one FMNMX at 16
+    # lanes/clk/SMSP + one FADD per (set, env)) is 64 (set,env)/clk/SM.
+    evals = float(E_PAPER) * res["k3_sets"]
     k3_avg = float(np.mean(k3_ms))
-    achieved = ops / (k3_avg * 1e-3) / 1e12
+    achieved = evals / (k3_avg * 1e-3) / 1e12
     peak = nsm * 128 * sm_max * 1e6 / 1e12
+    peak_fp32 = nsm * 64 * sm_max * 1e6 / 1e12
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "k3_dram_bytes.json")))["bytes_per_launch"]
@@ -295,13 +306,16 @@ def main():
                 "h2d_bytes_per_step": int(T.nbytes), "d2h_bytes_per_step": int(d2h_e2e)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "alu", "kernel": "k_exh_tiled (k=3)", "achieved": achieved,
-                     "peak": peak, "unit": "Top/s", "frac": achieved / peak, "traffic": traffic,
-                     "ops_per_set": 2 * E_PAPER,
-                     "peak_basis": f"{nsm} SMs x 128 lanes/clk x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz): "
-                                   "one min + one add per (set, env)",
+                     "peak": peak, "unit": "T(set,env)/s", "frac": achieved / peak, "traffic": traffic,
+                     "work_per_set": f"{E_PAPER} (set,env) evaluations = {E_PAPER} min + {E_PAPER} add",
+                     "peak_basis": f"ALU-pipe min ceiling: {nsm} SMs x 4 SMSP x 16 lanes/clk x 2 mins "
+                                   f"(f16x2 HMNMX2) x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                     "fp32_roofline": {"peak": peak_fp32, "frac": achieved / peak_fp32,
+                                       "basis": "one FMNMX (16 lanes/clk/SMSP) + one FADD per (set, env)"},
                      "kernel_ms": k3_avg, "kernel_share_of_step": k3_avg / (ms / args.steps)},
         "cpu_baseline": cpu,
         "clocks": clocks,
+        "clocks_e2e": clocks_e2e,
         "parity": {"k3_best": list(res["r3"]["best"]), "k3_matches_oracle_golden": gold,
                    "k3_candidates_refined": res["k3_cand"]},
     }

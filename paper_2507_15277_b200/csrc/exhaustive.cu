@@ -357,22 +357,32 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 mbar_wait(&full[slot], (G / XT_S) & 1u);
                 const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + tx * 2;
                 const uint16_t *A = As + (int64_t)q * XT_K * XT_R + ty * 4;
-#pragma unroll 4
-                for (int e = 0; e < XT_K; e += 2) {
-                    const uint2 a0 = *reinterpret_cast<const uint2 *>(A + e * XT_R);
-                    const uint2 a1 = *reinterpret_cast<const uint2 *>(A + e * XT_R + 64);
-                    const uint2 c0 = *reinterpret_cast<const uint2 *>(A + (e + 1) * XT_R);
-                    const uint2 c1 = *reinterpret_cast<const uint2 *>(A + (e + 1) * XT_R + 64);
-                    const uint2 b = *reinterpret_cast<const uint2 *>(B + e * (XT_C / 2));
-                    const uint2 d = *reinterpret_cast<const uint2 *>(B + (e + 1) * (XT_C / 2));
-                    const uint32_t av[8] = {bcast_lo(a0.x), bcast_hi(a0.x), bcast_lo(a0.y), bcast_hi(a0.y),
-                                            bcast_lo(a1.x), bcast_hi(a1.x), bcast_lo(a1.y), bcast_hi(a1.y)};
-                    const uint32_t cv[8] = {bcast_lo(c0.x), bcast_hi(c0.x), bcast_lo(c0.y), bcast_hi(c0.y),
-                                            bcast_lo(c1.x), bcast_hi(c1.x), bcast_lo(c1.y), bcast_hi(c1.y)};
+#pragma unroll 2
+                for (int e = 0; e < XT_K; e += 4) {
+                    // 4 envs: A rows (8 fp16 per env as 2 x uint2), B column pairs (half2)
+                    uint2 ar[4][2], bc[4];
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        ar[t][0] = *reinterpret_cast<const uint2 *>(A + (e + t) * XT_R);
+                        ar[t][1] = *reinterpret_cast<const uint2 *>(A + (e + t) * XT_R + 64);
+                        bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; i++) {
-                        fhadd2(acc[i][0], acc[i][1], hadd2(hmin2(av[i], b.x), hmin2(cv[i], d.x)));
-                        fhadd2(acc[i][2], acc[i][3], hadd2(hmin2(av[i], b.y), hmin2(cv[i], d.y)));
+                        uint32_t av[4];
+#pragma unroll
+                        for (int t = 0; t < 4; t++) {
+                            const uint32_t w = (i & 4) ? (((i & 2) ? ar[t][1].y : ar[t][1].x))
+                                                       : (((i & 2) ? ar[t][0].y : ar[t][0].x));
+                            av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                        }
+                        // fp16 tree over the 4 envs, then 2 FHADD into fp32
+                        fhadd2(acc[i][0], acc[i][1],
+                               hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
+                                     hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))));
+                        fhadd2(acc[i][2], acc[i][3],
+                               hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                     hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))));
                     }
                 }
                 __syncwarp();
@@ -624,11 +634,13 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
 
     // error model of the fp16 tier:
     //   |s_hat - s| <= eta_rel * s + eta_abs
-    //   eta_rel: fp16 rounding of each term (2^-11) + fp16 pair add (2^-11) +
-    //            fp32 accumulation of E_pad/2 pair sums; eta_abs: fp16 subnormals
+    //   eta_rel: fp16 rounding of each term (2^-11) + 2-level fp16 tree (2 x 2^-11)
+    //            + fp32 accumulation of E_pad/4 group sums; eta_abs: fp16 subnormals
     const double u16 = std::ldexp(1.0, -11), u32 = std::ldexp(1.0, -24);
-    const double npair = (double)v->E_pad / 2.0 + 2.0;
-    const double eta_rel = (2.0 * u16 + u16 * u16 + npair * u32 / (1.0 - npair * u32)) * 1.01;
+    // terms rounded to fp16 (u16), a 2-level fp16 tree over 4 envs (2 u16), fp32
+    // accumulation of E_pad/4 group sums
+    const double ngrp = (double)v->E_pad / 4.0 + 2.0;
+    const double eta_rel = (3.0 * u16 + 3.0 * u16 * u16 + ngrp * u32 / (1.0 - ngrp * u32)) * 1.01;
     const double eta_abs = 2.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
     const double kap = (1.0 + eta_rel) / (1.0 - eta_rel) * (1.0 + 1e-6);
     auto f_up = [](double x) -> float {
