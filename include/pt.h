@@ -176,6 +176,7 @@ typedef struct {
     int32_t exh_passes;      /* 1, or 2 after a candidate-buffer overflow */
     int32_t exh_kernel;      /* 0 = tiled fp32 (min,+), 1 = generic fp64 */
     double greedy_ms;        /* CUDA-event time of the last greedy selection */
+    int64_t greedy_candidates; /* streamed greedy: configs re-scored in fp64 (all steps) */
 } pt_stats;
 
 pt_status pt_get_stats(const pt_ctx *ctx, pt_stats *out);

@@ -134,28 +134,40 @@ __global__ void __launch_bounds__(256) k_greedy_resident(const double *__restric
 // ---------------------------------------------------------------------------
 // STREAM: fp32 scan + single-CTA fp64 window refine
 // ---------------------------------------------------------------------------
-// key[c] (minimised): step 0 -> sum_e l32[c][e];  later -> -sum_e max(0, cur-l)
+// key[c] (minimised): step 0 -> sum_e l32[c][e];  later -> -sum_e max(0, cur-l).
+// Each block also writes the two smallest keys it produced (blk2[blockIdx]).
+// Odd steps scan the configurations in reverse so the L2-resident tail of the
+// previous step's stream is read first.
 __global__ void __launch_bounds__(256) k_greedy_scan(const float *__restrict__ l32, int64_t C,
                                                       int64_t E_pad,
                                                       const float *__restrict__ cur32,
                                                       const uint32_t *__restrict__ taken,
-                                                      int gain_mode, float *__restrict__ key)
+                                                      int gain_mode, int reverse,
+                                                      int64_t cached_from,
+                                                      float *__restrict__ key,
+                                                      float2 *__restrict__ blk2)
 {
     extern __shared__ float cur_s[];
+    __shared__ float w1[8], w2[8];
     for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) cur_s[e] = cur32[e];
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nq = E_pad >> 2;
     const float4 *cur4 = reinterpret_cast<const float4 *>(cur_s);
-    for (int64_t c = gw; c < C; c += nw) {
+    float k1 = INFINITY, k2 = INFINITY;
+    for (int64_t cc = gw; cc < C; cc += nw) {
+        const int64_t c = reverse ? C - 1 - cc : cc;
         const float4 *col = reinterpret_cast<const float4 *>(l32 + c * E_pad);
+        // the tail of this step's stream stays in L2 (normal loads) for the next,
+        // reversed, step; the rest streams with evict-first loads
+        const bool keep = cc >= cached_from;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
         if (gain_mode) {
 #pragma unroll 8
             for (int64_t q = lane; q < nq; q += 32) {
-                float4 v = __ldcs(col + q);
+                float4 v = keep ? __ldg(col + q) : __ldcs(col + q);
                 float4 m = cur4[q];
                 a0 += fmaxf(m.x - v.x, 0.f);
                 a1 += fmaxf(m.y - v.y, 0.f);
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(256) k_greedy_scan(const float *__restrict__ l
         } else {
 #pragma unroll 8
             for (int64_t q = lane; q < nq; q += 32) {
-                float4 v = __ldcs(col + q);
+                float4 v = keep ? __ldg(col + q) : __ldcs(col + q);
                 a0 += v.x;
                 a1 += v.y;
                 a2 += v.z;
@@ -174,10 +186,36 @@ __global__ void __launch_bounds__(256) k_greedy_scan(const float *__restrict__ l
         }
         float acc = (a0 + a1) + (a2 + a3);
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-            bool tk = taken[c >> 5] >> (c & 31) & 1u;
-            key[c] = tk ? INFINITY : (gain_mode ? -acc : acc);
+        const bool tk = taken[c >> 5] >> (c & 31) & 1u;
+        const float kv = tk ? INFINITY : (gain_mode ? -acc : acc);
+        if (lane == 0) key[c] = kv;
+        if (kv < k1) {
+            k2 = k1;
+            k1 = kv;
+        } else if (kv < k2) {
+            k2 = kv;
         }
+    }
+    // block: two smallest key values (each warp holds them for distinct configs)
+    if (lane == 0) {
+        w1[warp] = k1;
+        w2[warp] = k2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float b1 = INFINITY, b2 = INFINITY;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            const float xs[2] = {w1[w], w2[w]};
+            for (int u = 0; u < 2; u++) {
+                if (xs[u] < b1) {
+                    b2 = b1;
+                    b1 = xs[u];
+                } else if (xs[u] < b2) {
+                    b2 = xs[u];
+                }
+            }
+        }
+        blk2[blockIdx.x] = make_float2(b1, b2);
     }
 }
 
@@ -187,81 +225,129 @@ struct pick_state {
 
 // one CTA of 1024 threads
 __global__ void __launch_bounds__(1024) k_greedy_pick(
-    const float *__restrict__ key, int64_t C, const double *__restrict__ l64, int64_t E_pad,
+    const float *__restrict__ key, const float2 *__restrict__ blk2, int nblk, int64_t C,
+    const double *__restrict__ l64, int64_t E_pad,
     int64_t E, float *__restrict__ cur32, double *__restrict__ cur64,
     uint32_t *__restrict__ taken, pick_state *__restrict__ st, int t, int gain_mode,
     double gamma, int32_t *__restrict__ cand, int32_t *__restrict__ out_idx,
     double *__restrict__ s1_tr, double *__restrict__ s2_tr, int32_t *__restrict__ ncand_tr)
 {
     __shared__ double rs1[32], rs2[32];
-    __shared__ int rc1[32], rc2[32];
     __shared__ int ncand;
     __shared__ double thr;
     __shared__ int cstar;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // 1. two smallest keys (ties by index)
-    double s1 = INFINITY, s2 = INFINITY;
-    int c1 = PT_BIGI, c2 = PT_BIGI;
-    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) top2_ins(s1, c1, s2, c2, (double)key[c], (int)c);
-    warp_top2(s1, c1, s2, c2);
+    double s1, s2;
+    int c1, c2;
+    // 1. two smallest key values over all configurations (from the per-block pairs)
+    float f1 = INFINITY, f2 = INFINITY;
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+        const float2 r = blk2[b];
+        const float xs[2] = {r.x, r.y};
+        for (int u = 0; u < 2; u++) {
+            if (xs[u] < f1) {
+                f2 = f1;
+                f1 = xs[u];
+            } else if (xs[u] < f2) {
+                f2 = xs[u];
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const float a1 = __shfl_xor_sync(0xffffffffu, f1, o);
+        const float a2 = __shfl_xor_sync(0xffffffffu, f2, o);
+        // merge two sorted pairs (values of distinct configurations)
+        const float n1 = fminf(f1, a1);
+        const float n2 = fminf(fmaxf(f1, a1), fminf(f2, a2));
+        f1 = n1;
+        f2 = n2;
+    }
     if (lane == 0) {
-        rs1[warp] = s1; rs2[warp] = s2; rc1[warp] = c1; rc2[warp] = c2;
+        rs1[warp] = f1;
+        rs2[warp] = f2;
     }
     if (threadIdx.x == 0) ncand = 0;
     __syncthreads();
     if (warp == 0) {
-        s1 = rs1[lane]; s2 = rs2[lane]; c1 = rc1[lane]; c2 = rc2[lane];
-        warp_top2(s1, c1, s2, c2);
+        f1 = rs1[lane];
+        f2 = rs2[lane];
+        for (int o = 16; o; o >>= 1) {
+            const float a1 = __shfl_xor_sync(0xffffffffu, f1, o);
+            const float a2 = __shfl_xor_sync(0xffffffffu, f2, o);
+            const float n1 = fminf(f1, a1);
+            const float n2 = fminf(fmaxf(f1, a1), fminf(f2, a2));
+            f1 = n1;
+            f2 = n2;
+        }
         if (lane == 0) {
+            const double s1k = f1, s2k = f2;
             // window: keep every c that could be one of the
             // two exact best configurations
             const double u = 5.9604644775390625e-08;   // 2^-24
             if (!gain_mode) {
                 // key = s_hat >= 0, |s_hat - s| <= gamma*s
-                thr = (s2 == INFINITY) ? INFINITY : s2 * (1.0 + gamma) / (1.0 - gamma) * (1.0 + 1e-12);
+                thr = (s2k == INFINITY) ? INFINITY : s2k * (1.0 + gamma) / (1.0 - gamma) * (1.0 + 1e-12);
             } else {
                 // key = -g_hat; |g_hat - g| <= delta = 2u*S + gamma*g_max
-                const double gmax = -s1;
+                const double gmax = -s1k;
                 const double delta = (2.0 * u * st->S + gamma * gmax) * 1.01 + 1e-300;
-                thr = (s2 == INFINITY) ? INFINITY : s2 + 2.0 * delta;
+                thr = (s2k == INFINITY) ? INFINITY : s2k + 2.0 * delta;
             }
         }
     }
     __syncthreads();
-    // 2. collect candidates
+    // 2. collect candidates (float4 sweep of the keys)
     const double th = thr;
-    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
-        float kv = key[c];
+    const int64_t C4 = C >> 2;
+    const float4 *key4 = reinterpret_cast<const float4 *>(key);
+    for (int64_t q0 = 0; q0 < C4; q0 += 8 * (int64_t)blockDim.x) {
+        float4 kv[8];   // 8 independent loads in flight per thread
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const int64_t q = q0 + r * (int64_t)blockDim.x + threadIdx.x;
+            kv[r] = q < C4 ? key4[q] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const int64_t q = q0 + r * (int64_t)blockDim.x + threadIdx.x;
+            const float xs[4] = {kv[r].x, kv[r].y, kv[r].z, kv[r].w};
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (xs[u] != INFINITY && (double)xs[u] <= th) cand[atomicAdd(&ncand, 1)] = (int32_t)(4 * q + u);
+        }
+    }
+    for (int64_t c = 4 * C4 + threadIdx.x; c < C; c += blockDim.x) {
+        const float kv = key[c];
         if (kv != INFINITY && (double)kv <= th) cand[atomicAdd(&ncand, 1)] = (int32_t)c;
     }
     __syncthreads();
-    // 3. exact fp64 re-score: warp per candidate, lanes over envs
+    // 3. exact fp64 re-score of each candidate by the whole block (envs strided
+    //    over 1024 threads, fixed-order block reduction: deterministic)
     const int n = ncand;
     s1 = s2 = INFINITY;
     c1 = c2 = PT_BIGI;
-    for (int q = warp; q < n; q += 32) {
+    for (int q = 0; q < n; q++) {
         const int c = cand[q];
         const double *col = l64 + (int64_t)c * E_pad;
-        double acc = 0.0;
-        for (int64_t e = lane; e < E_pad; e += 32) acc += fmin(cur64[e], col[e]);
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        top2_ins(s1, c1, s2, c2, acc, c);
-    }
-    if (lane == 0) {
-        rs1[warp] = s1; rs2[warp] = s2; rc1[warp] = c1; rc2[warp] = c2;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        s1 = rs1[lane]; s2 = rs2[lane]; c1 = rc1[lane]; c2 = rc2[lane];
-        warp_top2(s1, c1, s2, c2);
-        if (lane == 0) {
-            cstar = c1;
-            out_idx[t] = c1;
-            s1_tr[t] = s1;
-            s2_tr[t] = s2;
-            ncand_tr[t] = n;
-            taken[c1 >> 5] |= 1u << (c1 & 31);
+        double part = 0.0;
+        for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) part += fmin(cur64[e], col[e]);
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) rs2[warp] = part;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double acc = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) acc += rs2[w];
+            top2_ins(s1, c1, s2, c2, acc, c);
         }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        cstar = c1;
+        out_idx[t] = c1;
+        s1_tr[t] = s1;
+        s2_tr[t] = s2;
+        ncand_tr[t] = n;
+        taken[c1 >> 5] |= 1u << (c1 & 31);
     }
     __syncthreads();
     // 4. commit: cur <- min(cur, l[c*]); S = sum over real envs (block reduce)
@@ -350,7 +436,8 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
                o_taken = take(sizeof(uint32_t) * nwords), o_c32 = take(sizeof(float) * E_pad),
                o_c64 = take(sizeof(double) * E_pad), o_st = take(sizeof(pick_state)),
                o_idx = take(sizeof(int32_t) * k), o_s1 = take(sizeof(double) * k),
-               o_s2 = take(sizeof(double) * k), o_nc = take(sizeof(int32_t) * k);
+               o_s2 = take(sizeof(double) * k), o_nc = take(sizeof(int32_t) * k),
+               o_blk = take(sizeof(float2) * (size_t)ctx->num_sms * 32);
         void *scr = nullptr;
         PT_TRY(pt_scratch(ctx, off, &scr));
         char *b = (char *)scr;
@@ -362,6 +449,7 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
         pick_state *st = (pick_state *)(b + o_st);
         int32_t *d_idx = (int32_t *)(b + o_idx), *d_nc = (int32_t *)(b + o_nc);
         double *d_s1 = (double *)(b + o_s1), *d_s2 = (double *)(b + o_s2);
+        float2 *blk2 = (float2 *)(b + o_blk);
         PT_CK(cudaMemsetAsync(taken, 0, sizeof(uint32_t) * nwords, s));
         PT_CK(cudaMemsetAsync(st, 0, sizeof(pick_state), s));
         k_fill_f64<<<(unsigned)((E_pad + 255) / 256), 256, 0, s>>>(cur64, E_pad, INFINITY);
@@ -371,16 +459,24 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
         if (smem > 48 * 1024)
             PT_CK(cudaFuncSetAttribute(k_greedy_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
+        // k_greedy_scan's fp32 sum: each lane keeps 4 accumulators over E_pad/128
+        // float4 slots, then (a0+a1)+(a2+a3) and a 5-level xor tree: every term
+        // passes through at most E_pad/128 + 7 roundings (plus 1 for the term
+        // itself in gain mode) -> Higham gamma_n with n = E_pad/128 + 8.
         const double u = 5.9604644775390625e-08;
-        const double n = (double)E_pad + 2.0;
+        const double n = (double)((E_pad + 127) / 128) + 8.0;
         const double gamma = n * u / (1.0 - n * u) * 1.01;
         int occ = 0;
         PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_scan, 256, smem));
         const int64_t want_blocks = (C * 32 + 255) / 256;
         const int grid = (int)std::min<int64_t>(want_blocks, (int64_t)ctx->num_sms * std::max(occ, 1));
+        // keep the last ~80 MB of each step's stream L2-resident (L2 is ~126 MB)
+        const int64_t keep_cfgs = (int64_t)(80.0 * (1 << 20) / (4.0 * (double)E_pad));
+        const int64_t cached_from = std::max<int64_t>(0, C - keep_cfgs);
         for (int t = 0; t < k; t++) {
-            k_greedy_scan<<<grid, 256, smem, s>>>(v->l32, C, E_pad, cur32, taken, t > 0, key);
-            k_greedy_pick<<<1, 1024, 0, s>>>(key, C, v->l64, E_pad, v->E, cur32, cur64, taken, st,
+            k_greedy_scan<<<grid, 256, smem, s>>>(v->l32, C, E_pad, cur32, taken, t > 0, t & 1,
+                                                  cached_from, key, blk2);
+            k_greedy_pick<<<1, 1024, 0, s>>>(key, blk2, grid, C, v->l64, E_pad, v->E, cur32, cur64, taken, st,
                                              t, t > 0, gamma, cand, d_idx, d_s1, d_s2, d_nc);
             ctx->stats.launches += 2;
         }
@@ -388,6 +484,12 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
         PT_CK(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
         PT_CK(cudaMemcpyAsync(s1_trace, d_s1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
         PT_CK(cudaMemcpyAsync(s2_trace, d_s2, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+        std::vector<int32_t> nc(k);
+        PT_CK(cudaMemcpyAsync(nc.data(), d_nc, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+        PT_CK(cudaStreamSynchronize(s));
+        int64_t tot = 0;
+        for (int t = 0; t < k; t++) tot += nc[t];
+        ctx->stats.greedy_candidates = tot;
     }
     PT_CK(cudaEventRecord(ctx->ev1, s));
     PT_CK(cudaStreamSynchronize(s));

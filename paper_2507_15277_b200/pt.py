@@ -31,7 +31,8 @@ class pt_stats(ct.Structure):
     _fields_ = [("launches", ct.c_int64), ("exh_main_ms", ct.c_double), ("exh_sets", ct.c_int64),
                 ("exh_slots", ct.c_int64), ("exh_env_pad", ct.c_int64),
                 ("exh_candidates", ct.c_int64), ("exh_passes", ct.c_int32),
-                ("exh_kernel", ct.c_int32), ("greedy_ms", ct.c_double)]
+                ("exh_kernel", ct.c_int32), ("greedy_ms", ct.c_double),
+                ("greedy_candidates", ct.c_int64)]
 
 
 class PTError(RuntimeError):
