@@ -234,6 +234,8 @@ struct XParams {
     unsigned *cand_n;
     unsigned cap;
     const uint16_t *hT;
+    const uint16_t *hTile;
+    int64_t n_ct;
 };
 
 #define XT_THREADS 288
@@ -298,21 +300,27 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
 
         if (warp == XT_CONS / 32) {
             // ---------------- producer warp ----------------
-            int q = 0;
-            int64_t col = lo + (int64_t)tk.y * XT_C;
-            uint32_t G = steps;
-            for (int g = 0; g < nsteps; g++, G++) {
-                const int slot = G % XT_S;
-                mbar_wait(&empty[slot], ((G / XT_S) & 1u) ^ 1u);
-                if (lane == 0) mbar_expect_tx(&full[slot], XT_K * XT_BROW);
-                __syncwarp();
-                bulk_g2s(Bs + slot * XT_K * (XT_C / 2) + lane * (XT_C / 2),
-                         p.hT + (int64_t)(q * XT_K + lane) * p.C_pad + col, XT_BROW, &full[slot]);
-                if (++q == nkc) {
-                    q = 0;
-                    col += XT_C;
+            // column tile starting at config `col` (8-aligned) = shift s, tile ct
+            // of hTile; each stage is one contiguous 32-env x 64-config block
+            if (lane == 0) {
+                int q = 0;
+                int64_t col = lo + (int64_t)tk.y * XT_C;
+                uint32_t G = steps;
+                for (int g = 0; g < nsteps; g++, G++) {
+                    const int slot = G % XT_S;
+                    const uint32_t par = ((G / XT_S) & 1u) ^ 1u;
+                    while (!mbar_try(&empty[slot], par)) __nanosleep(128);
+                    const int64_t sh = (col >> 3) & 7, ct = (col - 8 * sh) >> 6;
+                    const uint16_t *src = p.hTile + ((sh * p.n_ct + ct) * p.E_pad + (int64_t)q * XT_K) * XT_C;
+                    mbar_expect_tx(&full[slot], XT_K * XT_BROW);
+                    bulk_g2s(Bs + slot * XT_K * (XT_C / 2), src, XT_K * XT_BROW, &full[slot]);
+                    if (++q == nkc) {
+                        q = 0;
+                        col += XT_C;
+                    }
                 }
             }
+            __syncwarp();
         } else {
             // ---------------- consumers ----------------
             // stage A for the whole task: A[e][r] = min over the row's members
@@ -431,6 +439,18 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
         }
         steps += nsteps;
     }
+}
+
+// hTile[s][ct][e][j] = hT[e][64*ct + 8*s + j]  (0 beyond the padded row)
+__global__ void k_tile_hT(const uint16_t *__restrict__ hT, int64_t E_pad, int64_t C_pad, int64_t n_ct,
+                          uint16_t *__restrict__ hTile)
+{
+    const int64_t blk = blockIdx.x;                  // (s, ct, e)
+    const int64_t e = blk % E_pad, sct = blk / E_pad;
+    const int64_t ct = sct % n_ct, sh = sct / n_ct;
+    const int j = threadIdx.x;                       // 64 threads
+    const int64_t c = 64 * ct + 8 * sh + j;
+    hTile[blk * 64 + j] = c < C_pad ? hT[e * C_pad + c] : (uint16_t)0;
 }
 
 // ---------------------------------------------------------------------------
@@ -657,6 +677,15 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const float kappa = f_up(kap);
     const float beta = f_up(eta_abs * (kap + 1.0) * (1.0 + 1e-6));
 
+    if (!v->hTile) {
+        pt_view *mv = const_cast<pt_view *>(v);
+        mv->n_ct = (v->C_pad + XT_C - 1) / XT_C;
+        PT_TRY(pt_dalloc(ctx, (void **)&mv->hTile, sizeof(uint16_t) * 8 * mv->n_ct * v->E_pad * XT_C));
+        k_tile_hT<<<(unsigned)(8 * mv->n_ct * v->E_pad), 64, 0, s>>>(v->hT, v->E_pad, v->C_pad, mv->n_ct,
+                                                                   mv->hTile);
+        ctx->stats.launches++;
+        PT_CK(cudaGetLastError());
+    }
     const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
                         sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
     PT_CK(cudaFuncSetAttribute(k_exh_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -703,6 +732,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.cand_n = cn;
         p.cap = cap;
         p.hT = v->hT;
+        p.hTile = v->hTile;
+        p.n_ct = v->n_ct;
         int occ = 1;
         PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_tiled, XT_THREADS, smem));
         const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);

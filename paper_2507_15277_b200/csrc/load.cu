@@ -102,6 +102,7 @@ void pt_view_free(pt_ctx *ctx, pt_view &v)
         pt_dfree(ctx, v.l32);
         pt_dfree(ctx, v.l64);
         pt_dfree(ctx, v.hT);
+        pt_dfree(ctx, v.hTile);
     }
     v = pt_view();
 }

@@ -45,6 +45,11 @@ struct pt_view {
     float *l32 = nullptr;
     double *l64 = nullptr;
     uint16_t *hT = nullptr;
+    // hTile[s][ct][e][64]: hT re-laid out in 64-config column tiles starting at
+    // config 64*ct + 8*s (s = 0..7), so any 8-aligned 32-env x 64-config tile is
+    // one contiguous 4 KB block (one bulk copy).  Built on first exhaustive use.
+    uint16_t *hTile = nullptr;
+    int64_t n_ct = 0;
     bool owned = false;
 };
 
