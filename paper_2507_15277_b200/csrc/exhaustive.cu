@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
     __syncthreads();
 
     uint32_t steps = 0;   // pipeline steps of all previous tasks (same in every thread)
-    const int tx = tid & 15, ty = (tid >> 4) & 15;
+    const int tx = lane & 7, ty = lane >> 3;
     float b1 = INFINITY, b2 = INFINITY, published = INFINITY;
 
     for (;;) {
@@ -357,83 +357,94 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
 #pragma unroll
                 for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
 
+            // warp w covers rows 32*(w>>1) .. +31 and columns 32*(w&1) .. +31 of the
+            // 128x64 tile; a thread holds 8 consecutive rows (one 16-byte LDS) x 4
+            // consecutive columns (one 8-byte LDS)
+            const int r0 = 32 * (warp >> 1) + 8 * ty;
+            const int c0 = 32 * (warp & 1) + 4 * tx;
             int q = 0;
-            int64_t l0 = lo + (int64_t)tk.y * XT_C + tx * 4;
+            int64_t ltile = lo + (int64_t)tk.y * XT_C;     // first column of the current tile
             uint32_t G = steps;
             for (int g = 0; g < nsteps; g++, G++) {
                 const int slot = G % XT_S;
                 mbar_wait(&full[slot], (G / XT_S) & 1u);
-                const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + tx * 2;
-                const uint16_t *A = As + (int64_t)q * XT_K * XT_R + ty * 4;
+                // the whole warp's column half lies past the last config: skip the math
+                const bool skip = ltile + 32 * (warp & 1) >= p.C;
+                if (!skip) {
+                    const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
+                    const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
 #pragma unroll 2
-                for (int e = 0; e < XT_K; e += 4) {
-                    // 4 envs: A rows (8 fp16 per env as 2 x uint2), B column pairs (half2)
-                    uint2 ar[4][2], bc[4];
-#pragma unroll
-                    for (int t = 0; t < 4; t++) {
-                        ar[t][0] = *reinterpret_cast<const uint2 *>(A + (e + t) * XT_R);
-                        ar[t][1] = *reinterpret_cast<const uint2 *>(A + (e + t) * XT_R + 64);
-                        bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
-                    }
-#pragma unroll
-                    for (int i = 0; i < 8; i++) {
-                        uint32_t av[4];
+                    for (int e = 0; e < XT_K; e += 4) {
+                        uint4 ar[4];
+                        uint2 bc[4];
 #pragma unroll
                         for (int t = 0; t < 4; t++) {
-                            const uint32_t w = (i & 4) ? (((i & 2) ? ar[t][1].y : ar[t][1].x))
-                                                       : (((i & 2) ? ar[t][0].y : ar[t][0].x));
-                            av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                            ar[t] = *reinterpret_cast<const uint4 *>(A + (e + t) * XT_R);
+                            bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
                         }
-                        // fp16 tree over the 4 envs, then 2 FHADD into fp32
-                        fhadd2(acc[i][0], acc[i][1],
-                               hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
-                                     hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))));
-                        fhadd2(acc[i][2], acc[i][3],
-                               hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
-                                     hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))));
+#pragma unroll
+                        for (int i = 0; i < 8; i++) {
+                            uint32_t av[4];
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                const uint32_t w = (i >> 1) == 0 ? ar[t].x : (i >> 1) == 1 ? ar[t].y
+                                                                 : (i >> 1) == 2 ? ar[t].z : ar[t].w;
+                                av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                            }
+                            // fp16 tree over the 4 envs, then 2 FHADD into fp32
+                            fhadd2(acc[i][0], acc[i][1],
+                                   hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
+                                         hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))));
+                            fhadd2(acc[i][2], acc[i][3],
+                                   hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                         hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))));
+                        }
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
                 if (++q == nkc) {
                     q = 0;
-                    // epilogue of one column tile: mask, window test, candidate append
-                    const float Uv = __uint_as_float(*(volatile unsigned *)p.U);
-                    const float tau = fminf(p.tau_seed, fmaf(Uv, p.kappa, p.beta));
+                    if (!skip) {
+                        // epilogue of one column tile: mask, window test, candidate append
+                        const float Uv = __uint_as_float(*(volatile unsigned *)p.U);
+                        const float tau = fminf(p.tau_seed, fmaf(Uv, p.kappa, p.beta));
+                        const int64_t l0 = ltile + c0;
 #pragma unroll
-                    for (int i = 0; i < 8; i++) {
-                        const int r = (i < 4) ? ty * 4 + i : 64 + ty * 4 + (i - 4);
-                        const int last = last_s[r];
+                        for (int i = 0; i < 8; i++) {
+                            const int r = r0 + i;
+                            const int last = last_s[r];
 #pragma unroll
-                        for (int j = 0; j < 4; j++) {
-                            const int64_t l = l0 + j;
-                            const float sh = acc[i][j];
-                            acc[i][j] = 0.0f;
-                            if (l < p.C && l > last) {
-                                if (sh < b1) {
-                                    b2 = b1;
-                                    b1 = sh;
-                                } else if (sh < b2) {
-                                    b2 = sh;
-                                }
-                                if (sh <= tau) {
-                                    const unsigned idx = atomicAdd(p.cand_n, 1u);
-                                    if (idx < p.cap) {
-                                        p.cand_key[idx] = ((unsigned long long)(R0 + r) << KEY_BITS) |
-                                                          (unsigned long long)l;
-                                        p.cand_s[idx] = sh;
+                            for (int j = 0; j < 4; j++) {
+                                const int64_t l = l0 + j;
+                                const float sh = acc[i][j];
+                                acc[i][j] = 0.0f;
+                                if (l < p.C && l > last) {
+                                    if (sh < b1) {
+                                        b2 = b1;
+                                        b1 = sh;
+                                    } else if (sh < b2) {
+                                        b2 = sh;
+                                    }
+                                    if (sh <= tau) {
+                                        const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                        if (idx < p.cap) {
+                                            p.cand_key[idx] = ((unsigned long long)(R0 + r) << KEY_BITS) |
+                                                              (unsigned long long)l;
+                                            p.cand_s[idx] = sh;
+                                        }
                                     }
                                 }
                             }
                         }
+                        float wb = b2;
+                        for (int o = 16; o; o >>= 1) wb = fminf(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+                        if (lane == 0 && wb < published) {
+                            atomicMin(p.U, __float_as_uint(wb));
+                            published = wb;
+                        }
                     }
-                    l0 += XT_C;
-                    float wb = b2;
-                    for (int o = 16; o; o >>= 1) wb = fminf(wb, __shfl_xor_sync(0xffffffffu, wb, o));
-                    if (lane == 0 && wb < published) {
-                        atomicMin(p.U, __float_as_uint(wb));
-                        published = wb;
-                    }
+                    ltile += XT_C;
                 }
             }
         }
