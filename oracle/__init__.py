@@ -44,8 +44,12 @@ def _load():
         lib.or_greedy.argtypes = [P, i64, i64, P, ct.c_int, P, ct.c_int, P, P, P]
         lib.or_holdout.argtypes = [P, i64, i64, P, i32, ct.c_int, ct.c_int, ct.c_int,
                                    P, P, P, P, P]
+        lib.or_fleet_rate.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, P, ct.c_int, P]
+        lib.or_fleet_exhaustive.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, ct.c_int,
+                                            P, P, P, P, P]
+        lib.or_fleet_greedy.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, ct.c_int, P, P, P]
         for f in (lib.or_normalize, lib.or_score, lib.or_exhaustive, lib.or_greedy,
-                  lib.or_holdout):
+                  lib.or_holdout, lib.or_fleet_rate, lib.or_fleet_exhaustive, lib.or_fleet_greedy):
             f.restype = ct.c_int
         _lib = lib
     return _lib
@@ -75,6 +79,7 @@ class Oracle:
 
     def __init__(self, T, env_device=None):
         T = np.ascontiguousarray(T, dtype=np.float32)
+        self.T = T
         assert T.ndim == 2
         self.E, self.C = T.shape
         self.best = np.empty(self.E, np.float64)
@@ -146,3 +151,49 @@ class Oracle:
                             _p(kidx)), "or_holdout")
         return ([int(x) for x in idx], float(g[0]), float(g[1]), float(g[2]),
                 [int(x) for x in kidx])
+
+    # ---- fleet objective (Eq. 2) --------------------------------------------
+    def set_fleet(self, q_dev, q_env):
+        """quantity(d) per device id and quantity(i) per environment."""
+        assert self.env_device is not None
+        self.q_dev = np.ascontiguousarray(q_dev, dtype=np.float64)
+        self.q_env = np.ascontiguousarray(q_env, dtype=np.float64)
+
+    def _fleet_args(self):
+        return (_p(self.T), self.E, self.C, _p(self.best), self.penalty, _p(self.env_device),
+                len(self.q_dev), _p(self.q_dev), _p(self.q_env))
+
+    def fleet_rate(self, sets, mask=None):
+        sets = np.asarray(sets, dtype=np.int32)
+        one = sets.ndim == 1
+        sets = np.atleast_2d(sets)
+        m = self._mask(mask)
+        out = np.empty(len(sets))
+        r = np.zeros(1)
+        for q, s in enumerate(sets):
+            s = np.ascontiguousarray(s)
+            _chk(_load().or_fleet_rate(*self._fleet_args(), _p(m), _p(s), len(s), _p(r)), "or_fleet_rate")
+            out[q] = r[0]
+        return float(out[0]) if one else out
+
+    def fleet_exhaustive(self, k, mask=None):
+        m = self._mask(mask)
+        b = np.zeros(k, np.int32)
+        ru = np.zeros(k, np.int32)
+        rb = np.zeros(1)
+        rr = np.full(1, np.nan)
+        nf = np.zeros(1, np.int32)
+        _chk(_load().or_fleet_exhaustive(*self._fleet_args(), _p(m), k, _p(b), _p(rb), _p(ru), _p(rr),
+                                         _p(nf)), "or_fleet_exhaustive")
+        return (tuple(int(x) for x in b), float(rb[0]),
+                tuple(int(x) for x in ru) if nf[0] >= 2 else None, float(rr[0]))
+
+    def fleet_greedy(self, k, mask=None):
+        m = self._mask(mask)
+        idx = np.zeros(k, np.int32)
+        rt = np.zeros(k)
+        gp = np.zeros(k)
+        _chk(_load().or_fleet_greedy(*self._fleet_args(), _p(m), k, _p(idx), _p(rt), _p(gp)),
+             "or_fleet_greedy")
+        return [int(x) for x in idx], rt, gp
+

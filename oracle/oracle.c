@@ -353,3 +353,133 @@ out:
     free(tr); free(te); free(tmp); free(gt); free(gp);
     return rc;
 }
+
+/* ---- fleet objective, Eq. 2 (Sec. 4.4.2) -------------------- */
+
+/*
+ * or_fleet_rate -- the rate at which the fleet completes tasks:
+ *
+ *   R(S) = sum_{d} quantity(d) / sum_{i} y'_{d,i}(S) * quantity(i)
+ *
+ * y'_{d,i}(S) = min_{c in S} T[(d,i)][c], the runtime of the best member of S
+ * on that environment (best-member reading, as for Eq. 1); a missing
+ * cell costs penalty * best[e] (reading c4).  The inner sum runs over the
+ * environments of device d in scope (a device's task = its available inputs,
+ * P:L487); devices with no environment in scope do not contribute.
+ *   T         env-major runtimes (ld = C), NaN/inf = missing
+ *   best, penalty   from or_normalize
+ *   env_device int32[E]; q_dev double[n_dev] indexed by device id;
+ *   q_env     double[E] = quantity(i) of each environment's input
+ * Units: tasks per millisecond.
+ */
+static double rt_cell(const float *T, int64_t C, const double *best, double penalty,
+                      int64_t e, int32_t c)
+{
+    float t = T[e * C + c];
+    return isfinite(t) ? (double)t : penalty * best[e];
+}
+
+int or_fleet_rate(const float *T, int64_t E, int64_t C, const double *best, double penalty,
+                  const int32_t *env_device, int32_t n_dev, const double *q_dev,
+                  const double *q_env, const uint8_t *mask, const int32_t *set, int k,
+                  double *R_out)
+{
+    if (k <= 0) return OR_EEMPTY;
+    for (int u = 0; u < k; u++)
+        if (set[u] < 0 || set[u] >= C) return OR_EINVAL;
+    double *den = calloc((size_t)n_dev, sizeof(double));
+    int *present = calloc((size_t)n_dev, sizeof(int));
+    if (!den || !present) { free(den); free(present); return OR_ENOMEM; }
+    int any = 0;
+    for (int64_t e = 0; e < E; e++) {
+        if (mask && !mask[e]) continue;
+        int32_t d = env_device[e];
+        if (d < 0 || d >= n_dev) { free(den); free(present); return OR_EINVAL; }
+        double y = rt_cell(T, C, best, penalty, e, set[0]);
+        for (int u = 1; u < k; u++) {
+            double v = rt_cell(T, C, best, penalty, e, set[u]);
+            if (v < y) y = v;
+        }
+        den[d] += y * q_env[e];
+        present[d] = 1;
+        any = 1;
+    }
+    if (!any) { free(den); free(present); return OR_EEMPTY; }
+    double R = 0.0;
+    for (int32_t d = 0; d < n_dev; d++)
+        if (present[d]) R += q_dev[d] / den[d];
+    free(den); free(present);
+    *R_out = R;
+    return OR_OK;
+}
+
+/*
+ * or_fleet_exhaustive -- exhaustive search maximising R (the tuner minimises
+ * its reciprocal): every k-subset in lexicographic order, strict '>'
+ * (first in lex order wins ties).  Writes best and runner-up and their R.
+ * Single-threaded (test sizes only).
+ */
+int or_fleet_exhaustive(const float *T, int64_t E, int64_t C, const double *best, double penalty,
+                        const int32_t *env_device, int32_t n_dev, const double *q_dev,
+                        const double *q_env, const uint8_t *mask, int k,
+                        int32_t *best_set, double *R_best, int32_t *runner_set, double *R_runner,
+                        int *n_found)
+{
+    if (k <= 0 || k > 32 || k > C) return OR_EINVAL;
+    int32_t s[32];
+    top2 res;
+    memset(&res, 0, sizeof res);
+    for (int u = 0; u < k; u++) s[u] = u;
+    for (;;) {
+        double R;
+        int rc = or_fleet_rate(T, E, C, best, penalty, env_device, n_dev, q_dev, q_env, mask, s, k, &R);
+        if (rc) return rc;
+        top2_offer(&res, R, s, k);          /* top2 orders by higher value first */
+        int u = k - 1;
+        while (u >= 0 && s[u] == (int32_t)(C - k + u)) u--;
+        if (u < 0) break;
+        s[u]++;
+        for (int v = u + 1; v < k; v++) s[v] = s[v - 1] + 1;
+    }
+    *n_found = res.have;
+    if (res.have >= 1) { memcpy(best_set, res.s1, sizeof(int32_t) * (size_t)k); *R_best = res.L1; }
+    if (res.have >= 2) { memcpy(runner_set, res.s2, sizeof(int32_t) * (size_t)k); *R_runner = res.L2; }
+    return OR_OK;
+}
+
+/*
+ * or_fleet_greedy -- greedy forward selection maximising R: at each step
+ * evaluate R(S u {c}) for every c not in S (ascending), take the maximum,
+ * ties to the lowest c.  Writes picks, R trace and the top-two gap per step.
+ */
+int or_fleet_greedy(const float *T, int64_t E, int64_t C, const double *best, double penalty,
+                    const int32_t *env_device, int32_t n_dev, const double *q_dev,
+                    const double *q_env, const uint8_t *mask, int k,
+                    int32_t *out_idx, double *R_trace, double *gap_trace)
+{
+    if (k <= 0 || k > C || k > 64) return OR_EINVAL;
+    int32_t S[65];
+    uint8_t *in = calloc((size_t)C, 1);
+    if (!in) return OR_ENOMEM;
+    for (int t = 0; t < k; t++) {
+        double R1 = -INFINITY, R2 = -INFINITY;
+        int32_t c1 = -1;
+        for (int64_t c = 0; c < C; c++) {
+            if (in[c]) continue;
+            S[t] = (int32_t)c;
+            double R;
+            int rc = or_fleet_rate(T, E, C, best, penalty, env_device, n_dev, q_dev, q_env, mask, S, t + 1, &R);
+            if (rc) { free(in); return rc; }
+            if (c1 < 0 || R > R1) { R2 = R1; R1 = R; c1 = (int32_t)c; }
+            else if (R > R2) R2 = R;
+        }
+        S[t] = c1;
+        in[c1] = 1;
+        out_idx[t] = c1;
+        R_trace[t] = R1;
+        gap_trace[t] = (R2 == -INFINITY) ? INFINITY : R1 - R2;
+    }
+    free(in);
+    return OR_OK;
+}
+
