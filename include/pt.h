@@ -51,8 +51,10 @@ typedef enum {
 } pt_status;
 
 typedef enum {
-    PT_OBJ_GEOMEAN = 0,   /* Eq. 1 library objective (graded path) */
-    PT_OBJ_FLEET = 1      /* Eq. 2 fleet rate -- NEXT, returns PT_EINVAL for now */
+    PT_OBJ_GEOMEAN = 0,   /* Eq. 1 library objective: G = geomean efficiency (graded path) */
+    PT_OBJ_FLEET = 1      /* Eq. 2 fleet rate R (tasks/ms); needs pt_set_fleet.
+                             Reported in the out_G slots; sets are ranked by R desc
+                             (the tuner minimises 1/R), ties as above */
 } pt_objective;
 
 /* pt_load_perf flags */
@@ -164,6 +166,20 @@ pt_status pt_merge_top2(const double *s, const int32_t *tuples, int32_t n_rec, i
 pt_status pt_eval_holdout(pt_ctx *ctx, int32_t heldout_device, int32_t k, int32_t method,
                           int32_t *out_idx, double *out_G_train, double *out_G_unseen,
                           double *out_G_known, int32_t *out_known_idx);
+
+/*
+ * pt_set_fleet -- quantities for the fleet objective, Eq. 2:
+ *   R(S) = sum_d quantity(d) / sum_{i} y'_{d,i}(S) * quantity(i),
+ *   y'_{d,i}(S) = min_{c in S} T[(d,i)][c]  (best member; a missing cell costs
+ *   the dataset-max slowdown x best[e]).  The inner sum runs over the
+ *   environments of device d in scope; a device with none does not contribute.
+ *   q_device  host double[n_device], quantity(d) for device ids 0..n_device-1
+ *   q_env     host double[n_env], quantity(i) of each environment's input
+ * Copied; the context keeps them until the next call.
+ * Errors: PT_EINVAL (an env's device id outside [0, n_device), q <= 0).
+ */
+pt_status pt_set_fleet(pt_ctx *ctx, const double *q_device, int32_t n_device,
+                       const double *q_env);
 
 /* Per-context counters (for bench.py's roofline and gpu_launches fields). */
 typedef struct {

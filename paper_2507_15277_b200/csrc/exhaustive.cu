@@ -598,6 +598,25 @@ __global__ void __launch_bounds__(256) k_exh_generic(const double *__restrict__ 
     }
 }
 
+// one-CTA (s, tuple) top-2 over n records on the device -> host
+pt_status pt_top2_records(pt_ctx *ctx, const double *d_s, const int32_t *d_t, int64_t n, int k,
+                          double *s_out, int32_t *t_out)
+{
+    double *os = nullptr;
+    int32_t *ot = nullptr;
+    PT_TRY(pt_dalloc(ctx, (void **)&os, sizeof(double) * 2));
+    PT_TRY(pt_dalloc(ctx, (void **)&ot, sizeof(int32_t) * 2 * k));
+    k_top2<<<1, 256, 0, ctx->stream>>>(d_s, d_t, n, k, os, ot);
+    ctx->stats.launches++;
+    PT_CK(cudaGetLastError());
+    PT_CK(cudaMemcpyAsync(s_out, os, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    PT_CK(cudaMemcpyAsync(t_out, ot, sizeof(int32_t) * 2 * k, cudaMemcpyDeviceToHost, ctx->stream));
+    pt_dfree(ctx, os);
+    pt_dfree(ctx, ot);
+    PT_CK(cudaStreamSynchronize(ctx->stream));
+    return PT_OK;
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -849,10 +868,25 @@ extern "C" pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *e
                                         double *out_G_runner, double *out_s)
 {
     if (!ctx || !out_idx || !out_G) return pt_fail(PT_EINVAL, "NULL argument");
-    if (objective != PT_OBJ_GEOMEAN)
-        return pt_fail(PT_EINVAL, "objective %d not implemented (Eq. 2 fleet rate is NEXT)",
-                       objective);
+    if (objective != PT_OBJ_GEOMEAN && objective != PT_OBJ_FLEET)
+        return pt_fail(PT_EINVAL, "unknown objective %d", objective);
     PT_CK(cudaSetDevice(ctx->dev));
+    if (objective == PT_OBJ_FLEET) {
+        std::vector<int32_t> runner(k > 0 ? k : 1);
+        double R[2], cost[2];
+        int nf = 0;
+        PT_TRY(pt_fleet_exhaustive(ctx, k, env_mask, shard_rank, shard_count, out_idx, runner.data(),
+                                   R, cost, &nf));
+        *out_G = R[0];
+        if (out_runner_idx)
+            for (int u = 0; u < k; u++) out_runner_idx[u] = runner[u];
+        if (out_G_runner) *out_G_runner = R[1];
+        if (out_s) {
+            out_s[0] = cost[0];
+            out_s[1] = cost[1];
+        }
+        return PT_OK;
+    }
     const pt_view *v = nullptr;
     PT_TRY(pt_get_view(ctx, env_mask, &v));
     std::vector<int32_t> runner(k > 0 ? k : 1);

@@ -504,10 +504,10 @@ extern "C" pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env
                                       double *out_gap_trace)
 {
     if (!ctx || !out_idx) return pt_fail(PT_EINVAL, "NULL argument");
-    if (objective != PT_OBJ_GEOMEAN)
-        return pt_fail(PT_EINVAL, "objective %d not implemented (Eq. 2 fleet rate is NEXT)",
-                       objective);
+    if (objective != PT_OBJ_GEOMEAN && objective != PT_OBJ_FLEET)
+        return pt_fail(PT_EINVAL, "unknown objective %d", objective);
     PT_CK(cudaSetDevice(ctx->dev));
+    if (objective == PT_OBJ_FLEET) return pt_fleet_greedy(ctx, k, env_mask, out_idx, out_G_trace, out_gap_trace);
     const pt_view *v = nullptr;
     PT_TRY(pt_get_view(ctx, env_mask, &v));
     std::vector<double> s1(k > 0 ? k : 1), s2(k > 0 ? k : 1);

@@ -414,7 +414,10 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
         cleanup();
         return bail(st);
     }
-    cleanup();
+    // keep the runtimes (env-major fp32) for objectives on raw times (Eq. 2)
+    ctx->T32 = dT;
+    pt_dfree(ctx, rowmax);
+    pt_dfree(ctx, status);
     cudaError_t ce = cudaStreamSynchronize(ctx->stream);
     if (ce != cudaSuccess || cudaGetLastError() != cudaSuccess)
         return bail(pt_fail(PT_ECUDA, "normalise kernel failed: %s", cudaGetErrorString(ce)));
@@ -438,6 +441,11 @@ extern "C" void pt_free(pt_ctx *ctx)
     for (auto &sc : ctx->scopes) pt_view_free(ctx, sc.view);
     pt_dfree(ctx, ctx->best);
     pt_dfree(ctx, ctx->scratch);
+    pt_dfree(ctx, ctx->T32);
+    pt_dfree(ctx, ctx->fl.tcm);
+    pt_dfree(ctx, ctx->fl.w);
+    pt_dfree(ctx, ctx->fl.qdev);
+    pt_dfree(ctx, ctx->fl.seg);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);

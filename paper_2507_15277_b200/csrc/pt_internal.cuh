@@ -61,6 +61,19 @@ struct pt_scope {   // one cached compacted scope
     uint64_t last_use = 0;
 };
 
+// fleet objective (Eq. 2) data, built by pt_set_fleet
+struct pt_fleet {
+    bool set = false;
+    int32_t n_dev = 0;
+    double *tcm = nullptr;    // [C][E_pad] runtimes (missing -> penalty*best), envs grouped by device
+    double *w = nullptr;      // [E_pad] quantity(i) of each (permuted) env, 0 for padding
+    double *qdev = nullptr;   // [n_dev] quantity(d)
+    int32_t *seg = nullptr;   // [n_dev+1] env offsets of each device's segment
+    std::vector<int32_t> perm;      // permuted position -> original env
+    std::vector<int32_t> h_seg;
+    std::vector<double> h_w, h_qdev;
+};
+
 struct pt_ctx {
     int dev = 0;
     cudaStream_t stream = nullptr;
@@ -71,6 +84,8 @@ struct pt_ctx {
     bool have_device = false;
     double penalty = 1.0;
     double *best = nullptr;   // [E] fp64, each env's Oracle
+    float *T32 = nullptr;     // [E][C] fp32 runtimes as loaded (NaN/inf = missing)
+    pt_fleet fl;
     pt_view full;
     // scope cache (LRU of compacted scopes)
     std::vector<pt_scope> scopes;
@@ -101,6 +116,14 @@ pt_status pt_exhaustive_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t s
                              double *s_out, int *n_found);
 pt_status pt_score_view(pt_ctx *ctx, const pt_view *v, const int32_t *d_sets, int64_t n_sets,
                         int32_t k, double *d_s);
+// fleet objective (fleet.cu): rates of sets / greedy / exhaustive, env_mask may be NULL
+pt_status pt_fleet_score(pt_ctx *ctx, const int32_t *d_sets, int64_t n_sets, int32_t k,
+                         const uint8_t *env_mask, double *d_R);
+pt_status pt_fleet_greedy(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t *out_idx,
+                          double *R_trace, double *gap_trace);
+pt_status pt_fleet_exhaustive(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
+                              int32_t shard_count, int32_t *best, int32_t *runner, double *R_out,
+                              double *cost_out, int *n_found);
 
 
 // ---------------------------------------------------------------------------

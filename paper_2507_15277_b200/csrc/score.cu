@@ -67,13 +67,12 @@ extern "C" pt_status pt_score_sets(pt_ctx *ctx, const int32_t *sets, int64_t n_s
 {
     if (!ctx || (!sets && n_sets > 0) || (!out_G && n_sets > 0) || n_sets < 0)
         return pt_fail(PT_EINVAL, "NULL argument");
-    if (objective != PT_OBJ_GEOMEAN)
-        return pt_fail(PT_EINVAL, "objective %d not implemented (Eq. 2 fleet rate is NEXT)",
-                       objective);
+    if (objective != PT_OBJ_GEOMEAN && objective != PT_OBJ_FLEET)
+        return pt_fail(PT_EINVAL, "unknown objective %d", objective);
     if (k < 1) return pt_fail(PT_EEMPTY, "empty set (k < 1)");
     PT_CK(cudaSetDevice(ctx->dev));
     const pt_view *v = nullptr;
-    PT_TRY(pt_get_view(ctx, env_mask, &v));
+    if (objective == PT_OBJ_GEOMEAN) PT_TRY(pt_get_view(ctx, env_mask, &v));
     if (n_sets == 0) return PT_OK;
     const bool sets_dev = pt_is_device_ptr(sets), out_dev = pt_is_device_ptr(out_G);
     const size_t set_bytes = sizeof(int32_t) * (size_t)n_sets * k;
@@ -87,10 +86,14 @@ extern "C" pt_status pt_score_sets(pt_ctx *ctx, const int32_t *sets, int64_t n_s
         PT_CK(cudaMemcpyAsync(tmp, sets, set_bytes, cudaMemcpyHostToDevice, ctx->stream));
         d_sets = tmp;
     }
-    PT_TRY(pt_score_view(ctx, v, d_sets, n_sets, k, d_s));
-    k_s_to_G<<<(unsigned)((n_sets + 255) / 256), 256, 0, ctx->stream>>>(d_s, n_sets,
-                                                                       1.0 / (double)v->E);
-    ctx->stats.launches++;
+    if (objective == PT_OBJ_FLEET) {
+        PT_TRY(pt_fleet_score(ctx, d_sets, n_sets, k, env_mask, d_s));
+    } else {
+        PT_TRY(pt_score_view(ctx, v, d_sets, n_sets, k, d_s));
+        k_s_to_G<<<(unsigned)((n_sets + 255) / 256), 256, 0, ctx->stream>>>(d_s, n_sets,
+                                                                           1.0 / (double)v->E);
+        ctx->stats.launches++;
+    }
     if (!out_dev)
         PT_CK(cudaMemcpyAsync(out_G, d_s, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     PT_CK(cudaStreamSynchronize(ctx->stream));

@@ -24,7 +24,8 @@ PT_OBJ_GEOMEAN, PT_OBJ_FLEET = 0, 1
 PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM = 0x1, 0x2, 0x4
 
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
-           "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_free", "pt_last_error")
+           "pt_merge_top2", "pt_eval_holdout", "pt_set_fleet", "pt_get_stats", "pt_free",
+           "pt_last_error")
 
 
 class pt_stats(ct.Structure):
@@ -59,12 +60,13 @@ def lib():
         L.pt_merge_top2.argtypes = [P, P, i32, i32, P, P, P]
         L.pt_eval_holdout.argtypes = [P, i32, i32, i32, P, P, P, P, P]
         L.pt_get_stats.argtypes = [P, ct.POINTER(pt_stats)]
+        L.pt_set_fleet.argtypes = [P, P, i32, P]
         L.pt_free.argtypes = [P]
         L.pt_free.restype = None
         L.pt_last_error.argtypes = []
         L.pt_last_error.restype = ct.c_char_p
         for f in ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
-                  "pt_merge_top2", "pt_eval_holdout", "pt_get_stats"):
+                  "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_set_fleet"):
             getattr(L, f).restype = ct.c_int
         _lib = L
     return _lib
@@ -139,8 +141,16 @@ def pt_load_perf(times_ms, env_device=None, flags=0, device=0, stream=None) -> P
     return PtContext(h, E, C)
 
 
-def pt_score_sets(ctx, sets, env_mask=None, out=None):
-    """G of each set.  sets: [n][k] int32 (numpy or torch); returns numpy (or fills `out`)."""
+def pt_set_fleet(ctx, q_device, q_env):
+    """Quantities for the fleet objective (Eq. 2): quantity(d) per device id, quantity(i) per env."""
+    qd = _np(q_device, np.float64)
+    qe = _np(q_env, np.float64)
+    _chk(lib().pt_set_fleet(ctx.handle, _ptr(qd), len(qd), _ptr(qe)), "pt_set_fleet")
+
+
+def pt_score_sets(ctx, sets, env_mask=None, out=None, objective=PT_OBJ_GEOMEAN):
+    """G (or fleet rate R) of each set.  sets: [n][k] int32 (numpy or torch); returns numpy
+    (or fills `out`)."""
     if hasattr(sets, "data_ptr"):
         n, k = sets.shape
         s = sets
@@ -148,28 +158,30 @@ def pt_score_sets(ctx, sets, env_mask=None, out=None):
         s = np.atleast_2d(_np(sets, np.int32))
         n, k = s.shape
     res = out if out is not None else np.empty(n, np.float64)
-    _chk(lib().pt_score_sets(ctx.handle, _ptr(s), n, k, _ptr(_mask(env_mask)), PT_OBJ_GEOMEAN,
+    _chk(lib().pt_score_sets(ctx.handle, _ptr(s), n, k, _ptr(_mask(env_mask)), objective,
                              _ptr(res)), "pt_score_sets")
     return res
 
 
-def pt_greedy_select(ctx, k, env_mask=None):
-    """Greedy forward selection: (indices, G_trace, gap_trace)."""
+def pt_greedy_select(ctx, k, env_mask=None, objective=PT_OBJ_GEOMEAN):
+    """Greedy forward selection: (indices, G_trace (or R_trace), gap_trace)."""
     idx = np.zeros(k, np.int32)
     gt = np.zeros(k, np.float64)
     gp = np.zeros(k, np.float64)
-    _chk(lib().pt_greedy_select(ctx.handle, k, _ptr(_mask(env_mask)), PT_OBJ_GEOMEAN, _ptr(idx),
+    _chk(lib().pt_greedy_select(ctx.handle, k, _ptr(_mask(env_mask)), objective, _ptr(idx),
                                 _ptr(gt), _ptr(gp)), "pt_greedy_select")
     return [int(x) for x in idx], gt, gp
 
 
-def pt_exhaustive_best(ctx, k, env_mask=None, shard_rank=0, shard_count=1):
-    """Exhaustive k-subset search (one shard): dict(best, G, runner, G_runner, s)."""
+def pt_exhaustive_best(ctx, k, env_mask=None, shard_rank=0, shard_count=1,
+                       objective=PT_OBJ_GEOMEAN):
+    """Exhaustive k-subset search (one shard): dict(best, G, runner, G_runner, s).
+    For PT_OBJ_FLEET, G/G_runner hold the fleet rates and s the costs 1/R."""
     b = np.zeros(k, np.int32)
     r = np.zeros(k, np.int32)
     g = np.zeros(2, np.float64)
     s = np.zeros(2, np.float64)
-    _chk(lib().pt_exhaustive_best(ctx.handle, k, _ptr(_mask(env_mask)), PT_OBJ_GEOMEAN,
+    _chk(lib().pt_exhaustive_best(ctx.handle, k, _ptr(_mask(env_mask)), objective,
                                   shard_rank, shard_count, _ptr(b), _ptr(g[0:1]), _ptr(r),
                                   _ptr(g[1:2]), _ptr(s)), "pt_exhaustive_best")
     has1, has2 = np.isfinite(s[0]), np.isfinite(s[1])
