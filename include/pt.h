@@ -168,6 +168,22 @@ pt_status pt_eval_holdout(pt_ctx *ctx, int32_t heldout_device, int32_t k, int32_
                           double *out_G_known, int32_t *out_known_idx);
 
 /*
+ * pt_swap_search -- deterministic best-improvement swap local search over
+ * k-sets (the stand-in for the paper's heuristic search over variant
+ * combinations, Sec. 4.3.1).  From `init` (host
+ * int32[k], distinct) or, if NULL, the greedy k-set, every move evaluates all
+ * k*(C-k) swaps exactly (fp64) and applies the best if it strictly improves G
+ * (ties -> lexicographically smallest resulting sorted tuple); stops at a local
+ * optimum or after max_moves moves.
+ *   out_idx   host int32[k], the final set ascending;  out_G its G;
+ *   out_moves host or NULL: moves applied.
+ * PT_OBJ_GEOMEAN only.  Errors: PT_EINVAL (k < 1, k >= C, k > 32, bad init).
+ */
+pt_status pt_swap_search(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t objective,
+                         int32_t max_moves, const int32_t *init, int32_t *out_idx, double *out_G,
+                         int32_t *out_moves);
+
+/*
  * pt_set_fleet -- quantities for the fleet objective, Eq. 2:
  *   R(S) = sum_d quantity(d) / sum_{i} y'_{d,i}(S) * quantity(i),
  *   y'_{d,i}(S) = min_{c in S} T[(d,i)][c]  (best member; a missing cell costs

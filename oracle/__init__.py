@@ -48,8 +48,10 @@ def _load():
         lib.or_fleet_exhaustive.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, ct.c_int,
                                             P, P, P, P, P]
         lib.or_fleet_greedy.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, ct.c_int, P, P, P]
+        lib.or_swap_search.argtypes = [P, i64, i64, P, ct.c_int, P, ct.c_int, P, P, P]
         for f in (lib.or_normalize, lib.or_score, lib.or_exhaustive, lib.or_greedy,
-                  lib.or_holdout, lib.or_fleet_rate, lib.or_fleet_exhaustive, lib.or_fleet_greedy):
+                  lib.or_holdout, lib.or_fleet_rate, lib.or_fleet_exhaustive, lib.or_fleet_greedy,
+                  lib.or_swap_search):
             f.restype = ct.c_int
         _lib = lib
     return _lib
@@ -151,6 +153,17 @@ class Oracle:
                             _p(kidx)), "or_holdout")
         return ([int(x) for x in idx], float(g[0]), float(g[1]), float(g[2]),
                 [int(x) for x in kidx])
+
+    def swap_search(self, k, mask=None, init=None, max_moves=1000):
+        """Best-improvement swap local search from greedy (or init): (set, G, moves)."""
+        m = self._mask(mask)
+        ini = None if init is None else np.ascontiguousarray(np.asarray(init, dtype=np.int32))
+        out = np.zeros(k, np.int32)
+        g = np.zeros(1)
+        mv = np.zeros(1, np.int32)
+        _chk(_load().or_swap_search(_p(self.logeff), self.E, self.C, _p(m), k, _p(ini), max_moves,
+                                    _p(out), _p(g), _p(mv)), "or_swap_search")
+        return tuple(int(x) for x in out), float(g[0]), int(mv[0])
 
     # ---- fleet objective (Eq. 2) --------------------------------------------
     def set_fleet(self, q_dev, q_env):

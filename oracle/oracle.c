@@ -483,3 +483,74 @@ int or_fleet_greedy(const float *T, int64_t E, int64_t C, const double *best, do
     return OR_OK;
 }
 
+/* ---- swap local search ------------------- */
+
+/*
+ * or_swap_search -- deterministic best-improvement swap local search, the
+ * stand-in for the paper's heuristic/stochastic search over sets (P:L280,
+ * Sec. 4.3.1; "PortabilityTune"): start from the greedy k-set (or
+ * `init` if given); repeatedly evaluate every swap (a in S out, b not in S in)
+ * with the full Eq. 1 score, take the best (highest L; ties -> the
+ * lexicographically smallest resulting sorted tuple); apply it if it strictly
+ * improves L, else stop.  At most max_moves moves.
+ * Writes the final sorted set, its G and the number of moves applied.
+ */
+static int cmp_i32(const void *a, const void *b)
+{
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+
+int or_swap_search(const double *logeff, int64_t E, int64_t C, const uint8_t *mask, int k,
+                   const int32_t *init, int max_moves, int32_t *out_set, double *G_out,
+                   int *moves_out)
+{
+    if (k <= 0 || k > 32 || k >= C) return OR_EINVAL;
+    int64_t *envs = malloc(sizeof(int64_t) * (size_t)E);
+    uint8_t *in = calloc((size_t)C, 1);
+    if (!envs || !in) { free(envs); free(in); return OR_ENOMEM; }
+    int64_t ne = scope_list(mask, E, envs);
+    if (ne == 0) { free(envs); free(in); return OR_EEMPTY; }
+    int32_t S[32], T[32], Tb[32];
+    if (init) {
+        memcpy(S, init, sizeof(int32_t) * (size_t)k);
+    } else {
+        double *gt = malloc(sizeof(double) * (size_t)k), *gp = malloc(sizeof(double) * (size_t)k);
+        int rc = or_greedy(logeff, E, C, mask, k, NULL, 0, S, gt, gp);
+        free(gt); free(gp);
+        if (rc) { free(envs); free(in); return rc; }
+    }
+    qsort(S, (size_t)k, sizeof(int32_t), cmp_i32);
+    for (int u = 0; u < k; u++) in[S[u]] = 1;
+    double L = logsum(logeff, C, envs, ne, S, k);
+    int moves = 0;
+    while (moves < max_moves) {
+        double Lb = -INFINITY;
+        int have = 0;
+        for (int a = 0; a < k; a++)
+            for (int64_t b = 0; b < C; b++) {
+                if (in[b]) continue;
+                memcpy(T, S, sizeof(int32_t) * (size_t)k);
+                T[a] = (int32_t)b;
+                qsort(T, (size_t)k, sizeof(int32_t), cmp_i32);
+                double Lt = logsum(logeff, C, envs, ne, T, k);
+                if (!have || precedes(Lt, T, Lb, Tb, k)) {
+                    Lb = Lt;
+                    memcpy(Tb, T, sizeof(int32_t) * (size_t)k);
+                    have = 1;
+                }
+            }
+        if (!have || !(Lb > L)) break;
+        for (int u = 0; u < k; u++) in[S[u]] = 0;
+        memcpy(S, Tb, sizeof(int32_t) * (size_t)k);
+        for (int u = 0; u < k; u++) in[S[u]] = 1;
+        L = Lb;
+        moves++;
+    }
+    memcpy(out_set, S, sizeof(int32_t) * (size_t)k);
+    *G_out = exp(L / (double)ne);
+    *moves_out = moves;
+    free(envs); free(in);
+    return OR_OK;
+}
+

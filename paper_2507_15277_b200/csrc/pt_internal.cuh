@@ -180,3 +180,4 @@ __host__ __device__ static inline bool pt_key_less(double sa, const int32_t *a, 
 }
 
 #define PT_MAXK 8
+#define PT_SWAP_MAXK 32

@@ -24,8 +24,8 @@ PT_OBJ_GEOMEAN, PT_OBJ_FLEET = 0, 1
 PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM = 0x1, 0x2, 0x4
 
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
-           "pt_merge_top2", "pt_eval_holdout", "pt_set_fleet", "pt_get_stats", "pt_free",
-           "pt_last_error")
+           "pt_merge_top2", "pt_eval_holdout", "pt_swap_search", "pt_set_fleet", "pt_get_stats",
+           "pt_free", "pt_last_error")
 
 
 class pt_stats(ct.Structure):
@@ -61,12 +61,14 @@ def lib():
         L.pt_eval_holdout.argtypes = [P, i32, i32, i32, P, P, P, P, P]
         L.pt_get_stats.argtypes = [P, ct.POINTER(pt_stats)]
         L.pt_set_fleet.argtypes = [P, P, i32, P]
+        L.pt_swap_search.argtypes = [P, i32, P, i32, i32, P, P, P, P]
         L.pt_free.argtypes = [P]
         L.pt_free.restype = None
         L.pt_last_error.argtypes = []
         L.pt_last_error.restype = ct.c_char_p
         for f in ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
-                  "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_set_fleet"):
+                  "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_set_fleet",
+                  "pt_swap_search"):
             getattr(L, f).restype = ct.c_int
         _lib = L
     return _lib
@@ -188,6 +190,17 @@ def pt_exhaustive_best(ctx, k, env_mask=None, shard_rank=0, shard_count=1,
     return {"best": tuple(int(x) for x in b) if has1 else None, "G": float(g[0]),
             "runner": tuple(int(x) for x in r) if has2 else None, "G_runner": float(g[1]),
             "s": (float(s[0]), float(s[1]))}
+
+
+def pt_swap_search(ctx, k, env_mask=None, init=None, max_moves=1000):
+    """Swap local search from greedy (or init): (sorted set, G, moves)."""
+    out = np.zeros(k, np.int32)
+    g = np.zeros(1)
+    mv = np.zeros(1, np.int32)
+    ini = None if init is None else _np(init, np.int32)
+    _chk(lib().pt_swap_search(ctx.handle, k, _ptr(_mask(env_mask)), PT_OBJ_GEOMEAN, max_moves,
+                              _ptr(ini), _ptr(out), _ptr(g), _ptr(mv)), "pt_swap_search")
+    return tuple(int(x) for x in out), float(g[0]), int(mv[0])
 
 
 def pt_merge_top2(s, tuples, k):
