@@ -44,6 +44,12 @@
 // ---------------------------------------------------------------------------
 // work list
 // ---------------------------------------------------------------------------
+// first column of a row tile whose first row's largest member is j0: j0 + 1
+// rounded down to 8 configs (16-byte aligned fp16 rows); the extra columns are
+// <= every row's largest member and masked.  Used by the task builder AND the
+// kernel so both cover exactly [tile_lo, tile_lo + 64 * n_ct) >= [j0+1, C).
+__host__ __device__ static inline int64_t tile_lo(int64_t j0) { return (j0 + 1) & ~(int64_t)7; }
+
 struct pt_tasks {
     int m = 0;
     int64_t C = 0;
@@ -80,8 +86,8 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **ou
     for (int64_t t = 0; t < n_rt; t++) {
         int32_t mem[PT_MAXK];
         pt_unrank_colex(t * XT_R, m, C, mem);
-        const int64_t ncols = C - (mem[m - 1] + 1);
-        if (ncols > 0) total_ct += (ncols + XT_C - 1) / XT_C;
+        if (mem[m - 1] + 1 >= C) continue;
+        total_ct += (C - tile_lo(mem[m - 1]) + XT_C - 1) / XT_C;
     }
     const int64_t umax = std::max<int64_t>(1, std::min<int64_t>(XT_UMAX, total_ct / (8 * std::max(ctx->num_sms, 1))));
     for (int64_t t = 0; t < n_rt; t++) {
@@ -89,10 +95,9 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **ou
         int32_t mem[PT_MAXK];
         pt_unrank_colex(R0, m, C, mem);
         const int64_t j0 = mem[m - 1];
-        const int64_t lo = j0 + 1;
-        const int64_t ncols = C - lo;
-        if (ncols <= 0) continue;
-        const int64_t n_ct = (ncols + XT_C - 1) / XT_C;
+        if (j0 + 1 >= C) continue;                    // no column l > j0
+        const int64_t lo = tile_lo(j0);
+        const int64_t n_ct = (C - lo + XT_C - 1) / XT_C;
         for (int64_t u0 = 0; u0 < n_ct; u0 += umax) {
             const int64_t u1 = std::min(n_ct, u0 + umax);
             const int64_t clo = lo + u0 * XT_C, chi = std::min(C, lo + u1 * XT_C);
@@ -293,9 +298,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
         const int64_t R0 = (int64_t)tk.x * XT_R;
         int32_t mem0[PT_MAXK];
         pt_unrank_colex(R0, p.m, p.C, mem0);
-        // first column of the row tile, rounded down to 16 bytes (8 configs);
-        // the extra columns are <= the row's largest element and masked
-        const int64_t lo = ((int64_t)mem0[p.m - 1] + 1) & ~(int64_t)7;
+        const int64_t lo = tile_lo(mem0[p.m - 1]);
         const int nsteps = (tk.z - tk.y) * nkc;
 
         if (warp == XT_CONS / 32) {
