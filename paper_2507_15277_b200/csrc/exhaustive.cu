@@ -31,6 +31,8 @@
 #include <tuple>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "pt_internal.cuh"
 
 #define XT_R 128    // rows per CTA tile
@@ -159,9 +161,21 @@ __device__ __forceinline__ bool mbar_try(uint64_t *b, uint32_t parity)
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase
+// completes (or the hint expires) instead of spinning through issue slots
+__device__ __forceinline__ bool mbar_try_sleep(uint64_t *b, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
 {
-    while (!mbar_try(b, parity)) {
+    while (!mbar_try_sleep(b, parity)) {
     }
 }
 // bulk async copy global -> shared on the TMA engine (SASS UBLKCP), completion
@@ -194,6 +208,14 @@ __device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b)
 {
     uint32_t r;
     asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+// relu(a - b) per half on the FMA pipe (HFMA2.RELU b * -1 + a): with it
+// sum_e min(a, b) = sum_e a - sum_e relu(a - b)
+__device__ __forceinline__ uint32_t hrelu_sub2(uint32_t a, uint32_t b)
+{
+    uint32_t r;
+    asm("fma.rn.relu.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(0xBC00BC00u), "r"(a));
     return r;
 }
 // (acc_lo, acc_hi) += (f32(p.lo), f32(p.hi)): two FHADD (fp32 += fp16)
@@ -230,10 +252,10 @@ struct XParams {
     const int4 *tasks;
     int task_hi;              // end of this shard's task range
     int *task_ctr;            // dynamic scheduler (starts at the shard's first task)
-    float tau_seed;           // threshold seeded by greedy's exact runner-up score
-    float kappa;              // tau(U) = U * kappa + beta (rounded up)
-    float beta;
-    unsigned *U;              // float bits: min over warps of their 2nd-smallest s_hat
+    float tau_seed;           // upper bound of s_(2): greedy's exact runner-up score (rounded up)
+    float c1, c2, c3, c4;     // min form: LB = RD(s*c1 - c2), UB = RU(s*c3 + c4)
+    float eta_A, eta_abs_r;   // relu form: |s_hat - s| <= eta_A * sumA_row + eta_abs_r
+    unsigned *U;              // float bits: min over warps of their 2nd-smallest upper bound
     unsigned long long *cand_key;
     float *cand_s;
     unsigned *cand_n;
@@ -243,6 +265,13 @@ struct XParams {
     int64_t n_ct;
 };
 
+// Rows (of a thread's 8) whose 2nd column pair uses the relu form on the FMA pipe
+// instead of HMNMX2 on the ALU pipe.  Measured on B200 (k=3 paper shape): 0 ->
+// 14.02 ms, 1 -> 14.12, 2 -> 14.12, 4 -> 14.85, 8 -> 16.3 -- the FMA pipe is as
+// loaded as the ALU pipe (FHADD), so the default keeps every unit on HMNMX2.
+#ifndef RELU_ROWS
+#define RELU_ROWS 0
+#endif
 #define XT_THREADS 288
 #define XT_CONS 256
 #define XT_BROW (XT_C * 2)     // bytes of one env row of a column tile
@@ -268,7 +297,9 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
     uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2
     uint16_t *As = reinterpret_cast<uint16_t *>(Bs + XT_S * XT_K * (XT_C / 2)); // [E_pad][128] fp16
     int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);                // [128]
-    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);              // [S]
+    float *sumA_s = reinterpret_cast<float *>(last_s + XT_R);                  // [128] sum_e A
+    float *bnd_s = sumA_s + XT_R;                                              // [128] relu-form bound
+    uint64_t *full = reinterpret_cast<uint64_t *>(bnd_s + XT_R);               // [S]
     uint64_t *empty = full + XT_S;                                             // [S]
     int4 *task_s = reinterpret_cast<int4 *>(empty + XT_S);
 
@@ -312,7 +343,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 for (int g = 0; g < nsteps; g++, G++) {
                     const int slot = G % XT_S;
                     const uint32_t par = ((G / XT_S) & 1u) ^ 1u;
-                    while (!mbar_try(&empty[slot], par)) __nanosleep(128);
+                    mbar_wait(&empty[slot], par);
                     const int64_t sh = (col >> 3) & 7, ct = (col - 8 * sh) >> 6;
                     const uint16_t *src = p.hTile + ((sh * p.n_ct + ct) * p.E_pad + (int64_t)q * XT_K) * XT_C;
                     mbar_expect_tx(&full[slot], XT_K * XT_BROW);
@@ -353,6 +384,16 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 }
             }
             named_sync(1, XT_CONS);
+            // row sums of A (fp32, e ascending) for the relu-form units, and
+            // their error bound eta_A * sumA + eta_abs (rounded up)
+            if (RELU_ROWS > 0 && tid < XT_R) {
+                float sa = 0.0f;
+                for (int64_t e = 0; e < p.E_pad; e++)
+                    sa += __half2float(__ushort_as_half(As[e * XT_R + tid]));
+                sumA_s[tid] = sa;
+                bnd_s[tid] = __fmaf_ru(p.eta_A, sa, p.eta_abs_r);
+            }
+            if (RELU_ROWS > 0) named_sync(1, XT_CONS);
 
             float acc[8][4];
 #pragma unroll
@@ -394,13 +435,21 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                                                                  : (i >> 1) == 2 ? ar[t].z : ar[t].w;
                                 av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
                             }
-                            // fp16 tree over the 4 envs, then 2 FHADD into fp32
+                            // fp16 tree over the 4 envs, then 2 FHADD into fp32.
+                            // Units (i < 4, column pair 1) use the relu form on the
+                            // FMA pipe, the rest HMNMX2 on the ALU pipe: balances
+                            // the two pipes (1/4 of the units relu)
                             fhadd2(acc[i][0], acc[i][1],
                                    hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
                                          hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))));
-                            fhadd2(acc[i][2], acc[i][3],
-                                   hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
-                                         hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))));
+                            if (i < RELU_ROWS)
+                                fhadd2(acc[i][2], acc[i][3],
+                                       hadd2(hadd2(hrelu_sub2(av[0], bc[0].y), hrelu_sub2(av[1], bc[1].y)),
+                                             hadd2(hrelu_sub2(av[2], bc[2].y), hrelu_sub2(av[3], bc[3].y))));
+                            else
+                                fhadd2(acc[i][2], acc[i][3],
+                                       hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                             hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))));
                         }
                     }
                 }
@@ -409,32 +458,42 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 if (++q == nkc) {
                     q = 0;
                     if (!skip) {
-                        // epilogue of one column tile: mask, window test, candidate append
-                        const float Uv = __uint_as_float(*(volatile unsigned *)p.U);
-                        const float tau = fminf(p.tau_seed, fmaf(Uv, p.kappa, p.beta));
+                        // epilogue of one column tile: per-set lower/upper bounds of
+                        // the exact score, window test, candidate append
+                        const float tau = fminf(p.tau_seed, __uint_as_float(*(volatile unsigned *)p.U));
                         const int64_t l0 = ltile + c0;
 #pragma unroll
                         for (int i = 0; i < 8; i++) {
                             const int r = r0 + i;
                             const int last = last_s[r];
+                            const float sA = RELU_ROWS > 0 ? sumA_s[r] : 0.0f;
+                            const float bA = RELU_ROWS > 0 ? bnd_s[r] : 0.0f;
 #pragma unroll
                             for (int j = 0; j < 4; j++) {
                                 const int64_t l = l0 + j;
-                                const float sh = acc[i][j];
+                                float lb, ub;
+                                if (i < RELU_ROWS && j >= 2) {   // relu form: s_hat = sum A - sum relu
+                                    const float sh = sA - acc[i][j];
+                                    lb = __fsub_rd(sh, bA);
+                                    ub = __fadd_ru(sh, bA);
+                                } else {                 // min form
+                                    lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
+                                    ub = __fmaf_ru(acc[i][j], p.c3, p.c4);
+                                }
                                 acc[i][j] = 0.0f;
                                 if (l < p.C && l > last) {
-                                    if (sh < b1) {
+                                    if (ub < b1) {
                                         b2 = b1;
-                                        b1 = sh;
-                                    } else if (sh < b2) {
-                                        b2 = sh;
+                                        b1 = ub;
+                                    } else if (ub < b2) {
+                                        b2 = ub;
                                     }
-                                    if (sh <= tau) {
+                                    if (lb <= tau) {
                                         const unsigned idx = atomicAdd(p.cand_n, 1u);
                                         if (idx < p.cap) {
                                             p.cand_key[idx] = ((unsigned long long)(R0 + r) << KEY_BITS) |
                                                               (unsigned long long)l;
-                                            p.cand_s[idx] = sh;
+                                            p.cand_s[idx] = lb;
                                         }
                                     }
                                 }
@@ -685,30 +744,40 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     s_out[0] = s_out[1] = INFINITY;
     if (ta >= tb) return PT_OK;
 
-    // error model of the fp16 tier:
-    //   |s_hat - s| <= eta_rel * s + eta_abs
-    //   eta_rel: fp16 rounding of each term (2^-11) + 2-level fp16 tree (2 x 2^-11)
-    //            + fp32 accumulation of E_pad/4 group sums; eta_abs: fp16 subnormals
+    // error model of the fp16 tier; per set:
+    //   min form : |s_hat - s| <= eta_rel * s + eta_abs
+    //              (fp16 terms u16, 2-level fp16 tree 2 u16, fp32 sum of E_pad/4 groups)
+    //   relu form: s_hat = sum_e a - sum_e relu(a-b): |s_hat - s| <= eta_A * sumA + eta_abs_r
+    //              (u16 quantisation + relu rounding u16 + tree 2 u16 + fp32 sums + the
+    //              final subtraction, all relative to sumA >= s)
+    // The kernel turns them into a lower bound LB <= s <= UB per set (directed rounding)
+    // and keeps every set with LB <= min(tau_seed, U), U = smallest 2nd-best UB seen.
     const double u16 = std::ldexp(1.0, -11), u32 = std::ldexp(1.0, -24);
-    // terms rounded to fp16 (u16), a 2-level fp16 tree over 4 envs (2 u16), fp32
-    // accumulation of E_pad/4 group sums
     const double ngrp = (double)v->E_pad / 4.0 + 2.0;
-    const double eta_rel = (3.0 * u16 + 3.0 * u16 * u16 + ngrp * u32 / (1.0 - ngrp * u32)) * 1.01;
-    const double eta_abs = 2.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
-    const double kap = (1.0 + eta_rel) / (1.0 - eta_rel) * (1.0 + 1e-6);
+    const double gam = ngrp * u32 / (1.0 - ngrp * u32);
+    const double gamE = ((double)v->E_pad + 2.0) * u32 / (1.0 - ((double)v->E_pad + 2.0) * u32);
+    const double eta_rel = (3.0 * u16 + 3.0 * u16 * u16 + gam) * 1.01;
+    const double eta_abs = 3.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
+    const double eta_A = (4.0 * u16 + 6.0 * u16 * u16 + gam + 2.0 * gamE + 4.0 * u32) * 1.02;
+    const double eta_abs_r = 4.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
     auto f_up = [](double x) -> float {
         if (!(x < 3.0e38)) return INFINITY;
         float f = (float)x;
         if ((double)f < x) f = nextafterf(f, INFINITY);
         return f;
     };
+    auto f_dn = [](double x) -> float {
+        float f = (float)x;
+        if ((double)f > x) f = nextafterf(f, -INFINITY);
+        return f;
+    };
     // seed: exact score of greedy's runner-up set at its last step (>= s_(2))
     std::vector<int32_t> gidx(k);
     std::vector<double> gs1(k), gs2(k);
     PT_TRY(pt_greedy_view(ctx, v, k, gidx.data(), gs1.data(), gs2.data()));
-    const float tau_seed = f_up((gs2[k - 1] * (1.0 + eta_rel) + eta_abs) * (1.0 + 1e-6));
-    const float kappa = f_up(kap);
-    const float beta = f_up(eta_abs * (kap + 1.0) * (1.0 + 1e-6));
+    const float tau_seed = f_up(gs2[k - 1] * (1.0 + 1e-9) + 1e-30);
+    const double c1d = 1.0 / (1.0 + eta_rel), c3d = 1.0 / (1.0 - eta_rel);
+    const float c1 = f_dn(c1d), c2 = f_up(eta_abs), c3 = f_up(c3d), c4 = f_up(eta_abs * c3d * (1.0 + 1e-6));
 
     if (!v->hTile) {
         pt_view *mv = const_cast<pt_view *>(v);
@@ -720,7 +789,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         PT_CK(cudaGetLastError());
     }
     const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
-                        sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
+                        sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 2 * sizeof(uint64_t) * XT_S +
+                        sizeof(int4);
     PT_CK(cudaFuncSetAttribute(k_exh_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
     unsigned cap = 1u << 20;
@@ -757,8 +827,12 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.task_hi = tb;
         p.task_ctr = ctr;
         p.tau_seed = tau_pass;
-        p.kappa = kappa;
-        p.beta = beta;
+        p.c1 = c1;
+        p.c2 = c2;
+        p.c3 = c3;
+        p.c4 = c4;
+        p.eta_A = f_up(eta_A);
+        p.eta_abs_r = f_up(eta_abs_r);
         p.U = U;
         p.cand_key = ckey;
         p.cand_s = cq;
@@ -785,7 +859,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         ctx->stats.exh_passes = pass + 1;
         float Uf;
         memcpy(&Uf, &hU, sizeof Uf);
-        const float tau_final = std::min(tau_pass, f_up((double)Uf * kap + eta_abs * (kap + 1.0)));
+        const float tau_final = std::min(tau_pass, Uf);
         if (n_cand > cap) {
             // overflow: rerun with the final threshold and room for every survivor
             cap = n_cand;
