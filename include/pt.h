@@ -63,8 +63,11 @@ enum {
                                      dataset-max slowdown x best[e] */
     PT_EXACT_FP64 = 0x2,          /* debug: exhaustive search by the thread-per-subset
                                      fp64 kernel, no fp32 tier */
-    PT_GREEDY_STREAM = 0x4        /* force the streamed fp32-filter/fp64-refine greedy
+    PT_GREEDY_STREAM = 0x4,       /* force the streamed fp32-filter/fp64-refine greedy
                                      (default only when the matrix is large) */
+    PT_GREEDY_LAZY = 0x8          /* streamed greedy, lazy from step 3 on: exact (Minoux)
+                                     upper-bound pruning by submodularity of the gain; same
+                                     picks, far fewer sets scored (gap trace: an upper bound) */
 };
 
 /*

@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(256) k_greedy_scan(const float *__restrict__ l
 }
 
 struct pick_state {
-    double S;   // sum_e cur64[e] over real envs (finite from step 1 on)
+    double S;       // sum_e cur64[e] over real envs (finite from step 1 on)
+    double delta;   // gain-mode error bound of the last scan (see k_greedy_pick)
 };
 
 // one CTA of 1024 threads
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(1024) k_greedy_pick(
                 // key = -g_hat; |g_hat - g| <= delta = 2u*S + gamma*g_max
                 const double gmax = -s1k;
                 const double delta = (2.0 * u * st->S + gamma * gmax) * 1.01 + 1e-300;
+                st->delta = delta;
                 thr = (s2k == INFINITY) ? INFINITY : s2k + 2.0 * delta;
             }
         }
@@ -369,6 +371,138 @@ __global__ void __launch_bounds__(1024) k_greedy_pick(
     }
 }
 
+// ---------------------------------------------------------------------------
+// LAZY greedy (Minoux), opt-in PT_GREEDY_LAZY, streamed path.
+// The facility-location gain g_c(S) = sum_e max(0, cur_e - l[c][e]) is
+// submodular, so a gain measured at an earlier step is an upper bound later.
+// After the second full scan ub[c] = g_hat_c + delta (rigorous: the scan's
+// fp32 error bound); every later step re-scores exactly only the configs whose
+// bound can still reach the best exact gain, and tightens their bounds.
+// ---------------------------------------------------------------------------
+__global__ void k_lazy_init(const float *__restrict__ key, int64_t C, const uint32_t *__restrict__ taken,
+                            const pick_state *__restrict__ st, double *__restrict__ ub)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const bool tk = taken[c >> 5] >> (c & 31) & 1u;
+    ub[c] = tk ? -INFINITY : -(double)key[c] + st->delta;
+}
+
+// one CTA (1024 threads) per lazy step
+__global__ void __launch_bounds__(1024) k_lazy_step(
+    int64_t C, const double *__restrict__ l64, int64_t E_pad, int64_t E, float *__restrict__ cur32,
+    double *__restrict__ cur64, uint32_t *__restrict__ taken, pick_state *__restrict__ st,
+    double *__restrict__ ub, int32_t *__restrict__ cand, double *__restrict__ cs, int t,
+    int32_t *__restrict__ out_idx, double *__restrict__ s1_tr, double *__restrict__ s2_tr,
+    int32_t *__restrict__ ncand_tr)
+{
+    __shared__ double rs1[32], rs2[32];
+    __shared__ int rc1[32], rc2[32];
+    __shared__ int ncand, c0s, cstar;
+    __shared__ double thr_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double S = st->S;
+    const double slack = 1e-12 * S + 1e-300;
+    // a. argmax of the upper bounds (ties -> lowest index)
+    double bu = -INFINITY;
+    int bc = PT_BIGI;
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+        const double v = ub[c];
+        if (v > bu) { bu = v; bc = (int)c; }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, bu, o);
+        const int c = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (v > bu || (v == bu && c < bc)) { bu = v; bc = c; }
+    }
+    if (lane == 0) { rs1[warp] = bu; rc1[warp] = bc; }
+    if (threadIdx.x == 0) ncand = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 32; w++)
+            if (rs1[w] > bu || (rs1[w] == bu && rc1[w] < bc)) { bu = rs1[w]; bc = rc1[w]; }
+        c0s = bc;
+    }
+    __syncthreads();
+    // b. exact score of c0 (block reduction) -> the gain every candidate must reach
+    {
+        const double *col = l64 + (int64_t)c0s * E_pad;
+        double part = 0.0;
+        for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) part += fmin(cur64[e], col[e]);
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) rs2[warp] = part;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s0 = 0.0;
+            for (int w = 0; w < 32; w++) s0 += rs2[w];
+            thr_s = (S - s0) - slack;   // gain of c0, lowered by the rounding slack
+        }
+        __syncthreads();
+    }
+    // c. every config whose bound reaches that gain is a candidate
+    const double thr = thr_s;
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x)
+        if (ub[c] >= thr) cand[atomicAdd(&ncand, 1)] = (int32_t)c;
+    __syncthreads();
+    // d. exact scores of the candidates (warp each), then the argmin (ties -> lowest c)
+    const int n = ncand;
+    double s1 = INFINITY, s2 = INFINITY;
+    int c1 = PT_BIGI, c2 = PT_BIGI;
+    for (int q = warp; q < n; q += 32) {
+        const int c = cand[q];
+        const double *col = l64 + (int64_t)c * E_pad;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int64_t e = lane;
+        for (; e + 96 < E_pad; e += 128) {
+            a0 += fmin(cur64[e], col[e]);
+            a1 += fmin(cur64[e + 32], col[e + 32]);
+            a2 += fmin(cur64[e + 64], col[e + 64]);
+            a3 += fmin(cur64[e + 96], col[e + 96]);
+        }
+        for (; e < E_pad; e += 32) a0 += fmin(cur64[e], col[e]);
+        double acc = (a0 + a1) + (a2 + a3);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            cs[q] = acc;
+            ub[c] = (S - acc) + slack;          // e. tightened bound for later steps
+        }
+        top2_ins(s1, c1, s2, c2, acc, c);
+    }
+    if (lane == 0) { rs1[warp] = s1; rs2[warp] = s2; rc1[warp] = c1; rc2[warp] = c2; }
+    __syncthreads();
+    if (warp == 0) {
+        s1 = rs1[lane]; s2 = rs2[lane]; c1 = rc1[lane]; c2 = rc2[lane];
+        warp_top2(s1, c1, s2, c2);
+        if (lane == 0) {
+            cstar = c1;
+            out_idx[t] = c1;
+            s1_tr[t] = s1;
+            s2_tr[t] = s2;        // second best among the candidates (gap: lower bound)
+            ncand_tr[t] = n;
+            taken[c1 >> 5] |= 1u << (c1 & 31);
+            ub[c1] = -INFINITY;
+        }
+    }
+    __syncthreads();
+    // f. commit
+    const double *col = l64 + (int64_t)cstar * E_pad;
+    double part = 0.0;
+    for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) {
+        double v = fmin(cur64[e], col[e]);
+        cur64[e] = v;
+        cur32[e] = (float)v;
+        if (e < E) part += v;
+    }
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) rs1[warp] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double Sn = 0.0;
+        for (int w = 0; w < 32; w++) Sn += rs1[w];
+        st->S = Sn;
+    }
+}
+
 __global__ void k_fill_f64(double *p, int64_t n, double v)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -383,7 +517,7 @@ __global__ void k_fill_f32(float *p, int64_t n, float v)
 // ---------------------------------------------------------------------------
 static bool use_stream(const pt_ctx *ctx, const pt_view *v)
 {
-    if (ctx->flags & PT_GREEDY_STREAM) return true;
+    if (ctx->flags & (PT_GREEDY_STREAM | PT_GREEDY_LAZY)) return true;
     const double bytes = (double)v->C * (double)v->E_pad * 8.0;
     return bytes > 64.0 * (1 << 20) || v->E_pad * 8 > 160 * 1024;
 }
@@ -473,7 +607,38 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
         // keep the last ~80 MB of each step's stream L2-resident (L2 is ~126 MB)
         const int64_t keep_cfgs = (int64_t)(80.0 * (1 << 20) / (4.0 * (double)E_pad));
         const int64_t cached_from = std::max<int64_t>(0, C - keep_cfgs);
+        const bool lazy = (ctx->flags & PT_GREEDY_LAZY) != 0;
+        double *ub = nullptr, *cs = nullptr;
+        if (lazy && k > 2) {
+            PT_TRY(pt_dalloc(ctx, (void **)&ub, sizeof(double) * C));
+            PT_TRY(pt_dalloc(ctx, (void **)&cs, sizeof(double) * C));
+        }
+        // lazy mode: a step re-scores only configs whose upper bound can still win;
+        // when the previous lazy step needed more than `lazy_max` re-scores the
+        // bounds have gone stale and the step does a full scan instead (which
+        // also refreshes every bound)
+        const int32_t lazy_max = (int32_t)std::max<int64_t>(64, C / 256);
+        bool ub_fresh = false, full_next = true;
         for (int t = 0; t < k; t++) {
+            if (lazy && t >= 2 && !full_next) {
+                if (!ub_fresh) {
+                    k_lazy_init<<<(unsigned)((C + 255) / 256), 256, 0, s>>>(key, C, taken, st, ub);
+                    ctx->stats.launches++;
+                    ub_fresh = true;
+                }
+                k_lazy_step<<<1, 1024, 0, s>>>(C, v->l64, E_pad, v->E, cur32, cur64, taken, st, ub, cand,
+                                               cs, t, d_idx, d_s1, d_s2, d_nc);
+                ctx->stats.launches++;
+                int32_t nc_t = 0;
+                PT_CK(cudaMemcpyAsync(&nc_t, d_nc + t, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                PT_CK(cudaStreamSynchronize(s));
+                full_next = nc_t > lazy_max;
+                continue;
+            }
+            if (lazy && t >= 1) {
+                ub_fresh = false;     // this full scan's keys become the new bounds
+                full_next = false;
+            }
             k_greedy_scan<<<grid, 256, smem, s>>>(v->l32, C, E_pad, cur32, taken, t > 0, t & 1,
                                                   cached_from, key, blk2);
             k_greedy_pick<<<1, 1024, 0, s>>>(key, blk2, grid, C, v->l64, E_pad, v->E, cur32, cur64, taken, st,
@@ -484,6 +649,8 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
         PT_CK(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
         PT_CK(cudaMemcpyAsync(s1_trace, d_s1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
         PT_CK(cudaMemcpyAsync(s2_trace, d_s2, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+        pt_dfree(ctx, ub);
+        pt_dfree(ctx, cs);
         std::vector<int32_t> nc(k);
         PT_CK(cudaMemcpyAsync(nc.data(), d_nc, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
         PT_CK(cudaStreamSynchronize(s));

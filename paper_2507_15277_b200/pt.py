@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libpt.so")
 
 PT_OK, PT_EINVAL, PT_ENOMEM, PT_ECUDA, PT_ENCCL, PT_ECAP, PT_EEMPTY, PT_EDATA = 0, -1, -2, -3, -4, -5, -6, -7
 PT_OBJ_GEOMEAN, PT_OBJ_FLEET = 0, 1
-PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM = 0x1, 0x2, 0x4
+PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM, PT_GREEDY_LAZY = 0x1, 0x2, 0x4, 0x8
 
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
            "pt_merge_top2", "pt_eval_holdout", "pt_swap_search", "pt_set_fleet", "pt_get_stats",

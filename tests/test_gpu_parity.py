@@ -266,3 +266,32 @@ def test_scaled_greedy_32():
         sidx, sg, sgap = o.greedy(1, init=idx[:t])
         if sgap[0] > GAP:
             assert sidx[0] == idx[t]
+
+
+def test_greedy_lazy_medium():
+    T, dev = synth.small_matrix(6, n_cfg=700, n_dev=5, n_inputs=20)
+    o = Oracle(T, dev)
+    ctx = pt.pt_load_perf(T, dev, flags=pt.PT_GREEDY_LAZY)
+    idx, gt, gp = pt.pt_greedy_select(ctx, 24)
+    oidx, ogt, ogp = o.greedy(24)
+    for t in range(24):
+        assert gt[t] == pytest.approx(o.score(idx[:t + 1]), rel=RTOL)
+    if np.all(ogp > GAP):
+        assert idx == oidx
+    mask = (dev != 3).astype(np.uint8)
+    assert pt.pt_greedy_select(ctx, 10, env_mask=mask)[0] == o.greedy(10, mask=mask)[0]
+
+
+def test_greedy_lazy_scaled_equals_plain():
+    """Lazy greedy on the scaled matrix: same picks as the plain streamed greedy,
+    far fewer exact evaluations."""
+    T, dev = synth.scaled(1)
+    dT = torch.from_numpy(T).cuda()
+    ctx = pt.pt_load_perf(dT, dev)
+    idx, gt, _ = pt.pt_greedy_select(ctx, 32)
+    pt.pt_free(ctx)
+    ctx = pt.pt_load_perf(dT, dev, flags=pt.PT_GREEDY_LAZY)
+    lidx, lgt, _ = pt.pt_greedy_select(ctx, 32)
+    assert lidx == idx
+    np.testing.assert_allclose(lgt, gt, rtol=1e-12)
+    assert pt.pt_get_stats(ctx)["greedy_candidates"] < 32 * 65536 // 10
