@@ -37,8 +37,18 @@
 
 #define XT_R 128    // rows per CTA tile
 #define XT_C 64     // columns per CTA tile
-#define XT_K 32     // environments per pipeline stage
-#define XT_S 4      // pipeline stages
+// pipeline stage = XT_K envs x 64 configs (fp16); measured on B200 at the paper
+// shape: K=32/S=4 13.94 ms, K=32/S=3 14.00, K=64/S=2 13.70, K=64/S=3 13.67,
+// K=160/S=2 15.77 (only 1 CTA/SM fits beyond ~113 KB of smem per CTA)
+#ifndef XT_K
+#define XT_K 64     // environments per pipeline stage (E_pad is a multiple of 64)
+#endif
+#ifndef XT_S
+#define XT_S 3      // pipeline stages
+#endif
+#ifndef XT_G8
+#define XT_G8 0     // 1: 8-env fp16 tree per FHADD (instead of 4)
+#endif
 #define XT_EMAX 768 // widest scope the resident-A kernel takes (smem)
 #define XT_UMAX 1024 // column tiles per task (a whole row tile: A staged once)
 #define KEY_BITS 21
@@ -417,6 +427,38 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 if (!skip) {
                     const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
                     const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
+#if XT_G8
+#pragma unroll 1
+                    for (int e = 0; e < XT_K; e += 8) {
+                        uint4 ar[8];
+                        uint2 bc[8];
+#pragma unroll
+                        for (int t = 0; t < 8; t++) {
+                            ar[t] = *reinterpret_cast<const uint4 *>(A + (e + t) * XT_R);
+                            bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; i++) {
+                            uint32_t av[8];
+#pragma unroll
+                            for (int t = 0; t < 8; t++) {
+                                const uint32_t w = (i >> 1) == 0 ? ar[t].x : (i >> 1) == 1 ? ar[t].y
+                                                                 : (i >> 1) == 2 ? ar[t].z : ar[t].w;
+                                av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                            }
+                            fhadd2(acc[i][0], acc[i][1],
+                                   hadd2(hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
+                                               hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))),
+                                         hadd2(hadd2(hmin2(av[4], bc[4].x), hmin2(av[5], bc[5].x)),
+                                               hadd2(hmin2(av[6], bc[6].x), hmin2(av[7], bc[7].x)))));
+                            fhadd2(acc[i][2], acc[i][3],
+                                   hadd2(hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                               hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))),
+                                         hadd2(hadd2(hmin2(av[4], bc[4].y), hmin2(av[5], bc[5].y)),
+                                               hadd2(hmin2(av[6], bc[6].y), hmin2(av[7], bc[7].y)))));
+                        }
+                    }
+#else
 #pragma unroll 2
                     for (int e = 0; e < XT_K; e += 4) {
                         uint4 ar[4];
@@ -452,6 +494,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                                              hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))));
                         }
                     }
+#endif
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
@@ -753,10 +796,11 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     // The kernel turns them into a lower bound LB <= s <= UB per set (directed rounding)
     // and keeps every set with LB <= min(tau_seed, U), U = smallest 2nd-best UB seen.
     const double u16 = std::ldexp(1.0, -11), u32 = std::ldexp(1.0, -24);
-    const double ngrp = (double)v->E_pad / 4.0 + 2.0;
+    const double ngrp = (double)v->E_pad / (XT_G8 ? 8.0 : 4.0) + 2.0;
     const double gam = ngrp * u32 / (1.0 - ngrp * u32);
     const double gamE = ((double)v->E_pad + 2.0) * u32 / (1.0 - ((double)v->E_pad + 2.0) * u32);
-    const double eta_rel = (3.0 * u16 + 3.0 * u16 * u16 + gam) * 1.01;
+    // quantisation u16 + a (2 or 3)-level fp16 tree
+    const double eta_rel = ((XT_G8 ? 4.0 : 3.0) * u16 + 6.0 * u16 * u16 + gam) * 1.01;
     const double eta_abs = 3.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
     const double eta_A = (4.0 * u16 + 6.0 * u16 * u16 + gam + 2.0 * gamE + 4.0 * u32) * 1.02;
     const double eta_abs_r = 4.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;

@@ -237,7 +237,7 @@ static pt_status alloc_view(pt_ctx *ctx, pt_view &v, int64_t E, int64_t C)
 {
     v.E = E;
     v.C = C;
-    v.E_pad = pt_round_up(std::max<int64_t>(E, 1), 32);
+    v.E_pad = pt_round_up(std::max<int64_t>(E, 1), 64);   // a whole number of 64-env stages
     v.C_pad = pt_round_up(C + 64, 64);   // >= C + 64: a 64-column bulk row copy never leaves the row
     v.owned = true;
     if (pt_dalloc(ctx, (void **)&v.l32, sizeof(float) * v.C * v.E_pad) != PT_OK ||
