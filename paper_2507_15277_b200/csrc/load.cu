@@ -241,8 +241,7 @@ static pt_status alloc_view(pt_ctx *ctx, pt_view &v, int64_t E, int64_t C)
     v.C_pad = pt_round_up(C + 64, 64);   // >= C + 64: a 64-column bulk row copy never leaves the row
     v.owned = true;
     if (pt_dalloc(ctx, (void **)&v.l32, sizeof(float) * v.C * v.E_pad) != PT_OK ||
-        pt_dalloc(ctx, (void **)&v.l64, sizeof(double) * v.C * v.E_pad) != PT_OK ||
-        pt_dalloc(ctx, (void **)&v.hT, sizeof(uint16_t) * v.E_pad * v.C_pad) != PT_OK) {
+        pt_dalloc(ctx, (void **)&v.l64, sizeof(double) * v.C * v.E_pad) != PT_OK) {
         pt_view_free(ctx, v);
         return pt_fail(PT_ENOMEM, "device allocation for a %lld x %lld view failed",
                        (long long)E, (long long)C);
@@ -250,9 +249,13 @@ static pt_status alloc_view(pt_ctx *ctx, pt_view &v, int64_t E, int64_t C)
     return PT_OK;
 }
 
-// fp16 tier of a view (env-major copy of l64 rounded to nearest fp16)
-static pt_status quantize_view(pt_ctx *ctx, pt_view &v)
+// fp16 tier of a view (env-major copy of l64 rounded to nearest fp16), built on
+// the first exhaustive search that needs it
+pt_status pt_view_fp16(pt_ctx *ctx, const pt_view *cv)
 {
+    pt_view &v = *const_cast<pt_view *>(cv);
+    if (v.hT) return PT_OK;
+    PT_TRY(pt_dalloc(ctx, (void **)&v.hT, sizeof(uint16_t) * v.E_pad * v.C_pad));
     PT_CK(cudaMemsetAsync(v.hT, 0, sizeof(uint16_t) * v.E_pad * v.C_pad, ctx->stream));
     dim3 grid((unsigned)((v.C + 31) / 32), (unsigned)((v.E_pad + 31) / 32));
     k_half<<<grid, dim3(32, 8), 0, ctx->stream>>>(v.l64, v.E, v.C, v.E_pad, v.C_pad, v.hT);
@@ -308,7 +311,6 @@ pt_status pt_get_view(pt_ctx *ctx, const uint8_t *env_mask, const pt_view **out)
     ctx->stats.launches += 1;
     PT_CK(cudaGetLastError());
     pt_dfree(ctx, d_idx);
-    PT_TRY(quantize_view(ctx, s));
     slot->mask.assign(env_mask, env_mask + ctx->E);
     slot->last_use = ctx->tick;
     *out = &s;
@@ -409,11 +411,6 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
     dim3 grid((unsigned)((C + 31) / 32), (unsigned)((v.E_pad + 31) / 32));
     k_ell<<<grid, dim3(32, 8), 0, ctx->stream>>>(dT, E, C, ctx->best, pen, v.E_pad, v.l32, v.l64);
     ctx->stats.launches++;
-    st = quantize_view(ctx, v);
-    if (st != PT_OK) {
-        cleanup();
-        return bail(st);
-    }
     // keep the runtimes (env-major fp32) for objectives on raw times (Eq. 2)
     ctx->T32 = dT;
     pt_dfree(ctx, rowmax);

@@ -105,6 +105,8 @@ pt_status pt_scratch(pt_ctx *ctx, size_t bytes, void **p);
 // resolve a mask into a view (NULL -> full); E_scope returned in view->E
 pt_status pt_get_view(pt_ctx *ctx, const uint8_t *env_mask, const pt_view **out);
 void pt_view_free(pt_ctx *ctx, pt_view &v);
+// build the view's fp16 tier (hT) if it does not exist yet
+pt_status pt_view_fp16(pt_ctx *ctx, const pt_view *v);
 // true if p is device (or managed) memory
 bool pt_is_device_ptr(const void *p);
 
