@@ -8,10 +8,10 @@ of the whole hot path over that matrix:
   + pt_greedy_select k=24                     (42,324 sets)
   + pt_exhaustive_best k=2                    (1,574,425 sets)
   + pt_exhaustive_best k=3                    (930,485,175 sets)
-  + pt_eval_holdout, 5 folds, greedy k=5      (88,655 sets)
+  + pt_eval_holdout_all, 5 folds, greedy k=5  (88,655 sets)
 With N GPUs the exhaustive searches are sharded across ranks and merged with an
 NCCL all-gather of the (score, tuple) records (strong scaling: the job is fixed);
-greedy and load run on every rank; holdout folds are dealt round-robin.
+load, greedy and the (batched, one-launch) holdout run on every rank.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {pt,reference}]
 """
@@ -230,7 +230,6 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     flush.fill_(0)                     # load the fill kernel's module before any timing
     torch.cuda.synchronize()
-    folds = [d for d in range(5) if d % world == rank]
 
     def step(src):
         """One pass of the whole hot path; returns (results, d2h bytes)."""
@@ -242,7 +241,7 @@ def main():
         r3 = pt.exhaustive_best_distributed(ctx, 3) if world > 1 else pt.pt_exhaustive_best(ctx, 3)
         st3 = pt.pt_get_stats(ctx)
         d2h += 2 * (2 * 3 * 4 + 4 * 8)
-        hold = [pt.pt_eval_holdout(ctx, d, K_HOLDOUT, 0) for d in folds]
+        hold = pt.pt_eval_holdout_all(ctx, K_HOLDOUT, 5)      # all 5 folds, one batched launch
         d2h += len(hold) * (2 * K_HOLDOUT * 4 + 3 * 8)
         st_end = pt.pt_get_stats(ctx)
         pt.pt_free(ctx)

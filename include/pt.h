@@ -171,6 +171,17 @@ pt_status pt_eval_holdout(pt_ctx *ctx, int32_t heldout_device, int32_t k, int32_
                           double *out_G_known, int32_t *out_known_idx);
 
 /*
+ * pt_eval_holdout_all -- pt_eval_holdout (method 0, greedy) for every device
+ * d = 0..D-1 at once (D = 1 + the largest env_device id), computed in one
+ * batched launch.  Outputs are [D][k] / [D] host arrays in the same meaning as
+ * pt_eval_holdout; *out_n_device (host, or NULL) receives D.
+ * Errors: as pt_eval_holdout; PT_EEMPTY if some device has no environment.
+ */
+pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t *out_idx, double *out_G_train,
+                              double *out_G_unseen, double *out_G_known, int32_t *out_known_idx,
+                              int32_t *out_n_device);
+
+/*
  * pt_swap_search -- deterministic best-improvement swap local search over
  * k-sets (the stand-in for the paper's heuristic search over variant
  * combinations, Sec. 4.3.1).  From `init` (host

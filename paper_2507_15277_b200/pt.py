@@ -24,7 +24,7 @@ PT_OBJ_GEOMEAN, PT_OBJ_FLEET = 0, 1
 PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM, PT_GREEDY_LAZY = 0x1, 0x2, 0x4, 0x8
 
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
-           "pt_merge_top2", "pt_eval_holdout", "pt_swap_search", "pt_set_fleet", "pt_get_stats",
+           "pt_merge_top2", "pt_eval_holdout", "pt_eval_holdout_all", "pt_swap_search", "pt_set_fleet", "pt_get_stats",
            "pt_free", "pt_last_error")
 
 
@@ -62,13 +62,14 @@ def lib():
         L.pt_get_stats.argtypes = [P, ct.POINTER(pt_stats)]
         L.pt_set_fleet.argtypes = [P, P, i32, P]
         L.pt_swap_search.argtypes = [P, i32, P, i32, i32, P, P, P, P]
+        L.pt_eval_holdout_all.argtypes = [P, i32, P, P, P, P, P, P]
         L.pt_free.argtypes = [P]
         L.pt_free.restype = None
         L.pt_last_error.argtypes = []
         L.pt_last_error.restype = ct.c_char_p
         for f in ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
                   "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_set_fleet",
-                  "pt_swap_search"):
+                  "pt_swap_search", "pt_eval_holdout_all"):
             getattr(L, f).restype = ct.c_int
         _lib = L
     return _lib
@@ -225,6 +226,21 @@ def pt_eval_holdout(ctx, heldout_device, k, method=0):
                                _ptr(g[1:2]), _ptr(g[2:3]), _ptr(kidx)), "pt_eval_holdout")
     return {"idx": [int(x) for x in idx], "G_train": float(g[0]), "G_unseen": float(g[1]),
             "G_known": float(g[2]), "known_idx": [int(x) for x in kidx]}
+
+
+def pt_eval_holdout_all(ctx, k, n_device):
+    """All leave-one-device-out folds (greedy) in one batched call: list of dicts like
+    pt_eval_holdout, one per device id 0..n_device-1."""
+    D = n_device
+    idx = np.zeros((D, k), np.int32)
+    kidx = np.zeros((D, k), np.int32)
+    gtr, gun, gkn = np.zeros(D), np.zeros(D), np.zeros(D)
+    nd = np.zeros(1, np.int32)
+    _chk(lib().pt_eval_holdout_all(ctx.handle, k, _ptr(idx), _ptr(gtr), _ptr(gun), _ptr(gkn),
+                                   _ptr(kidx), _ptr(nd)), "pt_eval_holdout_all")
+    assert int(nd[0]) == D, (int(nd[0]), D)
+    return [{"idx": [int(x) for x in idx[d]], "G_train": float(gtr[d]), "G_unseen": float(gun[d]),
+             "G_known": float(gkn[d]), "known_idx": [int(x) for x in kidx[d]]} for d in range(D)]
 
 
 def pt_get_stats(ctx):

@@ -295,3 +295,15 @@ def test_greedy_lazy_scaled_equals_plain():
     assert lidx == idx
     np.testing.assert_allclose(lgt, gt, rtol=1e-12)
     assert pt.pt_get_stats(ctx)["greedy_candidates"] < 32 * 65536 // 10
+
+
+def test_holdout_all_batched(paper1):
+    T, dev, o = paper1
+    ctx = pt.pt_load_perf(T, dev)
+    res = pt.pt_eval_holdout_all(ctx, 5, 5)
+    for d in range(5):
+        h = pt.pt_eval_holdout(ctx, d, 5, 0)
+        idx, gtr, gun, gkn, kidx = o.holdout(d, 5, method=0)
+        assert res[d]["idx"] == idx == h["idx"] and res[d]["known_idx"] == kidx
+        for key, want in (("G_train", gtr), ("G_unseen", gun), ("G_known", gkn)):
+            assert res[d][key] == pytest.approx(want, rel=RTOL)
