@@ -198,6 +198,22 @@ pt_status pt_swap_search(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_
                          int32_t *out_moves);
 
 /*
+ * pt_kmeans_select -- the paper's k-means selector (Sec. 4.3.2):
+ * environments in scope are points of their slowdowns T/best over all
+ * configurations; k centroids by Lloyd iterations from a deterministic maximin
+ * initialisation (the point nearest the mean, then successive farthest points);
+ * an emptied cluster is re-seeded with the point farthest from its centroid;
+ * stops when no assignment changes or after max_iter passes.  Per centroid the
+ * configuration with the smallest centroid slowdown is selected;
+ * duplicates collapse.  fp64 in a fixed order (bit-identical to the oracle).
+ *   out_idx host int32[k]: the selection ascending, *out_n (<= k) entries;
+ *   out_G   host or NULL: its Eq. 1 G on the scope; out_iters host or NULL.
+ * Errors: PT_EINVAL (k < 1, k > 32, k > #envs in scope), PT_EEMPTY.
+ */
+pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t max_iter,
+                           int32_t *out_idx, int32_t *out_n, double *out_G, int32_t *out_iters);
+
+/*
  * pt_set_fleet -- quantities for the fleet objective, Eq. 2:
  *   R(S) = sum_d quantity(d) / sum_{i} y'_{d,i}(S) * quantity(i),
  *   y'_{d,i}(S) = min_{c in S} T[(d,i)][c]  (best member; a missing cell costs

@@ -24,7 +24,8 @@ PT_OBJ_GEOMEAN, PT_OBJ_FLEET = 0, 1
 PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM, PT_GREEDY_LAZY = 0x1, 0x2, 0x4, 0x8
 
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
-           "pt_merge_top2", "pt_eval_holdout", "pt_eval_holdout_all", "pt_swap_search", "pt_set_fleet", "pt_get_stats",
+           "pt_merge_top2", "pt_eval_holdout", "pt_eval_holdout_all", "pt_swap_search",
+           "pt_kmeans_select", "pt_set_fleet", "pt_get_stats",
            "pt_free", "pt_last_error")
 
 
@@ -63,13 +64,14 @@ def lib():
         L.pt_set_fleet.argtypes = [P, P, i32, P]
         L.pt_swap_search.argtypes = [P, i32, P, i32, i32, P, P, P, P]
         L.pt_eval_holdout_all.argtypes = [P, i32, P, P, P, P, P, P]
+        L.pt_kmeans_select.argtypes = [P, i32, P, i32, P, P, P, P]
         L.pt_free.argtypes = [P]
         L.pt_free.restype = None
         L.pt_last_error.argtypes = []
         L.pt_last_error.restype = ct.c_char_p
         for f in ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
                   "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_set_fleet",
-                  "pt_swap_search", "pt_eval_holdout_all"):
+                  "pt_swap_search", "pt_eval_holdout_all", "pt_kmeans_select"):
             getattr(L, f).restype = ct.c_int
         _lib = L
     return _lib
@@ -202,6 +204,17 @@ def pt_swap_search(ctx, k, env_mask=None, init=None, max_moves=1000):
     _chk(lib().pt_swap_search(ctx.handle, k, _ptr(_mask(env_mask)), PT_OBJ_GEOMEAN, max_moves,
                               _ptr(ini), _ptr(out), _ptr(g), _ptr(mv)), "pt_swap_search")
     return tuple(int(x) for x in out), float(g[0]), int(mv[0])
+
+
+def pt_kmeans_select(ctx, k, env_mask=None, max_iter=100):
+    """k-means selector (Sec. 4.3.2): (sorted unique selection, G, iterations)."""
+    out = np.zeros(k, np.int32)
+    n = np.zeros(1, np.int32)
+    g = np.zeros(1)
+    it = np.zeros(1, np.int32)
+    _chk(lib().pt_kmeans_select(ctx.handle, k, _ptr(_mask(env_mask)), max_iter, _ptr(out), _ptr(n),
+                                _ptr(g), _ptr(it)), "pt_kmeans_select")
+    return tuple(int(x) for x in out[:n[0]]), float(g[0]), int(it[0])
 
 
 def pt_merge_top2(s, tuples, k):

@@ -1,0 +1,52 @@
+"""GPU parity for the k-means selector: the whole Lloyd
+trajectory is computed in the same order without FMA contraction, so the
+selection AND the iteration count must equal the oracle's exactly."""
+import numpy as np
+import pytest
+
+from conftest import read_golden
+from oracle import Oracle
+from paper_2507_15277_b200 import pt, synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_hand_fixture():
+    g = read_golden("kmeans_hand.txt")
+    T = np.array([[float(x) for x in r[1:]] for r in g if r[0] == "t"], np.float32)
+    ctx = pt.pt_load_perf(T)
+    sel, G, it = pt.pt_kmeans_select(ctx, 2)
+    row = next(r for r in g if r[0] == "select")
+    assert sel == tuple(int(x) for x in row[1].split(",")) and it == int(row[3])
+
+
+@pytest.mark.parametrize("seed,C,nd,ni", [(1, 60, 3, 6), (2, 300, 4, 12), (3, 130, 2, 40)])
+def test_random(seed, C, nd, ni):
+    T, dev = synth.small_matrix(seed, n_cfg=C, n_dev=nd, n_inputs=ni)
+    T[1, 3] = np.nan
+    o = Oracle(T, dev)
+    ctx = pt.pt_load_perf(T, dev)
+    for k in (1, 2, 5, 9):
+        sel, G, it = pt.pt_kmeans_select(ctx, k)
+        osel, oit, _ = o.kmeans(k)
+        assert sel == osel and it == oit
+        assert G == pytest.approx(o.score(list(sel)), rel=1e-12)
+    mask = (dev != 0).astype(np.uint8)
+    assert pt.pt_kmeans_select(ctx, 4, env_mask=mask)[0] == o.kmeans(4, mask=mask)[0]
+
+
+def test_paper_shape():
+    T, dev = synth.paper_matrix(1)
+    o = Oracle(T, dev)
+    ctx = pt.pt_load_perf(T, dev)
+    for k in (3, 10, 24):
+        sel, G, it = pt.pt_kmeans_select(ctx, k)
+        osel, oit, _ = o.kmeans(k)
+        assert sel == osel and it == oit
