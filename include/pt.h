@@ -142,6 +142,24 @@ pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, in
                              int32_t *out_runner_idx, double *out_G_runner, double *out_s);
 
 /*
+ * pt_greedy_sharded -- the greedy selection with the configurations sharded
+ * across ranks: rank shard_rank streams only its
+ * contiguous 1/shard_count of the configurations each step, finds its exact
+ * local top-2 (s, config), and the ranks exchange those records through
+ * `allgather` (the caller's collective, e.g. NCCL via torch.distributed); every
+ * rank merges them identically (s asc, config asc) and commits the winner from
+ * its own copy of the matrix.  Result identical to pt_greedy_select on every rank.
+ *   allgather(user, mine, n, all): gather n doubles from every rank into
+ *     all[rank * n ...] (rank order); return 0 on success.  Called k times, on
+ *     the calling thread.
+ * Errors: as pt_greedy_select; PT_ENCCL if the callback fails.
+ */
+typedef int (*pt_allgather_fn)(void *user, const double *mine, int32_t n, double *all);
+pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
+                            int32_t shard_count, pt_allgather_fn allgather, void *user,
+                            int32_t *out_idx, double *out_G_trace, double *out_gap_trace);
+
+/*
  * pt_merge_top2 -- host-only: merge n_rec (s, sorted k-tuple) records (e.g.
  * gathered from every shard/rank) into the best two in (s asc, tuple asc)
  * order.  s = +inf marks an absent record.

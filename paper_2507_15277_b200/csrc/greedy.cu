@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(256) k_greedy_scan(const float *__restrict__ l
                                                       const float *__restrict__ cur32,
                                                       const uint32_t *__restrict__ taken,
                                                       int gain_mode, int reverse,
-                                                      int64_t cached_from,
-                                                      float *__restrict__ key,
+                                                      int64_t cached_from, int64_t c_lo,
+                                                      int64_t c_hi, float *__restrict__ key,
                                                       float2 *__restrict__ blk2)
 {
     extern __shared__ float cur_s[];
@@ -157,8 +157,9 @@ __global__ void __launch_bounds__(256) k_greedy_scan(const float *__restrict__ l
     const int64_t nq = E_pad >> 2;
     const float4 *cur4 = reinterpret_cast<const float4 *>(cur_s);
     float k1 = INFINITY, k2 = INFINITY;
-    for (int64_t cc = gw; cc < C; cc += nw) {
-        const int64_t c = reverse ? C - 1 - cc : cc;
+    const int64_t ns = c_hi - c_lo;   // this shard's configs [c_lo, c_hi)
+    for (int64_t cc = gw; cc < ns; cc += nw) {
+        const int64_t c = c_lo + (reverse ? ns - 1 - cc : cc);
         const float4 *col = reinterpret_cast<const float4 *>(l32 + c * E_pad);
         // the tail of this step's stream stays in L2 (normal loads) for the next,
         // reversed, step; the rest streams with evict-first loads
@@ -231,7 +232,8 @@ __global__ void __launch_bounds__(1024) k_greedy_pick(
     int64_t E, float *__restrict__ cur32, double *__restrict__ cur64,
     uint32_t *__restrict__ taken, pick_state *__restrict__ st, int t, int gain_mode,
     double gamma, int32_t *__restrict__ cand, int32_t *__restrict__ out_idx,
-    double *__restrict__ s1_tr, double *__restrict__ s2_tr, int32_t *__restrict__ ncand_tr)
+    double *__restrict__ s1_tr, double *__restrict__ s2_tr, int32_t *__restrict__ ncand_tr,
+    int64_t c_lo, int64_t c_hi, double4 *__restrict__ local_rec)
 {
     __shared__ double rs1[32], rs2[32];
     __shared__ int ncand;
@@ -300,9 +302,10 @@ __global__ void __launch_bounds__(1024) k_greedy_pick(
     __syncthreads();
     // 2. collect candidates (float4 sweep of the keys)
     const double th = thr;
-    const int64_t C4 = C >> 2;
+    // (shard [c_lo, c_hi): c_lo is a multiple of 4 -- see pt_greedy_sharded)
+    const int64_t C4 = c_lo / 4 + ((c_hi - c_lo) >> 2);
     const float4 *key4 = reinterpret_cast<const float4 *>(key);
-    for (int64_t q0 = 0; q0 < C4; q0 += 8 * (int64_t)blockDim.x) {
+    for (int64_t q0 = c_lo / 4; q0 < C4; q0 += 8 * (int64_t)blockDim.x) {
         float4 kv[8];   // 8 independent loads in flight per thread
 #pragma unroll
         for (int r = 0; r < 8; r++) {
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(1024) k_greedy_pick(
                 if (xs[u] != INFINITY && (double)xs[u] <= th) cand[atomicAdd(&ncand, 1)] = (int32_t)(4 * q + u);
         }
     }
-    for (int64_t c = 4 * C4 + threadIdx.x; c < C; c += blockDim.x) {
+    for (int64_t c = 4 * C4 + threadIdx.x; c < c_hi; c += blockDim.x) {
         const float kv = key[c];
         if (kv != INFINITY && (double)kv <= th) cand[atomicAdd(&ncand, 1)] = (int32_t)c;
     }
@@ -342,6 +345,13 @@ __global__ void __launch_bounds__(1024) k_greedy_pick(
             top2_ins(s1, c1, s2, c2, acc, c);
         }
         __syncthreads();
+    }
+    if (local_rec) {   // sharded: report this shard's exact top-2, commit later
+        if (threadIdx.x == 0) {
+            *local_rec = make_double4(s1, s2, (double)c1, (double)c2);
+            ncand_tr[t] = n;
+        }
+        return;
     }
     if (threadIdx.x == 0) {
         cstar = c1;
@@ -367,6 +377,46 @@ __global__ void __launch_bounds__(1024) k_greedy_pick(
     if (threadIdx.x == 0) {
         double S = 0.0;
         for (int w = 0; w < 32; w++) S += rs1[w];
+        st->S = S;
+    }
+}
+
+// sharded greedy: commit the globally chosen configuration (same on every rank)
+__global__ void __launch_bounds__(1024) k_greedy_commit(const double4 *__restrict__ grec,
+                                                         const double *__restrict__ l64,
+                                                         int64_t E_pad, int64_t E,
+                                                         float *__restrict__ cur32,
+                                                         double *__restrict__ cur64,
+                                                         uint32_t *__restrict__ taken,
+                                                         pick_state *__restrict__ st, int t,
+                                                         int32_t *__restrict__ out_idx,
+                                                         double *__restrict__ s1_tr,
+                                                         double *__restrict__ s2_tr)
+{
+    __shared__ double rs[32];
+    const double4 g = *grec;
+    const int cs = (int)g.z;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        out_idx[t] = cs;
+        s1_tr[t] = g.x;
+        s2_tr[t] = g.y;
+        taken[cs >> 5] |= 1u << (cs & 31);
+    }
+    const double *col = l64 + (int64_t)cs * E_pad;
+    double part = 0.0;
+    for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) {
+        double v = fmin(cur64[e], col[e]);
+        cur64[e] = v;
+        cur32[e] = (float)v;
+        if (e < E) part += v;
+    }
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) rs[warp] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double S = 0.0;
+        for (int w = 0; w < 32; w++) S += rs[w];
         st->S = S;
     }
 }
@@ -640,9 +690,9 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
                 full_next = false;
             }
             k_greedy_scan<<<grid, 256, smem, s>>>(v->l32, C, E_pad, cur32, taken, t > 0, t & 1,
-                                                  cached_from, key, blk2);
+                                                  cached_from, 0, C, key, blk2);
             k_greedy_pick<<<1, 1024, 0, s>>>(key, blk2, grid, C, v->l64, E_pad, v->E, cur32, cur64, taken, st,
-                                             t, t > 0, gamma, cand, d_idx, d_s1, d_s2, d_nc);
+                                             t, t > 0, gamma, cand, d_idx, d_s1, d_s2, d_nc, 0, C, nullptr);
             ctx->stats.launches += 2;
         }
         PT_CK(cudaGetLastError());
@@ -687,3 +737,136 @@ extern "C" pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env
     }
     return PT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// pt_greedy_sharded (SURVEY §8(e) "greedy, scaled", NEXT #3): the configurations
+// are cut into shard_count contiguous ranges; this rank streams only its range
+// (1/N of the matrix per step -- L2-sized at N = 8 for the scaled matrix), picks
+// its exact local top-2 (fp32 window + fp64 refine, as the streamed path), and
+// the ranks all-gather those 2 records (4 doubles) through the caller's
+// callback; every rank merges them identically and commits the winner from its
+// own replica of the matrix (no column broadcast needed).
+// ---------------------------------------------------------------------------
+extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
+                                       int32_t shard_count, pt_allgather_fn allgather, void *user,
+                                       int32_t *out_idx, double *out_G_trace, double *out_gap_trace)
+{
+    if (!ctx || !out_idx || !allgather) return pt_fail(PT_EINVAL, "NULL argument");
+    if (shard_count < 1 || shard_rank < 0 || shard_rank >= shard_count)
+        return pt_fail(PT_EINVAL, "bad shard %d of %d", shard_rank, shard_count);
+    PT_CK(cudaSetDevice(ctx->dev));
+    const pt_view *v = nullptr;
+    PT_TRY(pt_get_view(ctx, env_mask, &v));
+    const int64_t C = v->C, E_pad = v->E_pad;
+    if (k < 1 || k > C) return pt_fail(PT_EINVAL, "k=%d outside [1, %lld]", k, (long long)C);
+    // shard boundaries on multiples of 64 configs
+    auto bound = [&](int64_t r) { return std::min(C, (C * r / shard_count + 63) / 64 * 64); };
+    const int64_t c_lo = bound(shard_rank), c_hi = bound(shard_rank + 1);
+    cudaStream_t s = ctx->stream;
+    const int64_t nwords = (C + 31) / 32;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
+    const size_t o_key = take(sizeof(float) * C), o_cand = take(sizeof(int32_t) * C),
+                 o_taken = take(sizeof(uint32_t) * nwords), o_c32 = take(sizeof(float) * E_pad),
+                 o_c64 = take(sizeof(double) * E_pad), o_st = take(sizeof(pick_state)),
+                 o_idx = take(sizeof(int32_t) * k), o_s1 = take(sizeof(double) * k),
+                 o_s2 = take(sizeof(double) * k), o_nc = take(sizeof(int32_t) * k),
+                 o_blk = take(sizeof(float2) * (size_t)ctx->num_sms * 32), o_rec = take(sizeof(double4) * 2);
+    void *scr = nullptr;
+    PT_TRY(pt_scratch(ctx, off, &scr));
+    char *b = (char *)scr;
+    float *key = (float *)(b + o_key);
+    int32_t *cand = (int32_t *)(b + o_cand), *d_idx = (int32_t *)(b + o_idx), *d_nc = (int32_t *)(b + o_nc);
+    uint32_t *taken = (uint32_t *)(b + o_taken);
+    float *cur32 = (float *)(b + o_c32);
+    double *cur64 = (double *)(b + o_c64), *d_s1 = (double *)(b + o_s1), *d_s2 = (double *)(b + o_s2);
+    pick_state *st = (pick_state *)(b + o_st);
+    float2 *blk2 = (float2 *)(b + o_blk);
+    double4 *rec = (double4 *)(b + o_rec);   // [0] local, [1] global
+    PT_CK(cudaMemsetAsync(taken, 0, sizeof(uint32_t) * nwords, s));
+    PT_CK(cudaMemsetAsync(st, 0, sizeof(pick_state), s));
+    PT_CK(cudaMemsetAsync(key, 0x7f, sizeof(float) * C, s));   // large finite: never a candidate
+    k_fill_f64<<<(unsigned)((E_pad + 255) / 256), 256, 0, s>>>(cur64, E_pad, INFINITY);
+    k_fill_f32<<<(unsigned)((E_pad + 255) / 256), 256, 0, s>>>(cur32, E_pad, INFINITY);
+    ctx->stats.launches += 2;
+    const size_t smem = sizeof(float) * E_pad;
+    if (smem > 48 * 1024)
+        PT_CK(cudaFuncSetAttribute(k_greedy_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const double u = 5.9604644775390625e-08;
+    const double n = (double)((E_pad + 127) / 128) + 8.0;
+    const double gamma = n * u / (1.0 - n * u) * 1.01;
+    int occ = 0;
+    PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_scan, 256, smem));
+    const int64_t ns = std::max<int64_t>(c_hi - c_lo, 1);
+    const int grid = (int)std::min<int64_t>((ns * 32 + 255) / 256, (int64_t)ctx->num_sms * std::max(occ, 1));
+    const int64_t keep_cfgs = (int64_t)(80.0 * (1 << 20) / (4.0 * (double)E_pad));
+    const int64_t cached_from = std::max<int64_t>(0, ns - keep_cfgs);
+    std::vector<double> mine(4), all(4 * (size_t)shard_count);
+    int64_t n_cand = 0;
+    PT_CK(cudaEventRecord(ctx->ev0, s));
+    for (int t = 0; t < k; t++) {
+        double4 hl = make_double4(INFINITY, INFINITY, (double)PT_BIGI, (double)PT_BIGI);
+        if (c_hi > c_lo) {
+            k_greedy_scan<<<grid, 256, smem, s>>>(v->l32, C, E_pad, cur32, taken, t > 0, t & 1, cached_from,
+                                                  c_lo, c_hi, key, blk2);
+            k_greedy_pick<<<1, 1024, 0, s>>>(key, blk2, grid, C, v->l64, E_pad, v->E, cur32, cur64, taken,
+                                             st, t, t > 0, gamma, cand, d_idx, d_s1, d_s2, d_nc, c_lo, c_hi,
+                                             rec);
+            ctx->stats.launches += 2;
+            PT_CK(cudaMemcpyAsync(&hl, rec, sizeof(double4), cudaMemcpyDeviceToHost, s));
+            int32_t nc = 0;
+            PT_CK(cudaMemcpyAsync(&nc, d_nc + t, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            PT_CK(cudaStreamSynchronize(s));
+            n_cand += nc;
+        }
+        mine[0] = hl.x;
+        mine[1] = hl.y;
+        mine[2] = hl.z;
+        mine[3] = hl.w;
+        if (allgather(user, mine.data(), 4, all.data()) != 0)
+            return pt_fail(PT_ENCCL, "all-gather callback failed at step %d", t);
+        // merge every rank's records in rank order: (s asc, config asc)
+        double s1 = INFINITY, s2 = INFINITY;
+        int64_t c1 = PT_BIGI, c2 = PT_BIGI;
+        for (int r = 0; r < shard_count; r++)
+            for (int q = 0; q < 2; q++) {
+                const double sv = all[4 * r + q];
+                const int64_t cv = (int64_t)all[4 * r + 2 + q];
+                if (!(sv < INFINITY)) continue;
+                if (sv < s1 || (sv == s1 && cv < c1)) {
+                    s2 = s1;
+                    c2 = c1;
+                    s1 = sv;
+                    c1 = cv;
+                } else if (cv != c1 && (sv < s2 || (sv == s2 && cv < c2))) {
+                    s2 = sv;
+                    c2 = cv;
+                }
+            }
+        if (!(s1 < INFINITY)) return pt_fail(PT_EINVAL, "no candidate left at step %d", t);
+        const double4 g = make_double4(s1, s2, (double)c1, (double)c2);
+        PT_CK(cudaMemcpyAsync(rec + 1, &g, sizeof(double4), cudaMemcpyHostToDevice, s));
+        k_greedy_commit<<<1, 1024, 0, s>>>(rec + 1, v->l64, E_pad, v->E, cur32, cur64, taken, st, t, d_idx,
+                                           d_s1, d_s2);
+        ctx->stats.launches++;
+    }
+    PT_CK(cudaEventRecord(ctx->ev1, s));
+    PT_CK(cudaGetLastError());
+    std::vector<double> h1(k), h2(k);
+    PT_CK(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+    PT_CK(cudaMemcpyAsync(h1.data(), d_s1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    PT_CK(cudaMemcpyAsync(h2.data(), d_s2, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    PT_CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->stats.greedy_ms = ms;
+    ctx->stats.greedy_candidates = n_cand;
+    const double invE = 1.0 / (double)v->E;
+    for (int t = 0; t < k; t++) {
+        const double g1 = exp(-h1[t] * invE);
+        if (out_G_trace) out_G_trace[t] = g1;
+        if (out_gap_trace) out_gap_trace[t] = std::isinf(h2[t]) ? INFINITY : g1 - exp(-h2[t] * invE);
+    }
+    return PT_OK;
+}
+

@@ -25,8 +25,13 @@ PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM, PT_GREEDY_LAZY = 0x1, 0
 
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
            "pt_merge_top2", "pt_eval_holdout", "pt_eval_holdout_all", "pt_swap_search",
-           "pt_kmeans_select", "pt_set_fleet", "pt_get_stats",
+           "pt_kmeans_select", "pt_set_fleet", "pt_get_stats", "pt_greedy_sharded",
            "pt_free", "pt_last_error")
+
+
+# int (*)(void *user, const double *mine, int32_t n, double *all)
+ALLGATHER_FN = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.POINTER(ct.c_double), ct.c_int32,
+                            ct.POINTER(ct.c_double))
 
 
 class pt_stats(ct.Structure):
@@ -65,6 +70,7 @@ def lib():
         L.pt_swap_search.argtypes = [P, i32, P, i32, i32, P, P, P, P]
         L.pt_eval_holdout_all.argtypes = [P, i32, P, P, P, P, P, P]
         L.pt_kmeans_select.argtypes = [P, i32, P, i32, P, P, P, P]
+        L.pt_greedy_sharded.argtypes = [P, i32, P, i32, i32, ALLGATHER_FN, P, P, P, P]
         L.pt_free.argtypes = [P]
         L.pt_free.restype = None
         L.pt_last_error.argtypes = []
@@ -176,6 +182,60 @@ def pt_greedy_select(ctx, k, env_mask=None, objective=PT_OBJ_GEOMEAN):
     _chk(lib().pt_greedy_select(ctx.handle, k, _ptr(_mask(env_mask)), objective, _ptr(idx),
                                 _ptr(gt), _ptr(gp)), "pt_greedy_select")
     return [int(x) for x in idx], gt, gp
+
+
+def pt_greedy_sharded(ctx, k, allgather, shard_rank=0, shard_count=1, env_mask=None):
+    """Column-sharded greedy: this rank scans configurations shard `shard_rank` of
+    `shard_count`; `allgather(mine)` takes this rank's 4 float64 record values
+    and returns the (shard_count * 4) values of every rank in rank order.
+    Returns (indices, G_trace, gap_trace), the same on every rank."""
+    err = []
+
+    def _cb(_user, mine, n, all_out):
+        try:
+            got = np.ascontiguousarray(allgather(np.ctypeslib.as_array(mine, (n,)).copy()),
+                                       dtype=np.float64).reshape(-1)
+            if got.size != n * shard_count:
+                raise ValueError(f"allgather returned {got.size} values, want {n * shard_count}")
+            ct.memmove(all_out, got.ctypes.data, got.nbytes)
+            return 0
+        except BaseException as ex:   # reported after the C call returns
+            err.append(ex)
+            return 1
+
+    cb = ALLGATHER_FN(_cb)
+    idx = np.zeros(k, np.int32)
+    gt = np.zeros(k, np.float64)
+    gp = np.zeros(k, np.float64)
+    rc = lib().pt_greedy_sharded(ctx.handle, k, _ptr(_mask(env_mask)), shard_rank, shard_count, cb,
+                                 None, _ptr(idx), _ptr(gt), _ptr(gp))
+    if err:
+        raise err[0]
+    _chk(rc, "pt_greedy_sharded")
+    return [int(x) for x in idx], gt, gp
+
+
+def greedy_select_distributed(ctx, k, env_mask=None, group=None):
+    """pt_greedy_sharded with the per-step record exchange done by
+    torch.distributed.all_gather (NCCL over NVLink for a cuda group, gloo on CPU):
+    rank r of world W scans configuration shard r of W."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    nccl = world > 1 and dist.get_backend(group) == "nccl"
+
+    def allgather(mine):
+        if world == 1:
+            return mine
+        t = torch.from_numpy(mine)
+        if nccl:
+            t = t.cuda()
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t, group=group)
+        return torch.cat([o.cpu() for o in out]).numpy()
+
+    return pt_greedy_sharded(ctx, k, allgather, rank, world, env_mask)
 
 
 def pt_exhaustive_best(ctx, k, env_mask=None, shard_rank=0, shard_count=1,

@@ -41,6 +41,12 @@ def test_nccl_world1_distributed_search():
             b, gb, ru, gr = o.exhaustive(k)
             assert r["best"] == b and r["runner"] == ru
             assert r["G"] == pytest.approx(gb, rel=1e-12)
+        # column-sharded greedy with the NCCL record exchange (world 1)
+        idx, gt, _ = pt.greedy_select_distributed(ctx, 12)
+        oidx, ogt, ogp = o.greedy(12)
+        np.testing.assert_allclose(gt, ogt, rtol=1e-9)
+        if np.all(ogp > 1e-9):
+            assert idx == oidx
         # the all-gather itself on the nccl group
         t = torch.tensor([[1.0, 2.0]], device="cuda")
         out = [torch.empty_like(t)]
