@@ -35,8 +35,22 @@
 
 #include "pt_internal.cuh"
 
-#define XT_R 128    // rows per CTA tile
+#define XT_R 128    // rows per CTA tile (k_exh_tiled)
+#ifndef XM_TC
+#define XM_TC 4     // k_exh_mma: columns per thread (4: 8x4 sets per thread, 32x64 CTA tile; 8: 8x8, 64x64)
+#endif
+#define XM_R (XM_TC == 8 ? 64 : 32)   // rows per CTA tile (k_exh_mma)
 #define XT_C 64     // columns per CTA tile
+// Kernel choice.  Measured on B200 at the paper shape (k=3, 1775 x 320):
+//   XT_MMA=0  k_exh_tiled (packed-fp16 tree)      13.66 ms   (default)
+//   XT_MMA=1  k_exh_mma   (HMNMX2 + HMMA sum)      17.7 ms  (XM_TC=4), 21.9 ms (XM_TC=8)
+// The HMMA kernel issues 0.67 instructions per (set, env) instead of 1.19 and its
+// window is ~3x tighter (49 vs 184 survivors), but a shared-memory load feeding
+// HMNMX2 -> HMMA stalls the loop (tools/ubench4.cu: 87% of the ALU ceiling with
+// register operands, 60% with the operands from shared memory), so it stays opt-in.
+#ifndef XT_MMA
+#define XT_MMA 0    // 1: tensor-summed kernel k_exh_mma, 0: packed-fp16 tree kernel k_exh_tiled
+#endif
 // pipeline stage = XT_K envs x 64 configs (fp16); measured on B200 at the paper
 // shape: K=32/S=4 13.94 ms, K=32/S=3 14.00, K=64/S=2 13.70, K=64/S=3 13.67,
 // K=160/S=2 15.77 (only 1 CTA/SM fits beyond ~113 KB of smem per CTA)
@@ -73,12 +87,12 @@ struct pt_tasks {
 
 // The work list depends only on (device, C, m, #SMs): built once per process
 // and shared by every context (a fresh pt_load_perf does not rebuild it).
-static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **out)
+static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, pt_tasks **out)
 {
     static std::mutex mu;
-    static std::map<std::tuple<int, int64_t, int, int>, pt_tasks *> cache;
+    static std::map<std::tuple<int, int64_t, int, int, int>, pt_tasks *> cache;
     std::lock_guard<std::mutex> g(mu);
-    const auto key = std::make_tuple(ctx->dev, v->C, m, ctx->num_sms);
+    const auto key = std::make_tuple(ctx->dev, v->C, m, ctx->num_sms, rows);
     auto it = cache.find(key);
     if (it != cache.end()) {
         *out = it->second;
@@ -89,7 +103,7 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **ou
     T->C = v->C;
     const int64_t C = v->C;
     const int64_t n_rows = pt_binom(C, m);
-    const int64_t n_rt = (n_rows + XT_R - 1) / XT_R;
+    const int64_t n_rt = (n_rows + rows - 1) / rows;
     T->slot_pre.push_back(0);
     T->set_pre.push_back(0);
     // task granularity: whole row tiles (A staged once) unless that leaves too
@@ -97,13 +111,13 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **ou
     int64_t total_ct = 0;
     for (int64_t t = 0; t < n_rt; t++) {
         int32_t mem[PT_MAXK];
-        pt_unrank_colex(t * XT_R, m, C, mem);
+        pt_unrank_colex(t * rows, m, C, mem);
         if (mem[m - 1] + 1 >= C) continue;
         total_ct += (C - tile_lo(mem[m - 1]) + XT_C - 1) / XT_C;
     }
     const int64_t umax = std::max<int64_t>(1, std::min<int64_t>(XT_UMAX, total_ct / (8 * std::max(ctx->num_sms, 1))));
     for (int64_t t = 0; t < n_rt; t++) {
-        const int64_t R0 = t * XT_R, R1 = std::min(n_rows, R0 + XT_R);
+        const int64_t R0 = t * rows, R1 = std::min(n_rows, R0 + rows);
         int32_t mem[PT_MAXK];
         pt_unrank_colex(R0, m, C, mem);
         const int64_t j0 = mem[m - 1];
@@ -123,7 +137,7 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, pt_tasks **ou
                 if (chi > first) useful += (b - a) * (chi - first);
             }
             T->h.push_back(make_int4((int)t, (int)u0, (int)u1, 0));
-            T->slot_pre.push_back(T->slot_pre.back() + (u1 - u0) * XT_R * XT_C);
+            T->slot_pre.push_back(T->slot_pre.back() + (u1 - u0) * rows * XT_C);
             T->set_pre.push_back(T->set_pre.back() + useful);
         }
     }
@@ -273,6 +287,8 @@ struct XParams {
     const uint16_t *hT;
     const uint16_t *hTile;
     int64_t n_ct;
+    const uint16_t *hC;       // k_exh_mma: config-major fp16 (A staging)
+    const uint32_t *hPair;    // k_exh_mma: env-pair column tiles
 };
 
 // Rows (of a thread's 8) whose 2nd column pair uses the relu form on the FMA pipe
@@ -423,7 +439,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 const int slot = G % XT_S;
                 mbar_wait(&full[slot], (G / XT_S) & 1u);
                 // the whole warp's column half lies past the last config: skip the math
-                const bool skip = ltile + 32 * (warp & 1) >= p.C;
+                const bool skip = ltile + (XM_TC == 8 ? 0 : 32 * (warp & 1)) >= p.C;
                 if (!skip) {
                     const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
                     const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
@@ -555,6 +571,288 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
         }
         steps += nsteps;
     }
+}
+
+// ---------------------------------------------------------------------------
+// the tensor-summed (min,+) kernel (default)
+//
+// The mins stay on the ALU pipe (HMNMX2, two environments of one set per
+// instruction); the across-environment sum of Eq. 1 moves to the legacy tensor
+// path: the mins are laid out as the A fragment of mma.sync.m16n8k16 (f16 in,
+// f32 accumulate, SASS HMMA.16816.F32) and B is a 0/1 selector,
+//     B[k][n] = 1 iff (k < 8) == (n even),
+// so output column n even accumulates A[m][0..7] and n odd A[m][8..15]: each
+// MMA row carries TWO sets (its k < 8 and k >= 8 halves), and every thread's
+// four accumulator registers are four different sets -- no wasted registers.
+// Per thread and MMA: 4 HMNMX2 (4 sets x 1 env pair) + 1 HMMA; the 4 lanes of
+// a quad hold the same 4 sets at 4 different env pairs (the MMA adds them).
+// Measured (tools/ubench3.cu): HMMA.16816 issues at 0.5 per SM per clock, i.e.
+// 256 mins / 8 cycles / SMSP -- exactly the HMNMX2 rate, so the two pipes are
+// balanced and the issue port carries 0.67 instructions per (set, env) instead
+// of 1.19 for the HADD2/FHADD tree.
+// Numerics: the mins are exact fp16 values (min commutes with RN16), products
+// by the selector's 1.0 are exact, and the only extra error is the tensor
+// accumulation (measured <= 2.2 ulp per MMA, tools/mma_acc_probe.cu; the
+// window assumes 2^-18 relative per MMA -- DESIGN.md "Numerics").
+//
+// CTA tile 32 rows x 64 columns; warp w: rows 8*(w>>1) .. +7 (shared by the
+// warp's 8 quads: one broadcast LDS), columns 32*(w&1) + 4*quad .. +3.
+// smem A: [E_pad/2][XM_R + 4] u32 env pairs (the +4 spreads the 4 lanes of a
+// quad over distinct banks); B ring: XT_S stages of [XT_K/2][64] u32.
+// ---------------------------------------------------------------------------
+#define XM_AST (XM_R + 4)
+#ifndef XM_VOL
+#define XM_VOL 0    // 1: mma asm volatile (pins the MMA order)
+#endif
+#ifndef XM_UNROLL
+#define XM_UNROLL 2
+#endif
+static constexpr int kXmUnroll = XM_UNROLL;
+// bank swizzle of hPair: 16-byte chunk ch of env pair pp is stored at chunk
+// ch ^ pair_swz(pp & 3) (see the B loads in k_exh_mma)
+__host__ __device__ __forceinline__ int pair_swz(int q)
+{
+    return XM_TC == 8 ? ((q & 1) | ((q & 2) << 1)) : (q << 1);
+}
+
+__device__ __forceinline__ void mma_sum(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1)
+{
+#if XM_VOL
+    asm volatile(
+#else
+    asm(
+#endif
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+#ifndef XM_MAXREG
+#define XM_MAXREG (XM_TC == 8 ? 112 : 96)   // 2 CTAs x 288 threads x 112 = 64,512 of 65,536 registers
+#endif
+__global__ void __maxnreg__(XM_MAXREG) k_exh_mma(const XParams p)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                  // [S][XT_K/2][64]
+    uint32_t *As = Bs + XT_S * (XT_K / 2) * XT_C;                       // [E_pad/2][XM_AST]
+    int *last_s = reinterpret_cast<int *>(As + (p.E_pad / 2) * XM_AST);  // [XM_R]
+    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XM_R);        // [S]
+    uint64_t *empty = full + XT_S;                                       // [S]
+    int4 *task_s = reinterpret_cast<int4 *>(empty + XT_S);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nkc = (int)(p.E_pad / XT_K);
+    if (tid == 0) {
+        for (int s = 0; s < XT_S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], XT_CONS / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    uint32_t steps = 0;
+    const int g = lane >> 2, q = lane & 3;
+    const int r0 = XM_TC == 8 ? 8 * warp : 8 * (warp >> 1);
+    const int c0 = XM_TC == 8 ? 8 * g : 32 * (warp & 1) + 4 * g;
+    const uint32_t one2 = 0x3C003C00u;
+    const uint32_t sel0 = (g & 1) ? 0u : one2, sel1 = (g & 1) ? one2 : 0u;
+    float b1 = INFINITY, published = INFINITY;
+
+    for (;;) {
+        if (tid == 0) {
+            int ti = atomicAdd(p.task_ctr, 1);
+            *task_s = ti < p.task_hi ? p.tasks[ti] : make_int4(-1, 0, 0, 0);
+        }
+        __syncthreads();
+        const int4 tk = *task_s;
+        if (tk.x < 0) break;
+        const int64_t R0 = (int64_t)tk.x * XM_R;
+        int32_t mem0[PT_MAXK];
+        pt_unrank_colex(R0, p.m, p.C, mem0);
+        const int64_t lo = tile_lo(mem0[p.m - 1]);
+        const int nsteps = (tk.z - tk.y) * nkc;
+
+        if (warp == XT_CONS / 32) {
+            // ---------------- producer warp: one 8 KB bulk copy per stage ----------------
+            if (lane == 0) {
+                int qs = 0;
+                int64_t col = lo + (int64_t)tk.y * XT_C;
+                uint32_t G = steps;
+                for (int gs = 0; gs < nsteps; gs++, G++) {
+                    const int slot = G % XT_S;
+                    const uint32_t par = ((G / XT_S) & 1u) ^ 1u;
+                    mbar_wait(&empty[slot], par);
+                    const int64_t sh = (col >> 3) & 7, ct = (col - 8 * sh) >> 6;
+                    const uint32_t *src =
+                        p.hPair + ((sh * p.n_ct + ct) * (p.E_pad / 2) + (int64_t)qs * (XT_K / 2)) * XT_C;
+                    mbar_expect_tx(&full[slot], XT_K * XT_BROW);
+                    bulk_g2s(Bs + slot * (XT_K / 2) * XT_C, src, XT_K * XT_BROW, &full[slot]);
+                    if (++qs == nkc) {
+                        qs = 0;
+                        col += XT_C;
+                    }
+                }
+            }
+            __syncwarp();
+        } else {
+            // ---------------- consumers ----------------
+            // stage A pairs: As[pp][r] = min over the row's members of (env 2pp, 2pp+1)
+            {
+                constexpr int TPR = XT_CONS / XM_R;   // staging threads per row
+                const int r = tid / TPR, sub = tid % TPR;
+                const int64_t R = R0 + r;
+                int32_t mem[PT_MAXK];
+                const bool valid = R < p.n_rows;
+                if (valid) pt_unrank_colex(R, p.m, p.C, mem);
+                else for (int u = 0; u < p.m; u++) mem[u] = 0;
+                if (sub == 0) last_s[r] = valid ? mem[p.m - 1] : 0x7fffffff;
+                for (int64_t ch = sub; ch < p.E_pad / 8; ch += TPR) {
+                    uint4 v = __ldg(reinterpret_cast<const uint4 *>(p.hC + (int64_t)mem[0] * p.E_pad) + ch);
+                    for (int u = 1; u < p.m; u++) {
+                        const uint4 w =
+                            __ldg(reinterpret_cast<const uint4 *>(p.hC + (int64_t)mem[u] * p.E_pad) + ch);
+                        v.x = hmin2(v.x, w.x);
+                        v.y = hmin2(v.y, w.y);
+                        v.z = hmin2(v.z, w.z);
+                        v.w = hmin2(v.w, w.w);
+                    }
+                    if (!valid) v = make_uint4(0, 0, 0, 0);
+                    uint32_t *dst = As + 4 * ch * XM_AST + r;
+                    dst[0] = v.x;
+                    dst[XM_AST] = v.y;
+                    dst[2 * XM_AST] = v.z;
+                    dst[3 * XM_AST] = v.w;
+                }
+            }
+            named_sync(1, XT_CONS);
+
+            float acc[4][XM_TC / 2][4];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < XM_TC / 2; j++)
+#pragma unroll
+                    for (int t = 0; t < 4; t++) acc[i][j][t] = 0.0f;
+
+            int qs = 0;
+            int64_t ltile = lo + (int64_t)tk.y * XT_C;
+            uint32_t G = steps;
+            for (int gs = 0; gs < nsteps; gs++, G++) {
+                const int slot = G % XT_S;
+                mbar_wait(&full[slot], (G / XT_S) & 1u);
+                const bool skip = ltile + (XM_TC == 8 ? 0 : 32 * (warp & 1)) >= p.C;
+                if (!skip) {
+                    // hPair is stored swizzled (pair_swz): the 8 lanes of a quarter-warp
+                    // phase (2 quads x 4 env pairs) hit 8 distinct bank groups
+                    const uint32_t *B = Bs + slot * (XT_K / 2) * XT_C + q * XT_C +
+                                        4 * ((c0 >> 2) ^ pair_swz(q));
+#if XM_TC == 8
+                    const uint32_t *B2 = Bs + slot * (XT_K / 2) * XT_C + q * XT_C +
+                                         4 * (((c0 >> 2) + 1) ^ pair_swz(q));
+#endif
+                    const uint32_t *A = As + ((int64_t)qs * (XT_K / 2) + q) * XM_AST + r0;
+#pragma unroll kXmUnroll
+                    for (int kk = 0; kk < XT_K / 8; kk++) {
+                        const uint4 al = *reinterpret_cast<const uint4 *>(A + 4 * kk * XM_AST);
+                        const uint4 ah = *reinterpret_cast<const uint4 *>(A + 4 * kk * XM_AST + 4);
+                        const uint4 bv = *reinterpret_cast<const uint4 *>(B + 4 * kk * XT_C);
+                        const uint32_t a[8] = {al.x, al.y, al.z, al.w, ah.x, ah.y, ah.z, ah.w};
+#if XM_TC == 8
+                        const uint4 bw = *reinterpret_cast<const uint4 *>(B2 + 4 * kk * XT_C);
+                        const uint32_t b[8] = {bv.x, bv.y, bv.z, bv.w, bw.x, bw.y, bw.z, bw.w};
+#else
+                        const uint32_t b[4] = {bv.x, bv.y, bv.z, bv.w};
+#endif
+#pragma unroll
+                        for (int i = 0; i < 4; i++)
+#pragma unroll
+                            for (int j = 0; j < XM_TC / 2; j++)
+                                mma_sum(acc[i][j], hmin2(a[2 * i], b[2 * j]), hmin2(a[2 * i + 1], b[2 * j]),
+                                        hmin2(a[2 * i], b[2 * j + 1]), hmin2(a[2 * i + 1], b[2 * j + 1]),
+                                        sel0, sel1);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                if (++qs == nkc) {
+                    qs = 0;
+                    if (!skip) {
+                        // epilogue of one column tile.  The 4 lanes of a quad hold the same
+                        // 32 sums; lane q takes row pair i = q (selected without branching,
+                        // so all 32 lanes work on distinct sets).  Each lane tracks only its
+                        // smallest upper bound b1; the warp's 2nd-smallest b1 bounds s_(2)
+                        // (lanes own disjoint sets).
+                        const float tau = fminf(p.tau_seed, __uint_as_float(*(volatile unsigned *)p.U));
+                        const int lbase = (int)(ltile + c0);
+                        const int last0 = last_s[r0 + 2 * q], last1 = last_s[r0 + 2 * q + 1];
+#pragma unroll
+                        for (int j = 0; j < XM_TC / 2; j++)
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                // acc[i][j]: {row 2i col 2j, row 2i col 2j+1, row 2i+1 col 2j, row 2i+1 col 2j+1}
+                                const float sh = q == 0 ? acc[0][j][t] : q == 1 ? acc[1][j][t]
+                                               : q == 2 ? acc[2][j][t] : acc[3][j][t];
+                                const int l = lbase + 2 * j + (t & 1);
+                                const int last = (t >> 1) ? last1 : last0;
+                                if (l < (int)p.C && l > last) {
+                                    b1 = fminf(b1, __fmaf_ru(sh, p.c3, p.c4));
+                                    const float lb = __fmaf_rd(sh, p.c1, -p.c2);
+                                    if (lb <= tau) {
+                                        const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                        if (idx < p.cap) {
+                                            const int r = r0 + 2 * q + (t >> 1);
+                                            p.cand_key[idx] = ((unsigned long long)(R0 + r) << KEY_BITS) |
+                                                              (unsigned long long)l;
+                                            p.cand_s[idx] = lb;
+                                        }
+                                    }
+                                }
+                            }
+#pragma unroll
+                        for (int i = 0; i < 4; i++)
+#pragma unroll
+                            for (int j = 0; j < XM_TC / 2; j++)
+#pragma unroll
+                                for (int t = 0; t < 4; t++) acc[i][j][t] = 0.0f;
+                        // warp: two smallest lane minima (merge of sorted pairs)
+                        float m1 = b1, m2 = INFINITY;
+                        for (int o = 16; o; o >>= 1) {
+                            const float a1 = __shfl_xor_sync(0xffffffffu, m1, o);
+                            const float a2 = __shfl_xor_sync(0xffffffffu, m2, o);
+                            const float n1 = fminf(m1, a1);
+                            m2 = fminf(fmaxf(m1, a1), fminf(m2, a2));
+                            m1 = n1;
+                        }
+                        if (lane == 0 && m2 < published) {
+                            atomicMin(p.U, __float_as_uint(m2));
+                            published = m2;
+                        }
+                    }
+                    ltile += XT_C;
+                }
+            }
+        }
+        steps += nsteps;
+    }
+}
+
+// hPair[s][ct][pp][j'] = hT[2pp][c] | hT[2pp+1][c] << 16, c = 64*ct + 8*s + j, stored at the
+// swizzled position j' = 4*((j/4) ^ pair_swz(pp%4)) + j%4
+__global__ void k_tile_pairs(const uint16_t *__restrict__ hT, int64_t E_pad, int64_t C_pad, int64_t n_ct,
+                             uint32_t *__restrict__ hPair)
+{
+    const int64_t blk = blockIdx.x;                  // (s, ct, pp)
+    const int64_t np = E_pad / 2;
+    const int64_t pp = blk % np, sct = blk / np;
+    const int64_t ct = sct % n_ct, sh = sct / n_ct;
+    const int j = threadIdx.x;                       // 64 threads
+    const int64_t c = 64 * ct + 8 * sh + j;
+    uint32_t w = 0;
+    if (c < C_pad) w = (uint32_t)hT[(2 * pp) * C_pad + c] | ((uint32_t)hT[(2 * pp + 1) * C_pad + c] << 16);
+    hPair[blk * 64 + 4 * ((j >> 2) ^ pair_swz((int)(pp & 3))) + (j & 3)] = w;   // swizzled (see k_exh_mma)
 }
 
 // hTile[s][ct][e][j] = hT[e][64*ct + 8*s + j]  (0 beyond the padded row)
@@ -767,7 +1065,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     cudaStream_t s = ctx->stream;
     const int m = k - 1;
     pt_tasks *T = nullptr;
-    PT_TRY(build_tasks(ctx, v, m, &T));
+    PT_TRY(build_tasks(ctx, v, m, XT_MMA ? XM_R : XT_R, &T));
     const int n_tasks = (int)T->h.size();
     // equal-work contiguous shard of the task list
     const int64_t total = T->slot_pre.back();
@@ -800,8 +1098,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const double gam = ngrp * u32 / (1.0 - ngrp * u32);
     const double gamE = ((double)v->E_pad + 2.0) * u32 / (1.0 - ((double)v->E_pad + 2.0) * u32);
     // quantisation u16 + a (2 or 3)-level fp16 tree
-    const double eta_rel = ((XT_G8 ? 4.0 : 3.0) * u16 + 6.0 * u16 * u16 + gam) * 1.01;
-    const double eta_abs = 3.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
+    const double eta_rel16 = ((XT_G8 ? 4.0 : 3.0) * u16 + 6.0 * u16 * u16 + gam) * 1.01;
+    const double eta_abs16 = 3.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
     const double eta_A = (4.0 * u16 + 6.0 * u16 * u16 + gam + 2.0 * gamE + 4.0 * u32) * 1.02;
     const double eta_abs_r = 4.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
     auto f_up = [](double x) -> float {
@@ -820,6 +1118,17 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     std::vector<double> gs1(k), gs2(k);
     PT_TRY(pt_greedy_view(ctx, v, k, gidx.data(), gs1.data(), gs2.data()));
     const float tau_seed = f_up(gs2[k - 1] * (1.0 + 1e-9) + 1e-30);
+#if XT_MMA
+    // tensor-summed kernel: fp16 terms u16 (the mins are exact fp16 values), then
+    // E_pad/8 chained MMA accumulations, each assumed within 2^-18 relative of
+    // its exact result (measured worst 2^-22.1, tools/mma_acc_probe.cu)
+    const double n_mma = (double)v->E_pad / 8.0, d_mma = std::ldexp(1.0, -18);
+    const double gam_mma = n_mma * d_mma / (1.0 - n_mma * d_mma);
+    const double eta_rel = (u16 + gam_mma + u16 * gam_mma) * 1.01;
+    const double eta_abs = (double)v->E_pad * std::ldexp(1.0, -25) * (1.0 + gam_mma) * 1.01;
+#else
+    const double eta_rel = eta_rel16, eta_abs = eta_abs16;
+#endif
     const double c1d = 1.0 / (1.0 + eta_rel), c3d = 1.0 / (1.0 - eta_rel);
     const float c1 = f_dn(c1d), c2 = f_up(eta_abs), c3 = f_up(c3d), c4 = f_up(eta_abs * c3d * (1.0 + 1e-6));
 
@@ -833,10 +1142,25 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());
     }
+#if XT_MMA
+    if (!v->hPair) {
+        pt_view *mv = const_cast<pt_view *>(v);
+        PT_TRY(pt_dalloc(ctx, (void **)&mv->hPair, sizeof(uint32_t) * 8 * mv->n_ct * (v->E_pad / 2) * XT_C));
+        k_tile_pairs<<<(unsigned)(8 * mv->n_ct * (v->E_pad / 2)), 64, 0, s>>>(v->hT, v->E_pad, v->C_pad,
+                                                                            mv->n_ct, mv->hPair);
+        ctx->stats.launches++;
+        PT_CK(cudaGetLastError());
+    }
+    auto kern = k_exh_mma;
+    const size_t smem = sizeof(uint32_t) * XT_S * (XT_K / 2) * XT_C + sizeof(uint32_t) * (v->E_pad / 2) * XM_AST +
+                        sizeof(int) * XM_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
+#else
+    auto kern = k_exh_tiled;
     const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
                         sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 2 * sizeof(uint64_t) * XT_S +
                         sizeof(int4);
-    PT_CK(cudaFuncSetAttribute(k_exh_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+#endif
+    PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
     unsigned cap = 1u << 20;
     unsigned n_cand = 0;
@@ -886,11 +1210,13 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.hT = v->hT;
         p.hTile = v->hTile;
         p.n_ct = v->n_ct;
+        p.hC = v->hC;
+        p.hPair = v->hPair;
         int occ = 1;
-        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_tiled, XT_THREADS, smem));
+        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT_THREADS, smem));
         const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
         PT_CK(cudaEventRecord(ctx->ev0, s));
-        k_exh_tiled<<<grid, XT_THREADS, smem, s>>>(p);
+        kern<<<grid, XT_THREADS, smem, s>>>(p);
         PT_CK(cudaEventRecord(ctx->ev1, s));
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());

@@ -50,6 +50,12 @@ struct pt_view {
     // one contiguous 4 KB block (one bulk copy).  Built on first exhaustive use.
     uint16_t *hTile = nullptr;
     int64_t n_ct = 0;
+    // tensor-summed exhaustive kernel (k_exh_mma) operands:
+    //   hC    [C_pad][E_pad] fp16, config-major: the same RN16(l64) values as hT
+    //   hPair [8][n_ct][E_pad/2][64] u32: hTile with env pairs (2p, 2p+1) packed
+    //         into one f16x2 word per config (low half = env 2p)
+    uint16_t *hC = nullptr;
+    uint32_t *hPair = nullptr;
     bool owned = false;
 };
 
