@@ -167,34 +167,49 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
-def measure_scaled(pt, synth, local, pk, steps=3):
+def measure_scaled(pt, synth, local, pk, steps=3, world=1):
     """Secondary line, BASELINE config 5: greedy k=32 on the scaled 65,536 x 4,096
-    matrix (HBM-bound: every step streams the whole fp32 matrix, 1 GiB)."""
+    matrix (HBM-bound: every step streams the whole fp32 matrix, 1 GiB).  With
+    world > 1 the configurations are sharded (pt_greedy_sharded: each rank
+    streams 1/world of the matrix per step, 2 records all-gathered over the
+    process group); the time is the max over ranks."""
     import torch
     T, dev = synth.scaled(1)
     dT = torch.from_numpy(T).cuda()
     del T
     ctx = pt.pt_load_perf(dT, dev, device=local)
-    pt.pt_greedy_select(ctx, 32)                      # warm-up
+
+    def run():
+        if world > 1:
+            return pt.greedy_select_distributed(ctx, 32)
+        return pt.pt_greedy_select(ctx, 32)
+
+    run()                                             # warm-up
     ms = []
     for _ in range(steps):
-        pt.pt_greedy_select(ctx, 32)
+        run()
         ms.append(pt.pt_get_stats(ctx)["greedy_ms"])
     st = pt.pt_get_stats(ctx)
     pt.pt_free(ctx)
     del dT
     torch.cuda.empty_cache()
     t = float(np.median(ms))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
     C, E = 65536, 4096
     sets = sum(C - i for i in range(32))
     bytes_ = 32.0 * C * E * 4                          # algorithmic: one fp32 read per (config, env) per step
     gbs = bytes_ / (t * 1e-3) / 1e9
-    peak = pk.get("hbm_gbs", 6650.0)
-    return {"workload": "scaled synthetic 65,536 configs x 4,096 envs (64 devices x 64 inputs), greedy k=32",
+    peak = pk.get("hbm_gbs", 6650.0) * world
+    return {"workload": "scaled synthetic 65,536 configs x 4,096 envs (64 devices x 64 inputs), greedy k=32"
+                        + (f", configs sharded x{world} (pt_greedy_sharded)" if world > 1 else ""),
             "value": sets / (t * 1e-3), "unit": "sets/s", "ms": t,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                          "basis": "4 B per (candidate, env) per step over the whole selection "
-                                  "(scan + window pick), MEASURED_PEAKS hbm_gbs"},
+                                  "(scan + window pick), MEASURED_PEAKS hbm_gbs (x world for sharded runs)"},
             "fp64_refined_candidates": st["greedy_candidates"]}
 
 
@@ -313,7 +328,7 @@ def main():
         rate, cores, sample = oracle_sample_rate(T, dev)
         cpu = {"value": rate, "unit": "sets/s", "cores": cores, "kind": "oracle", "sample": sample}
 
-    scaled = None if args.no_scaled else measure_scaled(pt, synth, local, pk)
+    scaled = None if args.no_scaled else measure_scaled(pt, synth, local, pk, world=world)
 
     import json as _j
     gold = None

@@ -160,6 +160,22 @@ pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int
                             int32_t *out_idx, double *out_G_trace, double *out_gap_trace);
 
 /*
+ * pt_greedy_sharded_dev -- pt_greedy_sharded with a STREAM-ORDERED exchange and
+ * no host synchronisation inside the k-step loop: `mine` and `all` are DEVICE
+ * pointers (4 doubles; shard_count * 4 doubles) and `stream` is the context's
+ * cudaStream_t.  The callback must enqueue the all-gather so that `all` is
+ * complete, in stream order, before any later work on `stream` (e.g. an NCCL
+ * all-gather on that stream, or a wait on its completion event); the merge of
+ * the records and the commit then run on the device.  Same results as
+ * pt_greedy_sharded.
+ * Errors: as pt_greedy_sharded.
+ */
+typedef int (*pt_dev_allgather_fn)(void *user, const double *mine, int32_t n, double *all, void *stream);
+pt_status pt_greedy_sharded_dev(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
+                                int32_t shard_count, pt_dev_allgather_fn allgather, void *user,
+                                int32_t *out_idx, double *out_G_trace, double *out_gap_trace);
+
+/*
  * pt_merge_top2 -- host-only: merge n_rec (s, sorted k-tuple) records (e.g.
  * gathered from every shard/rank) into the best two in (s asc, tuple asc)
  * order.  s = +inf marks an absent record.

@@ -317,7 +317,14 @@ __device__ __forceinline__ uint32_t bcast_hi(uint32_t w)
     return r;
 }
 
+#ifndef XT_MAXREG
+#define XT_MAXREG 0   // 0: __launch_bounds__(288, 2) (ptxas picks 96); else __maxnreg__(XT_MAXREG)
+#endif
+#if XT_MAXREG
+__global__ void __maxnreg__(XT_MAXREG) k_exh_tiled(const XParams p)
+#else
 __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
+#endif
 {
     extern __shared__ __align__(128) unsigned char smem[];
     uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2

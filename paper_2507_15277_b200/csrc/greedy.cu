@@ -381,8 +381,11 @@ __global__ void __launch_bounds__(1024) k_greedy_pick(
     }
 }
 
-// sharded greedy: commit the globally chosen configuration (same on every rank)
-__global__ void __launch_bounds__(1024) k_greedy_commit(const double4 *__restrict__ grec,
+// sharded greedy: merge the n_rank x 2 all-gathered records (s1, s2, c1, c2 per
+// rank) into the global top-2 (s asc, config asc; identical on every rank) and
+// commit the winner
+__global__ void __launch_bounds__(1024) k_greedy_commit(const double *__restrict__ all, int n_rank,
+                                                         int *__restrict__ fail,
                                                          const double *__restrict__ l64,
                                                          int64_t E_pad, int64_t E,
                                                          float *__restrict__ cur32,
@@ -394,7 +397,31 @@ __global__ void __launch_bounds__(1024) k_greedy_commit(const double4 *__restric
                                                          double *__restrict__ s2_tr)
 {
     __shared__ double rs[32];
-    const double4 g = *grec;
+    __shared__ double4 gsh;
+    if (threadIdx.x == 0) {
+        double s1 = INFINITY, s2 = INFINITY, c1 = (double)PT_BIGI, c2 = (double)PT_BIGI;
+        for (int r = 0; r < n_rank; r++)
+            for (int q = 0; q < 2; q++) {
+                const double sv = all[4 * r + q], cv = all[4 * r + 2 + q];
+                if (!(sv < INFINITY)) continue;
+                if (sv < s1 || (sv == s1 && cv < c1)) {
+                    s2 = s1;
+                    c2 = c1;
+                    s1 = sv;
+                    c1 = cv;
+                } else if (cv != c1 && (sv < s2 || (sv == s2 && cv < c2))) {
+                    s2 = sv;
+                    c2 = cv;
+                }
+            }
+        if (!(s1 < INFINITY)) {
+            *fail = 1;
+            c1 = 0.0;   // stay in bounds; the host reports the failure
+        }
+        gsh = make_double4(s1, s2, c1, c2);
+    }
+    __syncthreads();
+    const double4 g = gsh;
     const int cs = (int)g.z;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -747,11 +774,12 @@ extern "C" pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env
 // callback; every rank merges them identically and commits the winner from its
 // own replica of the matrix (no column broadcast needed).
 // ---------------------------------------------------------------------------
-extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
-                                       int32_t shard_count, pt_allgather_fn allgather, void *user,
-                                       int32_t *out_idx, double *out_G_trace, double *out_gap_trace)
+static pt_status greedy_sharded_impl(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
+                                     int32_t shard_count, pt_allgather_fn allgather,
+                                     pt_dev_allgather_fn dev_allgather, void *user, int32_t *out_idx,
+                                     double *out_G_trace, double *out_gap_trace)
 {
-    if (!ctx || !out_idx || !allgather) return pt_fail(PT_EINVAL, "NULL argument");
+    if (!ctx || !out_idx || (!allgather && !dev_allgather)) return pt_fail(PT_EINVAL, "NULL argument");
     if (shard_count < 1 || shard_rank < 0 || shard_rank >= shard_count)
         return pt_fail(PT_EINVAL, "bad shard %d of %d", shard_rank, shard_count);
     PT_CK(cudaSetDevice(ctx->dev));
@@ -771,7 +799,8 @@ extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *en
                  o_c64 = take(sizeof(double) * E_pad), o_st = take(sizeof(pick_state)),
                  o_idx = take(sizeof(int32_t) * k), o_s1 = take(sizeof(double) * k),
                  o_s2 = take(sizeof(double) * k), o_nc = take(sizeof(int32_t) * k),
-                 o_blk = take(sizeof(float2) * (size_t)ctx->num_sms * 32), o_rec = take(sizeof(double4) * 2);
+                 o_blk = take(sizeof(float2) * (size_t)ctx->num_sms * 32), o_rec = take(sizeof(double4) * 2),
+                 o_all = take(sizeof(double) * 4 * (size_t)shard_count), o_fail = take(sizeof(int));
     void *scr = nullptr;
     PT_TRY(pt_scratch(ctx, off, &scr));
     char *b = (char *)scr;
@@ -782,7 +811,13 @@ extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *en
     double *cur64 = (double *)(b + o_c64), *d_s1 = (double *)(b + o_s1), *d_s2 = (double *)(b + o_s2);
     pick_state *st = (pick_state *)(b + o_st);
     float2 *blk2 = (float2 *)(b + o_blk);
-    double4 *rec = (double4 *)(b + o_rec);   // [0] local, [1] global
+    double4 *rec = (double4 *)(b + o_rec);   // [0] this rank's local top-2
+    double *d_all = (double *)(b + o_all);
+    int *d_fail = (int *)(b + o_fail);
+    PT_CK(cudaMemsetAsync(d_fail, 0, sizeof(int), s));
+    // a rank with an empty shard reports no candidate
+    const double4 none = make_double4(INFINITY, INFINITY, (double)PT_BIGI, (double)PT_BIGI);
+    if (!(c_hi > c_lo)) PT_CK(cudaMemcpyAsync(rec, &none, sizeof(double4), cudaMemcpyHostToDevice, s));
     PT_CK(cudaMemsetAsync(taken, 0, sizeof(uint32_t) * nwords, s));
     PT_CK(cudaMemsetAsync(st, 0, sizeof(pick_state), s));
     PT_CK(cudaMemsetAsync(key, 0x7f, sizeof(float) * C, s));   // large finite: never a candidate
@@ -805,7 +840,25 @@ extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *en
     int64_t n_cand = 0;
     PT_CK(cudaEventRecord(ctx->ev0, s));
     for (int t = 0; t < k; t++) {
-        double4 hl = make_double4(INFINITY, INFINITY, (double)PT_BIGI, (double)PT_BIGI);
+        if (dev_allgather) {
+            // stream-ordered exchange: no host synchronisation inside the loop
+            if (c_hi > c_lo) {
+                k_greedy_scan<<<grid, 256, smem, s>>>(v->l32, C, E_pad, cur32, taken, t > 0, t & 1,
+                                                      cached_from, c_lo, c_hi, key, blk2);
+                k_greedy_pick<<<1, 1024, 0, s>>>(key, blk2, grid, C, v->l64, E_pad, v->E, cur32, cur64, taken,
+                                                 st, t, t > 0, gamma, cand, d_idx, d_s1, d_s2, d_nc, c_lo,
+                                                 c_hi, rec);
+                ctx->stats.launches += 2;
+            }
+            PT_CK(cudaGetLastError());
+            if (dev_allgather(user, (const double *)rec, 4, d_all, (void *)s) != 0)
+                return pt_fail(PT_ENCCL, "device all-gather callback failed at step %d", t);
+            k_greedy_commit<<<1, 1024, 0, s>>>(d_all, shard_count, d_fail, v->l64, E_pad, v->E, cur32, cur64,
+                                               taken, st, t, d_idx, d_s1, d_s2);
+            ctx->stats.launches += 1;
+            continue;
+        }
+        double4 hl = none;
         if (c_hi > c_lo) {
             k_greedy_scan<<<grid, 256, smem, s>>>(v->l32, C, E_pad, cur32, taken, t > 0, t & 1, cached_from,
                                                   c_lo, c_hi, key, blk2);
@@ -825,33 +878,27 @@ extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *en
         mine[3] = hl.w;
         if (allgather(user, mine.data(), 4, all.data()) != 0)
             return pt_fail(PT_ENCCL, "all-gather callback failed at step %d", t);
-        // merge every rank's records in rank order: (s asc, config asc)
-        double s1 = INFINITY, s2 = INFINITY;
-        int64_t c1 = PT_BIGI, c2 = PT_BIGI;
-        for (int r = 0; r < shard_count; r++)
-            for (int q = 0; q < 2; q++) {
-                const double sv = all[4 * r + q];
-                const int64_t cv = (int64_t)all[4 * r + 2 + q];
-                if (!(sv < INFINITY)) continue;
-                if (sv < s1 || (sv == s1 && cv < c1)) {
-                    s2 = s1;
-                    c2 = c1;
-                    s1 = sv;
-                    c1 = cv;
-                } else if (cv != c1 && (sv < s2 || (sv == s2 && cv < c2))) {
-                    s2 = sv;
-                    c2 = cv;
-                }
-            }
-        if (!(s1 < INFINITY)) return pt_fail(PT_EINVAL, "no candidate left at step %d", t);
-        const double4 g = make_double4(s1, s2, (double)c1, (double)c2);
-        PT_CK(cudaMemcpyAsync(rec + 1, &g, sizeof(double4), cudaMemcpyHostToDevice, s));
-        k_greedy_commit<<<1, 1024, 0, s>>>(rec + 1, v->l64, E_pad, v->E, cur32, cur64, taken, st, t, d_idx,
-                                           d_s1, d_s2);
+        // the merge runs in the commit kernel (same code as the device-exchange path);
+        // the host only checks that some rank still had a candidate
+        bool any = false;
+        for (int r = 0; r < shard_count; r++) any = any || all[4 * r] < INFINITY;
+        if (!any) return pt_fail(PT_EINVAL, "no candidate left at step %d", t);
+        PT_CK(cudaMemcpyAsync(d_all, all.data(), sizeof(double) * 4 * shard_count, cudaMemcpyHostToDevice, s));
+        k_greedy_commit<<<1, 1024, 0, s>>>(d_all, shard_count, d_fail, v->l64, E_pad, v->E, cur32, cur64, taken,
+                                           st, t, d_idx, d_s1, d_s2);
         ctx->stats.launches++;
     }
     PT_CK(cudaEventRecord(ctx->ev1, s));
     PT_CK(cudaGetLastError());
+    if (dev_allgather) {
+        int fail = 0;
+        std::vector<int32_t> nc(k, 0);
+        PT_CK(cudaMemcpyAsync(&fail, d_fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+        if (c_hi > c_lo) PT_CK(cudaMemcpyAsync(nc.data(), d_nc, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
+        PT_CK(cudaStreamSynchronize(s));
+        if (fail) return pt_fail(PT_EINVAL, "no candidate left (all-gathered records empty)");
+        for (int t = 0; t < k; t++) n_cand += nc[t];
+    }
     std::vector<double> h1(k), h2(k);
     PT_CK(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
     PT_CK(cudaMemcpyAsync(h1.data(), d_s1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
@@ -870,3 +917,20 @@ extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *en
     return PT_OK;
 }
 
+extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
+                                       int32_t shard_count, pt_allgather_fn allgather, void *user,
+                                       int32_t *out_idx, double *out_G_trace, double *out_gap_trace)
+{
+    if (!allgather) return pt_fail(PT_EINVAL, "NULL argument");
+    return greedy_sharded_impl(ctx, k, env_mask, shard_rank, shard_count, allgather, nullptr, user, out_idx,
+                               out_G_trace, out_gap_trace);
+}
+
+extern "C" pt_status pt_greedy_sharded_dev(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
+                                           int32_t shard_count, pt_dev_allgather_fn allgather, void *user,
+                                           int32_t *out_idx, double *out_G_trace, double *out_gap_trace)
+{
+    if (!allgather) return pt_fail(PT_EINVAL, "NULL argument");
+    return greedy_sharded_impl(ctx, k, env_mask, shard_rank, shard_count, nullptr, allgather, user, out_idx,
+                               out_G_trace, out_gap_trace);
+}

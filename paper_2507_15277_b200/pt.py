@@ -26,12 +26,25 @@ PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM, PT_GREEDY_LAZY = 0x1, 0
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
            "pt_merge_top2", "pt_eval_holdout", "pt_eval_holdout_all", "pt_swap_search",
            "pt_kmeans_select", "pt_set_fleet", "pt_get_stats", "pt_greedy_sharded",
+           "pt_greedy_sharded_dev",
            "pt_free", "pt_last_error")
 
 
 # int (*)(void *user, const double *mine, int32_t n, double *all)
 ALLGATHER_FN = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.POINTER(ct.c_double), ct.c_int32,
                             ct.POINTER(ct.c_double))
+
+
+# int (*)(void *user, const double *mine, int32_t n, double *all, void *stream)  (device pointers)
+DEV_ALLGATHER_FN = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_int32, ct.c_void_p, ct.c_void_p)
+
+
+class _DevView:
+    """Zero-copy view of n float64 at a device pointer (for torch.as_tensor)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
 
 
 class pt_stats(ct.Structure):
@@ -71,6 +84,7 @@ def lib():
         L.pt_eval_holdout_all.argtypes = [P, i32, P, P, P, P, P, P]
         L.pt_kmeans_select.argtypes = [P, i32, P, i32, P, P, P, P]
         L.pt_greedy_sharded.argtypes = [P, i32, P, i32, i32, ALLGATHER_FN, P, P, P, P]
+        L.pt_greedy_sharded_dev.argtypes = [P, i32, P, i32, i32, DEV_ALLGATHER_FN, P, P, P, P]
         L.pt_free.argtypes = [P]
         L.pt_free.restype = None
         L.pt_last_error.argtypes = []
@@ -215,15 +229,73 @@ def pt_greedy_sharded(ctx, k, allgather, shard_rank=0, shard_count=1, env_mask=N
     return [int(x) for x in idx], gt, gp
 
 
-def greedy_select_distributed(ctx, k, env_mask=None, group=None):
-    """pt_greedy_sharded with the per-step record exchange done by
-    torch.distributed.all_gather (NCCL over NVLink for a cuda group, gloo on CPU):
-    rank r of world W scans configuration shard r of W."""
+def pt_greedy_sharded_dev(ctx, k, allgather, shard_rank=0, shard_count=1, env_mask=None):
+    """Column-sharded greedy with a stream-ordered exchange (no host sync inside
+    the k-step loop).  `allgather(mine, out, stream)` gets torch CUDA views of
+    this rank's 4 record values and of the (shard_count * 4) output, and the
+    context's stream (torch.cuda stream object); it must enqueue the gather so
+    `out` is complete in that stream's order.  Returns (indices, G_trace, gap_trace)."""
+    import torch
+    err = []
+
+    views = {}   # the pointers and stream are fixed for the whole call: build the views once
+
+    def _cb(_user, mine, n, all_out, stream):
+        try:
+            key = (mine, all_out, stream)
+            if key not in views:
+                views[key] = (torch.as_tensor(_DevView(mine, n), device="cuda"),
+                              torch.as_tensor(_DevView(all_out, n * shard_count), device="cuda"),
+                              torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream())
+            mt, at, st = views[key]
+            allgather(mt, at, st)
+            return 0
+        except BaseException as ex:   # reported after the C call returns
+            err.append(ex)
+            return 1
+
+    cb = DEV_ALLGATHER_FN(_cb)
+    idx = np.zeros(k, np.int32)
+    gt = np.zeros(k, np.float64)
+    gp = np.zeros(k, np.float64)
+    rc = lib().pt_greedy_sharded_dev(ctx.handle, k, _ptr(_mask(env_mask)), shard_rank, shard_count, cb,
+                                     None, _ptr(idx), _ptr(gt), _ptr(gp))
+    if err:
+        raise err[0]
+    _chk(rc, "pt_greedy_sharded_dev")
+    return [int(x) for x in idx], gt, gp
+
+
+def greedy_select_distributed(ctx, k, env_mask=None, group=None, on_device=None):
+    """Column-sharded greedy over a torch.distributed group: rank r of world W
+    scans configuration shard r of W and the 2 exact records per rank are
+    all-gathered every step.  on_device (default: True for an NCCL group) uses
+    pt_greedy_sharded_dev with an NCCL all_gather_into_tensor enqueued on the
+    library's stream (over NVLink; no host round trip per step); otherwise the
+    records go through the host (pt_greedy_sharded; gloo)."""
     import torch
     import torch.distributed as dist
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     nccl = world > 1 and dist.get_backend(group) == "nccl"
+    if on_device is None:
+        on_device = nccl
+
+    if on_device:
+        def dev_allgather(mine, out, stream):
+            if world == 1:
+                with torch.cuda.stream(stream):
+                    out.copy_(mine)
+            elif nccl:
+                with torch.cuda.stream(stream):
+                    dist.all_gather_into_tensor(out, mine, group=group)
+            else:   # host-staged (gloo)
+                stream.synchronize()
+                parts = [torch.empty(mine.numel(), dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, mine.cpu(), group=group)
+                with torch.cuda.stream(stream):
+                    out.copy_(torch.cat(parts))
+        return pt_greedy_sharded_dev(ctx, k, dev_allgather, rank, world, env_mask)
 
     def allgather(mine):
         if world == 1:

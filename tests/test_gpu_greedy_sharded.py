@@ -41,14 +41,30 @@ class _Exchange:
         return allgather
 
 
-def run_sharded(T, dev, k, world, mask=None):
+    def dev_rank_fn(self, r):
+        """stream-ordered flavour: device views in, host-staged exchange"""
+        def allgather(mine, out, stream):
+            stream.synchronize()
+            self.buf[r] = mine.cpu().numpy().copy()
+            self.bar.wait()
+            cat = torch.from_numpy(np.concatenate(self.buf))
+            self.bar.wait()
+            with torch.cuda.stream(stream):
+                out.copy_(cat)
+        return allgather
+
+
+def run_sharded(T, dev, k, world, mask=None, on_device=False):
     ctxs = [pt.pt_load_perf(T, dev) for _ in range(world)]
     ex = _Exchange(world)
     res, errs = [None] * world, []
 
     def body(r):
         try:
-            res[r] = pt.pt_greedy_sharded(ctxs[r], k, ex.rank_fn(r), r, world, env_mask=mask)
+            if on_device:
+                res[r] = pt.pt_greedy_sharded_dev(ctxs[r], k, ex.dev_rank_fn(r), r, world, env_mask=mask)
+            else:
+                res[r] = pt.pt_greedy_sharded(ctxs[r], k, ex.rank_fn(r), r, world, env_mask=mask)
         except BaseException as e:   # surface in the main thread
             errs.append(e)
             ex.bar.abort()
@@ -68,11 +84,12 @@ def plain(T, dev, k, mask=None):
     return pt.pt_greedy_select(ctx, k, env_mask=mask)
 
 
+@pytest.mark.parametrize("on_device", [False, True])
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_sharded_equals_streamed(world):
+def test_sharded_equals_streamed(world, on_device):
     T, dev = synth.small_matrix(11, n_cfg=700, n_dev=5, n_inputs=20)
     idx, gt, gp = plain(T, dev, 24)
-    for ridx, rgt, rgp in run_sharded(T, dev, 24, world):
+    for ridx, rgt, rgp in run_sharded(T, dev, 24, world, on_device=on_device):
         assert ridx == idx
         np.testing.assert_array_equal(rgt, gt)
         np.testing.assert_array_equal(rgp, gp)
@@ -89,9 +106,11 @@ def test_sharded_empty_shards_and_k_equals_C():
     T, dev = synth.small_matrix(12, n_cfg=100, n_dev=3, n_inputs=10)
     idx, gt, gp = plain(T, dev, 100)
     assert sorted(idx) == list(range(100))
-    for ridx, rgt, rgp in run_sharded(T, dev, 100, 8):
-        assert ridx == idx
-        np.testing.assert_array_equal(rgt, gt)
+    for on_device in (False, True):
+        for ridx, rgt, rgp in run_sharded(T, dev, 100, 8, on_device=on_device):
+            assert ridx == idx
+            np.testing.assert_array_equal(rgt, gt)
+            assert np.isinf(rgp[-1])
     assert np.isinf(gp[-1])
 
 
@@ -113,9 +132,10 @@ def test_sharded_scaled_8():
     ctx = pt.pt_load_perf(dT, dev)
     idx, gt, _ = pt.pt_greedy_select(ctx, 32)
     pt.pt_free(ctx)
-    for ridx, rgt, _ in run_sharded(dT, dev, 32, 8):
-        assert ridx == idx
-        np.testing.assert_array_equal(rgt, gt)
+    for on_device in (False, True):
+        for ridx, rgt, _ in run_sharded(dT, dev, 32, 8, on_device=on_device):
+            assert ridx == idx
+            np.testing.assert_array_equal(rgt, gt)
 
 
 def test_callback_failure_reported():
@@ -129,3 +149,9 @@ def test_callback_failure_reported():
         pt.pt_greedy_sharded(ctx, 4, bad, 0, 2)
     with pytest.raises(pt.PTError):
         pt.pt_greedy_sharded(ctx, 4, lambda m: m, 2, 2)   # shard_rank >= shard_count
+
+    def bad_dev(mine, out, stream):
+        raise RuntimeError("nccl down")
+
+    with pytest.raises(RuntimeError, match="nccl down"):
+        pt.pt_greedy_sharded_dev(ctx, 4, bad_dev, 0, 2)
