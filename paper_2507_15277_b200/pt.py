@@ -275,20 +275,21 @@ def greedy_select_distributed(ctx, k, env_mask=None, group=None, on_device=None)
     records go through the host (pt_greedy_sharded; gloo)."""
     import torch
     import torch.distributed as dist
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    nccl = world > 1 and dist.get_backend(group) == "nccl"
+    init = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank(group) if init else 0
+    world = dist.get_world_size(group) if init else 1
+    nccl = init and dist.get_backend(group) == "nccl"
     if on_device is None:
         on_device = nccl
 
     if on_device:
         def dev_allgather(mine, out, stream):
-            if world == 1:
-                with torch.cuda.stream(stream):
-                    out.copy_(mine)
-            elif nccl:
+            if nccl:   # enqueued on the library's stream: no host round trip
                 with torch.cuda.stream(stream):
                     dist.all_gather_into_tensor(out, mine, group=group)
+            elif world == 1:
+                with torch.cuda.stream(stream):
+                    out.copy_(mine)
             else:   # host-staged (gloo)
                 stream.synchronize()
                 parts = [torch.empty(mine.numel(), dtype=torch.float64) for _ in range(world)]
@@ -298,7 +299,7 @@ def greedy_select_distributed(ctx, k, env_mask=None, group=None, on_device=None)
         return pt_greedy_sharded_dev(ctx, k, dev_allgather, rank, world, env_mask)
 
     def allgather(mine):
-        if world == 1:
+        if world == 1 and not nccl:
             return mine
         t = torch.from_numpy(mine)
         if nccl:
