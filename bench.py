@@ -63,14 +63,22 @@ class ClockSampler:
         self.gpu, self.period, self.rows, self.stop = gpu, period, [], threading.Event()
         self.max_mhz = None
 
-    def _run(self):
+    def _init(self):
+        # NVML initialised before the timed region starts (in __enter__, ahead of
+        # the first event record), not concurrently with it
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
+            self.h = None
+
+    def _run(self):
+        if self.h is None:
             return
+        pynvml, h = self.nv, self.h
         while not self.stop.is_set():
             try:
                 sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
@@ -81,6 +89,7 @@ class ClockSampler:
             self.stop.wait(self.period)
 
     def __enter__(self):
+        self._init()
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
         return self

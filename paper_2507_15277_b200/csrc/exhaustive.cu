@@ -846,6 +846,16 @@ __global__ void __maxnreg__(XM_MAXREG) k_exh_mma(const XParams p)
     }
 }
 
+// hC[c][e] = the same fp16(l64[c][e]) as hT, config-major (0 for padded configs)
+__global__ void k_half_cfg(const double *__restrict__ l64, int64_t E, int64_t C, int64_t E_pad,
+                           int64_t C_pad, uint16_t *__restrict__ hC)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= C_pad * E_pad) return;
+    const int64_t c = i / E_pad, e = i % E_pad;
+    hC[i] = (c < C && e < E) ? __half_as_ushort(__double2half(l64[c * E_pad + e])) : (uint16_t)0;
+}
+
 // hPair[s][ct][pp][j'] = hT[2pp][c] | hT[2pp+1][c] << 16, c = 64*ct + 8*s + j, stored at the
 // swizzled position j' = 4*((j/4) ^ pair_swz(pp%4)) + j%4
 __global__ void k_tile_pairs(const uint16_t *__restrict__ hT, int64_t E_pad, int64_t C_pad, int64_t n_ct,
@@ -1150,6 +1160,13 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         PT_CK(cudaGetLastError());
     }
 #if XT_MMA
+    if (!v->hC) {
+        pt_view *mv = const_cast<pt_view *>(v);
+        PT_TRY(pt_dalloc(ctx, (void **)&mv->hC, sizeof(uint16_t) * v->E_pad * v->C_pad));
+        k_half_cfg<<<(unsigned)((v->C_pad * v->E_pad + 255) / 256), 256, 0, s>>>(v->l64, v->E, v->C, v->E_pad,
+                                                                                v->C_pad, mv->hC);
+        ctx->stats.launches++;
+    }
     if (!v->hPair) {
         pt_view *mv = const_cast<pt_view *>(v);
         PT_TRY(pt_dalloc(ctx, (void **)&mv->hPair, sizeof(uint32_t) * 8 * mv->n_ct * (v->E_pad / 2) * XT_C));

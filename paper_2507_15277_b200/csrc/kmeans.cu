@@ -166,6 +166,8 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
     PT_TRY(pt_dalloc(ctx, (void **)&d_cnt, sizeof(int32_t) * k));
     PT_TRY(pt_dalloc(ctx, (void **)&d_sel, sizeof(int32_t) * k));
     PT_CK(cudaMemcpyAsync(d_envs, envs.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice, s));
+    // the whole D block is copied back each time, only nc columns are written
+    PT_CK(cudaMemsetAsync(D, 0, sizeof(double) * ne * KM_MAXK, s));
     k_km_build<<<(unsigned)C, 128, 0, s>>>(ctx->T32, C, ctx->best, ctx->penalty, d_envs, ne, X);
     const unsigned gc = (unsigned)((C + 127) / 128), gq = (unsigned)((ne + 127) / 128);
     std::vector<double> hD(ne * KM_MAXK), dmin(ne);

@@ -234,16 +234,6 @@ __global__ void k_half(const double *__restrict__ l64, int64_t E, int64_t C, int
     }
 }
 
-// hC[c][e] = the same fp16(l64[c][e]) as hT, config-major (0 for padded configs)
-__global__ void k_half_cfg(const double *__restrict__ l64, int64_t E, int64_t C, int64_t E_pad,
-                           int64_t C_pad, uint16_t *__restrict__ hC)
-{
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= C_pad * E_pad) return;
-    const int64_t c = i / E_pad, e = i % E_pad;
-    hC[i] = (c < C && e < E) ? __half_as_ushort(__double2half(l64[c * E_pad + e])) : (uint16_t)0;
-}
-
 // ---------------------------------------------------------------------------
 static pt_status alloc_view(pt_ctx *ctx, pt_view &v, int64_t E, int64_t C)
 {
@@ -271,10 +261,7 @@ pt_status pt_view_fp16(pt_ctx *ctx, const pt_view *cv)
     PT_CK(cudaMemsetAsync(v.hT, 0, sizeof(uint16_t) * v.E_pad * v.C_pad, ctx->stream));
     dim3 grid((unsigned)((v.C + 31) / 32), (unsigned)((v.E_pad + 31) / 32));
     k_half<<<grid, dim3(32, 8), 0, ctx->stream>>>(v.l64, v.E, v.C, v.E_pad, v.C_pad, v.hT);
-    PT_TRY(pt_dalloc(ctx, (void **)&v.hC, sizeof(uint16_t) * v.E_pad * v.C_pad));
-    k_half_cfg<<<(unsigned)((v.C_pad * v.E_pad + 255) / 256), 256, 0, ctx->stream>>>(v.l64, v.E, v.C, v.E_pad,
-                                                                                  v.C_pad, v.hC);
-    ctx->stats.launches += 2;
+    ctx->stats.launches += 1;
     PT_CK(cudaGetLastError());
     return PT_OK;
 }
