@@ -61,8 +61,17 @@
 #define XT_S 3      // pipeline stages
 #endif
 #ifndef XT_G8
-#define XT_G8 0     // 1: 8-env fp16 tree per FHADD (instead of 4)
+#define XT_G8 2     // 0: one 4-env fp16 tree per FHADD; 1: one 8-env tree; 2: XT_NG 4-env trees chained in fp16
+// measured (k=3, paper shape): 0 -> 13.67 ms, 2/NG=2 -> 13.48, 2/NG=4 -> 13.37 (unroll 2), 2/NG=8 -> 13.42
 #endif
+#ifndef XT_PUNROLL
+#define XT_PUNROLL 2  // unroll of the 4*XT_NG-env loop for XT_G8 == 2
+#endif
+[[maybe_unused]] static constexpr int kXtPUnroll = XT_PUNROLL;
+#ifndef XT_NG
+#define XT_NG 4       // XT_G8 == 2: 4-env tree results summed in fp16 per FHADD (XT_K % (4 NG) == 0)
+#endif
+static_assert(XT_K % (4 * XT_NG) == 0, "a pipeline stage must hold whole fp16 chains");
 #define XT_EMAX 768 // widest scope the resident-A kernel takes (smem)
 #define XT_UMAX 1024 // column tiles per task (a whole row tile: A staged once)
 #define KEY_BITS 21
@@ -450,7 +459,50 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 if (!skip) {
                     const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
                     const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
-#if XT_G8
+#if XT_G8 == 2
+                    // XT_NG 4-env fp16 trees per unit summed in fp16 (one HADD2 each) before
+                    // the two FHADD: (8 NG + 1) slots per 8 NG (set, env) pairs of columns
+                    // instead of 9 NG; the running fp16 partial waits in pp[][] (16 registers)
+                    // while the next group loads
+#pragma unroll kXtPUnroll
+                    for (int e = 0; e < XT_K; e += 4 * XT_NG) {
+                        uint32_t pp[8][2];
+#pragma unroll
+                        for (int gq = 0; gq < XT_NG; gq++) {
+                            uint4 ar[4];
+                            uint2 bc[4];
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                ar[t] = *reinterpret_cast<const uint4 *>(A + (e + 4 * gq + t) * XT_R);
+                                bc[t] = *reinterpret_cast<const uint2 *>(B + (e + 4 * gq + t) * (XT_C / 2));
+                            }
+#pragma unroll
+                            for (int i = 0; i < 8; i++) {
+                                uint32_t av[4];
+#pragma unroll
+                                for (int t = 0; t < 4; t++) {
+                                    const uint32_t w = (i >> 1) == 0 ? ar[t].x : (i >> 1) == 1 ? ar[t].y
+                                                                     : (i >> 1) == 2 ? ar[t].z : ar[t].w;
+                                    av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                                }
+                                const uint32_t tx = hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
+                                                          hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x)));
+                                const uint32_t ty = hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                                          hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y)));
+                                if (gq == 0) {
+                                    pp[i][0] = tx;
+                                    pp[i][1] = ty;
+                                } else if (gq < XT_NG - 1) {
+                                    pp[i][0] = hadd2(pp[i][0], tx);
+                                    pp[i][1] = hadd2(pp[i][1], ty);
+                                } else {
+                                    fhadd2(acc[i][0], acc[i][1], hadd2(pp[i][0], tx));
+                                    fhadd2(acc[i][2], acc[i][3], hadd2(pp[i][1], ty));
+                                }
+                            }
+                        }
+                    }
+#elif XT_G8
 #pragma unroll 1
                     for (int e = 0; e < XT_K; e += 8) {
                         uint4 ar[8];
@@ -614,7 +666,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
 #ifndef XM_UNROLL
 #define XM_UNROLL 2
 #endif
-static constexpr int kXmUnroll = XM_UNROLL;
+[[maybe_unused]] static constexpr int kXmUnroll = XM_UNROLL;
 // bank swizzle of hPair: 16-byte chunk ch of env pair pp is stored at chunk
 // ch ^ pair_swz(pp & 3) (see the B loads in k_exh_mma)
 __host__ __device__ __forceinline__ int pair_swz(int q)
@@ -1111,11 +1163,14 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     // The kernel turns them into a lower bound LB <= s <= UB per set (directed rounding)
     // and keeps every set with LB <= min(tau_seed, U), U = smallest 2nd-best UB seen.
     const double u16 = std::ldexp(1.0, -11), u32 = std::ldexp(1.0, -24);
-    const double ngrp = (double)v->E_pad / (XT_G8 ? 8.0 : 4.0) + 2.0;
+    // envs per fp32 addition and fp16 rounding levels per term (quantisation + tree + fp16 chain)
+    const double env_per_add = XT_G8 == 2 ? 4.0 * XT_NG : XT_G8 ? 8.0 : 4.0;
+    const double lv16 = XT_G8 == 2 ? 2.0 + XT_NG : XT_G8 ? 4.0 : 3.0;
+    const double ngrp = (double)v->E_pad / env_per_add + 2.0;
     const double gam = ngrp * u32 / (1.0 - ngrp * u32);
     const double gamE = ((double)v->E_pad + 2.0) * u32 / (1.0 - ((double)v->E_pad + 2.0) * u32);
     // quantisation u16 + a (2 or 3)-level fp16 tree
-    const double eta_rel16 = ((XT_G8 ? 4.0 : 3.0) * u16 + 6.0 * u16 * u16 + gam) * 1.01;
+    const double eta_rel16 = (lv16 * u16 + lv16 * lv16 * u16 * u16 + gam) * 1.01;
     const double eta_abs16 = 3.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
     const double eta_A = (4.0 * u16 + 6.0 * u16 * u16 + gam + 2.0 * gamE + 4.0 * u32) * 1.02;
     const double eta_abs_r = 4.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
