@@ -487,8 +487,14 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                                 }
                                 const uint32_t tx = hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
                                                           hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x)));
-                                const uint32_t ty = hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
-                                                          hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y)));
+                                // rows i < RELU_ROWS: the second column pair in relu form on the
+                                // FMA pipe (balances the ALU pipe; epilogue: s_hat = sum A - sum relu)
+                                const uint32_t ty =
+                                    i < RELU_ROWS
+                                        ? hadd2(hadd2(hrelu_sub2(av[0], bc[0].y), hrelu_sub2(av[1], bc[1].y)),
+                                                hadd2(hrelu_sub2(av[2], bc[2].y), hrelu_sub2(av[3], bc[3].y)))
+                                        : hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                                hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y)));
                                 if (gq == 0) {
                                     pp[i][0] = tx;
                                     pp[i][1] = ty;
@@ -1172,7 +1178,11 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     // quantisation u16 + a (2 or 3)-level fp16 tree
     const double eta_rel16 = (lv16 * u16 + lv16 * lv16 * u16 * u16 + gam) * 1.01;
     const double eta_abs16 = 3.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
-    const double eta_A = (4.0 * u16 + 6.0 * u16 * u16 + gam + 2.0 * gamE + 4.0 * u32) * 1.02;
+    // relu form: quantisation of A and B (2 u16 sumA: relu is 1-Lipschitz and nonzero only
+    // where b < a), sumA's own quantisation (u16), and L16 + 1 fp16 roundings on the relu
+    // terms (HFMA2 + tree + chain), all relative to sumA >= s; plus the fp32 sums
+    const double lvr = lv16 + 3.0;
+    const double eta_A = (lvr * u16 + lvr * lvr * u16 * u16 + gam + 2.0 * gamE + 4.0 * u32) * 1.02;
     const double eta_abs_r = 4.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
     auto f_up = [](double x) -> float {
         if (!(x < 3.0e38)) return INFINITY;

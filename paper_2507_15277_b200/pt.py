@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpt.so")
+LIB_PATH = os.environ.get("PT_LIB") or os.path.join(_HERE, "libpt.so")   # PT_LIB: a variant build (tests)
 
 PT_OK, PT_EINVAL, PT_ENOMEM, PT_ECUDA, PT_ENCCL, PT_ECAP, PT_EEMPTY, PT_EDATA = 0, -1, -2, -3, -4, -5, -6, -7
 PT_OBJ_GEOMEAN, PT_OBJ_FLEET = 0, 1
