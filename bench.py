@@ -49,9 +49,14 @@ def peaks():
         return {}
 
 
+# BENCH_SAME_GPU=1 (debug only): every rank on cuda:0 with the gloo backend, to smoke-test
+# the multi-process path on a one-GPU box; never used for a reported number
+SAME_GPU = os.environ.get("BENCH_SAME_GPU") == "1"
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
-            int(os.environ.get("LOCAL_RANK", 0)))
+            0 if SAME_GPU else int(os.environ.get("LOCAL_RANK", 0)))
 
 
 class ClockSampler:
@@ -245,7 +250,10 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SAME_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
 
     T, dev = synth.paper_matrix(args.seed)
@@ -306,6 +314,8 @@ def main():
 
     ms, k3_ms, launches, res, d2h, clocks = timed(dT, args.steps, args.warmup)
     ms_e2e, _, _, _, d2h_e2e, clocks_e2e = timed(hT, args.steps, 1)
+    # secondary config-5 line: every rank takes part (sharded greedy for world > 1)
+    scaled = None if args.no_scaled else measure_scaled(pt, synth, local, peaks(), world=world)
 
     if rank != 0:
         if world > 1:
@@ -337,7 +347,6 @@ def main():
         rate, cores, sample = oracle_sample_rate(T, dev)
         cpu = {"value": rate, "unit": "sets/s", "cores": cores, "kind": "oracle", "sample": sample}
 
-    scaled = None if args.no_scaled else measure_scaled(pt, synth, local, pk, world=world)
 
     import json as _j
     gold = None
@@ -359,7 +368,7 @@ def main():
         "data": "synthetic (seeded generator, paper shape; private dataset unavailable)",
         "config": {"workload": WORKLOAD, "sets_per_step": SETS_PER_STEP, "seed": args.seed,
                    "l2": "flushed between steps (256 MiB write, inside the timed region)",
-                   "parallelism": f"subset-space shards x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"subset-space shards x{world}" + (" (DEBUG: all ranks on one GPU, gloo)" if SAME_GPU else "")) if world > 1 else "single GPU"},
         "e2e": {"value": SETS_PER_STEP * args.steps / (ms_e2e * 1e-3), "unit": "sets/s",
                 "h2d_bytes_per_step": int(T.nbytes), "d2h_bytes_per_step": int(d2h_e2e)},
         "gpu_launches": int(launches),
