@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 const int slot = G % XT_S;
                 mbar_wait(&full[slot], (G / XT_S) & 1u);
                 // the whole warp's column half lies past the last config: skip the math
-                const bool skip = ltile + (XM_TC == 8 ? 0 : 32 * (warp & 1)) >= p.C;
+                const bool skip = ltile + 32 * (warp & 1) >= p.C;
                 if (!skip) {
                     const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
                     const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
