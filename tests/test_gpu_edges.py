@@ -103,3 +103,24 @@ def test_every_subset_is_evaluated(C, k):
         assert st["exh_candidates"] == st["exh_sets"]
         tot += st["exh_candidates"]
     assert tot == math.comb(C, k)
+
+
+def test_near_tie_below_fp16_resolution():
+    """Clones of the best triple's members, each 2e-6 slower everywhere: every
+    triple using a clone is worse than the best by ~1e-7..1e-6 in G -- far below
+    what the packed-fp16 filter resolves (2^-11 relative), far above the 1e-9
+    bar: the window must keep them and the fp64 refine must order them exactly
+    (best, runner-up and both G), as the oracle does."""
+    T, dev = synth.small_matrix(17, n_cfg=160, n_dev=3, n_inputs=12)
+    b = Oracle(T, dev).exhaustive(3)[0]
+    T = T.copy()
+    T[:, 150:153] = T[:, list(b)] * np.float32(1.0 + 2e-6)
+    o = Oracle(T, dev)
+    ob, og, orr, ogr = o.exhaustive(3)
+    assert ob == b and any(c >= 150 for c in orr)
+    assert 1e-9 < og - ogr < 1e-5
+    ctx = pt.pt_load_perf(T, dev)
+    r = pt.pt_exhaustive_best(ctx, 3)
+    assert r["best"] == ob and r["runner"] == orr
+    assert r["G"] == pytest.approx(og, rel=1e-12) and r["G_runner"] == pytest.approx(ogr, rel=1e-12)
+    assert pt.pt_get_stats(ctx)["exh_candidates"] >= 4   # the near-tied sets all reached the refine
