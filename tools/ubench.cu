@@ -49,6 +49,16 @@ __global__ void __launch_bounds__(256) kern(float *out, const float *in, unsigne
                              : "+f"(a[i]), "+f"(a[i + 1]) : "f"(b[i]), "f"(b[i + 1]));
             if (OP == 8) asm volatile("min.s32 %0, %0, %1;" : "+r"(*(int *)&a[i]) : "r"(*(int *)&b[i]));   // IMNMX
             if (OP == 9) asm volatile("min.f16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));  // HMNMX2
+            if (OP == 12) asm volatile("min.u16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));  // VIMNMX.U16x2
+            if (OP == 13) {   // alternate HMNMX2 / VIMNMX.U16x2: do they share a pipe?
+                if (i & 1) asm volatile("min.u16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));
+                else asm volatile("min.f16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));
+            }
+            if (OP == 14) asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(a[i]) : "f"(b[i]), "f"(b[(i + 1) % CH]));  // FMNMX3
+            if (OP == 15) {   // alternate HMNMX2 / HADD2 (ALU + FMA pipes)
+                if (i & 1) asm volatile("add.rn.f16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));
+                else asm volatile("min.f16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));
+            }
             if (OP == 10) {  // |a-b| accumulate: FADD + FADD(|.|)
                 float d;
                 asm volatile("sub.f32 %0, %1, %2;" : "=f"(d) : "f"(a[i]), "f"(b[i]));
@@ -119,5 +129,9 @@ int main()
     run<8>("IMNMX", 1, nsm);
     run<9>("HMNMX2 (f16x2 words)", 1, nsm);
     run<10>("sub+abs-add (evals)", 1, nsm);
+    run<12>("VIMNMX.U16x2 (words)", 1, nsm);
+    run<13>("HMNMX2|VIMNMX.U16x2 alt", 1, nsm);
+    run<14>("FMNMX3", 1, nsm);
+    run<15>("HMNMX2|HADD2 alt", 1, nsm);
     return 0;
 }
