@@ -336,9 +336,15 @@ def main():
     achieved = evals / (k3_avg * 1e-3) / 1e12
     peak = nsm * 128 * sm_max * 1e6 / 1e12
     peak_fp32 = nsm * 64 * sm_max * 1e6 / 1e12
-    traffic = None
+    traffic, l2 = None, None
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "k3_dram_bytes.json")))["bytes_per_launch"]
+        prof = json.load(open(os.path.join(ROOT, "profiles", "k3_dram_bytes.json")))
+        traffic = prof["bytes_per_launch"]
+        if prof.get("l2_bytes_per_launch"):
+            l2 = {"bytes_per_launch": prof["l2_bytes_per_launch"],
+                  "GB_s": prof["l2_bytes_per_launch"] / (k3_avg * 1e-3) / 1e9,
+                  "pct_of_peak": prof.get("l2_throughput_pct_of_peak"),
+                  "source": "ncu lts__t_sectors.sum x 32 B and lts__throughput, one --set full capture"}
     except Exception:
         pass
 
@@ -376,10 +382,13 @@ def main():
                      "peak": peak, "unit": "T(set,env)/s", "frac": achieved / peak, "traffic": traffic,
                      "work_per_set": f"{E_PAPER} (set,env) evaluations = {E_PAPER} min + {E_PAPER} add",
                      "peak_basis": f"ALU-pipe min ceiling: {nsm} SMs x 4 SMSP x 16 lanes/clk x 2 mins "
-                                   f"(f16x2 HMNMX2) x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                                   f"(f16x2 HMNMX2) x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); "
+                                   "the packed adds (HADD2, half rate on the FMA pipe) and the issue "
+                                   "port have the same ceiling (DESIGN.md 6.1)",
                      "fp32_roofline": {"peak": peak_fp32, "frac": achieved / peak_fp32,
                                        "basis": "one FMNMX (16 lanes/clk/SMSP) + one FADD per (set, env)"},
-                     "kernel_ms": k3_avg, "kernel_share_of_step": k3_avg / (ms / args.steps)},
+                     "kernel_ms": k3_avg, "kernel_share_of_step": k3_avg / (ms / args.steps),
+                     "l2": l2},
         "cpu_baseline": cpu,
         "clocks": clocks,
         "clocks_e2e": clocks_e2e,

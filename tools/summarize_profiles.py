@@ -41,7 +41,9 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__bytes_read.sum.per_second",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__registers_per_thread",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_sectors.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "launch__registers_per_thread",
         "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.per_cycle_active",
         "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers"]
 
@@ -76,8 +78,13 @@ open(os.path.join(out, "k3_ncu_summary.txt"), "w").write("\n".join(k3) + "\n")
 unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 b = sum(float(vals[k][0].replace(",", "")) * unit.get(vals[k][1], 1)
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in vals)
+l2 = float(vals["lts__t_sectors.sum"][0].replace(",", "")) * 32 if "lts__t_sectors.sum" in vals else None
+l2pct = float(vals["lts__throughput.avg.pct_of_peak_sustained_elapsed"][0]) \
+    if "lts__throughput.avg.pct_of_peak_sustained_elapsed" in vals else None
 json.dump({"kernel": "k_exh_tiled k=3 paper shape", "bytes_per_launch": b,
-           "source": f"profiles/{rnd}/k3_ncu_summary.txt (dram__bytes_read.sum + dram__bytes_write.sum)"},
+           "l2_bytes_per_launch": l2, "l2_throughput_pct_of_peak": l2pct,
+           "source": f"profiles/{rnd}/k3_ncu_summary.txt (dram__bytes_read.sum + dram__bytes_write.sum; "
+                     "lts__t_sectors.sum x 32 B; lts__throughput)"},
           open(os.path.join(ROOT, "profiles", "k3_dram_bytes.json"), "w"), indent=1)
 sc, _ = summary(scanrep, "k_greedy_scan, scaled greedy step (65,536 configs x 4,096 envs, 1 GiB fp32 stream)")
 open(os.path.join(out, "scan_ncu_summary.txt"), "w").write("\n".join(sc) + "\n")
