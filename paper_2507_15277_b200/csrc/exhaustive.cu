@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
 
     uint32_t steps = 0;   // pipeline steps of all previous tasks (same in every thread)
     const int tx = lane & 7, ty = lane >> 3;
-    float b1 = INFINITY, b2 = INFINITY, published = INFINITY;
+    float bA = INFINITY, bB = INFINITY, published = INFINITY;   // acc-domain group minima (window U)
 
     for (;;) {
         if (tid == 0) {
@@ -426,16 +426,6 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 }
             }
             named_sync(1, XT_CONS);
-            // row sums of A (fp32, e ascending) for the relu-form units, and
-            // their error bound eta_A * sumA + eta_abs (rounded up)
-            if (RELU_ROWS > 0 && tid < XT_R) {
-                float sa = 0.0f;
-                for (int64_t e = 0; e < p.E_pad; e++)
-                    sa += __half2float(__ushort_as_half(As[e * XT_R + tid]));
-                sumA_s[tid] = sa;
-                bnd_s[tid] = __fmaf_ru(p.eta_A, sa, p.eta_abs_r);
-            }
-            if (RELU_ROWS > 0) named_sync(1, XT_CONS);
 
             float acc[8][4];
 #pragma unroll
@@ -448,33 +438,105 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
             // consecutive columns (one 8-byte LDS)
             const int r0 = 32 * (warp >> 1) + 8 * ty;
             const int c0 = 32 * (warp & 1) + 4 * tx;
-            int q = 0;
+            // colex order: a row's largest member is non-decreasing in its rank (padding
+            // rows hold INT_MAX), so the thread's last row bounds all eight
+            const int last7 = last_s[r0 + 7];
+            uint32_t slot = steps % XT_S, phase = (steps / XT_S) & 1u;
             int64_t ltile = lo + (int64_t)tk.y * XT_C;     // first column of the current tile
-            uint32_t G = steps;
-            for (int g = 0; g < nsteps; g++, G++) {
-                const int slot = G % XT_S;
-                mbar_wait(&full[slot], (G / XT_S) & 1u);
+            for (int ct = tk.y; ct < tk.z; ct++, ltile += XT_C) {
                 // the whole warp's column half lies past the last config: skip the math
                 const bool skip = ltile + 32 * (warp & 1) >= p.C;
-                if (!skip) {
-                    const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
-                    const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
+                // window threshold for this tile's epilogue, loaded before the math so the
+                // L2 latency hides behind it (a stale value is only a looser bound)
+                const unsigned Ubits = *(volatile unsigned *)p.U;
+                for (int q = 0; q < nkc; q++) {
+                    mbar_wait(&full[slot], phase);
+                    if (!skip) {
+                        const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
+                        const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
 #if XT_G8 == 2
-                    // XT_NG 4-env fp16 trees per unit summed in fp16 (one HADD2 each) before
-                    // the two FHADD: (8 NG + 1) slots per 8 NG (set, env) pairs of columns
-                    // instead of 9 NG; the running fp16 partial waits in pp[][] (16 registers)
-                    // while the next group loads
+                        // XT_NG 4-env fp16 trees per unit summed in fp16 (one HADD2 each) before
+                        // the two FHADD: (8 NG + 1) slots per 8 NG (set, env) pairs of columns
+                        // instead of 9 NG; the running fp16 partial waits in pp[][] (16 registers)
+                        // while the next group loads
 #pragma unroll kXtPUnroll
-                    for (int e = 0; e < XT_K; e += 4 * XT_NG) {
-                        uint32_t pp[8][2];
+                        for (int e = 0; e < XT_K; e += 4 * XT_NG) {
+                            uint32_t pp[8][2];
 #pragma unroll
-                        for (int gq = 0; gq < XT_NG; gq++) {
+                            for (int gq = 0; gq < XT_NG; gq++) {
+                                uint4 ar[4];
+                                uint2 bc[4];
+#pragma unroll
+                                for (int t = 0; t < 4; t++) {
+                                    ar[t] = *reinterpret_cast<const uint4 *>(A + (e + 4 * gq + t) * XT_R);
+                                    bc[t] = *reinterpret_cast<const uint2 *>(B + (e + 4 * gq + t) * (XT_C / 2));
+                                }
+#pragma unroll
+                                for (int i = 0; i < 8; i++) {
+                                    uint32_t av[4];
+#pragma unroll
+                                    for (int t = 0; t < 4; t++) {
+                                        const uint32_t w = (i >> 1) == 0 ? ar[t].x : (i >> 1) == 1 ? ar[t].y
+                                                                         : (i >> 1) == 2 ? ar[t].z : ar[t].w;
+                                        av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                                    }
+                                    const uint32_t tx = hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
+                                                              hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x)));
+                                    const uint32_t ty = hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                                              hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y)));
+                                    if (gq == 0) {
+                                        pp[i][0] = tx;
+                                        pp[i][1] = ty;
+                                    } else if (gq < XT_NG - 1) {
+                                        pp[i][0] = hadd2(pp[i][0], tx);
+                                        pp[i][1] = hadd2(pp[i][1], ty);
+                                    } else {
+                                        fhadd2(acc[i][0], acc[i][1], hadd2(pp[i][0], tx));
+                                        fhadd2(acc[i][2], acc[i][3], hadd2(pp[i][1], ty));
+                                    }
+                                }
+                            }
+                        }
+#elif XT_G8
+#pragma unroll 1
+                        for (int e = 0; e < XT_K; e += 8) {
+                            uint4 ar[8];
+                            uint2 bc[8];
+#pragma unroll
+                            for (int t = 0; t < 8; t++) {
+                                ar[t] = *reinterpret_cast<const uint4 *>(A + (e + t) * XT_R);
+                                bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
+                            }
+#pragma unroll
+                            for (int i = 0; i < 8; i++) {
+                                uint32_t av[8];
+#pragma unroll
+                                for (int t = 0; t < 8; t++) {
+                                    const uint32_t w = (i >> 1) == 0 ? ar[t].x : (i >> 1) == 1 ? ar[t].y
+                                                                     : (i >> 1) == 2 ? ar[t].z : ar[t].w;
+                                    av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                                }
+                                fhadd2(acc[i][0], acc[i][1],
+                                       hadd2(hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
+                                                   hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))),
+                                             hadd2(hadd2(hmin2(av[4], bc[4].x), hmin2(av[5], bc[5].x)),
+                                                   hadd2(hmin2(av[6], bc[6].x), hmin2(av[7], bc[7].x)))));
+                                fhadd2(acc[i][2], acc[i][3],
+                                       hadd2(hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                                   hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))),
+                                             hadd2(hadd2(hmin2(av[4], bc[4].y), hmin2(av[5], bc[5].y)),
+                                                   hadd2(hmin2(av[6], bc[6].y), hmin2(av[7], bc[7].y)))));
+                            }
+                        }
+#else
+#pragma unroll 2
+                        for (int e = 0; e < XT_K; e += 4) {
                             uint4 ar[4];
                             uint2 bc[4];
 #pragma unroll
                             for (int t = 0; t < 4; t++) {
-                                ar[t] = *reinterpret_cast<const uint4 *>(A + (e + 4 * gq + t) * XT_R);
-                                bc[t] = *reinterpret_cast<const uint2 *>(B + (e + 4 * gq + t) * (XT_C / 2));
+                                ar[t] = *reinterpret_cast<const uint4 *>(A + (e + t) * XT_R);
+                                bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
                             }
 #pragma unroll
                             for (int i = 0; i < 8; i++) {
@@ -485,152 +547,86 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                                                                      : (i >> 1) == 2 ? ar[t].z : ar[t].w;
                                     av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
                                 }
-                                const uint32_t tx = hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
-                                                          hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x)));
-                                // rows i < RELU_ROWS: the second column pair in relu form on the
-                                // FMA pipe (balances the ALU pipe; epilogue: s_hat = sum A - sum relu)
-                                const uint32_t ty =
-                                    i < RELU_ROWS
-                                        ? hadd2(hadd2(hrelu_sub2(av[0], bc[0].y), hrelu_sub2(av[1], bc[1].y)),
-                                                hadd2(hrelu_sub2(av[2], bc[2].y), hrelu_sub2(av[3], bc[3].y)))
-                                        : hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
-                                                hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y)));
-                                if (gq == 0) {
-                                    pp[i][0] = tx;
-                                    pp[i][1] = ty;
-                                } else if (gq < XT_NG - 1) {
-                                    pp[i][0] = hadd2(pp[i][0], tx);
-                                    pp[i][1] = hadd2(pp[i][1], ty);
-                                } else {
-                                    fhadd2(acc[i][0], acc[i][1], hadd2(pp[i][0], tx));
-                                    fhadd2(acc[i][2], acc[i][3], hadd2(pp[i][1], ty));
-                                }
-                            }
-                        }
-                    }
-#elif XT_G8
-#pragma unroll 1
-                    for (int e = 0; e < XT_K; e += 8) {
-                        uint4 ar[8];
-                        uint2 bc[8];
-#pragma unroll
-                        for (int t = 0; t < 8; t++) {
-                            ar[t] = *reinterpret_cast<const uint4 *>(A + (e + t) * XT_R);
-                            bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
-                        }
-#pragma unroll
-                        for (int i = 0; i < 8; i++) {
-                            uint32_t av[8];
-#pragma unroll
-                            for (int t = 0; t < 8; t++) {
-                                const uint32_t w = (i >> 1) == 0 ? ar[t].x : (i >> 1) == 1 ? ar[t].y
-                                                                 : (i >> 1) == 2 ? ar[t].z : ar[t].w;
-                                av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
-                            }
-                            fhadd2(acc[i][0], acc[i][1],
-                                   hadd2(hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
-                                               hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))),
-                                         hadd2(hadd2(hmin2(av[4], bc[4].x), hmin2(av[5], bc[5].x)),
-                                               hadd2(hmin2(av[6], bc[6].x), hmin2(av[7], bc[7].x)))));
-                            fhadd2(acc[i][2], acc[i][3],
-                                   hadd2(hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
-                                               hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))),
-                                         hadd2(hadd2(hmin2(av[4], bc[4].y), hmin2(av[5], bc[5].y)),
-                                               hadd2(hmin2(av[6], bc[6].y), hmin2(av[7], bc[7].y)))));
-                        }
-                    }
-#else
-#pragma unroll 2
-                    for (int e = 0; e < XT_K; e += 4) {
-                        uint4 ar[4];
-                        uint2 bc[4];
-#pragma unroll
-                        for (int t = 0; t < 4; t++) {
-                            ar[t] = *reinterpret_cast<const uint4 *>(A + (e + t) * XT_R);
-                            bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
-                        }
-#pragma unroll
-                        for (int i = 0; i < 8; i++) {
-                            uint32_t av[4];
-#pragma unroll
-                            for (int t = 0; t < 4; t++) {
-                                const uint32_t w = (i >> 1) == 0 ? ar[t].x : (i >> 1) == 1 ? ar[t].y
-                                                                 : (i >> 1) == 2 ? ar[t].z : ar[t].w;
-                                av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
-                            }
-                            // fp16 tree over the 4 envs, then 2 FHADD into fp32.
-                            // Units (i < 4, column pair 1) use the relu form on the
-                            // FMA pipe, the rest HMNMX2 on the ALU pipe: balances
-                            // the two pipes (1/4 of the units relu)
-                            fhadd2(acc[i][0], acc[i][1],
-                                   hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
-                                         hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))));
-                            if (i < RELU_ROWS)
-                                fhadd2(acc[i][2], acc[i][3],
-                                       hadd2(hadd2(hrelu_sub2(av[0], bc[0].y), hrelu_sub2(av[1], bc[1].y)),
-                                             hadd2(hrelu_sub2(av[2], bc[2].y), hrelu_sub2(av[3], bc[3].y))));
-                            else
+                                // fp16 tree over the 4 envs, then 2 FHADD into fp32
+                                fhadd2(acc[i][0], acc[i][1],
+                                       hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
+                                             hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x))));
                                 fhadd2(acc[i][2], acc[i][3],
                                        hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
                                              hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y))));
+                            }
                         }
-                    }
 #endif
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[slot]);
+                    if (++slot == XT_S) {
+                        slot = 0;
+                        phase ^= 1u;
+                    }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
-                if (++q == nkc) {
-                    q = 0;
-                    if (!skip) {
-                        // epilogue of one column tile: per-set lower/upper bounds of
-                        // the exact score, window test, candidate append
-                        const float tau = fminf(p.tau_seed, __uint_as_float(*(volatile unsigned *)p.U));
-                        const int64_t l0 = ltile + c0;
+                if (skip) continue;
+                // ---- epilogue of one column tile ----
+                // LB = RD(acc*c1 - c2) and UB = RU(acc*c3 + c4) are non-decreasing in acc, so
+                // order statistics and the window test are taken on acc itself and mapped
+                // once.  Padding / ragged sets become +inf.
+                const int64_t l0 = ltile + c0;
+                if (!(l0 + 3 < p.C && l0 > last7)) {
 #pragma unroll
-                        for (int i = 0; i < 8; i++) {
-                            const int r = r0 + i;
-                            const int last = last_s[r];
-                            const float sA = RELU_ROWS > 0 ? sumA_s[r] : 0.0f;
-                            const float bA = RELU_ROWS > 0 ? bnd_s[r] : 0.0f;
+                    for (int i = 0; i < 8; i++) {
+                        const int last = last_s[r0 + i];
 #pragma unroll
-                            for (int j = 0; j < 4; j++) {
-                                const int64_t l = l0 + j;
-                                float lb, ub;
-                                if (i < RELU_ROWS && j >= 2) {   // relu form: s_hat = sum A - sum relu
-                                    const float sh = sA - acc[i][j];
-                                    lb = __fsub_rd(sh, bA);
-                                    ub = __fadd_ru(sh, bA);
-                                } else {                 // min form
-                                    lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
-                                    ub = __fmaf_ru(acc[i][j], p.c3, p.c4);
-                                }
-                                acc[i][j] = 0.0f;
-                                if (l < p.C && l > last) {
-                                    if (ub < b1) {
-                                        b2 = b1;
-                                        b1 = ub;
-                                    } else if (ub < b2) {
-                                        b2 = ub;
-                                    }
-                                    if (lb <= tau) {
-                                        const unsigned idx = atomicAdd(p.cand_n, 1u);
-                                        if (idx < p.cap) {
-                                            p.cand_key[idx] = ((unsigned long long)(R0 + r) << KEY_BITS) |
-                                                              (unsigned long long)l;
-                                            p.cand_s[idx] = lb;
-                                        }
-                                    }
+                        for (int j = 0; j < 4; j++)
+                            if (!(l0 + j < p.C && l0 + j > last)) acc[i][j] = INFINITY;
+                    }
+                }
+                // tile minima of two disjoint column groups (j < 2, j >= 2)
+                float tA = fminf(acc[0][0], acc[0][1]), tB = fminf(acc[0][2], acc[0][3]);
+#pragma unroll
+                for (int i = 1; i < 8; i++) {
+                    tA = fminf(tA, fminf(acc[i][0], acc[i][1]));
+                    tB = fminf(tB, fminf(acc[i][2], acc[i][3]));
+                }
+                bA = fminf(bA, tA);
+                bB = fminf(bB, tB);
+                const float tau = fminf(p.tau_seed, __uint_as_float(Ubits));
+                if (__fmaf_rd(fminf(tA, tB), p.c1, -p.c2) <= tau) {   // rare: some set is in the window
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const float lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
+                            if (acc[i][j] < INFINITY && lb <= tau) {
+                                const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                if (idx < p.cap) {
+                                    p.cand_key[idx] = ((unsigned long long)(R0 + r0 + i) << KEY_BITS) |
+                                                      (unsigned long long)(l0 + j);
+                                    p.cand_s[idx] = lb;
                                 }
                             }
                         }
-                        float wb = b2;
-                        for (int o = 16; o; o >>= 1) wb = fminf(wb, __shfl_xor_sync(0xffffffffu, wb, o));
-                        if (lane == 0 && wb < published) {
-                            atomicMin(p.U, __float_as_uint(wb));
-                            published = wb;
-                        }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
+                // U: the warp's 2nd-smallest group minimum.  bA and bB of all lanes are
+                // minima over disjoint sets of sets, so the two smallest belong to two
+                // distinct sets and UB(2nd) >= s_(2)
+                float x1 = fminf(bA, bB), x2 = fmaxf(bA, bB);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const float y1 = __shfl_xor_sync(0xffffffffu, x1, o);
+                    const float y2 = __shfl_xor_sync(0xffffffffu, x2, o);
+                    x2 = fminf(fmaxf(x1, y1), fminf(x2, y2));
+                    x1 = fminf(x1, y1);
+                }
+                if (lane == 0) {
+                    const float ub = __fmaf_ru(x2, p.c3, p.c4);
+                    if (ub < published) {
+                        atomicMin(p.U, __float_as_uint(ub));
+                        published = ub;
                     }
-                    ltile += XT_C;
                 }
             }
         }
