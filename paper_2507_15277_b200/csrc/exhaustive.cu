@@ -35,7 +35,15 @@
 
 #include "pt_internal.cuh"
 
-#define XT_R 128    // rows per CTA tile (k_exh_tiled)
+#ifndef XT_R
+#define XT_R 128    // rows per CTA tile (k_exh_tiled); its consumer warps = XT_R / 16
+#endif
+#ifndef XT_SB
+#define XT_SB 32    // k_exh_tiled A staging: loads in flight per member (E_pad % (2 XT_SB) == 0)
+#endif
+#ifndef XT_MINB
+#define XT_MINB 2   // k_exh_tiled CTAs per SM the register budget is sized for
+#endif
 #ifndef XM_TC
 #define XM_TC 4     // k_exh_mma: columns per thread (4: 8x4 sets per thread, 32x64 CTA tile; 8: 8x8, 64x64)
 #endif
@@ -307,8 +315,10 @@ struct XParams {
 #ifndef RELU_ROWS
 #define RELU_ROWS 0
 #endif
-#define XT_THREADS 288
+#define XT_THREADS 288      // k_exh_mma
 #define XT_CONS 256
+#define XT_TCONS (2 * XT_R)  // k_exh_tiled consumers: 2 warps (column halves) per 32 rows
+#define XT_TTHREADS (XT_TCONS + 32)
 #define XT_BROW (XT_C * 2)     // bytes of one env row of a column tile
 
 // broadcast one fp16 lane of a word to both halves (ptxas folds this into the
@@ -332,7 +342,7 @@ __device__ __forceinline__ uint32_t bcast_hi(uint32_t w)
 #if XT_MAXREG
 __global__ void __maxnreg__(XT_MAXREG) k_exh_tiled(const XParams p)
 #else
-__global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
+__global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParams p)
 #endif
 {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -350,7 +360,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
     if (tid == 0) {
         for (int s = 0; s < XT_S; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], XT_CONS / 32);
+            mbar_init(&empty[s], XT_TCONS / 32);
         }
         mbar_fence_init();
     }
@@ -374,7 +384,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
         const int64_t lo = tile_lo(mem0[p.m - 1]);
         const int nsteps = (tk.z - tk.y) * nkc;
 
-        if (warp == XT_CONS / 32) {
+        if (warp == XT_TCONS / 32) {
             // ---------------- producer warp ----------------
             // column tile starting at config `col` (8-aligned) = shift s, tile ct
             // of hTile; each stage is one contiguous 32-env x 64-config block
@@ -400,7 +410,7 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
         } else {
             // ---------------- consumers ----------------
             // stage A for the whole task: A[e][r] = min over the row's members
-            // (fp16, non-negative: integer order).  Loads are batched 8 deep.
+            // (fp16, non-negative: integer order).  Loads are batched XT_SB deep per member.
             {
                 const int r = tid & (XT_R - 1);
                 const int64_t R = R0 + r;
@@ -409,23 +419,23 @@ __global__ void __launch_bounds__(XT_THREADS, 2) k_exh_tiled(const XParams p)
                 if (valid) pt_unrank_colex(R, p.m, p.C, mem);
                 else for (int u = 0; u < p.m; u++) mem[u] = 0;
                 if (tid < XT_R) last_s[r] = valid ? mem[p.m - 1] : 0x7fffffff;
-                const int64_t e0 = tid >> 7;
-                for (int64_t eb = e0; eb < p.E_pad; eb += 16) {
-                    uint16_t v[8];
+                const int64_t e0 = tid / XT_R;
+                for (int64_t eb = e0; eb < p.E_pad; eb += 2 * XT_SB) {
+                    uint16_t v[XT_SB];
 #pragma unroll
-                    for (int t = 0; t < 8; t++) v[t] = p.hT[(eb + 2 * t) * p.C_pad + mem[0]];
+                    for (int t = 0; t < XT_SB; t++) v[t] = p.hT[(eb + 2 * t) * p.C_pad + mem[0]];
                     for (int u = 1; u < p.m; u++) {
-                        uint16_t w[8];
+                        uint16_t w[XT_SB];
 #pragma unroll
-                        for (int t = 0; t < 8; t++) w[t] = p.hT[(eb + 2 * t) * p.C_pad + mem[u]];
+                        for (int t = 0; t < XT_SB; t++) w[t] = p.hT[(eb + 2 * t) * p.C_pad + mem[u]];
 #pragma unroll
-                        for (int t = 0; t < 8; t++) v[t] = v[t] < w[t] ? v[t] : w[t];
+                        for (int t = 0; t < XT_SB; t++) v[t] = v[t] < w[t] ? v[t] : w[t];
                     }
 #pragma unroll
-                    for (int t = 0; t < 8; t++) As[(eb + 2 * t) * XT_R + r] = valid ? v[t] : (uint16_t)0;
+                    for (int t = 0; t < XT_SB; t++) As[(eb + 2 * t) * XT_R + r] = valid ? v[t] : (uint16_t)0;
                 }
             }
-            named_sync(1, XT_CONS);
+            named_sync(1, XT_TCONS);
 
             float acc[8][4];
 #pragma unroll
@@ -1298,10 +1308,10 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.hC = v->hC;
         p.hPair = v->hPair;
         int occ = 1;
-        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT_THREADS, smem));
+        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT_MMA ? XT_THREADS : XT_TTHREADS, smem));
         const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
         PT_CK(cudaEventRecord(ctx->ev0, s));
-        kern<<<grid, XT_THREADS, smem, s>>>(p);
+        kern<<<grid, XT_MMA ? XT_THREADS : XT_TTHREADS, smem, s>>>(p);
         PT_CK(cudaEventRecord(ctx->ev1, s));
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());

@@ -55,6 +55,24 @@ __device__ __forceinline__ void warp_top2(double &s1, int &c1, double &s2, int &
     }
 }
 
+// s = sum_e min(cur[e], col[e]) over this lane's envs (e = lane, lane+32, ...,
+// ascending: the fixed order of the reduction).  The column's loads are issued
+// before the sums so one candidate costs one L2 round trip, not E_pad/32.
+__device__ __forceinline__ double lane_sum_min(const double *cur, const double *__restrict__ col,
+                                               int64_t E_pad, int lane)
+{
+    double acc = 0.0;
+    for (int64_t e0 = lane; e0 < E_pad; e0 += 32 * 16) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) v[u] = e0 + 32 * u < E_pad ? __ldg(col + e0 + 32 * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; u++)
+            if (e0 + 32 * u < E_pad) acc += fmin(cur[e0 + 32 * u], v[u]);
+    }
+    return acc;
+}
+
 // ---------------------------------------------------------------------------
 // RESIDENT fp64 cooperative kernel
 // ---------------------------------------------------------------------------
@@ -84,8 +102,7 @@ __global__ void __launch_bounds__(256) k_greedy_resident(const double *__restric
         for (int64_t c = gw; c < C; c += nw) {
             if (taken[c >> 5] >> (c & 31) & 1u) continue;
             const double *col = l64 + c * E_pad;
-            double acc = 0.0;
-            for (int64_t e = lane; e < E_pad; e += 32) acc += fmin(cur[e], col[e]);
+            double acc = lane_sum_min(cur, col, E_pad, lane);
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             top2_ins(s1, c1, s2, c2, acc, (int)c);
         }
@@ -107,10 +124,17 @@ __global__ void __launch_bounds__(256) k_greedy_resident(const double *__restric
         if (warp == 0) {
             s1 = s2 = INFINITY;
             c1 = c2 = PT_BIGI;
-            for (int b = lane; b < (int)gridDim.x; b += 32) {
-                double4 r = blk[(t & 1) * gridDim.x + b];
-                top2_ins(s1, c1, s2, c2, r.x, (int)r.z);
-                top2_ins(s1, c1, s2, c2, r.y, (int)r.w);
+            for (int b0 = lane; b0 < (int)gridDim.x; b0 += 32 * 4) {   // 4 records in flight per lane
+                double4 r[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (b0 + 32 * u < (int)gridDim.x) r[u] = blk[(t & 1) * gridDim.x + b0 + 32 * u];
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (b0 + 32 * u < (int)gridDim.x) {
+                        top2_ins(s1, c1, s2, c2, r[u].x, (int)r[u].z);
+                        top2_ins(s1, c1, s2, c2, r[u].y, (int)r[u].w);
+                    }
             }
             warp_top2(s1, c1, s2, c2);
             if (lane == 0) {

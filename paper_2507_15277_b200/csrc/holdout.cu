@@ -112,8 +112,16 @@ __global__ void __launch_bounds__(256) k_greedy_multi(const double *__restrict__
         for (int64_t c = gw; c < C; c += nw) {
             if (taken[c >> 5] >> (c & 31) & 1u) continue;
             const double *col = l64 + c * E_pad;
+            // loads issued together (one L2 round trip per candidate); e ascending per lane
             double acc = 0.0;
-            for (int64_t e = lane; e < E_pad; e += 32) acc += wp[e] * fmin(cur[e], col[e]);
+            for (int64_t e0 = lane; e0 < E_pad; e0 += 32 * 16) {
+                double v[16];
+#pragma unroll
+                for (int u = 0; u < 16; u++) v[u] = e0 + 32 * u < E_pad ? __ldg(col + e0 + 32 * u) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 16; u++)
+                    if (e0 + 32 * u < E_pad) acc += wp[e0 + 32 * u] * fmin(cur[e0 + 32 * u], v[u]);
+            }
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             hb_top2(s1, c1, s2, c2, acc, (int)c);
         }
@@ -132,17 +140,34 @@ __global__ void __launch_bounds__(256) k_greedy_multi(const double *__restrict__
             blk[(t & 1) * gridDim.x + blockIdx.x] = make_double4(s1, s2, (double)c1, (double)c2);
         }
         grid.sync();
-        if (threadIdx.x == 0) {
+        if (warp == 0) {
+            // this problem's block records, read in parallel by the lanes; the top-2 of a
+            // strict (s, c) order does not depend on the merge order
             s1 = s2 = INFINITY;
             c1 = c2 = HB_BIGI;
-            for (int b = p; b < (int)gridDim.x; b += P) {   // this problem's blocks, fixed order
-                const double4 r = blk[(t & 1) * gridDim.x + b];
-                hb_top2(s1, c1, s2, c2, r.x, (int)r.z);
-                hb_top2(s1, c1, s2, c2, r.y, (int)r.w);
+            for (int b0 = p + P * lane; b0 < (int)gridDim.x; b0 += P * 32 * 2) {
+                double4 r[2];
+#pragma unroll
+                for (int u = 0; u < 2; u++)
+                    if (b0 + P * 32 * u < (int)gridDim.x) r[u] = blk[(t & 1) * gridDim.x + b0 + P * 32 * u];
+#pragma unroll
+                for (int u = 0; u < 2; u++)
+                    if (b0 + P * 32 * u < (int)gridDim.x) {
+                        hb_top2(s1, c1, s2, c2, r[u].x, (int)r[u].z);
+                        hb_top2(s1, c1, s2, c2, r[u].y, (int)r[u].w);
+                    }
             }
-            cstar = c1;
-            last_s = s1;
-            if (bi == 0) out_idx[(int64_t)p * k + t] = c1;
+            for (int o = 16; o; o >>= 1) {
+                const double a1 = __shfl_xor_sync(0xffffffffu, s1, o), a2 = __shfl_xor_sync(0xffffffffu, s2, o);
+                const int b1 = __shfl_xor_sync(0xffffffffu, c1, o), b2 = __shfl_xor_sync(0xffffffffu, c2, o);
+                hb_top2(s1, c1, s2, c2, a1, b1);
+                hb_top2(s1, c1, s2, c2, a2, b2);
+            }
+            if (lane == 0) {
+                cstar = c1;
+                last_s = s1;
+                if (bi == 0) out_idx[(int64_t)p * k + t] = c1;
+            }
         }
         __syncthreads();
         const int cs = cstar;
