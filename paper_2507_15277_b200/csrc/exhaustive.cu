@@ -952,31 +952,37 @@ __global__ void k_tile_hT(const uint16_t *__restrict__ hT, int64_t E_pad, int64_
 // fp64 refine of the survivors: warp per candidate, fixed shuffle tree
 // ---------------------------------------------------------------------------
 __global__ void k_exh_refine(const unsigned long long *__restrict__ key,
-                             const float *__restrict__ cs, unsigned n, float tau, int m, int64_t C,
+                             const float *__restrict__ cs, const unsigned *__restrict__ n_dev, unsigned cap,
+                             float tau_pass, const unsigned *__restrict__ U, int m, int64_t C,
                              const double *__restrict__ l64, int64_t E_pad,
                              double *__restrict__ out_s, int32_t *__restrict__ out_t)
 {
-    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // survivors = min(count, cap); final threshold = min(tau_pass, U) (the kernel's U
+    // is complete once this launch starts: stream order)
+    const int64_t n = min(*n_dev, cap);
+    const float tau = fminf(tau_pass, __uint_as_float(*U));
     const int lane = threadIdx.x & 31;
-    if (w >= n) return;
     const int k = m + 1;
-    int32_t tup[PT_MAXK];
-    const unsigned long long kv = key[w];
-    pt_unrank_colex((int64_t)(kv >> KEY_BITS), m, C, tup);
-    tup[m] = (int32_t)(kv & ((1ull << KEY_BITS) - 1));
-    if (lane < k) out_t[w * k + lane] = tup[lane];
-    if (cs[w] > tau) {
-        if (lane == 0) out_s[w] = INFINITY;
-        return;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int32_t tup[PT_MAXK];
+        const unsigned long long kv = key[w];
+        pt_unrank_colex((int64_t)(kv >> KEY_BITS), m, C, tup);
+        tup[m] = (int32_t)(kv & ((1ull << KEY_BITS) - 1));
+        if (lane < k) out_t[w * k + lane] = tup[lane];
+        if (cs[w] > tau) {
+            if (lane == 0) out_s[w] = INFINITY;
+            continue;
+        }
+        double acc = 0.0;
+        for (int64_t e = lane; e < E_pad; e += 32) {
+            double v = l64[(int64_t)tup[0] * E_pad + e];
+            for (int u = 1; u < k; u++) v = fmin(v, l64[(int64_t)tup[u] * E_pad + e]);
+            acc += v;
+        }
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out_s[w] = acc;
     }
-    double acc = 0.0;
-    for (int64_t e = lane; e < E_pad; e += 32) {
-        double v = l64[(int64_t)tup[0] * E_pad + e];
-        for (int u = 1; u < k; u++) v = fmin(v, l64[(int64_t)tup[u] * E_pad + e]);
-        acc += v;
-    }
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) out_s[w] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -1005,10 +1011,12 @@ __device__ __forceinline__ void rec_offer(Rec2 &r, double s, const int32_t *t, i
     }
 }
 
+// n records, or min(*n_dev, cap) when n_dev is given (a device-side count)
 __global__ void __launch_bounds__(256) k_top2(const double *__restrict__ s, const int32_t *__restrict__ t,
-                                             int64_t n, int k, double *__restrict__ out_s,
-                                             int32_t *__restrict__ out_t)
+                                             int64_t n, const unsigned *__restrict__ n_dev, unsigned cap,
+                                             int k, double *__restrict__ out_s, int32_t *__restrict__ out_t)
 {
+    if (n_dev) n = min(*n_dev, cap);
     __shared__ Rec2 sh[256];
     Rec2 r;
     r.s1 = r.s2 = INFINITY;
@@ -1090,14 +1098,15 @@ pt_status pt_top2_records(pt_ctx *ctx, const double *d_s, const int32_t *d_t, in
     int32_t *ot = nullptr;
     PT_TRY(pt_dalloc(ctx, (void **)&os, sizeof(double) * 2));
     PT_TRY(pt_dalloc(ctx, (void **)&ot, sizeof(int32_t) * 2 * k));
-    k_top2<<<1, 256, 0, ctx->stream>>>(d_s, d_t, n, k, os, ot);
+    k_top2<<<1, 256, 0, ctx->stream>>>(d_s, d_t, n, nullptr, 0, k, os, ot);
     ctx->stats.launches++;
     PT_CK(cudaGetLastError());
-    PT_CK(cudaMemcpyAsync(s_out, os, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
-    PT_CK(cudaMemcpyAsync(t_out, ot, sizeof(int32_t) * 2 * k, cudaMemcpyDeviceToHost, ctx->stream));
+    pt_hostio io(ctx);
+    PT_TRY(io.d2h(s_out, os, sizeof(double) * 2));
+    PT_TRY(io.d2h(t_out, ot, sizeof(int32_t) * 2 * k));
     pt_dfree(ctx, os);
     pt_dfree(ctx, ot);
-    PT_CK(cudaStreamSynchronize(ctx->stream));
+    PT_TRY(io.finish());
     return PT_OK;
 }
 
@@ -1122,12 +1131,13 @@ static pt_status run_generic(pt_ctx *ctx, const pt_view *v, int k, int64_t r0, i
     PT_CK(cudaEventRecord(ctx->ev0, s));
     k_exh_generic<<<nblk, 256, 0, s>>>(v->l64, v->C, v->E_pad, k, r0, r1, bs, bt);
     PT_CK(cudaEventRecord(ctx->ev1, s));
-    k_top2<<<1, 256, 0, s>>>(bs, bt, 2 * nblk, k, os, ot);
+    k_top2<<<1, 256, 0, s>>>(bs, bt, 2 * nblk, nullptr, 0, k, os, ot);
     ctx->stats.launches += 2;
     PT_CK(cudaGetLastError());
-    PT_CK(cudaMemcpyAsync(s_out, os, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
-    PT_CK(cudaMemcpyAsync(t_out, ot, sizeof(int32_t) * 2 * k, cudaMemcpyDeviceToHost, s));
-    PT_CK(cudaStreamSynchronize(s));
+    pt_hostio io(ctx);
+    PT_TRY(io.d2h(s_out, os, sizeof(double) * 2));
+    PT_TRY(io.d2h(t_out, ot, sizeof(int32_t) * 2 * k));
+    PT_TRY(io.finish());
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     ctx->stats.exh_main_ms = ms;
@@ -1278,8 +1288,9 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         double *rs = (double *)(b + o_rs), *os = (double *)(b + o_os);
         int32_t *rt = (int32_t *)(b + o_rt), *ot = (int32_t *)(b + o_ot);
         const unsigned u_init = 0x7f800000u;   // +inf
-        PT_CK(cudaMemcpyAsync(ctr, &ta, sizeof(int), cudaMemcpyHostToDevice, s));
-        PT_CK(cudaMemcpyAsync(U, &u_init, sizeof(unsigned), cudaMemcpyHostToDevice, s));
+        pt_hostio io(ctx);
+        PT_TRY(io.h2d(ctr, &ta, sizeof(int)));
+        PT_TRY(io.h2d(U, &u_init, sizeof(unsigned)));
         PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned), s));
         XParams p;
         p.C = v->C;
@@ -1315,34 +1326,35 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         PT_CK(cudaEventRecord(ctx->ev1, s));
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());
+        // refine + top-2 run on the device-side survivor count (no host round trip);
+        // one synchronisation returns the count, U and the exact top-2
+        k_exh_refine<<<(unsigned)(ctx->num_sms * 8), 256, 0, s>>>(ckey, cq, cn, cap, tau_pass, U, m, v->C,
+                                                                  v->l64, v->E_pad, rs, rt);
+        k_top2<<<1, 256, 0, s>>>(rs, rt, 0, cn, cap, k, os, ot);
+        ctx->stats.launches += 2;
+        PT_CK(cudaGetLastError());
         unsigned hU = 0;
-        PT_CK(cudaMemcpyAsync(&n_cand, cn, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-        PT_CK(cudaMemcpyAsync(&hU, U, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-        PT_CK(cudaStreamSynchronize(s));
+        PT_TRY(io.d2h(&n_cand, cn, sizeof(unsigned)));
+        PT_TRY(io.d2h(&hU, U, sizeof(unsigned)));
+        PT_TRY(io.d2h(s_out, os, sizeof(double) * 2));
+        PT_TRY(io.d2h(t_out, ot, sizeof(int32_t) * 2 * k));
+        PT_TRY(io.finish());
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
         if (pass == 0) ctx->stats.exh_main_ms = ms;
         ctx->stats.exh_passes = pass + 1;
         float Uf;
         memcpy(&Uf, &hU, sizeof Uf);
-        const float tau_final = std::min(tau_pass, Uf);
         if (n_cand > cap) {
             // overflow: rerun with the final threshold and room for every survivor
             cap = n_cand;
-            tau_pass = tau_final;
+            tau_pass = std::min(tau_pass, Uf);
             continue;
         }
         ctx->stats.exh_candidates = n_cand;
-        if (n_cand > 0) {
-            const int64_t threads = (int64_t)n_cand * 32;
-            k_exh_refine<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-                ckey, cq, n_cand, tau_final, m, v->C, v->l64, v->E_pad, rs, rt);
-            k_top2<<<1, 256, 0, s>>>(rs, rt, n_cand, k, os, ot);
-            ctx->stats.launches += 2;
-            PT_CK(cudaGetLastError());
-            PT_CK(cudaMemcpyAsync(s_out, os, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
-            PT_CK(cudaMemcpyAsync(t_out, ot, sizeof(int32_t) * 2 * k, cudaMemcpyDeviceToHost, s));
-            PT_CK(cudaStreamSynchronize(s));
+        if (n_cand == 0) {
+            s_out[0] = s_out[1] = INFINITY;
+            for (int u = 0; u < 2 * k; u++) t_out[u] = 0;
         }
         return PT_OK;
     }

@@ -124,13 +124,13 @@ __global__ void __launch_bounds__(256) k_greedy_resident(const double *__restric
         if (warp == 0) {
             s1 = s2 = INFINITY;
             c1 = c2 = PT_BIGI;
-            for (int b0 = lane; b0 < (int)gridDim.x; b0 += 32 * 4) {   // 4 records in flight per lane
-                double4 r[4];
+            for (int b0 = lane; b0 < (int)gridDim.x; b0 += 32 * 10) {   // 10 records in flight per lane
+                double4 r[10];
 #pragma unroll
-                for (int u = 0; u < 4; u++)
+                for (int u = 0; u < 10; u++)
                     if (b0 + 32 * u < (int)gridDim.x) r[u] = blk[(t & 1) * gridDim.x + b0 + 32 * u];
 #pragma unroll
-                for (int u = 0; u < 4; u++)
+                for (int u = 0; u < 10; u++)
                     if (b0 + 32 * u < (int)gridDim.x) {
                         top2_ins(s1, c1, s2, c2, r[u].x, (int)r[u].z);
                         top2_ins(s1, c1, s2, c2, r[u].y, (int)r[u].w);
@@ -630,9 +630,19 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
     const int64_t C = v->C, E_pad = v->E_pad;
     const int64_t nwords = (C + 31) / 32;
     cudaStream_t s = ctx->stream;
+    pt_hostio io(ctx);
+    std::vector<int32_t> nc;   // stream path: fp64 re-scores per step
     PT_CK(cudaEventRecord(ctx->ev0, s));
     if (!use_stream(ctx, v)) {
-        const int nblk = ctx->num_sms;
+        size_t smem = sizeof(double) * E_pad + sizeof(uint32_t) * nwords;
+        if (smem > 48 * 1024)
+            PT_CK(cudaFuncSetAttribute(k_greedy_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        int occ = 0;
+        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_resident, 256, smem));
+        if (occ < 1) return pt_fail(PT_ECUDA, "resident greedy kernel cannot be co-resident");
+        // 2 blocks per SM when they fit: at most one candidate per warp per step at the paper shape
+        const int nblk = ctx->num_sms * std::min(occ, 2);
         size_t bytes = pt_round_up(sizeof(double4) * 2 * nblk, 256) + 256 +
                        pt_round_up(sizeof(int32_t) * k, 256) + 2 * pt_round_up(sizeof(double) * k, 256);
         void *scr = nullptr;
@@ -645,13 +655,6 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
         double *d_s1 = (double *)p;
         p += pt_round_up(sizeof(double) * k, 256);
         double *d_s2 = (double *)p;
-        size_t smem = sizeof(double) * E_pad + sizeof(uint32_t) * nwords;
-        if (smem > 48 * 1024)
-            PT_CK(cudaFuncSetAttribute(k_greedy_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-        int occ = 0;
-        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_resident, 256, smem));
-        if (occ < 1) return pt_fail(PT_ECUDA, "resident greedy kernel cannot be co-resident");
         const double *l64 = v->l64;
         int kk = k;
         void *args[] = {(void *)&l64, (void *)&C, (void *)&E_pad, (void *)&kk, (void *)&blk,
@@ -659,9 +662,9 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
         PT_CK(cudaLaunchCooperativeKernel((void *)k_greedy_resident, dim3(nblk), dim3(256), args,
                                           smem, s));
         ctx->stats.launches++;
-        PT_CK(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
-        PT_CK(cudaMemcpyAsync(s1_trace, d_s1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
-        PT_CK(cudaMemcpyAsync(s2_trace, d_s2, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+        PT_TRY(io.d2h(out_idx, d_idx, sizeof(int32_t) * k));
+        PT_TRY(io.d2h(s1_trace, d_s1, sizeof(double) * k));
+        PT_TRY(io.d2h(s2_trace, d_s2, sizeof(double) * k));
     } else {
         // buffers: key[C] f32, cand[C] i32, taken[nwords], cur32[E_pad], cur64[E_pad],
         // st, traces
@@ -747,20 +750,21 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
             ctx->stats.launches += 2;
         }
         PT_CK(cudaGetLastError());
-        PT_CK(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
-        PT_CK(cudaMemcpyAsync(s1_trace, d_s1, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
-        PT_CK(cudaMemcpyAsync(s2_trace, d_s2, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+        PT_TRY(io.d2h(out_idx, d_idx, sizeof(int32_t) * k));
+        PT_TRY(io.d2h(s1_trace, d_s1, sizeof(double) * k));
+        PT_TRY(io.d2h(s2_trace, d_s2, sizeof(double) * k));
         pt_dfree(ctx, ub);
         pt_dfree(ctx, cs);
-        std::vector<int32_t> nc(k);
-        PT_CK(cudaMemcpyAsync(nc.data(), d_nc, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, s));
-        PT_CK(cudaStreamSynchronize(s));
+        nc.resize(k);
+        PT_TRY(io.d2h(nc.data(), d_nc, sizeof(int32_t) * k));
+    }
+    PT_CK(cudaEventRecord(ctx->ev1, s));
+    PT_TRY(io.finish());
+    if (!nc.empty()) {
         int64_t tot = 0;
         for (int t = 0; t < k; t++) tot += nc[t];
         ctx->stats.greedy_candidates = tot;
     }
-    PT_CK(cudaEventRecord(ctx->ev1, s));
-    PT_CK(cudaStreamSynchronize(s));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     ctx->stats.greedy_ms = ms;

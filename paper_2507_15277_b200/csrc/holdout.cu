@@ -226,7 +226,16 @@ extern "C" pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t *out_id
             hw[(size_t)(2 * d) * E_pad + e] = ctx->env_device[e] != d;
             hw[(size_t)(2 * d + 1) * E_pad + e] = ctx->env_device[e] == d;
         }
-    const int nblk = std::max(P, ctx->num_sms);
+    const int64_t nwords = (C + 31) / 32;
+    const size_t smem = sizeof(double) * E_pad + sizeof(uint32_t) * nwords;
+    if (smem > 48 * 1024)
+        PT_CK(cudaFuncSetAttribute(k_greedy_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_multi, 256, smem));
+    // up to 4 co-resident blocks per SM: more warps per problem, fewer candidates per warp
+    // (each candidate costs one L2 round trip per step)
+    const int nblk = std::max(P, ctx->num_sms * std::min(occ, 4));
+    if (occ * ctx->num_sms < nblk) return pt_fail(PT_ECUDA, "batched greedy cannot be co-resident");
     double *w = nullptr, *d_s = nullptr, *d_u = nullptr;
     double4 *blk = nullptr;
     int32_t *d_idx = nullptr;
@@ -235,14 +244,8 @@ extern "C" pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t *out_id
     PT_TRY(pt_dalloc(ctx, (void **)&d_idx, sizeof(int32_t) * P * k));
     PT_TRY(pt_dalloc(ctx, (void **)&d_s, sizeof(double) * P));
     PT_TRY(pt_dalloc(ctx, (void **)&d_u, sizeof(double) * D));
-    PT_CK(cudaMemcpyAsync(w, hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice, s));
-    const int64_t nwords = (C + 31) / 32;
-    const size_t smem = sizeof(double) * E_pad + sizeof(uint32_t) * nwords;
-    if (smem > 48 * 1024)
-        PT_CK(cudaFuncSetAttribute(k_greedy_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_multi, 256, smem));
-    if (occ * ctx->num_sms < nblk) return pt_fail(PT_ECUDA, "batched greedy cannot be co-resident");
+    pt_hostio io(ctx);
+    PT_TRY(io.h2d(w, hw.data(), sizeof(double) * hw.size()));
     const double *l64 = v.l64;
     int kk = k, PP = P;
     void *args[] = {(void *)&l64, (void *)&C, (void *)&E_pad, (void *)&kk, (void *)&PP, (void *)&w,
@@ -253,11 +256,11 @@ extern "C" pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t *out_id
     PT_CK(cudaGetLastError());
     std::vector<int32_t> hidx((size_t)P * k);
     std::vector<double> hs(P), hu(D);
-    PT_CK(cudaMemcpyAsync(hidx.data(), d_idx, sizeof(int32_t) * P * k, cudaMemcpyDeviceToHost, s));
-    PT_CK(cudaMemcpyAsync(hs.data(), d_s, sizeof(double) * P, cudaMemcpyDeviceToHost, s));
-    PT_CK(cudaMemcpyAsync(hu.data(), d_u, sizeof(double) * D, cudaMemcpyDeviceToHost, s));
+    PT_TRY(io.d2h(hidx.data(), d_idx, sizeof(int32_t) * P * k));
+    PT_TRY(io.d2h(hs.data(), d_s, sizeof(double) * P));
+    PT_TRY(io.d2h(hu.data(), d_u, sizeof(double) * D));
     for (void *p : {(void *)w, (void *)blk, (void *)d_idx, (void *)d_s, (void *)d_u}) pt_dfree(ctx, p);
-    PT_CK(cudaStreamSynchronize(s));
+    PT_TRY(io.finish());
     for (int32_t d = 0; d < D; d++) {
         const double etr = (double)(ctx->E - cnt[d]), ete = (double)cnt[d];
         for (int u = 0; u < k; u++) {

@@ -82,6 +82,55 @@ void pt_dfree(pt_ctx *ctx, void *p)
     if (p) cudaFreeAsync(p, ctx->stream);
 }
 
+static constexpr size_t kPinnedBytes = 1 << 20;
+static char *pinned_buffer()
+{
+    static thread_local char *buf = nullptr;   // lives for the thread (never freed)
+    if (!buf && cudaMallocHost((void **)&buf, kPinnedBytes) != cudaSuccess) {
+        cudaGetLastError();
+        buf = nullptr;
+    }
+    return buf;
+}
+
+pt_status pt_hostio::h2d(void *dev_dst, const void *host_src, size_t n)
+{
+    char *pin = pinned_buffer();
+    const size_t a = pt_round_up(off, 16);
+    if (pin && a + n <= kPinnedBytes) {
+        memcpy(pin + a, host_src, n);
+        off = a + n;
+        PT_CK(cudaMemcpyAsync(dev_dst, pin + a, n, cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+        PT_CK(cudaMemcpyAsync(dev_dst, host_src, n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return PT_OK;
+}
+
+pt_status pt_hostio::d2h(void *host_dst, const void *dev_src, size_t n)
+{
+    char *pin = pinned_buffer();
+    const size_t a = pt_round_up(off, 16);
+    if (pin && a + n <= kPinnedBytes) {
+        off = a + n;
+        PT_CK(cudaMemcpyAsync(pin + a, dev_src, n, cudaMemcpyDeviceToHost, ctx->stream));
+        items.push_back({host_dst, a, n});
+    } else {
+        PT_CK(cudaMemcpyAsync(host_dst, dev_src, n, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    return PT_OK;
+}
+
+pt_status pt_hostio::finish()
+{
+    PT_CK(cudaStreamSynchronize(ctx->stream));
+    char *pin = pinned_buffer();
+    for (const item &it : items) memcpy(it.dst, pin + it.off, it.n);
+    items.clear();
+    off = 0;
+    return PT_OK;
+}
+
 pt_status pt_scratch(pt_ctx *ctx, size_t bytes, void **p)
 {
     if (bytes > ctx->scratch_bytes) {
@@ -383,11 +432,9 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
     ctx->stats.launches++;
     std::vector<double> h_rowmax(E);
     std::vector<int> h_status(E);
-    cudaMemcpyAsync(h_rowmax.data(), rowmax, sizeof(double) * E, cudaMemcpyDeviceToHost,
-                    ctx->stream);
-    cudaMemcpyAsync(h_status.data(), status, sizeof(int) * E, cudaMemcpyDeviceToHost,
-                    ctx->stream);
-    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    pt_hostio io(ctx);
+    if (io.d2h(h_rowmax.data(), rowmax, sizeof(double) * E) != PT_OK ||
+        io.d2h(h_status.data(), status, sizeof(int) * E) != PT_OK || io.finish() != PT_OK) {
         cleanup();
         return bail(pt_fail(PT_ECUDA, "load: %s", cudaGetErrorString(cudaGetLastError())));
     }

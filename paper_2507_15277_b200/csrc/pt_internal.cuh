@@ -103,6 +103,23 @@ struct pt_ctx {
     pt_stats stats{};
 };
 
+// Small host<->device transfers of one API call through a pinned staging buffer
+// (thread-local, allocated once per thread): a pageable cudaMemcpyAsync is
+// synchronous (~10 us each on B200), a pinned one is a queued DMA.  Transfers are
+// stream-ordered on ctx->stream; finish() synchronises once and scatters the
+// device->host results to their destinations.  Larger transfers fall back to a
+// direct (pageable) copy.
+struct pt_hostio {
+    explicit pt_hostio(pt_ctx *c) : ctx(c) {}
+    pt_status h2d(void *dev_dst, const void *host_src, size_t n);
+    pt_status d2h(void *host_dst, const void *dev_src, size_t n);
+    pt_status finish();
+    pt_ctx *ctx;
+    size_t off = 0;
+    struct item { void *dst; size_t off, n; };
+    std::vector<item> items;
+};
+
 // stream-ordered device allocation from the device's (cached) memory pool
 pt_status pt_dalloc(pt_ctx *ctx, void **p, size_t bytes);
 void pt_dfree(pt_ctx *ctx, void *p);
