@@ -1230,6 +1230,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const double c1d = 1.0 / (1.0 + eta_rel), c3d = 1.0 / (1.0 - eta_rel);
     const float c1 = f_dn(c1d), c2 = f_up(eta_abs), c3 = f_up(c3d), c4 = f_up(eta_abs * c3d * (1.0 + 1e-6));
 
+    if (v->E_pad % XT_K != 0)   // a stage must not straddle the padded env range
+        return pt_fail(PT_EINVAL, "E_pad=%lld is not a multiple of the stage depth %d", (long long)v->E_pad, XT_K);
     PT_TRY(pt_view_fp16(ctx, v));
     if (!v->hTile) {
         pt_view *mv = const_cast<pt_view *>(v);
