@@ -104,12 +104,12 @@ struct pt_tasks {
 
 // The work list depends only on (device, C, m, #SMs): built once per process
 // and shared by every context (a fresh pt_load_perf does not rebuild it).
-static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, pt_tasks **out)
+static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, int cols, pt_tasks **out)
 {
     static std::mutex mu;
-    static std::map<std::tuple<int, int64_t, int, int, int>, pt_tasks *> cache;
+    static std::map<std::tuple<int, int64_t, int, int, int, int>, pt_tasks *> cache;
     std::lock_guard<std::mutex> g(mu);
-    const auto key = std::make_tuple(ctx->dev, v->C, m, ctx->num_sms, rows);
+    const auto key = std::make_tuple(ctx->dev, v->C, m, ctx->num_sms, rows, cols);
     auto it = cache.find(key);
     if (it != cache.end()) {
         *out = it->second;
@@ -130,7 +130,7 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, pt_
         int32_t mem[PT_MAXK];
         pt_unrank_colex(t * rows, m, C, mem);
         if (mem[m - 1] + 1 >= C) continue;
-        total_ct += (C - tile_lo(mem[m - 1]) + XT_C - 1) / XT_C;
+        total_ct += (C - tile_lo(mem[m - 1]) + cols - 1) / cols;
     }
     const int64_t umax = std::max<int64_t>(1, std::min<int64_t>(XT_UMAX, total_ct / (8 * std::max(ctx->num_sms, 1))));
     for (int64_t t = 0; t < n_rt; t++) {
@@ -140,10 +140,10 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, pt_
         const int64_t j0 = mem[m - 1];
         if (j0 + 1 >= C) continue;                    // no column l > j0
         const int64_t lo = tile_lo(j0);
-        const int64_t n_ct = (C - lo + XT_C - 1) / XT_C;
+        const int64_t n_ct = (C - lo + cols - 1) / cols;
         for (int64_t u0 = 0; u0 < n_ct; u0 += umax) {
             const int64_t u1 = std::min(n_ct, u0 + umax);
-            const int64_t clo = lo + u0 * XT_C, chi = std::min(C, lo + u1 * XT_C);
+            const int64_t clo = lo + u0 * cols, chi = std::min(C, lo + u1 * cols);
             // useful sets: rows grouped by their largest element j (colex)
             int64_t useful = 0;
             for (int64_t j = j0; j < C; j++) {
@@ -154,7 +154,7 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, pt_
                 if (chi > first) useful += (b - a) * (chi - first);
             }
             T->h.push_back(make_int4((int)t, (int)u0, (int)u1, 0));
-            T->slot_pre.push_back(T->slot_pre.back() + (u1 - u0) * rows * XT_C);
+            T->slot_pre.push_back(T->slot_pre.back() + (u1 - u0) * rows * cols);
             T->set_pre.push_back(T->set_pre.back() + useful);
         }
     }
@@ -641,6 +641,293 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
             }
         }
         steps += nsteps;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_exh_ws: warp-specialised persistent variant of k_exh_tiled (one CTA per
+// SM) for scopes where the double-buffered A tile fits (E_pad <= XW_EMAX).
+// Opt-in (XW_ENABLE=1): measured 13.54 ms vs 12.33 ms for k_exh_tiled at k=3 --
+// 18 warps cap the registers at 96 (spills), and one stager warp gathering
+// 82 K fp16 values per task cannot keep up with the small tasks at the end of
+// the decreasing-size queue.
+//   warps 0-15 : consumers; CTA tile 128 rows x 128 columns (warp w: rows
+//                32*(w>>2) + 8*ty, columns 32*(w&3) + 4*tx); the inner loop and
+//                the epilogue are k_exh_tiled's
+//   warp 16    : producer; streams 64-env x 128-config stages (two 8 KB bulk
+//                copies from hTile) through the XT_S-deep B ring
+//   warp 17    : stager; takes tasks from the dynamic queue and builds the NEXT
+//                task's A tile into the other half of a double buffer
+// The roles meet only on mbarriers -- B ring full/empty, A buffer full
+// (stager -> consumers, producer) and empty (consumers -> stager) -- so there
+// is no CTA-wide barrier between tasks: the A gather overlaps the math and a
+// fast warp runs on into the next task.
+// ---------------------------------------------------------------------------
+#ifndef XW_ENABLE
+#define XW_ENABLE 0                 // 1: k_exh_ws where it fits (measured slower)
+#endif
+#define XW_C 128                    // columns per CTA tile
+#define XW_CONS 512                 // consumer threads (16 warps)
+#define XW_THREADS (XW_CONS + 64)   // + producer + stager
+#define XW_EMAX 320                 // widest scope: 2 A buffers + the B ring fit 227 KB
+#ifndef XW_MAXREG
+#define XW_MAXREG 96   // 18 warps put 5 on one SM sub-partition: 5 x 32 x 104 > its 16 K registers
+#endif
+#define XW_SE 8                     // stager: envs per batch (4 rows x 8 envs x members in flight)
+
+__global__ void __maxnreg__(XW_MAXREG) k_exh_ws(const XParams p)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][2][K][32] half2
+    uint16_t *As0 = reinterpret_cast<uint16_t *>(Bs + XT_S * 2 * XT_K * 32);  // [2][E_pad][128] fp16
+    int *last_s0 = reinterpret_cast<int *>(As0 + 2 * p.E_pad * XT_R);         // [2][128]
+    int4 *task_s = reinterpret_cast<int4 *>(last_s0 + 2 * XT_R);              // [2]
+    uint64_t *full = reinterpret_cast<uint64_t *>(task_s + 2);                // [S]
+    uint64_t *empty = full + XT_S;                                            // [S]
+    uint64_t *afull = empty + XT_S;                                           // [2]
+    uint64_t *aempty = afull + 2;                                             // [2]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nkc = (int)(p.E_pad / XT_K);
+    if (tid == 0) {
+        for (int s = 0; s < XT_S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], XW_CONS / 32);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&afull[b], 1);
+            mbar_init(&aempty[b], XW_CONS / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == XW_CONS / 32 + 1) {
+        // ---------------- stager ----------------
+        for (uint32_t n = 0;; n++) {
+            const int b = n & 1;
+            mbar_wait(&aempty[b], ((n >> 1) & 1u) ^ 1u);
+            int ti = 0;
+            if (lane == 0) ti = atomicAdd(p.task_ctr, 1);
+            ti = __shfl_sync(0xffffffffu, ti, 0);
+            const int4 tk = ti < p.task_hi ? p.tasks[ti] : make_int4(-1, 0, 0, 0);
+            if (tk.x >= 0) {
+                // A[e][r] = min over row r's members (fp16 bits, non-negative: integer
+                // order); lane owns rows lane + 32 i
+                uint16_t *As = As0 + (int64_t)b * p.E_pad * XT_R;
+                int *last_s = last_s0 + b * XT_R;
+                const int64_t R0 = (int64_t)tk.x * XT_R;
+                int32_t mem[4][PT_MAXK];
+                bool valid[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int64_t R = R0 + lane + 32 * i;
+                    valid[i] = R < p.n_rows;
+                    if (valid[i]) pt_unrank_colex(R, p.m, p.C, mem[i]);
+                    else for (int u = 0; u < p.m; u++) mem[i][u] = 0;
+                    last_s[lane + 32 * i] = valid[i] ? mem[i][p.m - 1] : 0x7fffffff;
+                }
+                for (int64_t e0 = 0; e0 < p.E_pad; e0 += XW_SE) {
+                    uint16_t v[4][XW_SE];
+#pragma unroll
+                    for (int i = 0; i < 4; i++)
+#pragma unroll
+                        for (int t = 0; t < XW_SE; t++) v[i][t] = p.hT[(e0 + t) * p.C_pad + mem[i][0]];
+                    for (int u = 1; u < p.m; u++) {
+                        uint16_t w[4][XW_SE];
+#pragma unroll
+                        for (int i = 0; i < 4; i++)
+#pragma unroll
+                            for (int t = 0; t < XW_SE; t++) w[i][t] = p.hT[(e0 + t) * p.C_pad + mem[i][u]];
+#pragma unroll
+                        for (int i = 0; i < 4; i++)
+#pragma unroll
+                            for (int t = 0; t < XW_SE; t++) v[i][t] = v[i][t] < w[i][t] ? v[i][t] : w[i][t];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; i++)
+#pragma unroll
+                        for (int t = 0; t < XW_SE; t++)
+                            As[(e0 + t) * XT_R + lane + 32 * i] = valid[i] ? v[i][t] : (uint16_t)0;
+                }
+            }
+            if (lane == 0) task_s[b] = tk;
+            __threadfence_block();
+            __syncwarp();                        // every lane's A writes precede the release
+            if (lane == 0) mbar_arrive(&afull[b]);
+            if (tk.x < 0) break;
+        }
+    } else if (warp == XW_CONS / 32) {
+        // ---------------- producer ----------------
+        uint32_t G = 0;   // B-ring stages issued (lane 0)
+        for (uint32_t n = 0;; n++) {
+            const int b = n & 1;
+            mbar_wait(&afull[b], (n >> 1) & 1u);
+            const int4 tk = task_s[b];
+            if (tk.x < 0) break;
+            if (lane == 0) {
+                int32_t mem0[PT_MAXK];
+                pt_unrank_colex((int64_t)tk.x * XT_R, p.m, p.C, mem0);
+                int64_t col = tile_lo(mem0[p.m - 1]) + (int64_t)tk.y * XW_C;
+                for (int ct = tk.y; ct < tk.z; ct++, col += XW_C) {
+                    // 128 configs from `col` (8-aligned) = 64-config tiles c64 and c64 + 1 of
+                    // shift sh (hTile carries one zero tile of padding past the last)
+                    const int64_t sh = (col >> 3) & 7, c64 = (col - 8 * sh) >> 6;
+                    const uint16_t *src = p.hTile + (sh * p.n_ct + c64) * p.E_pad * 64;
+                    for (int q = 0; q < nkc; q++, G++) {
+                        const int slot = G % XT_S;
+                        mbar_wait(&empty[slot], ((G / XT_S) & 1u) ^ 1u);
+                        mbar_expect_tx(&full[slot], 2 * XT_K * 128);
+                        bulk_g2s(Bs + slot * 2 * XT_K * 32, src + (int64_t)q * XT_K * 64, XT_K * 128, &full[slot]);
+                        bulk_g2s(Bs + (slot * 2 + 1) * XT_K * 32, src + (p.E_pad + (int64_t)q * XT_K) * 64,
+                                 XT_K * 128, &full[slot]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- consumers ----------------
+        const int tx = lane & 7, ty = lane >> 3;
+        const int r0 = 32 * (warp >> 2) + 8 * ty;
+        const int cq = warp & 3;                         // 32-column quarter of the tile
+        const int c0 = 32 * cq + 4 * tx;                 // first of the thread's 4 columns
+        const int c0h = c0 - 64 * (cq >> 1);             // ... within its 64-column half
+        float bA = INFINITY, bB = INFINITY, published = INFINITY;   // acc-domain group minima (window U)
+        uint32_t slot = 0, phase = 0;
+        for (uint32_t n = 0;; n++) {
+            const int b = n & 1;
+            mbar_wait(&afull[b], (n >> 1) & 1u);
+            const int4 tk = task_s[b];
+            if (tk.x < 0) break;
+            const int64_t R0 = (int64_t)tk.x * XT_R;
+            const uint16_t *As = As0 + (int64_t)b * p.E_pad * XT_R;
+            const int *last_s = last_s0 + b * XT_R;
+            int32_t mem0[PT_MAXK];
+            pt_unrank_colex(R0, p.m, p.C, mem0);
+            // colex order: a row's largest member is non-decreasing in its rank (padding
+            // rows hold INT_MAX), so the thread's last row bounds all eight
+            const int last7 = last_s[r0 + 7];
+            float acc[8][4];
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
+            int64_t ltile = tile_lo(mem0[p.m - 1]) + (int64_t)tk.y * XW_C;
+            for (int ct = tk.y; ct < tk.z; ct++, ltile += XW_C) {
+                const bool skip = ltile + 32 * cq >= p.C;   // the warp's quarter lies past the last config
+                const unsigned Ubits = *(volatile unsigned *)p.U;
+                for (int q = 0; q < nkc; q++) {
+                    mbar_wait(&full[slot], phase);
+                    if (!skip) {
+                        const uint32_t *B = Bs + (slot * 2 + (cq >> 1)) * XT_K * 32 + c0h / 2;
+                        const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
+#pragma unroll kXtPUnroll
+                        for (int e = 0; e < XT_K; e += 4 * XT_NG) {
+                            uint32_t pp[8][2];
+#pragma unroll
+                            for (int gq = 0; gq < XT_NG; gq++) {
+                                uint4 ar[4];
+                                uint2 bc[4];
+#pragma unroll
+                                for (int t = 0; t < 4; t++) {
+                                    ar[t] = *reinterpret_cast<const uint4 *>(A + (e + 4 * gq + t) * XT_R);
+                                    bc[t] = *reinterpret_cast<const uint2 *>(B + (e + 4 * gq + t) * 32);
+                                }
+#pragma unroll
+                                for (int i = 0; i < 8; i++) {
+                                    uint32_t av[4];
+#pragma unroll
+                                    for (int t = 0; t < 4; t++) {
+                                        const uint32_t w = (i >> 1) == 0 ? ar[t].x : (i >> 1) == 1 ? ar[t].y
+                                                                         : (i >> 1) == 2 ? ar[t].z : ar[t].w;
+                                        av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                                    }
+                                    const uint32_t sx = hadd2(hadd2(hmin2(av[0], bc[0].x), hmin2(av[1], bc[1].x)),
+                                                              hadd2(hmin2(av[2], bc[2].x), hmin2(av[3], bc[3].x)));
+                                    const uint32_t sy = hadd2(hadd2(hmin2(av[0], bc[0].y), hmin2(av[1], bc[1].y)),
+                                                              hadd2(hmin2(av[2], bc[2].y), hmin2(av[3], bc[3].y)));
+                                    if (gq == 0) {
+                                        pp[i][0] = sx;
+                                        pp[i][1] = sy;
+                                    } else if (gq < XT_NG - 1) {
+                                        pp[i][0] = hadd2(pp[i][0], sx);
+                                        pp[i][1] = hadd2(pp[i][1], sy);
+                                    } else {
+                                        fhadd2(acc[i][0], acc[i][1], hadd2(pp[i][0], sx));
+                                        fhadd2(acc[i][2], acc[i][3], hadd2(pp[i][1], sy));
+                                    }
+                                }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[slot]);
+                    if (++slot == XT_S) {
+                        slot = 0;
+                        phase ^= 1u;
+                    }
+                }
+                if (skip) continue;
+                // ---- epilogue of one column tile (as k_exh_tiled) ----
+                const int64_t l0 = ltile + c0;
+                if (!(l0 + 3 < p.C && l0 > last7)) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        const int last = last_s[r0 + i];
+#pragma unroll
+                        for (int j = 0; j < 4; j++)
+                            if (!(l0 + j < p.C && l0 + j > last)) acc[i][j] = INFINITY;
+                    }
+                }
+                float tA = fminf(acc[0][0], acc[0][1]), tB = fminf(acc[0][2], acc[0][3]);
+#pragma unroll
+                for (int i = 1; i < 8; i++) {
+                    tA = fminf(tA, fminf(acc[i][0], acc[i][1]));
+                    tB = fminf(tB, fminf(acc[i][2], acc[i][3]));
+                }
+                bA = fminf(bA, tA);
+                bB = fminf(bB, tB);
+                const float tau = fminf(p.tau_seed, __uint_as_float(Ubits));
+                if (__fmaf_rd(fminf(tA, tB), p.c1, -p.c2) <= tau) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const float lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
+                            if (acc[i][j] < INFINITY && lb <= tau) {
+                                const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                if (idx < p.cap) {
+                                    p.cand_key[idx] = ((unsigned long long)(R0 + r0 + i) << KEY_BITS) |
+                                                      (unsigned long long)(l0 + j);
+                                    p.cand_s[idx] = lb;
+                                }
+                            }
+                        }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
+                float x1 = fminf(bA, bB), x2 = fmaxf(bA, bB);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const float y1 = __shfl_xor_sync(0xffffffffu, x1, o);
+                    const float y2 = __shfl_xor_sync(0xffffffffu, x2, o);
+                    x2 = fminf(fmaxf(x1, y1), fminf(x2, y2));
+                    x1 = fminf(x1, y1);
+                }
+                if (lane == 0) {
+                    const float ub = __fmaf_ru(x2, p.c3, p.c4);
+                    if (ub < published) {
+                        atomicMin(p.U, __float_as_uint(ub));
+                        published = ub;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&aempty[b]);
+        }
     }
 }
 
@@ -1156,7 +1443,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     cudaStream_t s = ctx->stream;
     const int m = k - 1;
     pt_tasks *T = nullptr;
-    PT_TRY(build_tasks(ctx, v, m, XT_MMA ? XM_R : XT_R, &T));
+    const bool ws = XW_ENABLE && !XT_MMA && v->E_pad <= XW_EMAX;   // warp-specialised kernel (A double-buffered)
+    PT_TRY(build_tasks(ctx, v, m, XT_MMA ? XM_R : XT_R, ws ? XW_C : XT_C, &T));
     const int n_tasks = (int)T->h.size();
     // equal-work contiguous shard of the task list
     const int64_t total = T->slot_pre.back();
@@ -1235,7 +1523,9 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     PT_TRY(pt_view_fp16(ctx, v));
     if (!v->hTile) {
         pt_view *mv = const_cast<pt_view *>(v);
-        mv->n_ct = (v->C_pad + XT_C - 1) / XT_C;
+        // 64-config tiles, plus one zero tile so a 128-config stage (k_exh_ws) never
+        // reads past the end
+        mv->n_ct = (v->C_pad + XT_C - 1) / XT_C + 1;
         PT_TRY(pt_dalloc(ctx, (void **)&mv->hTile, sizeof(uint16_t) * 8 * mv->n_ct * v->E_pad * XT_C));
         k_tile_hT<<<(unsigned)(8 * mv->n_ct * v->E_pad), 64, 0, s>>>(v->hT, v->E_pad, v->C_pad, mv->n_ct,
                                                                    mv->hTile);
@@ -1262,11 +1552,14 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const size_t smem = sizeof(uint32_t) * XT_S * (XT_K / 2) * XT_C + sizeof(uint32_t) * (v->E_pad / 2) * XM_AST +
                         sizeof(int) * XM_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
 #else
-    auto kern = k_exh_tiled;
-    const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
-                        sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 2 * sizeof(uint64_t) * XT_S +
-                        sizeof(int4);
+    auto kern = ws ? k_exh_ws : k_exh_tiled;
+    const size_t smem =
+        ws ? sizeof(uint32_t) * XT_S * 2 * XT_K * 32 + 2 * sizeof(uint16_t) * v->E_pad * XT_R +
+                 2 * sizeof(int) * XT_R + 2 * sizeof(int4) + 2 * sizeof(uint64_t) * (XT_S + 2)
+           : sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
+                 sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
 #endif
+    const int threads = XT_MMA ? XT_THREADS : ws ? XW_THREADS : XT_TTHREADS;
     PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
     unsigned cap = 1u << 20;
@@ -1321,10 +1614,10 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.hC = v->hC;
         p.hPair = v->hPair;
         int occ = 1;
-        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT_MMA ? XT_THREADS : XT_TTHREADS, smem));
+        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
         const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
         PT_CK(cudaEventRecord(ctx->ev0, s));
-        kern<<<grid, XT_MMA ? XT_THREADS : XT_TTHREADS, smem, s>>>(p);
+        kern<<<grid, threads, smem, s>>>(p);
         PT_CK(cudaEventRecord(ctx->ev1, s));
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());
