@@ -281,11 +281,15 @@ __device__ __forceinline__ void fhadd2(float &lo_acc, float &hi_acc, uint32_t p)
 // so the filter keeps every set that could be one of the exact best two and
 // the fp64 refine decides.
 //
-// Warp roles (288 threads): warps 0-7 compute (8 rows x 4 columns each, 128x64
-// per CTA), warp 8 is the producer: it streams 32-env x 64-config fp16 column
-// tiles of hT through the TMA engine (cp.async.bulk, one 128-byte row per
-// lane) into an XT_S-deep ring of full/empty mbarriers.  Consumers never wait
-// for each other inside a task.
+// Warps (256 threads, 2 CTAs per SM): 8 warps compute (8 rows x 4 columns per
+// thread, 128x64 per CTA).  64-env x 64-config fp16 column stages come from the
+// pre-tiled hTile through the TMA engine (cp.async.bulk, one 8 KB copy per
+// stage) into an XT_S-deep ring: full[] mbarriers count the bytes, and the
+// last warp to release a stage (shared-memory counter) issues its refill, so no
+// warp is spent on production and the SM keeps 16 warps at <= 128 registers
+// (with a 9th producer warp, 18 warps per SM cap the registers at 96: a
+// sub-partition's 16 K registers hold 5 warps of 96).  XT_NOPROD=0 restores
+// the producer warp.  Consumers never wait for each other inside a task.
 // ---------------------------------------------------------------------------
 struct XParams {
     int64_t C, C_pad, E_pad, n_rows;
@@ -318,7 +322,10 @@ struct XParams {
 #define XT_THREADS 288      // k_exh_mma
 #define XT_CONS 256
 #define XT_TCONS (2 * XT_R)  // k_exh_tiled consumers: 2 warps (column halves) per 32 rows
-#define XT_TTHREADS (XT_TCONS + 32)
+#ifndef XT_NOPROD
+#define XT_NOPROD 1   // 1: no producer warp; the last consumer warp to release a stage refills it (0: producer warp)
+#endif
+#define XT_TTHREADS (XT_TCONS + (XT_NOPROD ? 0 : 32))
 #define XT_BROW (XT_C * 2)     // bytes of one env row of a column tile
 
 // broadcast one fp16 lane of a word to both halves (ptxas folds this into the
@@ -354,6 +361,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
     uint64_t *full = reinterpret_cast<uint64_t *>(bnd_s + XT_R);               // [S]
     uint64_t *empty = full + XT_S;                                             // [S]
     int4 *task_s = reinterpret_cast<int4 *>(empty + XT_S);
+    int *relcnt = reinterpret_cast<int *>(task_s + 1);                         // [S] (XT_NOPROD)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nkc = (int)(p.E_pad / XT_K);
@@ -361,6 +369,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
         for (int s = 0; s < XT_S; s++) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], XT_TCONS / 32);
+            relcnt[s] = 0;
         }
         mbar_fence_init();
     }
@@ -383,8 +392,23 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
         pt_unrank_colex(R0, p.m, p.C, mem0);
         const int64_t lo = tile_lo(mem0[p.m - 1]);
         const int nsteps = (tk.z - tk.y) * nkc;
+#if XT_NOPROD
+        // stage g of this task (column tile tk.y + g / nkc, env chunk g % nkc) into its ring
+        // slot: one bulk copy, completion counted on full[slot]
+        auto issue = [&](int g) {
+            const int sl = (int)((steps + (uint32_t)g) % XT_S);
+            const int64_t col = lo + (int64_t)(tk.y + g / nkc) * XT_C;
+            const int64_t sh = (col >> 3) & 7, ct = (col - 8 * sh) >> 6;
+            const uint16_t *src = p.hTile + ((sh * p.n_ct + ct) * p.E_pad + (int64_t)(g % nkc) * XT_K) * XT_C;
+            mbar_expect_tx(&full[sl], XT_K * XT_BROW);
+            bulk_g2s(Bs + sl * XT_K * (XT_C / 2), src, XT_K * XT_BROW, &full[sl]);
+        };
+        // every warp has left the previous task (barrier above): the whole ring is free
+        if (tid == 0)
+            for (int g = 0; g < XT_S && g < nsteps; g++) issue(g);
+#endif
 
-        if (warp == XT_TCONS / 32) {
+        if (!XT_NOPROD && warp == XT_TCONS / 32) {
             // ---------------- producer warp ----------------
             // column tile starting at config `col` (8-aligned) = shift s, tile ct
             // of hTile; each stage is one contiguous 32-env x 64-config block
@@ -569,7 +593,22 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #endif
                     }
                     __syncwarp();
+#if XT_NOPROD
+                    if (lane == 0) {
+                        // release: the last of the consumer warps to finish this stage refills
+                        // the slot with stage g + S of the task
+                        __threadfence_block();
+                        if (atomicAdd(&relcnt[slot], 1) == XT_TCONS / 32 - 1) {
+                            relcnt[slot] = 0;
+                            __threadfence_block();
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            const int gn = (ct - tk.y) * nkc + q + XT_S;
+                            if (gn < nsteps) issue(gn);
+                        }
+                    }
+#else
                     if (lane == 0) mbar_arrive(&empty[slot]);
+#endif
                     if (++slot == XT_S) {
                         slot = 0;
                         phase ^= 1u;
@@ -1557,7 +1596,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         ws ? sizeof(uint32_t) * XT_S * 2 * XT_K * 32 + 2 * sizeof(uint16_t) * v->E_pad * XT_R +
                  2 * sizeof(int) * XT_R + 2 * sizeof(int4) + 2 * sizeof(uint64_t) * (XT_S + 2)
            : sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
-                 sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4);
+                 sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
 #endif
     const int threads = XT_MMA ? XT_THREADS : ws ? XW_THREADS : XT_TTHREADS;
     PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
