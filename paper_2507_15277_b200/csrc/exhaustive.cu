@@ -219,6 +219,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
     while (!mbar_try_sleep(b, parity)) {
     }
 }
+// non-blocking test of a phase
+__device__ __forceinline__ bool mbar_test(uint64_t *b, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+#ifndef XT_WAITNS
+#define XT_WAITNS 0   // > 0: consumers poll a B stage with test_wait + nanosleep backoff (cap in ns)
+#endif
+// wait for a B stage: with XT_WAITNS the warp sleeps between polls (exponential
+// backoff up to XT_WAITNS ns) instead of being woken by every barrier event of
+// the CTA -- fewer polling instructions competing for issue slots
+__device__ __forceinline__ void mbar_wait_stage(uint64_t *b, uint32_t parity)
+{
+#if XT_WAITNS > 0
+    if (mbar_test(b, parity)) return;
+    unsigned ns = 32;
+    while (!mbar_test(b, parity)) {
+        __nanosleep(ns);
+        ns = ns * 2 < XT_WAITNS ? ns * 2 : XT_WAITNS;
+    }
+#else
+    mbar_wait(b, parity);
+#endif
+}
 // bulk async copy global -> shared on the TMA engine (SASS UBLKCP), completion
 // counted on an mbarrier.  src/dst 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
@@ -484,7 +514,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                 // L2 latency hides behind it (a stale value is only a looser bound)
                 const unsigned Ubits = *(volatile unsigned *)p.U;
                 for (int q = 0; q < nkc; q++) {
-                    mbar_wait(&full[slot], phase);
+                    mbar_wait_stage(&full[slot], phase);
                     if (!skip) {
                         const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
                         const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
