@@ -386,9 +386,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
     uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2
     uint16_t *As = reinterpret_cast<uint16_t *>(Bs + XT_S * XT_K * (XT_C / 2)); // [E_pad][128] fp16
     int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);                // [128]
-    float *sumA_s = reinterpret_cast<float *>(last_s + XT_R);                  // [128] sum_e A
-    float *bnd_s = sumA_s + XT_R;                                              // [128] relu-form bound
-    uint64_t *full = reinterpret_cast<uint64_t *>(bnd_s + XT_R);               // [S]
+    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);              // [S]
     uint64_t *empty = full + XT_S;                                             // [S]
     int4 *task_s = reinterpret_cast<int4 *>(empty + XT_S);
     int *relcnt = reinterpret_cast<int *>(task_s + 1);                         // [S] (XT_NOPROD)
@@ -1292,16 +1290,18 @@ __global__ void k_tile_pairs(const uint16_t *__restrict__ hT, int64_t E_pad, int
     hPair[blk * 64 + 4 * ((j >> 2) ^ pair_swz((int)(pp & 3))) + (j & 3)] = w;   // swizzled (see k_exh_mma)
 }
 
-// hTile[s][ct][e][j] = hT[e][64*ct + 8*s + j]  (0 beyond the padded row)
-__global__ void k_tile_hT(const uint16_t *__restrict__ hT, int64_t E_pad, int64_t C_pad, int64_t n_ct,
-                          uint16_t *__restrict__ hTile)
+// hTile[sh][ct][e][0..64) = hT[e][64 ct + 8 sh + 0..64) (zero past C_pad): one block
+// per (sh, ct), 16-byte copies (C_pad and the 8-config shifts keep them aligned)
+__global__ void __launch_bounds__(256) k_tile_hT(const uint16_t *__restrict__ hT, int64_t E_pad, int64_t C_pad,
+                                                 int64_t n_ct, uint16_t *__restrict__ hTile)
 {
-    const int64_t blk = blockIdx.x;                  // (s, ct, e)
-    const int64_t e = blk % E_pad, sct = blk / E_pad;
-    const int64_t ct = sct % n_ct, sh = sct / n_ct;
-    const int j = threadIdx.x;                       // 64 threads
-    const int64_t c = 64 * ct + 8 * sh + j;
-    hTile[blk * 64 + j] = c < C_pad ? hT[e * C_pad + c] : (uint16_t)0;
+    const int64_t sct = blockIdx.x, ct = sct % n_ct, sh = sct / n_ct;
+    const int64_t c0 = 64 * ct + 8 * sh;
+    uint4 *dst = reinterpret_cast<uint4 *>(hTile + sct * E_pad * 64);
+    for (int64_t i = threadIdx.x; i < E_pad * 8; i += blockDim.x) {
+        const int64_t e = i >> 3, c = c0 + 8 * (i & 7);
+        dst[i] = c < C_pad ? *reinterpret_cast<const uint4 *>(hT + e * C_pad + c) : make_uint4(0, 0, 0, 0);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1569,10 +1569,13 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         return f;
     };
     // seed: exact score of greedy's runner-up set at its last step (>= s_(2))
-    std::vector<int32_t> gidx(k);
-    std::vector<double> gs1(k), gs2(k);
-    PT_TRY(pt_greedy_view(ctx, v, k, gidx.data(), gs1.data(), gs2.data()));
-    const float tau_seed = f_up(gs2[k - 1] * (1.0 + 1e-9) + 1e-30);
+    // (reused from an earlier greedy run of >= k steps on this view when there is one)
+    if (v->greedy_s2.size() < (size_t)k) {
+        std::vector<int32_t> gidx(k);
+        std::vector<double> gs1(k), gs2(k);
+        PT_TRY(pt_greedy_view(ctx, v, k, gidx.data(), gs1.data(), gs2.data()));
+    }
+    const float tau_seed = f_up(v->greedy_s2[k - 1] * (1.0 + 1e-9) + 1e-30);
 #if XT_MMA
     // tensor-summed kernel: fp16 terms u16 (the mins are exact fp16 values), then
     // E_pad/8 chained MMA accumulations, each assumed within 2^-18 relative of
@@ -1596,8 +1599,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         // reads past the end
         mv->n_ct = (v->C_pad + XT_C - 1) / XT_C + 1;
         PT_TRY(pt_dalloc(ctx, (void **)&mv->hTile, sizeof(uint16_t) * 8 * mv->n_ct * v->E_pad * XT_C));
-        k_tile_hT<<<(unsigned)(8 * mv->n_ct * v->E_pad), 64, 0, s>>>(v->hT, v->E_pad, v->C_pad, mv->n_ct,
-                                                                   mv->hTile);
+        k_tile_hT<<<(unsigned)(8 * mv->n_ct), 256, 0, s>>>(v->hT, v->E_pad, v->C_pad, mv->n_ct, mv->hTile);
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());
     }
@@ -1626,7 +1628,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         ws ? sizeof(uint32_t) * XT_S * 2 * XT_K * 32 + 2 * sizeof(uint16_t) * v->E_pad * XT_R +
                  2 * sizeof(int) * XT_R + 2 * sizeof(int4) + 2 * sizeof(uint64_t) * (XT_S + 2)
            : sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
-                 sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
+                 sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
 #endif
     const int threads = XT_MMA ? XT_THREADS : ws ? XW_THREADS : XT_TTHREADS;
     PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

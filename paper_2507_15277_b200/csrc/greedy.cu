@@ -760,6 +760,7 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
     }
     PT_CK(cudaEventRecord(ctx->ev1, s));
     PT_TRY(io.finish());
+    if ((size_t)k > v->greedy_s2.size()) v->greedy_s2.assign(s2_trace, s2_trace + k);
     if (!nc.empty()) {
         int64_t tot = 0;
         for (int t = 0; t < k; t++) tot += nc[t];

@@ -57,6 +57,10 @@ struct pt_view {
     uint16_t *hC = nullptr;
     uint32_t *hPair = nullptr;
     bool owned = false;
+    // exact greedy trace of the longest greedy run on this view (greedy is
+    // deterministic and prefix-consistent, so a k-step run answers every k' <= k):
+    // the exhaustive search reads its seed (runner-up score at step k) from here
+    mutable std::vector<double> greedy_s2;
 };
 
 struct pt_tasks;  // exhaustive work list (exhaustive.cu)
