@@ -321,6 +321,42 @@ __device__ __forceinline__ void fhadd2(float &lo_acc, float &hi_acc, uint32_t p)
 // sub-partition's 16 K registers hold 5 warps of 96).  XT_NOPROD=0 restores
 // the producer warp.  Consumers never wait for each other inside a task.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// XT_TC=1: tensor-summed variant of k_exh_tiled.  The mins stay on the ALU pipe
+// (HMNMX2: one set at two envs per instruction); the across-environment sum runs
+// on the tensor pipe as m16n8k16 HMMA (f16 in, f32 accumulate) with the 0/1
+// selector  B[k][n] = 1 iff floor(k/2) == n,  so C[m][n] += A[m][2n] + A[m][2n+1]:
+// one MMA tile is 16 x 8 = 128 distinct sets at one env pair, no accumulator is
+// duplicated.  Warp tile 32 rows x 32 columns = 8 MMA tiles (2 row blocks rb x 4
+// column blocks cb).  Thread (g = lane/4, q = lane%4) feeds rows {g, g+8, g+16,
+// g+24} x columns {q + 4j, j < 8} of the warp tile (one LDS.128 of A and two of B
+// per env pair: the smem layouts are permuted so they are contiguous) and holds
+// the sums of rows 16 rb + {g, g+8} x columns 8 cb + {2q, 2q+1} of tile (rb, cb).
+// Per env pair and thread: 3 LDS + 32 HMNMX2 + 8 HMMA for 64 (set, env)
+// evaluations = 0.67 issue slots per evaluation (tree: 1.09); the ALU (HMNMX2,
+// half rate) and the tensor pipe (HMMA.16816, 0.5 / SM / clk) both cap at 128
+// evaluations / clk / SM.
+// ---------------------------------------------------------------------------
+#ifndef XT_TC
+#define XT_TC 0
+#endif
+#ifndef XT_TCU
+#define XT_TCU 4      // XT_TC: unroll of the env-pair loop
+#endif
+[[maybe_unused]] static constexpr int kXtTcUnroll = XT_TCU;
+// row position inside a 32-row block: rows g, g+8, g+16, g+24 -> 4g .. 4g+3
+__host__ __device__ __forceinline__ int tc_rpos(int r) { return (r & ~31) | ((r & 7) << 2) | ((r >> 3) & 3); }
+// column position inside a 32-column half: columns q, q+4, ..., q+28 -> 8q .. 8q+7
+__host__ __device__ __forceinline__ int tc_cpos(int c) { return (c & ~31) | ((c & 3) << 3) | ((c >> 2) & 7); }
+__device__ __forceinline__ void tc_mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                       uint32_t b0, uint32_t b1)
+{
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 struct XParams {
     int64_t C, C_pad, E_pad, n_rows;
     int m;
@@ -404,7 +440,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
     __syncthreads();
 
     uint32_t steps = 0;   // pipeline steps of all previous tasks (same in every thread)
-    const int tx = lane & 7, ty = lane >> 3;
+    [[maybe_unused]] const int tx = lane & 7, ty = lane >> 3;
     float bA = INFINITY, bB = INFINITY, published = INFINITY;   // acc-domain group minima (window U)
 
     for (;;) {
@@ -472,6 +508,27 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                 else for (int u = 0; u < p.m; u++) mem[u] = 0;
                 if (tid < XT_R) last_s[r] = valid ? mem[p.m - 1] : 0x7fffffff;
                 const int64_t e0 = tid / XT_R;
+#if XT_TC
+                // env pairs (2 pp, 2 pp + 1) packed into one f16x2 word, row at tc_rpos(r)
+                uint32_t *Aw = reinterpret_cast<uint32_t *>(As);
+                const int rp = tc_rpos(r);
+                for (int64_t pb = e0; pb < p.E_pad / 2; pb += XT_SB) {
+                    uint16_t v[XT_SB];   // v[2t + h] = env 2 (pb + 2t) + h
+#pragma unroll
+                    for (int t = 0; t < XT_SB; t++) v[t] = p.hT[(2 * (pb + 2 * (t >> 1)) + (t & 1)) * p.C_pad + mem[0]];
+                    for (int u = 1; u < p.m; u++) {
+                        uint16_t w[XT_SB];
+#pragma unroll
+                        for (int t = 0; t < XT_SB; t++)
+                            w[t] = p.hT[(2 * (pb + 2 * (t >> 1)) + (t & 1)) * p.C_pad + mem[u]];
+#pragma unroll
+                        for (int t = 0; t < XT_SB; t++) v[t] = v[t] < w[t] ? v[t] : w[t];
+                    }
+#pragma unroll
+                    for (int t = 0; t < XT_SB / 2; t++)
+                        Aw[(pb + 2 * t) * XT_R + rp] = valid ? ((uint32_t)v[2 * t] | ((uint32_t)v[2 * t + 1] << 16)) : 0u;
+                }
+#else
                 for (int64_t eb = e0; eb < p.E_pad; eb += 2 * XT_SB) {
                     uint16_t v[XT_SB];
 #pragma unroll
@@ -486,6 +543,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #pragma unroll
                     for (int t = 0; t < XT_SB; t++) As[(eb + 2 * t) * XT_R + r] = valid ? v[t] : (uint16_t)0;
                 }
+#endif
             }
             named_sync(1, XT_TCONS);
 
@@ -498,11 +556,31 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
             // warp w covers rows 32*(w>>1) .. +31 and columns 32*(w&1) .. +31 of the
             // 128x64 tile; a thread holds 8 consecutive rows (one 16-byte LDS) x 4
             // consecutive columns (one 8-byte LDS)
+#if XT_TC
+            // warp tile rows r0 .. r0+31, columns cw .. cw+31; acc[4 rb + cb][t] is the set
+            // (row r0 + 16 rb + g + 8 (t>>1), column cw + 8 cb + 2 qd + (t&1))
+            const int gq = lane >> 2, qd = lane & 3;
+            const int r0 = 32 * (warp >> 1);
+            const int cw = 32 * (warp & 1);
+            const int c0 = cw + 2 * qd;                      // the thread's first column
+            const int last7 = last_s[r0 + 24 + gq];          // its last row (colex: largest last member)
+            const uint32_t one2 = 0x3C003C00u;               // f16x2 (1, 1)
+            const uint32_t sel0 = gq == qd ? one2 : 0u, sel1 = gq == qd + 4 ? one2 : 0u;
+#define XT_ROW(i, j) (r0 + 16 * ((i) >> 2) + gq + 8 * ((j) >> 1))
+#define XT_COL(i, j) (cw + 8 * ((i) & 3) + 2 * qd + ((j) & 1))
+#define XT_GRPB(i, j) (((i) & 3) >= 2)
+#define XT_SPAN 25                                       // thread's last column - first column
+#else
             const int r0 = 32 * (warp >> 1) + 8 * ty;
             const int c0 = 32 * (warp & 1) + 4 * tx;
             // colex order: a row's largest member is non-decreasing in its rank (padding
             // rows hold INT_MAX), so the thread's last row bounds all eight
             const int last7 = last_s[r0 + 7];
+#define XT_ROW(i, j) (r0 + (i))
+#define XT_COL(i, j) (c0 + (j))
+#define XT_GRPB(i, j) ((j) >= 2)
+#define XT_SPAN 3
+#endif
             uint32_t slot = steps % XT_S, phase = (steps / XT_S) & 1u;
             int64_t ltile = lo + (int64_t)tk.y * XT_C;     // first column of the current tile
             for (int ct = tk.y; ct < tk.z; ct++, ltile += XT_C) {
@@ -514,6 +592,26 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                 for (int q = 0; q < nkc; q++) {
                     mbar_wait_stage(&full[slot], phase);
                     if (!skip) {
+#if XT_TC
+                        const uint32_t *Bw = Bs + slot * XT_K * (XT_C / 2) + cw + 8 * qd;
+                        const uint32_t *Aw = reinterpret_cast<const uint32_t *>(As) +
+                                             (int64_t)q * (XT_K / 2) * XT_R + r0 + 4 * gq;
+#pragma unroll kXtTcUnroll
+                        for (int pp = 0; pp < XT_K / 2; pp++) {
+                            const uint4 av = *reinterpret_cast<const uint4 *>(Aw + pp * XT_R);
+                            const uint4 b0 = *reinterpret_cast<const uint4 *>(Bw + pp * XT_C);
+                            const uint4 b1 = *reinterpret_cast<const uint4 *>(Bw + pp * XT_C + 4);
+                            const uint32_t rv[4] = {av.x, av.y, av.z, av.w};
+                            const uint32_t cv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                            for (int rb = 0; rb < 2; rb++)
+#pragma unroll
+                                for (int cb = 0; cb < 4; cb++)
+                                    tc_mma(acc[4 * rb + cb], hmin2(rv[2 * rb], cv[2 * cb]),
+                                           hmin2(rv[2 * rb + 1], cv[2 * cb]), hmin2(rv[2 * rb], cv[2 * cb + 1]),
+                                           hmin2(rv[2 * rb + 1], cv[2 * cb + 1]), sel0, sel1);
+                        }
+#else
                         const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
                         const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
 #if XT_G8 == 2
@@ -619,6 +717,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                             }
                         }
 #endif
+#endif
                     }
                     __syncwarp();
 #if XT_NOPROD
@@ -648,22 +747,24 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                 // order statistics and the window test are taken on acc itself and mapped
                 // once.  Padding / ragged sets become +inf.
                 const int64_t l0 = ltile + c0;
-                if (!(l0 + 3 < p.C && l0 > last7)) {
+                if (!(l0 + XT_SPAN < p.C && l0 > last7)) {
 #pragma unroll
-                    for (int i = 0; i < 8; i++) {
-                        const int last = last_s[r0 + i];
+                    for (int i = 0; i < 8; i++)
 #pragma unroll
-                        for (int j = 0; j < 4; j++)
-                            if (!(l0 + j < p.C && l0 + j > last)) acc[i][j] = INFINITY;
+                        for (int j = 0; j < 4; j++) {
+                            const int64_t l = ltile + XT_COL(i, j);
+                            if (!(l < p.C && l > last_s[XT_ROW(i, j)])) acc[i][j] = INFINITY;
+                        }
+                }
+                // tile minima of two disjoint groups of the thread's sets
+                float tA = INFINITY, tB = INFINITY;
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        if (XT_GRPB(i, j)) tB = fminf(tB, acc[i][j]);
+                        else tA = fminf(tA, acc[i][j]);
                     }
-                }
-                // tile minima of two disjoint column groups (j < 2, j >= 2)
-                float tA = fminf(acc[0][0], acc[0][1]), tB = fminf(acc[0][2], acc[0][3]);
-#pragma unroll
-                for (int i = 1; i < 8; i++) {
-                    tA = fminf(tA, fminf(acc[i][0], acc[i][1]));
-                    tB = fminf(tB, fminf(acc[i][2], acc[i][3]));
-                }
                 bA = fminf(bA, tA);
                 bB = fminf(bB, tB);
                 const float tau = fminf(p.tau_seed, __uint_as_float(Ubits));
@@ -676,8 +777,8 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                             if (acc[i][j] < INFINITY && lb <= tau) {
                                 const unsigned idx = atomicAdd(p.cand_n, 1u);
                                 if (idx < p.cap) {
-                                    p.cand_key[idx] = ((unsigned long long)(R0 + r0 + i) << KEY_BITS) |
-                                                      (unsigned long long)(l0 + j);
+                                    p.cand_key[idx] = ((unsigned long long)(R0 + XT_ROW(i, j)) << KEY_BITS) |
+                                                      (unsigned long long)(ltile + XT_COL(i, j));
                                     p.cand_s[idx] = lb;
                                 }
                             }
@@ -709,6 +810,10 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
         }
         steps += nsteps;
     }
+#undef XT_ROW
+#undef XT_COL
+#undef XT_GRPB
+#undef XT_SPAN
 }
 
 // ---------------------------------------------------------------------------
@@ -1304,6 +1409,24 @@ __global__ void __launch_bounds__(256) k_tile_hT(const uint16_t *__restrict__ hT
     }
 }
 
+// XT_TC layout of the same tiles: hTileP[sh][ct][pp][tc_cpos(j)] = f16x2(hT[2pp][c], hT[2pp+1][c]),
+// c = 64 ct + 8 sh + j (zero past C_pad); same byte offsets per 64-env stage as hTile
+__global__ void __launch_bounds__(256) k_tile_pp(const uint16_t *__restrict__ hT, int64_t E_pad, int64_t C_pad,
+                                                 int64_t n_ct, uint32_t *__restrict__ hTileP)
+{
+    const int64_t sct = blockIdx.x, ct = sct % n_ct, sh = sct / n_ct;
+    const int64_t c0 = 64 * ct + 8 * sh;
+    uint32_t *dst = hTileP + sct * (E_pad / 2) * 64;
+    for (int64_t i = threadIdx.x; i < (E_pad / 2) * 64; i += blockDim.x) {
+        const int64_t pp = i >> 6;
+        const int j = (int)(i & 63);
+        const int64_t c = c0 + j;
+        uint32_t w = 0;
+        if (c < C_pad) w = (uint32_t)hT[(2 * pp) * C_pad + c] | ((uint32_t)hT[(2 * pp + 1) * C_pad + c] << 16);
+        dst[pp * 64 + tc_cpos(j)] = w;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // fp64 refine of the survivors: warp per candidate, fixed shuffle tree
 // ---------------------------------------------------------------------------
@@ -1584,6 +1707,14 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const double gam_mma = n_mma * d_mma / (1.0 - n_mma * d_mma);
     const double eta_rel = (u16 + gam_mma + u16 * gam_mma) * 1.01;
     const double eta_abs = (double)v->E_pad * std::ldexp(1.0, -25) * (1.0 + gam_mma) * 1.01;
+#elif XT_TC
+    // tensor-summed tiled kernel: fp16 terms u16 (the mins are exact fp16 values), then
+    // E_pad/2 chained MMA accumulations of one env pair each, each assumed within 2^-18
+    // relative of its exact result (as k_exh_mma; measured worst 2^-22.1)
+    const double n_mma = (double)v->E_pad / 2.0, d_mma = std::ldexp(1.0, -18);
+    const double gam_mma = n_mma * d_mma / (1.0 - n_mma * d_mma);
+    const double eta_rel = (u16 + gam_mma + u16 * gam_mma) * 1.01;
+    const double eta_abs = (double)v->E_pad * std::ldexp(1.0, -25) * (1.0 + gam_mma) * 1.01;
 #else
     const double eta_rel = eta_rel16, eta_abs = eta_abs16;
 #endif
@@ -1599,7 +1730,12 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         // reads past the end
         mv->n_ct = (v->C_pad + XT_C - 1) / XT_C + 1;
         PT_TRY(pt_dalloc(ctx, (void **)&mv->hTile, sizeof(uint16_t) * 8 * mv->n_ct * v->E_pad * XT_C));
+#if XT_TC
+        k_tile_pp<<<(unsigned)(8 * mv->n_ct), 256, 0, s>>>(v->hT, v->E_pad, v->C_pad, mv->n_ct,
+                                                           reinterpret_cast<uint32_t *>(mv->hTile));
+#else
         k_tile_hT<<<(unsigned)(8 * mv->n_ct), 256, 0, s>>>(v->hT, v->E_pad, v->C_pad, mv->n_ct, mv->hTile);
+#endif
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());
     }
