@@ -11,7 +11,8 @@ of the whole hot path over that matrix:
   + pt_eval_holdout_all, 5 folds, greedy k=5  (88,655 sets)
 With N GPUs the exhaustive searches are sharded across ranks and merged with an
 NCCL all-gather of the (score, tuple) records (strong scaling: the job is fixed);
-load, greedy and the (batched, one-launch) holdout run on every rank.
+every rank loads the matrix, greedy k=24 runs on rank 0 and the (batched,
+one-launch) holdout on rank 1 (both on rank 0 at N=1).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {pt,reference}]
 """
@@ -263,18 +264,27 @@ def main():
     flush.fill_(0)                     # load the fill kernel's module before any timing
     torch.cuda.synchronize()
 
+    # with N ranks the exhaustive searches are sharded; the two unsharded parts
+    # (greedy k=24 and the batched holdout) run once per job, on ranks 0 and 1
+    do_greedy = rank == 0
+    do_holdout = rank == 1 % world
+
     def step(src):
         """One pass of the whole hot path; returns (results, d2h bytes)."""
         ctx = pt.pt_load_perf(src, dev, device=local)
-        idx, gt, gp = pt.pt_greedy_select(ctx, K_GREEDY)
-        d2h = idx.__len__() * 4 + gt.nbytes + gp.nbytes
+        d2h = 0
+        idx = None
+        if do_greedy:
+            idx, gt, gp = pt.pt_greedy_select(ctx, K_GREEDY)
+            d2h += idx.__len__() * 4 + gt.nbytes + gp.nbytes
         r2 = pt.exhaustive_best_distributed(ctx, 2) if world > 1 else pt.pt_exhaustive_best(ctx, 2)
         st = pt.pt_get_stats(ctx)
         r3 = pt.exhaustive_best_distributed(ctx, 3) if world > 1 else pt.pt_exhaustive_best(ctx, 3)
         st3 = pt.pt_get_stats(ctx)
         d2h += 2 * (2 * 3 * 4 + 4 * 8)
-        hold = pt.pt_eval_holdout_all(ctx, K_HOLDOUT, 5)      # all 5 folds, one batched launch
-        d2h += len(hold) * (2 * K_HOLDOUT * 4 + 3 * 8)
+        if do_holdout:
+            hold = pt.pt_eval_holdout_all(ctx, K_HOLDOUT, 5)      # all 5 folds, one batched launch
+            d2h += len(hold) * (2 * K_HOLDOUT * 4 + 3 * 8)
         st_end = pt.pt_get_stats(ctx)
         pt.pt_free(ctx)
         return {"greedy": idx, "r2": r2, "r3": r3, "k3_ms": st3["exh_main_ms"],
@@ -314,6 +324,13 @@ def main():
 
     ms, k3_ms, launches, res, d2h, clocks = timed(dT, args.steps, args.warmup)
     ms_e2e, _, _, _, d2h_e2e, clocks_e2e = timed(hT, args.steps, 1)
+    h2d_e2e = int(T.nbytes) * world            # every rank loads the matrix
+    if world > 1:
+        # job totals: the copies and launches of every rank
+        agg = torch.tensor([float(d2h_e2e), float(launches)], dtype=torch.float64,
+                           device="cpu" if SAME_GPU else "cuda")
+        dist.all_reduce(agg)
+        d2h_e2e, launches = int(agg[0].item()), int(agg[1].item())
     # secondary config-5 line: every rank takes part (sharded greedy for world > 1)
     scaled = None if args.no_scaled else measure_scaled(pt, synth, local, peaks(), world=world)
 
@@ -376,7 +393,7 @@ def main():
                    "l2": "flushed between steps (256 MiB write, inside the timed region)",
                    "parallelism": (f"subset-space shards x{world}" + (" (DEBUG: all ranks on one GPU, gloo)" if SAME_GPU else "")) if world > 1 else "single GPU"},
         "e2e": {"value": SETS_PER_STEP * args.steps / (ms_e2e * 1e-3), "unit": "sets/s",
-                "h2d_bytes_per_step": int(T.nbytes), "d2h_bytes_per_step": int(d2h_e2e)},
+                "h2d_bytes_per_step": h2d_e2e, "d2h_bytes_per_step": int(d2h_e2e)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "alu", "kernel": "k_exh_tiled (k=3)", "achieved": achieved,
                      "peak": peak, "unit": "T(set,env)/s", "frac": achieved / peak, "traffic": traffic,
