@@ -340,6 +340,13 @@ __device__ __forceinline__ void fhadd2(float &lo_acc, float &hi_acc, uint32_t p)
 #ifndef XT_TC
 #define XT_TC 0
 #endif
+#ifndef XT_HALF
+#define XT_HALF 0   // 1 (with XT_NOPROD, not XT_TC): one B ring per 32-column half, 4 warps each
+#endif              //   (measured 12.08 vs 12.04 ms: the stage misses are not warp coupling)
+#define XT_BSTR (XT_HALF ? XT_C / 4 : XT_C / 2)   // u32 per env row of a warp's B stage
+#ifndef XT_PROBE
+#define XT_PROBE 0    // debug build: wait statistics in the tail of the candidate score buffer
+#endif
 #ifndef XT_TCU
 #define XT_TCU 4      // XT_TC: unroll of the env-pair loop
 #endif
@@ -422,18 +429,20 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
     uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2
     uint16_t *As = reinterpret_cast<uint16_t *>(Bs + XT_S * XT_K * (XT_C / 2)); // [E_pad][128] fp16
     int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);                // [128]
-    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);              // [S]
-    uint64_t *empty = full + XT_S;                                             // [S]
-    int4 *task_s = reinterpret_cast<int4 *>(empty + XT_S);
-    int *relcnt = reinterpret_cast<int *>(task_s + 1);                         // [S] (XT_NOPROD)
+    // B ring: XT_HALF ? [2 halves][S] stages of [K][32 cols] : [S] stages of [K][64 cols]
+    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);              // [2S]
+    uint64_t *empty = full + 2 * XT_S;                                         // [2S] (keeps task_s 16-aligned)
+    int4 *task_s = reinterpret_cast<int4 *>(empty + 2 * XT_S);
+    int *relcnt = reinterpret_cast<int *>(task_s + 1);                         // [2S] (XT_NOPROD)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nkc = (int)(p.E_pad / XT_K);
     if (tid == 0) {
         for (int s = 0; s < XT_S; s++) {
             mbar_init(&full[s], 1);
+            mbar_init(&full[XT_S + s], 1);
             mbar_init(&empty[s], XT_TCONS / 32);
-            relcnt[s] = 0;
+            relcnt[s] = relcnt[XT_S + s] = 0;
         }
         mbar_fence_init();
     }
@@ -459,17 +468,27 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #if XT_NOPROD
         // stage g of this task (column tile tk.y + g / nkc, env chunk g % nkc) into its ring
         // slot: one bulk copy, completion counted on full[slot]
-        auto issue = [&](int g) {
+        auto issue = [&](int g, int h) {
             const int sl = (int)((steps + (uint32_t)g) % XT_S);
             const int64_t col = lo + (int64_t)(tk.y + g / nkc) * XT_C;
             const int64_t sh = (col >> 3) & 7, ct = (col - 8 * sh) >> 6;
+#if XT_HALF
+            // half h of the stage: hTile is stored [sh][ct][half][e][32]
+            const uint16_t *src = p.hTile + (((sh * p.n_ct + ct) * 2 + h) * p.E_pad + (int64_t)(g % nkc) * XT_K) * 32;
+            mbar_expect_tx(&full[h * XT_S + sl], XT_K * 64);
+            bulk_g2s(Bs + (h * XT_S + sl) * XT_K * 16, src, XT_K * 64, &full[h * XT_S + sl]);
+#else
             const uint16_t *src = p.hTile + ((sh * p.n_ct + ct) * p.E_pad + (int64_t)(g % nkc) * XT_K) * XT_C;
             mbar_expect_tx(&full[sl], XT_K * XT_BROW);
             bulk_g2s(Bs + sl * XT_K * (XT_C / 2), src, XT_K * XT_BROW, &full[sl]);
+#endif
         };
         // every warp has left the previous task (barrier above): the whole ring is free
         if (tid == 0)
-            for (int g = 0; g < XT_S && g < nsteps; g++) issue(g);
+            for (int g = 0; g < XT_S && g < nsteps; g++) {
+                issue(g, 0);
+                if (XT_HALF) issue(g, 1);
+            }
 #endif
 
         if (!XT_NOPROD && warp == XT_TCONS / 32) {
@@ -590,7 +609,16 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                 // L2 latency hides behind it (a stale value is only a looser bound)
                 const unsigned Ubits = *(volatile unsigned *)p.U;
                 for (int q = 0; q < nkc; q++) {
-                    mbar_wait_stage(&full[slot], phase);
+#if XT_PROBE
+                    // debug: count stage waits that find the data missing, split into the first
+                    // stage of a task, the first stage of a later column tile, and the rest
+                    if (!mbar_test(&full[(XT_HALF ? (warp & 1) * XT_S : 0) + slot], phase) && lane == 0) {
+                        const int kind = (ct == tk.y && q == 0) ? 0 : (q == 0 ? 1 : 2);
+                        atomicAdd(reinterpret_cast<unsigned long long *>(p.cand_s) + (p.cap / 2 - 4 + kind), 1ull);
+                    }
+                    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(p.cand_s) + (p.cap / 2 - 1), 1ull);
+#endif
+                    mbar_wait_stage(&full[(XT_HALF ? (warp & 1) * XT_S : 0) + slot], phase);
                     if (!skip) {
 #if XT_TC
                         const uint32_t *Bw = Bs + slot * XT_K * (XT_C / 2) + cw + 8 * qd;
@@ -612,7 +640,11 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                                            hmin2(rv[2 * rb + 1], cv[2 * cb + 1]), sel0, sel1);
                         }
 #else
+#if XT_HALF
+                        const uint32_t *B = Bs + ((warp & 1) * XT_S + slot) * XT_K * 16 + (c0 & 31) / 2;
+#else
                         const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
+#endif
                         const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
 #if XT_G8 == 2
                         // XT_NG 4-env fp16 trees per unit summed in fp16 (one HADD2 each) before
@@ -629,7 +661,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #pragma unroll
                                 for (int t = 0; t < 4; t++) {
                                     ar[t] = *reinterpret_cast<const uint4 *>(A + (e + 4 * gq + t) * XT_R);
-                                    bc[t] = *reinterpret_cast<const uint2 *>(B + (e + 4 * gq + t) * (XT_C / 2));
+                                    bc[t] = *reinterpret_cast<const uint2 *>(B + (e + 4 * gq + t) * XT_BSTR);
                                 }
 #pragma unroll
                                 for (int i = 0; i < 8; i++) {
@@ -665,7 +697,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #pragma unroll
                             for (int t = 0; t < 8; t++) {
                                 ar[t] = *reinterpret_cast<const uint4 *>(A + (e + t) * XT_R);
-                                bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
+                                bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * XT_BSTR);
                             }
 #pragma unroll
                             for (int i = 0; i < 8; i++) {
@@ -696,7 +728,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #pragma unroll
                             for (int t = 0; t < 4; t++) {
                                 ar[t] = *reinterpret_cast<const uint4 *>(A + (e + t) * XT_R);
-                                bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * (XT_C / 2));
+                                bc[t] = *reinterpret_cast<const uint2 *>(B + (e + t) * XT_BSTR);
                             }
 #pragma unroll
                             for (int i = 0; i < 8; i++) {
@@ -725,12 +757,13 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                         // release: the last of the consumer warps to finish this stage refills
                         // the slot with stage g + S of the task
                         __threadfence_block();
-                        if (atomicAdd(&relcnt[slot], 1) == XT_TCONS / 32 - 1) {
-                            relcnt[slot] = 0;
+                        const int h = XT_HALF ? (warp & 1) : 0;
+                        if (atomicAdd(&relcnt[h * XT_S + slot], 1) == XT_TCONS / (XT_HALF ? 64 : 32) - 1) {
+                            relcnt[h * XT_S + slot] = 0;
                             __threadfence_block();
                             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                             const int gn = (ct - tk.y) * nkc + q + XT_S;
-                            if (gn < nsteps) issue(gn);
+                            if (gn < nsteps) issue(gn, h);
                         }
                     }
 #else
@@ -1405,7 +1438,12 @@ __global__ void __launch_bounds__(256) k_tile_hT(const uint16_t *__restrict__ hT
     uint4 *dst = reinterpret_cast<uint4 *>(hTile + sct * E_pad * 64);
     for (int64_t i = threadIdx.x; i < E_pad * 8; i += blockDim.x) {
         const int64_t e = i >> 3, c = c0 + 8 * (i & 7);
-        dst[i] = c < C_pad ? *reinterpret_cast<const uint4 *>(hT + e * C_pad + c) : make_uint4(0, 0, 0, 0);
+        const uint4 v = c < C_pad ? *reinterpret_cast<const uint4 *>(hT + e * C_pad + c) : make_uint4(0, 0, 0, 0);
+#if XT_HALF
+        dst[((i & 7) >> 2) * E_pad * 4 + e * 4 + (i & 3)] = v;   // [half][e][32]
+#else
+        dst[i] = v;
+#endif
     }
 }
 
@@ -1764,7 +1802,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         ws ? sizeof(uint32_t) * XT_S * 2 * XT_K * 32 + 2 * sizeof(uint16_t) * v->E_pad * XT_R +
                  2 * sizeof(int) * XT_R + 2 * sizeof(int4) + 2 * sizeof(uint64_t) * (XT_S + 2)
            : sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
-                 sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
+                 sizeof(int) * XT_R + 4 * sizeof(uint64_t) * XT_S + sizeof(int4) + 2 * sizeof(int) * XT_S;
 #endif
     const int threads = XT_MMA ? XT_THREADS : ws ? XW_THREADS : XT_TTHREADS;
     PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1823,6 +1861,9 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         int occ = 1;
         PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
         const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
+#if XT_PROBE
+        PT_CK(cudaMemsetAsync(cq + cap - 8, 0, 32, s));
+#endif
         PT_CK(cudaEventRecord(ctx->ev0, s));
         kern<<<grid, threads, smem, s>>>(p);
         PT_CK(cudaEventRecord(ctx->ev1, s));
@@ -1841,6 +1882,14 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         PT_TRY(io.d2h(s_out, os, sizeof(double) * 2));
         PT_TRY(io.d2h(t_out, ot, sizeof(int32_t) * 2 * k));
         PT_TRY(io.finish());
+#if XT_PROBE
+        {
+            unsigned long long w[4];
+            cudaMemcpy(w, cq + cap - 8, 32, cudaMemcpyDeviceToHost);
+            fprintf(stderr, "XT_PROBE k=%d waits: task-first %llu tile-first %llu other %llu of %llu stage waits\n", k,
+                    w[0], w[1], w[2], w[3]);
+        }
+#endif
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
         if (pass == 0) ctx->stats.exh_main_ms = ms;
