@@ -613,7 +613,12 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                     // debug: count stage waits that find the data missing, split into the first
                     // stage of a task, the first stage of a later column tile, and the rest
                     if (!mbar_test(&full[(XT_HALF ? (warp & 1) * XT_S : 0) + slot], phase) && lane == 0) {
+#if XT_PROBE == 2
+                        // breakdown: kind 0 = skipping warp, 1 = warp parity 0, 2 = parity 1
+                        const int kind = skip ? 0 : 1 + (warp & 1);
+#else
                         const int kind = (ct == tk.y && q == 0) ? 0 : (q == 0 ? 1 : 2);
+#endif
                         atomicAdd(reinterpret_cast<unsigned long long *>(p.cand_s) + (p.cap / 2 - 4 + kind), 1ull);
                     }
                     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(p.cand_s) + (p.cap / 2 - 1), 1ull);
