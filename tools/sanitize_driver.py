@@ -38,3 +38,11 @@ print("fleet exh", pt.pt_exhaustive_best(ctx, 2, objective=pt.PT_OBJ_FLEET)["bes
 print("fleet score", pt.pt_score_sets(ctx, np.array([[0, 1]], np.int32), objective=pt.PT_OBJ_FLEET))
 pt.pt_free(ctx)
 print("sanitize driver done")
+# multi-stage column tiles (E_pad = 192: three 64-env stages per tile, the ring wraps
+# inside a tile) for the producer-less release protocol
+T2, dev2 = synth.small_matrix(4, n_cfg=200, n_dev=3, n_inputs=64)
+ctx = pt.pt_load_perf(T2, dev2)
+pt.pt_greedy_select(ctx, 5)
+print("k3 multi-stage", pt.pt_exhaustive_best(ctx, 3)["best"], pt.pt_exhaustive_best(ctx, 2)["best"])
+pt.pt_free(ctx)
+print("sanitize driver done (multi-stage)")
