@@ -100,7 +100,58 @@ struct pt_tasks {
     std::vector<int64_t> slot_pre;    // prefix sums of slots per task
     std::vector<int64_t> set_pre;     // prefix sums of useful sets per task
     int4 *d = nullptr;                // device copy (lives for the process)
+    // multi-GPU shard plans, keyed by shard count: the tasks dealt to shards in snake
+    // order (0..N-1, N-1..0, ...) down the decreasing-size list, so every shard gets
+    // the same mix of large and small tasks and ends on small ones (a contiguous cut
+    // would hand shard 0 all of the largest tasks: a long tail at 8 GPUs)
+    struct plan {
+        int4 *d = nullptr;
+        std::vector<int> off;          // shard r owns d[off[r], off[r+1])
+        std::vector<int64_t> sets, slots;
+    };
+    std::map<int, plan> plans;
 };
+
+static pt_status shard_plan(pt_tasks *T, int N, const pt_tasks::plan **out)
+{
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = T->plans.find(N);
+    if (it != T->plans.end()) {
+        *out = &it->second;
+        return PT_OK;
+    }
+    const int n = (int)T->h.size();
+    std::vector<std::vector<int>> per(N);
+    for (int i = 0; i < n; i++) {
+        const int rnd = i / N, pos = i % N;
+        per[(rnd & 1) ? N - 1 - pos : pos].push_back(i);
+    }
+    pt_tasks::plan P;
+    std::vector<int4> h;
+    h.reserve(n);
+    P.off.push_back(0);
+    for (int r = 0; r < N; r++) {
+        int64_t se = 0, sl = 0;
+        for (int i : per[r]) {
+            h.push_back(T->h[i]);
+            se += T->set_pre[i + 1] - T->set_pre[i];
+            sl += T->slot_pre[i + 1] - T->slot_pre[i];
+        }
+        P.off.push_back((int)h.size());
+        P.sets.push_back(se);
+        P.slots.push_back(sl);
+    }
+    if (n > 0) {
+        if (cudaMalloc(&P.d, sizeof(int4) * n) != cudaSuccess) {
+            cudaGetLastError();
+            return pt_fail(PT_ENOMEM, "shard plan allocation failed");
+        }
+        cudaMemcpy(P.d, h.data(), sizeof(int4) * n, cudaMemcpyHostToDevice);
+    }
+    *out = &(T->plans[N] = std::move(P));
+    return PT_OK;
+}
 
 // The work list depends only on (device, C, m, #SMs): built once per process
 // and shared by every context (a fresh pt_load_perf does not rebuild it).
@@ -1681,18 +1732,22 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const bool ws = XW_ENABLE && !XT_MMA && v->E_pad <= XW_EMAX;   // warp-specialised kernel (A double-buffered)
     PT_TRY(build_tasks(ctx, v, m, XT_MMA ? XM_R : XT_R, ws ? XW_C : XT_C, &T));
     const int n_tasks = (int)T->h.size();
-    // equal-work contiguous shard of the task list
-    const int64_t total = T->slot_pre.back();
-    auto cut = [&](int64_t r) {
-        const int64_t target = total * r / shard_count;
-        return (int)(std::lower_bound(T->slot_pre.begin(), T->slot_pre.end(), target) -
-                     T->slot_pre.begin());
-    };
-    const int ta = std::min(cut(shard_rank), n_tasks), tb = std::min(cut(shard_rank + 1), n_tasks);
+    // this shard's tasks: the whole list, or its snake-dealt part (shard_plan)
+    const int4 *task_list = T->d;
+    int ta = 0, tb = n_tasks;
+    ctx->stats.exh_sets = T->set_pre.back();
+    ctx->stats.exh_slots = T->slot_pre.back();
+    if (shard_count > 1) {
+        const pt_tasks::plan *P = nullptr;
+        PT_TRY(shard_plan(T, shard_count, &P));
+        task_list = P->d;
+        ta = P->off[shard_rank];
+        tb = P->off[shard_rank + 1];
+        ctx->stats.exh_sets = P->sets[shard_rank];
+        ctx->stats.exh_slots = P->slots[shard_rank];
+    }
     ctx->stats.exh_kernel = 0;
     ctx->stats.exh_env_pad = v->E_pad;
-    ctx->stats.exh_sets = T->set_pre[tb] - T->set_pre[ta];
-    ctx->stats.exh_slots = T->slot_pre[tb] - T->slot_pre[ta];
     ctx->stats.exh_candidates = 0;
     ctx->stats.exh_passes = 0;
     ctx->stats.exh_main_ms = 0.0;
@@ -1843,7 +1898,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.E_pad = v->E_pad;
         p.n_rows = pt_binom(v->C, m);
         p.m = m;
-        p.tasks = T->d;
+        p.tasks = task_list;
         p.task_hi = tb;
         p.task_ctr = ctr;
         p.tau_seed = tau_pass;
