@@ -104,7 +104,7 @@ def test_medium_exhaustive(seed, C, ndev, nin):
     # sharded on one GPU (fake multi-GPU): merged shards == unsharded
     for k in (2, 3):
         want = o.exhaustive(k)
-        for shards in (2, 3, 8):
+        for shards in (2, 3, 8, 50):   # 50: more shards than tasks (empty shards)
             recs_s, recs_t = [], []
             total = 0
             for r in range(shards):
