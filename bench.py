@@ -333,6 +333,24 @@ def main():
         d2h_e2e, launches = int(agg[0].item()), int(agg[1].item())
     # secondary config-5 line: every rank takes part (sharded greedy for world > 1)
     scaled = None if args.no_scaled else measure_scaled(pt, synth, local, peaks(), world=world)
+    # shard balance of the k=3 search (single-GPU runs only): the N shards of the
+    # multi-GPU partition run one after another on this GPU; max over shards = the
+    # kernel time an N-GPU run would see per GPU.  A model, not a multi-GPU measurement.
+    shard_bal = None
+    if world == 1:
+        ctx = pt.pt_load_perf(dT, dev, device=local)
+        pt.pt_exhaustive_best(ctx, 3)
+        full_ms = pt.pt_get_stats(ctx)["exh_main_ms"]
+        shard_bal = {"basis": "k=3 kernel (CUDA events) of each shard of the N-way partition, "
+                              "run sequentially on this GPU", "full_ms": full_ms}
+        for n in (2, 4, 8):
+            t = []
+            for r in range(n):
+                pt.pt_exhaustive_best(ctx, 3, shard_rank=r, shard_count=n)
+                t.append(pt.pt_get_stats(ctx)["exh_main_ms"])
+            shard_bal[str(n)] = {"max_ms": max(t), "mean_ms": float(np.mean(t)),
+                                 "efficiency": full_ms / n / max(t)}
+        pt.pt_free(ctx)
 
     if rank != 0:
         if world > 1:
@@ -412,6 +430,7 @@ def main():
         "parity": {"k3_best": list(res["r3"]["best"]), "k3_matches_oracle_golden": gold,
                    "k3_candidates_refined": res["k3_cand"]},
         "scaled_greedy": scaled,
+        "k3_shard_balance": shard_bal,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
