@@ -229,6 +229,77 @@ def measure_scaled(pt, synth, local, pk, steps=3, world=1):
 
 
 
+FP64_PEAK_TFLOPS = 2 * 16.96   # tools/ubench_fp64.cu on this pool's B200: 58.3 DFMA/clk/SM (2 flops each)
+
+
+def measure_next_rows(pt, T, dev, local, cpu=True):
+    """The §8(f) NEXT rows at the paper shape, each timed on the device (CUDA events
+    around the call on the library's stream, median of 3 after a warm-up) beside the
+    CPU oracle on the same workload: fleet objective (Eq. 2) greedy k=24 and
+    exhaustive k=2, swap local search k=24, k-means k=24.  Work = (set, env)
+    evaluations of one min + one multiply-add (k-means: (point, centroid, dim) of
+    one subtract + one multiply-add), counted as 2 fp64 flops; roofline = the
+    measured DFMA rate."""
+    import torch
+    from oracle import Oracle
+    C, E = T.shape[1], T.shape[0]
+    qd = np.array([5.0, 2.0, 1.0, 3.0, 4.0])      # fleet mix (invented; tests/test_gpu_fleet.py)
+    qe = np.ones(len(dev))
+    ctx = pt.pt_load_perf(torch.from_numpy(T).cuda(), dev, device=local)
+    pt.pt_set_fleet(ctx, qd, qe)
+    o = Oracle(T, dev) if cpu else None
+    if o is not None:
+        o.set_fleet(qd, qe)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def dev_ms(fn):
+        fn()
+        ms = []
+        for _ in range(3):
+            e0.record()
+            r = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return float(np.median(ms)), r
+
+    def cpu_s(fn):
+        if o is None:
+            return None
+        t0 = time.perf_counter()
+        fn()
+        return time.perf_counter() - t0
+
+    rows = {}
+    ms, _ = dev_ms(lambda: pt.pt_greedy_select(ctx, 24, objective=pt.PT_OBJ_FLEET))
+    ev = sum(C - t for t in range(24)) * E
+    rows["fleet_greedy_k24"] = (ms, ev, sum(C - t for t in range(24)), cpu_s(lambda: o.fleet_greedy(24)))
+    ms, _ = dev_ms(lambda: pt.pt_exhaustive_best(ctx, 2, objective=pt.PT_OBJ_FLEET))
+    rows["fleet_exhaustive_k2"] = (ms, math.comb(C, 2) * E, math.comb(C, 2), cpu_s(lambda: o.fleet_exhaustive(2)))
+    ms, (_, _, moves) = dev_ms(lambda: pt.pt_swap_search(ctx, 24))
+    sets = (moves + 1) * 24 * (C - 24)
+    rows["swap_k24"] = (ms, sets * E, sets, cpu_s(lambda: o.swap_search(24)))
+    ms, (_, _, iters) = dev_ms(lambda: pt.pt_kmeans_select(ctx, 24))
+    rows["kmeans_k24"] = (ms, iters * E * 24 * C, None, cpu_s(lambda: o.kmeans(24)))
+    pt.pt_free(ctx)
+    out = {}
+    for name, (ms, evals, sets, cs) in rows.items():
+        fl = 2.0 * evals
+        r = {"ms": ms, "gflops": fl / (ms * 1e-3) / 1e9,
+             "roofline": {"bound": "fp64", "achieved": fl / (ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                          "unit": "TFLOP/s", "frac": fl / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS}}
+        if sets is not None:
+            r["sets_per_s"] = sets / (ms * 1e-3)
+        if cs is not None:
+            r["oracle_s"] = cs
+            r["oracle_sets_per_s"] = sets / cs if sets is not None else None
+        out[name] = r
+    if moves is not None:
+        out["swap_k24"]["moves"] = moves
+    out["kmeans_k24"]["iterations"] = iters
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -237,6 +308,7 @@ def main():
     ap.add_argument("--impl", default="pt", choices=["pt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
     ap.add_argument("--no-scaled", action="store_true",
                     help="skip the secondary config-5 measurement (scaled greedy, HBM-bound)")
     args = ap.parse_args()
@@ -333,6 +405,9 @@ def main():
         d2h_e2e, launches = int(agg[0].item()), int(agg[1].item())
     # secondary config-5 line: every rank takes part (sharded greedy for world > 1)
     scaled = None if args.no_scaled else measure_scaled(pt, synth, local, peaks(), world=world)
+    next_rows = None
+    if world == 1 and not args.no_next:
+        next_rows = measure_next_rows(pt, T, dev, local, cpu=not args.no_cpu_baseline)
     # shard balance of the k=3 search (single-GPU runs only): the N shards of the
     # multi-GPU partition run one after another on this GPU; max over shards = the
     # kernel time an N-GPU run would see per GPU.  A model, not a multi-GPU measurement.
@@ -431,6 +506,7 @@ def main():
                    "k3_candidates_refined": res["k3_cand"]},
         "scaled_greedy": scaled,
         "k3_shard_balance": shard_bal,
+        "next_rows": next_rows,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

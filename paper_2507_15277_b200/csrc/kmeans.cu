@@ -80,6 +80,39 @@ __global__ void __launch_bounds__(128) k_km_dist(const double *__restrict__ X, i
             if (j < nc) D[q * KM_MAXK + j] = acc[j];
 }
 
+// the same distances with one thread per (point, centroid): ne * nc threads instead of
+// ne (the per-thread loop over c ascending -- and so every result -- is unchanged)
+__global__ void __launch_bounds__(128) k_km_dist1(const double *__restrict__ X, int64_t ne, int64_t C,
+                                                 const double *__restrict__ M, int nc,
+                                                 double *__restrict__ D)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ne * nc) return;
+    const int64_t q = i % ne;
+    const int j = (int)(i / ne);
+    const double *m = M + (int64_t)j * C;
+    double acc = 0.0;
+    int64_t c = 0;
+    for (; c + 16 <= C; c += 16) {   // 16 loads in flight, then the sums in c order
+        double x[16], y[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            x[u] = X[(c + u) * ne + q];
+            y[u] = __ldg(m + c + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            const double t = __dsub_rn(x[u], y[u]);
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+    }
+    for (; c < C; c++) {
+        const double t = __dsub_rn(X[c * ne + q], __ldg(m + c));
+        acc = __dadd_rn(acc, __dmul_rn(t, t));
+    }
+    D[q * KM_MAXK + j] = acc;
+}
+
 // centroid update: M[j][c] = sum over points of cluster j (q ascending); counts on host
 __global__ void k_km_update(const double *__restrict__ X, int64_t ne, int64_t C,
                             const int32_t *__restrict__ asg, int k, const int32_t *__restrict__ cnt,
@@ -171,13 +204,14 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
     k_km_build<<<(unsigned)C, 128, 0, s>>>(ctx->T32, C, ctx->best, ctx->penalty, d_envs, ne, X);
     const unsigned gc = (unsigned)((C + 127) / 128), gq = (unsigned)((ne + 127) / 128);
     std::vector<double> hD(ne * KM_MAXK), dmin(ne);
+    (void)gq;
     auto dist = [&](const double *cent, int nc) -> pt_status {
-        k_km_dist<<<gq, 128, 0, s>>>(X, ne, C, cent, nc, D);
+        k_km_dist1<<<(unsigned)((ne * nc + 127) / 128), 128, 0, s>>>(X, ne, C, cent, nc, D);
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());
-        PT_CK(cudaMemcpyAsync(hD.data(), D, sizeof(double) * ne * KM_MAXK, cudaMemcpyDeviceToHost, s));
-        PT_CK(cudaStreamSynchronize(s));
-        return PT_OK;
+        pt_hostio io(ctx);
+        PT_TRY(io.d2h(hD.data(), D, sizeof(double) * ne * KM_MAXK));
+        return io.finish();
     };
     // init: the point nearest the mean, then successive farthest points (maximin)
     k_km_mean<<<gc, 128, 0, s>>>(X, ne, C, mean);
