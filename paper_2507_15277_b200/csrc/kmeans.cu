@@ -113,6 +113,37 @@ __global__ void __launch_bounds__(128) k_km_dist1(const double *__restrict__ X, 
     D[q * KM_MAXK + j] = acc;
 }
 
+// every point's distance to every point and to the mean (column ne), for the
+// maximin initialisation: P[q][r] is what k_km_dist1 returns for point q and a
+// centroid that is a copy of point r (or the mean) -- the same c-ascending sum
+__global__ void __launch_bounds__(128) k_km_pair(const double *__restrict__ X, int64_t ne, int64_t C,
+                                                const double *__restrict__ mean, double *__restrict__ P)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ne * (ne + 1)) return;
+    const int64_t q = i % ne, r = i / ne;
+    double acc = 0.0;
+    int64_t c = 0;
+    for (; c + 16 <= C; c += 16) {
+        double x[16], y[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            x[u] = X[(c + u) * ne + q];
+            y[u] = r < ne ? X[(c + u) * ne + r] : mean[c + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            const double t = __dsub_rn(x[u], y[u]);
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+    }
+    for (; c < C; c++) {
+        const double t = __dsub_rn(X[c * ne + q], r < ne ? X[c * ne + r] : mean[c]);
+        acc = __dadd_rn(acc, __dmul_rn(t, t));
+    }
+    P[q * (ne + 1) + r] = acc;
+}
+
 // centroid update: M[j][c] = sum over points of cluster j (q ascending); counts on host
 __global__ void k_km_update(const double *__restrict__ X, int64_t ne, int64_t C,
                             const int32_t *__restrict__ asg, int k, const int32_t *__restrict__ cnt,
@@ -213,21 +244,55 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
         PT_TRY(io.d2h(hD.data(), D, sizeof(double) * ne * KM_MAXK));
         return io.finish();
     };
-    // init: the point nearest the mean, then successive farthest points (maximin)
+    // init: the point nearest the mean, then successive farthest points (maximin).
+    // Every centroid of the init is a copy of a point, so up to 1,024 points one
+    // pairwise pass (+ the mean) answers all k distance passes; beyond that, one
+    // distance pass per centroid.
     k_km_mean<<<gc, 128, 0, s>>>(X, ne, C, mean);
     ctx->stats.launches += 2;
-    PT_TRY(dist(mean, 1));
+    const bool pairwise = ne <= 1024;
+    std::vector<double> hP;
+    if (pairwise) {
+        double *P = nullptr;
+        PT_TRY(pt_dalloc(ctx, (void **)&P, sizeof(double) * ne * (ne + 1)));
+        k_km_pair<<<(unsigned)((ne * (ne + 1) + 127) / 128), 128, 0, s>>>(X, ne, C, mean, P);
+        ctx->stats.launches++;
+        PT_CK(cudaGetLastError());
+        hP.resize((size_t)ne * (ne + 1));
+        pt_hostio io(ctx);
+        PT_TRY(io.d2h(hP.data(), P, sizeof(double) * ne * (ne + 1)));
+        pt_dfree(ctx, P);
+        PT_TRY(io.finish());
+    }
+    // (pairwise) distance of every point to the mean (r = ne) or to a copy of point r
+    auto point_dist = [&](int64_t r, std::vector<double> &out) -> pt_status {
+        for (int64_t q = 0; q < ne; q++) out[q] = hP[q * (ne + 1) + r];
+        return PT_OK;
+    };
+    std::vector<double> dq(ne);
     int64_t first = 0;
-    double bd = INFINITY;
-    for (int64_t q = 0; q < ne; q++)
-        if (hD[q * KM_MAXK] < bd) {
-            bd = hD[q * KM_MAXK];
-            first = q;
+    {
+        if (pairwise) {
+            PT_TRY(point_dist(ne, dq));
+        } else {
+            PT_TRY(dist(mean, 1));
+            for (int64_t q = 0; q < ne; q++) dq[q] = hD[q * KM_MAXK];
         }
+        double bd = INFINITY;
+        for (int64_t q = 0; q < ne; q++)
+            if (dq[q] < bd) {
+                bd = dq[q];
+                first = q;
+            }
+    }
     k_km_seed<<<gc, 128, 0, s>>>(X, ne, C, first, 0, M);
     ctx->stats.launches++;
-    PT_TRY(dist(M, 1));
-    for (int64_t q = 0; q < ne; q++) dmin[q] = hD[q * KM_MAXK];
+    if (pairwise) {
+        PT_TRY(point_dist(first, dmin));
+    } else {
+        PT_TRY(dist(M, 1));
+        for (int64_t q = 0; q < ne; q++) dmin[q] = hD[q * KM_MAXK];
+    }
     for (int j = 1; j < k; j++) {
         int64_t far = 0;
         double fd = -1.0;
@@ -238,8 +303,13 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
             }
         k_km_seed<<<gc, 128, 0, s>>>(X, ne, C, far, j, M);
         ctx->stats.launches++;
-        PT_TRY(dist(M + (int64_t)j * C, 1));
-        for (int64_t q = 0; q < ne; q++) dmin[q] = std::min(dmin[q], hD[q * KM_MAXK]);
+        if (pairwise) {
+            PT_TRY(point_dist(far, dq));
+        } else {
+            PT_TRY(dist(M + (int64_t)j * C, 1));
+            for (int64_t q = 0; q < ne; q++) dq[q] = hD[q * KM_MAXK];
+        }
+        for (int64_t q = 0; q < ne; q++) dmin[q] = std::min(dmin[q], dq[q]);
     }
     // Lloyd
     std::vector<int32_t> asg(ne, -1), cnt(k);

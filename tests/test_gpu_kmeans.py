@@ -50,3 +50,15 @@ def test_paper_shape():
         sel, G, it = pt.pt_kmeans_select(ctx, k)
         osel, oit, _ = o.kmeans(k)
         assert sel == osel and it == oit
+
+
+def test_many_points_per_pass_init():
+    """1,280 environments: above the pairwise-init limit (1,024 points), so the
+    maximin initialisation takes one distance pass per centroid."""
+    T, dev = synth.scaled(4, n_cfg=48, n_dev=20, n_inputs=64)
+    o = Oracle(T, dev)
+    ctx = pt.pt_load_perf(T, dev)
+    for k in (3, 7):
+        sel, G, it = pt.pt_kmeans_select(ctx, k)
+        osel, oit, _ = o.kmeans(k)
+        assert sel == osel and it == oit
