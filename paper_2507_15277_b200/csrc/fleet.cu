@@ -25,7 +25,7 @@
 __global__ void k_fleet_build(const float *__restrict__ T, int64_t E, int64_t C,
                               const double *__restrict__ best, double penalty,
                               const int32_t *__restrict__ perm, int64_t E_pad,
-                              double *__restrict__ tcm)
+                              double *__restrict__ tcm, double *__restrict__ tem)
 {
     const int64_t c = blockIdx.x;
     for (int64_t q = threadIdx.x; q < E_pad; q += blockDim.x) {
@@ -36,6 +36,7 @@ __global__ void k_fleet_build(const float *__restrict__ T, int64_t E, int64_t C,
             v = isfinite(t) ? (double)t : penalty * best[e];
         }
         tcm[c * E_pad + q] = v;
+        tem[q * C + c] = v;
     }
 }
 
@@ -206,7 +207,7 @@ __device__ __forceinline__ void frec_offer(FRec2 &r, double s, const int32_t *t,
     }
 }
 
-__global__ void __launch_bounds__(128) k_fleet_exh(const double *__restrict__ tcm, int64_t E_pad,
+__global__ void __launch_bounds__(128) k_fleet_exh(const double *__restrict__ tem, int64_t E_pad,
                                                   int64_t C, int k, int64_t r0, int64_t r1,
                                                   const double *__restrict__ w,
                                                   const int32_t *__restrict__ seg, int n_dev,
@@ -226,8 +227,10 @@ __global__ void __launch_bounds__(128) k_fleet_exh(const double *__restrict__ tc
         for (int d = 0; d < n_dev; d++) {
             double den = 0.0, wsum = 0.0;
             for (int q = seg[d]; q < seg[d + 1]; q++) {
-                double y = tcm[(int64_t)tup[0] * E_pad + q];
-                for (int u = 1; u < k; u++) y = fmin(y, tcm[(int64_t)tup[u] * E_pad + q]);
+                // env-major: consecutive subsets share their larger members and step
+                // the smallest, so a warp's loads of one env are (mostly) contiguous
+                double y = tem[(int64_t)q * C + tup[0]];
+                for (int u = 1; u < k; u++) y = fmin(y, tem[(int64_t)q * C + tup[u]]);
                 den += w[q] * y;
                 wsum += w[q];
             }
@@ -302,12 +305,13 @@ extern "C" pt_status pt_set_fleet(pt_ctx *ctx, const double *q_device, int32_t n
                           ctx->stream));
     if (!f.tcm) {
         PT_TRY(pt_dalloc(ctx, (void **)&f.tcm, sizeof(double) * C * E_pad));
+        PT_TRY(pt_dalloc(ctx, (void **)&f.tem, sizeof(double) * C * E_pad));
     }
     int32_t *d_perm = nullptr;
     PT_TRY(pt_dalloc(ctx, (void **)&d_perm, sizeof(int32_t) * E));
     PT_CK(cudaMemcpyAsync(d_perm, f.perm.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, ctx->stream));
     k_fleet_build<<<(unsigned)C, 128, 0, ctx->stream>>>(ctx->T32, E, C, ctx->best, ctx->penalty, d_perm,
-                                                       E_pad, f.tcm);
+                                                       E_pad, f.tcm, f.tem);
     ctx->stats.launches++;
     PT_CK(cudaGetLastError());
     pt_dfree(ctx, d_perm);
@@ -451,7 +455,7 @@ pt_status pt_fleet_exhaustive(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, i
         PT_TRY(pt_dalloc(ctx, (void **)&bs, sizeof(double) * 2 * nblk));
         PT_TRY(pt_dalloc(ctx, (void **)&bt, sizeof(int32_t) * 2 * nblk * k));
         PT_CK(cudaEventRecord(ctx->ev0, s));
-        k_fleet_exh<<<nblk, 128, 0, s>>>(ctx->fl.tcm, E_pad, C, k, r0, r1, w, ctx->fl.seg, ctx->fl.n_dev,
+        k_fleet_exh<<<nblk, 128, 0, s>>>(ctx->fl.tem, E_pad, C, k, r0, r1, w, ctx->fl.seg, ctx->fl.n_dev,
                                         ctx->fl.qdev, bs, bt);
         PT_CK(cudaEventRecord(ctx->ev1, s));
         ctx->stats.launches++;

@@ -489,6 +489,7 @@ extern "C" void pt_free(pt_ctx *ctx)
     pt_dfree(ctx, ctx->scratch);
     pt_dfree(ctx, ctx->T32);
     pt_dfree(ctx, ctx->fl.tcm);
+    pt_dfree(ctx, ctx->fl.tem);
     pt_dfree(ctx, ctx->fl.w);
     pt_dfree(ctx, ctx->fl.qdev);
     pt_dfree(ctx, ctx->fl.seg);

@@ -76,6 +76,7 @@ struct pt_fleet {
     bool set = false;
     int32_t n_dev = 0;
     double *tcm = nullptr;    // [C][E_pad] runtimes (missing -> penalty*best), envs grouped by device
+    double *tem = nullptr;    // [E_pad][C] the same values env-major (thread-per-subset exhaustive)
     double *w = nullptr;      // [E_pad] quantity(i) of each (permuted) env, 0 for padding
     double *qdev = nullptr;   // [n_dev] quantity(d)
     int32_t *seg = nullptr;   // [n_dev+1] env offsets of each device's segment
