@@ -64,6 +64,9 @@ extern "C" pt_status pt_eval_holdout(pt_ctx *ctx, int32_t heldout_device, int32_
 namespace cgh = cooperative_groups;
 
 #define HB_BIGI 0x7fffffff
+#ifndef XH_BPS
+#define XH_BPS 4   // batched holdout: co-resident blocks per SM
+#endif
 
 __device__ __forceinline__ void hb_top2(double &s1, int &c1, double &s2, int &c2, double s, int c)
 {
@@ -232,9 +235,9 @@ extern "C" pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t *out_id
         PT_CK(cudaFuncSetAttribute(k_greedy_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_multi, 256, smem));
-    // up to 4 co-resident blocks per SM: more warps per problem, fewer candidates per warp
+    // up to XH_BPS co-resident blocks per SM: more warps per problem, fewer candidates per warp
     // (each candidate costs one L2 round trip per step)
-    const int nblk = std::max(P, ctx->num_sms * std::min(occ, 4));
+    const int nblk = std::max(P, ctx->num_sms * std::min(occ, XH_BPS));
     if (occ * ctx->num_sms < nblk) return pt_fail(PT_ECUDA, "batched greedy cannot be co-resident");
     double *w = nullptr, *d_s = nullptr, *d_u = nullptr;
     double4 *blk = nullptr;
