@@ -399,7 +399,7 @@ __device__ __forceinline__ void fhadd2(float &lo_acc, float &hi_acc, uint32_t p)
 #define XT_PROBE 0    // debug build: wait statistics in the tail of the candidate score buffer
 #endif
 #ifndef XT_TCU
-#define XT_TCU 4      // XT_TC: unroll of the env-pair loop
+#define XT_TCU (XT_TC == 2 ? 32 : 4)   // XT_TC: unroll of the env-pair loop (the hybrid needs it whole)
 #endif
 [[maybe_unused]] static constexpr int kXtTcUnroll = XT_TCU;
 // row position inside a 32-row block: rows g, g+8, g+16, g+24 -> 4g .. 4g+3
@@ -632,14 +632,32 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
             const int gq = lane >> 2, qd = lane & 3;
             const int r0 = 32 * (warp >> 1);
             const int cw = 32 * (warp & 1);
-            const int c0 = cw + 2 * qd;                      // the thread's first column
+            const int c0 = cw + (XT_TC == 2 ? qd : 2 * qd);  // the thread's first column
             const int last7 = last_s[r0 + 24 + gq];          // its last row (colex: largest last member)
             const uint32_t one2 = 0x3C003C00u;               // f16x2 (1, 1)
             const uint32_t sel0 = gq == qd ? one2 : 0u, sel1 = gq == qd + 4 ? one2 : 0u;
+#if XT_TC == 2
+            // hybrid, split by sets: the warp tile's columns 0-15 (MMA tiles cb = 0, 1) are
+            // summed on the tensor pipe into accm[2 rb + cb][t], columns 16-31 by fp16 chains
+            // on the FMA pipe into acc[2 i' + 1][jj] (the thread's own input sets: row
+            // r0 + gq + 8 i', column cw + qd + 16 + 4 jj); at each epilogue the MMA sums move
+            // to their owners' acc[2 i'][j'] (row r0 + gq + 8 i', column cw + qd + 4 j')
+            float accm[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) accm[i][j] = 0.0f;
+            uint32_t hp[4][4];                               // fp16 chains of the tree sets
+#define XT_ROW(i, j) (r0 + gq + 8 * ((i) >> 1))
+#define XT_COL(i, j) (cw + qd + 4 * (((i) & 1) * 4 + (j)))
+#define XT_GRPB(i, j) ((i) & 1)
+#define XT_SPAN 28
+#else
 #define XT_ROW(i, j) (r0 + 16 * ((i) >> 2) + gq + 8 * ((j) >> 1))
 #define XT_COL(i, j) (cw + 8 * ((i) & 3) + 2 * qd + ((j) & 1))
 #define XT_GRPB(i, j) (((i) & 3) >= 2)
 #define XT_SPAN 25                                       // thread's last column - first column
+#endif
 #else
             const int r0 = 32 * (warp >> 1) + 8 * ty;
             const int c0 = 32 * (warp & 1) + 4 * tx;
@@ -687,6 +705,30 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                             const uint4 b1 = *reinterpret_cast<const uint4 *>(Bw + pp * XT_C + 4);
                             const uint32_t rv[4] = {av.x, av.y, av.z, av.w};
                             const uint32_t cv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#if XT_TC == 2
+#pragma unroll
+                            for (int rb = 0; rb < 2; rb++)
+#pragma unroll
+                                for (int cb = 0; cb < 2; cb++)
+                                    tc_mma(accm[2 * rb + cb], hmin2(rv[2 * rb], cv[2 * cb]),
+                                           hmin2(rv[2 * rb + 1], cv[2 * cb]), hmin2(rv[2 * rb], cv[2 * cb + 1]),
+                                           hmin2(rv[2 * rb + 1], cv[2 * cb + 1]), sel0, sel1);
+                            // tree sets: a set's two envs stay in the two lanes; 8 pairs (16 envs)
+                            // are chained in fp16, then both halves go to fp32
+                            const int u = pp & 7;   // position in the chain
+#pragma unroll
+                            for (int i = 0; i < 4; i++)
+#pragma unroll
+                                for (int jj = 0; jj < 4; jj++) {
+                                    const uint32_t m = hmin2(rv[i], cv[4 + jj]);
+                                    if (u == 0) hp[i][jj] = m;
+                                    else hp[i][jj] = hadd2(hp[i][jj], m);
+                                    if (u == 7) {
+                                        float &a = acc[2 * i + 1][jj];
+                                        fhadd2(a, a, hp[i][jj]);
+                                    }
+                                }
+#else
 #pragma unroll
                             for (int rb = 0; rb < 2; rb++)
 #pragma unroll
@@ -694,6 +736,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                                     tc_mma(acc[4 * rb + cb], hmin2(rv[2 * rb], cv[2 * cb]),
                                            hmin2(rv[2 * rb + 1], cv[2 * cb]), hmin2(rv[2 * rb], cv[2 * cb + 1]),
                                            hmin2(rv[2 * rb + 1], cv[2 * cb + 1]), sel0, sel1);
+#endif
                         }
 #else
 #if XT_HALF
@@ -831,6 +874,25 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                     }
                 }
                 if (skip) continue;
+#if XT_TC == 2
+                // move the MMA sums to their owners: own set (row g + 8 i', column qd + 4 j'),
+                // j' < 4, is C-fragment element (rb = i'>>1, cb = j'>>1, t = 2 (i'&1) + (qd&1))
+                // of quad lane (qd>>1) + 2 (j'&1); two shuffles (t even / odd) and a select
+#pragma unroll
+                for (int ip = 0; ip < 4; ip++)
+#pragma unroll
+                    for (int jp = 0; jp < 4; jp++) {
+                        const int src = (lane & ~3) | ((qd >> 1) + 2 * (jp & 1));
+                        const int reg = 2 * (ip >> 1) + (jp >> 1), th = ip & 1;
+                        const float v0 = __shfl_sync(0xffffffffu, accm[reg][2 * th], src);
+                        const float v1 = __shfl_sync(0xffffffffu, accm[reg][2 * th + 1], src);
+                        acc[2 * ip][jp] = (qd & 1) ? v1 : v0;
+                    }
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) accm[i][j] = 0.0f;
+#endif
                 // ---- epilogue of one column tile ----
                 // LB = RD(acc*c1 - c2) and UB = RU(acc*c3 + c4) are non-decreasing in acc, so
                 // order statistics and the window test are taken on acc itself and mapped
@@ -1805,6 +1867,16 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const double gam_mma = n_mma * d_mma / (1.0 - n_mma * d_mma);
     const double eta_rel = (u16 + gam_mma + u16 * gam_mma) * 1.01;
     const double eta_abs = (double)v->E_pad * std::ldexp(1.0, -25) * (1.0 + gam_mma) * 1.01;
+#elif XT_TC == 2
+    // hybrid: a set is summed either by MMA (E_pad/2 chained MMAs, 2^-18 each, as below)
+    // or by fp16 chains of 8 pairs (quantisation + 7 HADD2 = 8 roundings per term) into
+    // fp32 (E_pad/16 FHADD per set); bounded by the sum of both relative terms
+    const double n_mma = (double)v->E_pad / 2.0, d_mma = std::ldexp(1.0, -18);
+    const double gam_mma = n_mma * d_mma / (1.0 - n_mma * d_mma);
+    const double n32 = (double)v->E_pad / 16.0 + 3.0;
+    const double gam32 = n32 * u32 / (1.0 - n32 * u32);
+    const double eta_rel = (8.0 * u16 + 64.0 * u16 * u16 + gam32 + gam_mma + u16 * gam_mma) * 1.02;
+    const double eta_abs = 3.0 * (double)v->E_pad * std::ldexp(1.0, -25) * (1.0 + gam_mma) * 1.02;
 #elif XT_TC
     // tensor-summed tiled kernel: fp16 terms u16 (the mins are exact fp16 values), then
     // E_pad/2 chained MMA accumulations of one env pair each, each assumed within 2^-18
