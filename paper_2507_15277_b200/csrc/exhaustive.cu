@@ -399,7 +399,7 @@ __device__ __forceinline__ void fhadd2(float &lo_acc, float &hi_acc, uint32_t p)
 #define XT_PROBE 0    // debug build: wait statistics in the tail of the candidate score buffer
 #endif
 #ifndef XT_TCU
-#define XT_TCU (XT_TC == 2 ? 32 : 4)   // XT_TC: unroll of the env-pair loop (the hybrid needs it whole)
+#define XT_TCU (XT_TC >= 2 ? 32 : 4)   // XT_TC: unroll of the env-pair loop (the hybrid needs it whole)
 #endif
 [[maybe_unused]] static constexpr int kXtTcUnroll = XT_TCU;
 // row position inside a 32-row block: rows g, g+8, g+16, g+24 -> 4g .. 4g+3
@@ -480,8 +480,10 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
     uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2
     uint16_t *As = reinterpret_cast<uint16_t *>(Bs + XT_S * XT_K * (XT_C / 2)); // [E_pad][128] fp16
     int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);                // [128]
+    float *sumA_s = reinterpret_cast<float *>(last_s + XT_R);                  // [128] (XT_TC == 3)
+    float *bndA_s = sumA_s + XT_R;                                             // [128] (XT_TC == 3)
     // B ring: XT_HALF ? [2 halves][S] stages of [K][32 cols] : [S] stages of [K][64 cols]
-    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XT_R);              // [2S]
+    uint64_t *full = reinterpret_cast<uint64_t *>(bndA_s + XT_R);              // [2S]
     uint64_t *empty = full + 2 * XT_S;                                         // [2S] (keeps task_s 16-aligned)
     int4 *task_s = reinterpret_cast<int4 *>(empty + 2 * XT_S);
     int *relcnt = reinterpret_cast<int *>(task_s + 1);                         // [2S] (XT_NOPROD)
@@ -616,6 +618,23 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #endif
             }
             named_sync(1, XT_TCONS);
+#if XT_TC == 3
+            // relu-form sets need their row's sum_e A (fp32, pairs ascending) and its error
+            // bound eta_A * sumA + eta_abs_r (rounded up)
+            if (tid < XT_R) {
+                const uint32_t *Aw = reinterpret_cast<const uint32_t *>(As);
+                const int rp = tc_rpos(tid);
+                float sa = 0.0f;
+                for (int64_t pp = 0; pp < p.E_pad / 2; pp++) {
+                    const uint32_t w = Aw[pp * XT_R + rp];
+                    sa += __half2float(__ushort_as_half((unsigned short)(w & 0xffffu)));
+                    sa += __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+                }
+                sumA_s[tid] = sa;
+                bndA_s[tid] = __fmaf_ru(p.eta_A, sa, p.eta_abs_r);
+            }
+            named_sync(1, XT_TCONS);
+#endif
 
             float acc[8][4];
 #pragma unroll
@@ -632,11 +651,11 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
             const int gq = lane >> 2, qd = lane & 3;
             const int r0 = 32 * (warp >> 1);
             const int cw = 32 * (warp & 1);
-            const int c0 = cw + (XT_TC == 2 ? qd : 2 * qd);  // the thread's first column
+            const int c0 = cw + (XT_TC >= 2 ? qd : 2 * qd);  // the thread's first column
             const int last7 = last_s[r0 + 24 + gq];          // its last row (colex: largest last member)
             const uint32_t one2 = 0x3C003C00u;               // f16x2 (1, 1)
             const uint32_t sel0 = gq == qd ? one2 : 0u, sel1 = gq == qd + 4 ? one2 : 0u;
-#if XT_TC == 2
+#if XT_TC >= 2
             // hybrid, split by sets: the warp tile's columns 0-15 (MMA tiles cb = 0, 1) are
             // summed on the tensor pipe into accm[2 rb + cb][t], columns 16-31 by fp16 chains
             // on the FMA pipe into acc[2 i' + 1][jj] (the thread's own input sets: row
@@ -705,7 +724,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                             const uint4 b1 = *reinterpret_cast<const uint4 *>(Bw + pp * XT_C + 4);
                             const uint32_t rv[4] = {av.x, av.y, av.z, av.w};
                             const uint32_t cv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#if XT_TC == 2
+#if XT_TC >= 2
 #pragma unroll
                             for (int rb = 0; rb < 2; rb++)
 #pragma unroll
@@ -720,7 +739,12 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                             for (int i = 0; i < 4; i++)
 #pragma unroll
                                 for (int jj = 0; jj < 4; jj++) {
+#if XT_TC == 3
+                                    // columns 24-31: relu(a - b) on the FMA pipe instead of the min
+                                    const uint32_t m = jj >= 2 ? hrelu_sub2(rv[i], cv[4 + jj]) : hmin2(rv[i], cv[4 + jj]);
+#else
                                     const uint32_t m = hmin2(rv[i], cv[4 + jj]);
+#endif
                                     if (u == 0) hp[i][jj] = m;
                                     else hp[i][jj] = hadd2(hp[i][jj], m);
                                     if (u == 7) {
@@ -874,7 +898,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                     }
                 }
                 if (skip) continue;
-#if XT_TC == 2
+#if XT_TC >= 2
                 // move the MMA sums to their owners: own set (row g + 8 i', column qd + 4 j'),
                 // j' < 4, is C-fragment element (rb = i'>>1, cb = j'>>1, t = 2 (i'&1) + (qd&1))
                 // of quad lane (qd>>1) + 2 (j'&1); two shuffles (t even / odd) and a select
@@ -907,6 +931,42 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                             if (!(l < p.C && l > last_s[XT_ROW(i, j)])) acc[i][j] = INFINITY;
                         }
                 }
+#if XT_TC == 3
+                // relu sets (odd i, j >= 2): acc holds sum relu(a - b); bounds from the row sum.
+                // Bounds are computed explicitly (LB, UB) and the U minima kept in UB terms.
+                float lbv[8][4], tA = INFINITY, tB = INFINITY, tL = INFINITY;
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        float lb, ub;
+                        if (!(acc[i][j] < INFINITY)) {
+                            lb = ub = INFINITY;
+                        } else if ((i & 1) && j >= 2) {
+                            const int r = XT_ROW(i, j);
+                            const float sh = sumA_s[r] - acc[i][j];
+                            lb = __fsub_rd(sh, bndA_s[r]);
+                            ub = __fadd_ru(sh, bndA_s[r]);
+                        } else {
+                            lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
+                            ub = __fmaf_ru(acc[i][j], p.c3, p.c4);
+                        }
+                        lbv[i][j] = lb;
+                        tL = fminf(tL, lb);
+                        if (XT_GRPB(i, j)) tB = fminf(tB, ub);
+                        else tA = fminf(tA, ub);
+                    }
+                bA = fminf(bA, tA);
+                bB = fminf(bB, tB);
+                const float tau = fminf(p.tau_seed, __uint_as_float(Ubits));
+                if (tL <= tau) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const float lb = lbv[i][j];
+                            if (lb < INFINITY && lb <= tau) {
+#else
                 // tile minima of two disjoint groups of the thread's sets
                 float tA = INFINITY, tB = INFINITY;
 #pragma unroll
@@ -926,6 +986,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                         for (int j = 0; j < 4; j++) {
                             const float lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
                             if (acc[i][j] < INFINITY && lb <= tau) {
+#endif
                                 const unsigned idx = atomicAdd(p.cand_n, 1u);
                                 if (idx < p.cap) {
                                     p.cand_key[idx] = ((unsigned long long)(R0 + XT_ROW(i, j)) << KEY_BITS) |
@@ -951,7 +1012,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                     x1 = fminf(x1, y1);
                 }
                 if (lane == 0) {
-                    const float ub = __fmaf_ru(x2, p.c3, p.c4);
+                    const float ub = XT_TC == 3 ? x2 : __fmaf_ru(x2, p.c3, p.c4);   // (TC 3: already UB)
                     if (ub < published) {
                         atomicMin(p.U, __float_as_uint(ub));
                         published = ub;
@@ -1837,8 +1898,18 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     // relu form: quantisation of A and B (2 u16 sumA: relu is 1-Lipschitz and nonzero only
     // where b < a), sumA's own quantisation (u16), and L16 + 1 fp16 roundings on the relu
     // terms (HFMA2 + tree + chain), all relative to sumA >= s; plus the fp32 sums
+#if XT_TC == 3
+    // relu sets of the hybrid: quantisation of a and b (2 u16, relu is 1-Lipschitz), the
+    // HFMA2.RELU rounding and the 7 HADD2 of the 8-pair chain (8 u16), all relative to
+    // sumA >= s; the FHADD sums (E_pad/16 adds) and sumA's own fp32 sum and quantisation
+    const double lvr = 11.0;
+    const double n32r = (double)v->E_pad / 16.0 + 3.0;
+    const double gamr = n32r * u32 / (1.0 - n32r * u32);
+    const double eta_A = (lvr * u16 + lvr * lvr * u16 * u16 + u16 + gamr + 2.0 * gamE + 4.0 * u32) * 1.05;
+#else
     const double lvr = lv16 + 3.0;
     const double eta_A = (lvr * u16 + lvr * lvr * u16 * u16 + gam + 2.0 * gamE + 4.0 * u32) * 1.02;
+#endif
     const double eta_abs_r = 4.0 * (double)v->E_pad * std::ldexp(1.0, -25) * 1.01;
     auto f_up = [](double x) -> float {
         if (!(x < 3.0e38)) return INFINITY;
@@ -1867,7 +1938,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const double gam_mma = n_mma * d_mma / (1.0 - n_mma * d_mma);
     const double eta_rel = (u16 + gam_mma + u16 * gam_mma) * 1.01;
     const double eta_abs = (double)v->E_pad * std::ldexp(1.0, -25) * (1.0 + gam_mma) * 1.01;
-#elif XT_TC == 2
+#elif XT_TC >= 2
     // hybrid: a set is summed either by MMA (E_pad/2 chained MMAs, 2^-18 each, as below)
     // or by fp16 chains of 8 pairs (quantisation + 7 HADD2 = 8 roundings per term) into
     // fp32 (E_pad/16 FHADD per set); bounded by the sum of both relative terms
@@ -1934,7 +2005,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         ws ? sizeof(uint32_t) * XT_S * 2 * XT_K * 32 + 2 * sizeof(uint16_t) * v->E_pad * XT_R +
                  2 * sizeof(int) * XT_R + 2 * sizeof(int4) + 2 * sizeof(uint64_t) * (XT_S + 2)
            : sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
-                 sizeof(int) * XT_R + 4 * sizeof(uint64_t) * XT_S + sizeof(int4) + 2 * sizeof(int) * XT_S;
+                 sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 4 * sizeof(uint64_t) * XT_S + sizeof(int4) +
+                 2 * sizeof(int) * XT_S;
 #endif
     const int threads = XT_MMA ? XT_THREADS : ws ? XW_THREADS : XT_TTHREADS;
     PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
