@@ -480,10 +480,10 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
     uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2
     uint16_t *As = reinterpret_cast<uint16_t *>(Bs + XT_S * XT_K * (XT_C / 2)); // [E_pad][128] fp16
     int *last_s = reinterpret_cast<int *>(As + p.E_pad * XT_R);                // [128]
-    float *sumA_s = reinterpret_cast<float *>(last_s + XT_R);                  // [128] (XT_TC == 3)
-    float *bndA_s = sumA_s + XT_R;                                             // [128] (XT_TC == 3)
+    float *sumA_s = reinterpret_cast<float *>(last_s + XT_R);                  // [128] (XT_TC == 3 only)
+    [[maybe_unused]] float *bndA_s = sumA_s + XT_R;                            // [128] (XT_TC == 3 only)
     // B ring: XT_HALF ? [2 halves][S] stages of [K][32 cols] : [S] stages of [K][64 cols]
-    uint64_t *full = reinterpret_cast<uint64_t *>(bndA_s + XT_R);              // [2S]
+    uint64_t *full = reinterpret_cast<uint64_t *>(sumA_s + (XT_TC == 3 ? 2 * XT_R : 0));   // [2S]
     uint64_t *empty = full + 2 * XT_S;                                         // [2S] (keeps task_s 16-aligned)
     int4 *task_s = reinterpret_cast<int4 *>(empty + 2 * XT_S);
     int *relcnt = reinterpret_cast<int *>(task_s + 1);                         // [2S] (XT_NOPROD)
@@ -2005,8 +2005,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         ws ? sizeof(uint32_t) * XT_S * 2 * XT_K * 32 + 2 * sizeof(uint16_t) * v->E_pad * XT_R +
                  2 * sizeof(int) * XT_R + 2 * sizeof(int4) + 2 * sizeof(uint64_t) * (XT_S + 2)
            : sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
-                 sizeof(int) * XT_R + 2 * sizeof(float) * XT_R + 4 * sizeof(uint64_t) * XT_S + sizeof(int4) +
-                 2 * sizeof(int) * XT_S;
+                 sizeof(int) * XT_R + (XT_TC == 3 ? 2 * sizeof(float) * XT_R : 0) + 4 * sizeof(uint64_t) * XT_S +
+                 sizeof(int4) + 2 * sizeof(int) * XT_S;
 #endif
     const int threads = XT_MMA ? XT_THREADS : ws ? XW_THREADS : XT_TTHREADS;
     PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
