@@ -1924,10 +1924,13 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     };
     // seed: exact score of greedy's runner-up set at its last step (>= s_(2))
     // (reused from an earlier greedy run of >= k steps on this view when there is one)
+    // (a missing trace is computed for 4 steps -- the tiled kernel's largest k -- at once,
+    // so a k=2 search followed by a k=3 one seeds both from one cooperative greedy launch)
     if (v->greedy_s2.size() < (size_t)k) {
-        std::vector<int32_t> gidx(k);
-        std::vector<double> gs1(k), gs2(k);
-        PT_TRY(pt_greedy_view(ctx, v, k, gidx.data(), gs1.data(), gs2.data()));
+        const int kg = (int)std::min<int64_t>(std::max(k, 4), v->C);
+        std::vector<int32_t> gidx(kg);
+        std::vector<double> gs1(kg), gs2(kg);
+        PT_TRY(pt_greedy_view(ctx, v, kg, gidx.data(), gs1.data(), gs2.data()));
     }
     const float tau_seed = f_up(v->greedy_s2[k - 1] * (1.0 + 1e-9) + 1e-30);
 #if XT_MMA
