@@ -395,6 +395,9 @@ __device__ __forceinline__ void fhadd2(float &lo_acc, float &hi_acc, uint32_t p)
 #define XT_HALF 0   // 1 (with XT_NOPROD, not XT_TC): one B ring per 32-column half, 4 warps each
 #endif              //   (measured 12.08 vs 12.04 ms: the stage misses are not warp coupling)
 #define XT_BSTR (XT_HALF ? XT_C / 4 : XT_C / 2)   // u32 per env row of a warp's B stage
+#ifndef XT_SHAPE48
+#define XT_SHAPE48 0   // 1: 4 rows x 8 columns per thread (tree path)
+#endif
 #ifndef XT_PROBE
 #define XT_PROBE 0    // debug build: wait statistics in the tail of the candidate score buffer
 #endif
@@ -678,6 +681,17 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #define XT_SPAN 25                                       // thread's last column - first column
 #endif
 #else
+#if XT_SHAPE48
+            // 4 rows x 8 columns per thread (one 8-byte A LDS, one 16-byte B LDS per env);
+            // acc[i][j] is row r0 + (i>>1), column c0 + 4 (i&1) + j
+            const int r0 = 32 * (warp >> 1) + 4 * (lane >> 2);
+            const int c0 = 32 * (warp & 1) + 8 * (lane & 3);
+            const int last7 = last_s[r0 + 3];
+#define XT_ROW(i, j) (r0 + ((i) >> 1))
+#define XT_COL(i, j) (c0 + 4 * ((i) & 1) + (j))
+#define XT_GRPB(i, j) ((i) & 1)
+#define XT_SPAN 7
+#else
             const int r0 = 32 * (warp >> 1) + 8 * ty;
             const int c0 = 32 * (warp & 1) + 4 * tx;
             // colex order: a row's largest member is non-decreasing in its rank (padding
@@ -687,6 +701,7 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
 #define XT_COL(i, j) (c0 + (j))
 #define XT_GRPB(i, j) ((j) >= 2)
 #define XT_SPAN 3
+#endif
 #endif
             uint32_t slot = steps % XT_S, phase = (steps / XT_S) & 1u;
             int64_t ltile = lo + (int64_t)tk.y * XT_C;     // first column of the current tile
@@ -769,7 +784,44 @@ __global__ void __launch_bounds__(XT_TTHREADS, XT_MINB) k_exh_tiled(const XParam
                         const uint32_t *B = Bs + slot * XT_K * (XT_C / 2) + c0 / 2;
 #endif
                         const uint16_t *A = As + (int64_t)q * XT_K * XT_R + r0;
-#if XT_G8 == 2
+#if XT_SHAPE48
+#pragma unroll kXtPUnroll
+                        for (int e = 0; e < XT_K; e += 4 * XT_NG) {
+                            uint32_t pp[4][4];
+#pragma unroll
+                            for (int gq = 0; gq < XT_NG; gq++) {
+                                uint2 ar[4];
+                                uint4 bc[4];
+#pragma unroll
+                                for (int t = 0; t < 4; t++) {
+                                    ar[t] = *reinterpret_cast<const uint2 *>(A + (e + 4 * gq + t) * XT_R);
+                                    bc[t] = *reinterpret_cast<const uint4 *>(B + (e + 4 * gq + t) * XT_BSTR);
+                                }
+#pragma unroll
+                                for (int i = 0; i < 4; i++) {
+                                    uint32_t av[4];
+#pragma unroll
+                                    for (int t = 0; t < 4; t++) {
+                                        const uint32_t w = (i >> 1) == 0 ? ar[t].x : ar[t].y;
+                                        av[t] = (i & 1) ? bcast_hi(w) : bcast_lo(w);
+                                    }
+#pragma unroll
+                                    for (int j = 0; j < 4; j++) {
+                                        const uint32_t b0 = j == 0 ? bc[0].x : j == 1 ? bc[0].y : j == 2 ? bc[0].z : bc[0].w;
+                                        const uint32_t b1 = j == 0 ? bc[1].x : j == 1 ? bc[1].y : j == 2 ? bc[1].z : bc[1].w;
+                                        const uint32_t b2 = j == 0 ? bc[2].x : j == 1 ? bc[2].y : j == 2 ? bc[2].z : bc[2].w;
+                                        const uint32_t b3 = j == 0 ? bc[3].x : j == 1 ? bc[3].y : j == 2 ? bc[3].z : bc[3].w;
+                                        const uint32_t sx = hadd2(hadd2(hmin2(av[0], b0), hmin2(av[1], b1)),
+                                                                  hadd2(hmin2(av[2], b2), hmin2(av[3], b3)));
+                                        float *a2 = &acc[2 * i + (j >> 1)][2 * (j & 1)];
+                                        if (gq == 0) pp[i][j] = sx;
+                                        else if (gq < XT_NG - 1) pp[i][j] = hadd2(pp[i][j], sx);
+                                        else fhadd2(a2[0], a2[1], XT_NG == 1 ? sx : hadd2(pp[i][j], sx));
+                                    }
+                                }
+                            }
+                        }
+#elif XT_G8 == 2
                         // XT_NG 4-env fp16 trees per unit summed in fp16 (one HADD2 each) before
                         // the two FHADD: (8 NG + 1) slots per 8 NG (set, env) pairs of columns
                         // instead of 9 NG; the running fp16 partial waits in pp[][] (16 registers)

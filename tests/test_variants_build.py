@@ -22,6 +22,7 @@ VARIANTS = {
     "half_rings": ["-DXT_HALF=1"],
     "wait_backoff": ["-DXT_WAITNS=256"],
     "probe": ["-DXT_PROBE=2"],
+    "shape_4x8": ["-DXT_SHAPE48=1"],
 }
 
 
