@@ -337,13 +337,24 @@ def main():
     torch.cuda.synchronize()
 
     # with N ranks the exhaustive searches are sharded; the two unsharded parts
-    # (greedy k=24 and the batched holdout) run once per job, on ranks 0 and 1
+    # (greedy k=24 and the batched holdout) run once per job, on ranks 0 and 1, and
+    # those ranks take a correspondingly smaller share of the k=3 task list
+    # (pt_set_shard_weights; extra work from DESIGN.md 6.4/6.8: ~0.24 and ~0.16 ms
+    # against a k=3 search of ~12 ms on one GPU)
     do_greedy = rank == 0
     do_holdout = rank == 1 % world
+    shard_w = None
+    if world > 1:
+        extra = [0.0] * world
+        extra[0] += 0.24
+        extra[1 % world] += 0.16
+        shard_w = [max(0.2, 1.0 - x * world / 12.0) for x in extra]
 
     def step(src):
         """One pass of the whole hot path; returns (results, d2h bytes)."""
         ctx = pt.pt_load_perf(src, dev, device=local)
+        if shard_w is not None:
+            pt.pt_set_shard_weights(ctx, shard_w)
         d2h = 0
         idx = None
         if do_greedy:

@@ -123,9 +123,12 @@ pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int3
  * pt_exhaustive_best -- exhaustive search over every k-subset (P:L271-276,
  * Sec. 4.3.1; distinct unordered subsets of size exactly k).
  *   shard_rank, shard_count   this call searches shard `shard_rank` of
- *              `shard_count` equal-work contiguous pieces of the subset space
- *              (0, 1 = everything).  Results of all shards merged with
- *              pt_merge_top2 equal the unsharded result.
+ *              `shard_count` equal-work pieces of the subset space (0, 1 =
+ *              everything; the tiled search deals its decreasing-size task list
+ *              to the shards in snake order, or by pt_set_shard_weights; the
+ *              generic search (k > 4 or > 768 envs) cuts contiguous rank ranges).
+ *              Results of all shards merged with pt_merge_top2 equal the
+ *              unsharded result.
  *   out_idx        host int32[k]: best set, ascending.
  *   out_G          host: its G.
  *   out_runner_idx host int32[k] or NULL: the second set in (G desc, tuple asc)
@@ -140,6 +143,18 @@ pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, in
                              int32_t shard_rank, int32_t shard_count,
                              int32_t *out_idx, double *out_G,
                              int32_t *out_runner_idx, double *out_G_runner, double *out_s);
+
+/*
+ * pt_set_shard_weights -- relative work shares of the shards for later sharded
+ * exhaustive searches on this context with shard_count == n (heterogeneous
+ * ranks: e.g. a rank that also runs the unsharded greedy takes a smaller share).
+ * The tiled search deals its decreasing-size task list to the shard with the
+ * smallest weighted load (each shard's list stays decreasing); results are exact
+ * and identical for any weights.  weights: host double[n], each > 0 and finite,
+ * copied (caller keeps ownership); n = 0 or weights = NULL restores equal shares.
+ * Errors: PT_EINVAL (n < 0, a non-positive or non-finite weight).
+ */
+pt_status pt_set_shard_weights(pt_ctx *ctx, const double *weights, int32_t n);
 
 /*
  * pt_greedy_sharded -- the greedy selection with the configurations sharded

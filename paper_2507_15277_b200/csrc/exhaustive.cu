@@ -109,23 +109,39 @@ struct pt_tasks {
         std::vector<int> off;          // shard r owns d[off[r], off[r+1])
         std::vector<int64_t> sets, slots;
     };
-    std::map<int, plan> plans;
+    std::map<std::vector<double>, plan> plans;   // key: {N} or {N, w_0 .. w_N-1}
 };
 
-static pt_status shard_plan(pt_tasks *T, int N, const pt_tasks::plan **out)
+// w: empty = equal shares (snake deal); else per-shard weights (weighted greedy deal:
+// each task, largest first, to the shard whose load / weight would stay smallest)
+static pt_status shard_plan(pt_tasks *T, int N, const std::vector<double> &w, const pt_tasks::plan **out)
 {
     static std::mutex mu;
     std::lock_guard<std::mutex> g(mu);
-    auto it = T->plans.find(N);
+    std::vector<double> key{(double)N};
+    key.insert(key.end(), w.begin(), w.end());
+    auto it = T->plans.find(key);
     if (it != T->plans.end()) {
         *out = &it->second;
         return PT_OK;
     }
     const int n = (int)T->h.size();
     std::vector<std::vector<int>> per(N);
-    for (int i = 0; i < n; i++) {
-        const int rnd = i / N, pos = i % N;
-        per[(rnd & 1) ? N - 1 - pos : pos].push_back(i);
+    if (w.empty()) {
+        for (int i = 0; i < n; i++) {
+            const int rnd = i / N, pos = i % N;
+            per[(rnd & 1) ? N - 1 - pos : pos].push_back(i);
+        }
+    } else {
+        std::vector<double> load(N, 0.0);
+        for (int i = 0; i < n; i++) {
+            const double sz = (double)(T->slot_pre[i + 1] - T->slot_pre[i]);
+            int best = 0;
+            for (int r = 1; r < N; r++)
+                if ((load[r] + sz) / w[r] < (load[best] + sz) / w[best]) best = r;
+            load[best] += sz;
+            per[best].push_back(i);
+        }
     }
     pt_tasks::plan P;
     std::vector<int4> h;
@@ -149,7 +165,21 @@ static pt_status shard_plan(pt_tasks *T, int N, const pt_tasks::plan **out)
         }
         cudaMemcpy(P.d, h.data(), sizeof(int4) * n, cudaMemcpyHostToDevice);
     }
-    *out = &(T->plans[N] = std::move(P));
+    *out = &(T->plans[key] = std::move(P));
+    return PT_OK;
+}
+
+extern "C" pt_status pt_set_shard_weights(pt_ctx *ctx, const double *weights, int32_t n)
+{
+    if (!ctx || n < 0) return pt_fail(PT_EINVAL, "bad argument");
+    if (!weights || n == 0) {
+        ctx->shard_w.clear();
+        return PT_OK;
+    }
+    for (int r = 0; r < n; r++)
+        if (!(weights[r] > 0.0) || !std::isfinite(weights[r]))
+            return pt_fail(PT_EINVAL, "shard weight %d is %g (must be > 0 and finite)", r, weights[r]);
+    ctx->shard_w.assign(weights, weights + n);
     return PT_OK;
 }
 
@@ -1914,7 +1944,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     ctx->stats.exh_slots = T->slot_pre.back();
     if (shard_count > 1) {
         const pt_tasks::plan *P = nullptr;
-        PT_TRY(shard_plan(T, shard_count, &P));
+        static const std::vector<double> equal;
+        PT_TRY(shard_plan(T, shard_count, (int)ctx->shard_w.size() == shard_count ? ctx->shard_w : equal, &P));
         task_list = P->d;
         ta = P->off[shard_rank];
         tb = P->off[shard_rank + 1];

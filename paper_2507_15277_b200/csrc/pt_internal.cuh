@@ -92,6 +92,7 @@ struct pt_ctx {
     int num_sms = 0;
     int64_t E = 0, C = 0;
     std::vector<int32_t> env_device;
+    std::vector<double> shard_w;   // pt_set_shard_weights (empty = equal shares)
     bool have_device = false;
     double penalty = 1.0;
     double *best = nullptr;   // [E] fp64, each env's Oracle

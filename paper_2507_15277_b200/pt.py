@@ -26,7 +26,7 @@ PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM, PT_GREEDY_LAZY = 0x1, 0
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
            "pt_merge_top2", "pt_eval_holdout", "pt_eval_holdout_all", "pt_swap_search",
            "pt_kmeans_select", "pt_set_fleet", "pt_get_stats", "pt_greedy_sharded",
-           "pt_greedy_sharded_dev",
+           "pt_greedy_sharded_dev", "pt_set_shard_weights",
            "pt_free", "pt_last_error")
 
 
@@ -77,6 +77,7 @@ def lib():
         L.pt_greedy_select.argtypes = [P, i32, P, i32, P, P, P]
         L.pt_exhaustive_best.argtypes = [P, i32, P, i32, i32, i32, P, P, P, P, P]
         L.pt_merge_top2.argtypes = [P, P, i32, i32, P, P, P]
+        L.pt_set_shard_weights.argtypes = [P, P, i32]
         L.pt_eval_holdout.argtypes = [P, i32, i32, i32, P, P, P, P, P]
         L.pt_get_stats.argtypes = [P, ct.POINTER(pt_stats)]
         L.pt_set_fleet.argtypes = [P, P, i32, P]
@@ -348,6 +349,16 @@ def pt_kmeans_select(ctx, k, env_mask=None, max_iter=100):
     _chk(lib().pt_kmeans_select(ctx.handle, k, _ptr(_mask(env_mask)), max_iter, _ptr(out), _ptr(n),
                                 _ptr(g), _ptr(it)), "pt_kmeans_select")
     return tuple(int(x) for x in out[:n[0]]), float(g[0]), int(it[0])
+
+
+def pt_set_shard_weights(ctx, weights=None):
+    """Relative work shares of the shards of later sharded exhaustive searches with
+    shard_count == len(weights); None restores equal shares."""
+    if weights is None:
+        _chk(lib().pt_set_shard_weights(ctx.handle, None, 0), "pt_set_shard_weights")
+        return
+    w = _np(weights, np.float64)
+    _chk(lib().pt_set_shard_weights(ctx.handle, _ptr(w), len(w)), "pt_set_shard_weights")
 
 
 def pt_merge_top2(s, tuples, k):

@@ -89,3 +89,29 @@ def test_repeated_calls_reuse_staging():
     _check_exh(o, pt.pt_exhaustive_best(ctx, 2), 2)
     assert not math.isnan(e["G"])
     pt.pt_free(ctx)
+
+
+def test_weighted_shards():
+    """pt_set_shard_weights: shards of a weighted partition merge to the unsharded
+    result, cover every set exactly once, and take work in proportion to the weights."""
+    T, dev = synth.small_matrix(7, n_cfg=400, n_dev=3, n_inputs=16)
+    ctx = pt.pt_load_perf(torch.from_numpy(T).cuda(), dev)
+    full = pt.pt_exhaustive_best(ctx, 3)
+    w = [0.5, 1.0, 1.5]
+    pt.pt_set_shard_weights(ctx, w)
+    recs_s, recs_t, sets = [], [], []
+    for r in range(3):
+        res = pt.pt_exhaustive_best(ctx, 3, shard_rank=r, shard_count=3)
+        sets.append(pt.pt_get_stats(ctx)["exh_sets"])
+        for sv, tup in ((res["s"][0], res["best"]), (res["s"][1], res["runner"])):
+            recs_s.append(sv)
+            recs_t.append(tup if tup is not None else (-1,) * 3)
+    assert sum(sets) == math.comb(400, 3)
+    assert sets[0] < sets[1] < sets[2]
+    assert abs(sets[0] / sum(sets) - 0.5 / 3) < 0.05
+    b, ru, (s1, s2) = pt.pt_merge_top2(recs_s, recs_t, 3)
+    assert b == full["best"] and s1 == full["s"][0] and s2 == full["s"][1]
+    with pytest.raises(pt.PTError):
+        pt.pt_set_shard_weights(ctx, [1.0, 0.0])
+    pt.pt_set_shard_weights(ctx, None)   # equal shares again
+    pt.pt_free(ctx)

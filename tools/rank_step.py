@@ -9,6 +9,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2507_15277_b200 import pt, synth  # noqa: E402
 
+WEIGHTED = len(sys.argv) > 1 and sys.argv[1] == "weighted"   # the bench's shard weights
 T, dev = synth.paper_matrix(1)
 dT = torch.from_numpy(T).cuda()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -20,6 +21,11 @@ for N in (1, 2, 4, 8):
             torch.cuda.synchronize()
             e0.record()
             ctx = pt.pt_load_perf(dT, dev)
+            if N > 1 and WEIGHTED:
+                extra = [0.0] * N
+                extra[0] += 0.24
+                extra[1 % N] += 0.16
+                pt.pt_set_shard_weights(ctx, [max(0.2, 1.0 - x * N / 12.0) for x in extra])
             if r == 0:
                 pt.pt_greedy_select(ctx, 24)
             pt.pt_exhaustive_best(ctx, 2, shard_rank=r, shard_count=N)
