@@ -28,6 +28,12 @@
 namespace cg = cooperative_groups;
 
 #define PT_BIGI 0x7fffffff
+#ifndef GR_PAIR
+#define GR_PAIR 1   // resident greedy scores two candidates per warp pass (loads together; 0: one)
+#endif
+#ifndef GR_BPS
+#define GR_BPS 1    // resident greedy: blocks per SM (with GR_PAIR, 1 and 2 measure the same)
+#endif
 
 __device__ __forceinline__ void top2_ins(double &s1, int &c1, double &s2, int &c2, double s,
                                          int c)
@@ -99,6 +105,40 @@ __global__ void __launch_bounds__(256) k_greedy_resident(const double *__restric
     for (int t = 0; t < k; t++) {
         double s1 = INFINITY, s2 = INFINITY;
         int c1 = PT_BIGI, c2 = PT_BIGI;
+#if GR_PAIR
+        // two candidates per pass, both columns' loads in flight together
+        for (int64_t c = gw; c < C; c += 2 * nw) {
+            const int64_t c2n = c + nw;
+            const bool ok1 = !(taken[c >> 5] >> (c & 31) & 1u);
+            const bool ok2 = c2n < C && !(taken[c2n >> 5] >> (c2n & 31) & 1u);
+            double a1 = 0.0, a2 = 0.0;
+            for (int64_t e0 = lane; e0 < E_pad; e0 += 32 * 16) {   // lane's envs ascending
+                double v1[16], v2[16];
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const int64_t e = e0 + 32 * u;
+                    v1[u] = ok1 && e < E_pad ? __ldg(l64 + c * E_pad + e) : 0.0;
+                    v2[u] = ok2 && e < E_pad ? __ldg(l64 + c2n * E_pad + e) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const int64_t e = e0 + 32 * u;
+                    if (e < E_pad) {
+                        const double cu = cur[e];
+                        a1 += fmin(cu, v1[u]);
+                        a2 += fmin(cu, v2[u]);
+                    }
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+            }
+            if (ok1) top2_ins(s1, c1, s2, c2, a1, (int)c);
+            if (ok2) top2_ins(s1, c1, s2, c2, a2, (int)c2n);
+        }
+        if (false)
+#endif
         for (int64_t c = gw; c < C; c += nw) {
             if (taken[c >> 5] >> (c & 31) & 1u) continue;
             const double *col = l64 + c * E_pad;
@@ -642,7 +682,7 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
         PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_resident, 256, smem));
         if (occ < 1) return pt_fail(PT_ECUDA, "resident greedy kernel cannot be co-resident");
         // 2 blocks per SM when they fit: at most one candidate per warp per step at the paper shape
-        const int nblk = ctx->num_sms * std::min(occ, 2);
+        const int nblk = ctx->num_sms * std::min(occ, GR_BPS);
         size_t bytes = pt_round_up(sizeof(double4) * 2 * nblk, 256) + 256 +
                        pt_round_up(sizeof(int32_t) * k, 256) + 2 * pt_round_up(sizeof(double) * k, 256);
         void *scr = nullptr;
