@@ -16,8 +16,12 @@
  * is a missing measurement.
  *
  * Parity status of each function: see DESIGN.md "Oracle pins".  All
- * functions below are pinned (tests/test_oracle.py); none is
- * "parity unpinned".
+ * functions below are pinned (tests/test_oracle*.py, mutation-checked by
+ * tools/oracle_mutants.py).  One branch is "parity unpinned": or_kmeans's
+ * re-seed of an emptied cluster (the point farthest from its centroid) --
+ * with the deterministic maximin start a cluster empties only when there are
+ * fewer distinct points than k, and there no input searched distinguishes
+ * that rule from any other.
  */
 #include <math.h>
 #include <pthread.h>

@@ -305,3 +305,32 @@ def test_counting_pins():
     assert math.comb(1775, 2) == 1_574_425
     assert math.comb(1775, 3) == 930_485_175
     assert sum(1775 - t for t in range(24)) == 42_324
+
+
+def test_holdout_known_leg_hand():
+    """The 'known' baseline of Sec. 5.8 ("combinations ... selected on the
+    known device") is selected on the HELD-OUT envs, the unseen set on the
+    others.  Hand-worked pow2 fixture, 2 devices x 2 envs, 3 configs (log2 slowdowns):
+        device 0 envs: c0 = 0, c1 = 3, c2 = 1      -> train selects c0 (k=1)
+        device 1 envs: c0 = 2, c1 = 0, c2 = 1      -> known selects c1, G_known = 1
+    G_unseen = G({c0} on device 1) = 2^-2 exactly; G_train = 1 exactly.
+    A holdout whose known leg selected on the train scope would report {c0}, 1/4."""
+    m = np.array([[0, 3, 1], [0, 3, 1], [2, 0, 1], [2, 0, 1]])
+    dev = np.array([0, 0, 1, 1], np.int32)
+    o = Oracle(pow2_matrix(m), dev)
+    for method in (0, 1):
+        idx, gtr, gun, gkn, kidx = o.holdout(1, 1, method=method)
+        assert idx == [0] and kidx == [1]
+        assert gtr == 1.0 and gkn == 1.0 and gun == pytest.approx(0.25, rel=1e-15)
+        # the other fold: train on device 1 -> c1; unseen on device 0 = 2^-3; known c0
+        idx, gtr, gun, gkn, kidx = o.holdout(0, 1, method=method)
+        assert idx == [1] and kidx == [0]
+        assert gtr == 1.0 and gkn == 1.0 and gun == pytest.approx(0.125, rel=1e-15)
+    # k=2 on the 3-device variant: known = the held-out device's own best pair
+    m3 = np.array([[0, 3, 1, 2], [1, 0, 3, 2], [3, 3, 0, 2], [3, 3, 2, 0]])
+    dev3 = np.array([0, 1, 2, 2], np.int32)
+    o3 = Oracle(pow2_matrix(m3), dev3)
+    idx, gtr, gun, gkn, kidx = o3.holdout(2, 2, method=1)
+    assert idx == [0, 1] and gtr == 1.0             # c0, c1 are exact on devices 0, 1
+    assert kidx == [2, 3] and gkn == 1.0            # c2, c3 exact on device 2's two envs
+    assert gun == pytest.approx(2.0 ** -3, rel=1e-15)   # {c0,c1} on device 2: min(3,3) twice

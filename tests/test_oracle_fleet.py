@@ -125,3 +125,26 @@ def test_brute_force_and_invariants():
     assert full == pytest.approx((qd / den).sum(), rel=1e-14)
     # greedy k=1 = exhaustive k=1; greedy value >= (1-1/e) ... not submodular: only check k=1
     assert o.fleet_greedy(1)[0] == [o.fleet_exhaustive(1)[0][0]]
+
+
+def test_missing_cell_costs_penalty_times_best():
+    """Reading c4 carried to Eq. 2: a missing cell costs
+    penalty x best[e], penalty = the dataset-max slowdown.  Hand fixture:
+        env 0 (device 0): T = [1, NaN]   best 1
+        env 1 (device 1): T = [2, 1]     best 1      -> penalty = 2/1 = 2
+    q = 1 everywhere.  R({c1}) = 1/(2*1) + 1/1 = 3/2 (the missing cell costs 2 ms);
+    R({c0}) = 1/1 + 1/2 = 3/2; R({c0, c1}) = 1/1 + 1/1 = 2."""
+    T = np.array([[1.0, np.nan], [2.0, 1.0]], np.float32)
+    o = Oracle(T, np.array([0, 1], np.int32))
+    o.set_fleet([1.0, 1.0], [1.0, 1.0])
+    assert o.penalty == 2.0
+    assert o.fleet_rate([1]) == 1.5
+    assert o.fleet_rate([0]) == 1.5
+    assert o.fleet_rate([0, 1]) == 2.0
+    # a larger penalty (env 1's worst cell 8x its best) moves only the missing cell's cost
+    T2 = np.array([[1.0, np.nan], [8.0, 1.0]], np.float32)
+    o2 = Oracle(T2, np.array([0, 1], np.int32))
+    o2.set_fleet([1.0, 1.0], [1.0, 1.0])
+    assert o2.fleet_rate([1]) == pytest.approx(1 / 8 + 1, rel=1e-15)
+    b, rb, ru, rr = o2.fleet_exhaustive(1)
+    assert b == (0,) and rb == pytest.approx(1 + 1 / 8, rel=1e-15)   # ties by R; lex-first c0

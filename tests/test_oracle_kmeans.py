@@ -49,3 +49,18 @@ def test_planted_blocks_recovered():
         o = Oracle(T, dev)
         hits += o.kmeans(2)[0] == tuple(cols)
     assert hits >= 36
+
+
+def test_degenerate_reseed_branch():
+    """Fewer distinct points than k empties a cluster on the first pass (two
+    maximin centroids coincide), which exercises the re-seed branch.
+    Hand fixture: points (slowdown rows) p0 = p1 = (1, 4, 2), p2 = (4, 1, 2), k = 3:
+    the centroids are p0 (nearest the mean), p2 (farthest), p0 again (every point is
+    then at distance 0); the third cluster is empty and re-seeded with a point at
+    distance 0.  Every centroid sits on a point, so WCSS = 0, the assignment is
+    stable after the second pass, and the selection is {c0 (p0's best), c1 (p2's)}.
+    Whether the farthest-point rule or any other point re-seeds is not observable
+    here (the re-seed rule itself is parity unpinned)."""
+    T = np.array([[1, 4, 2], [1, 4, 2], [4, 1, 2]], np.float32)
+    sel, iters, w = Oracle(T).kmeans(3)
+    assert sel == (0, 1) and iters == 2 and np.all(w == 0.0)

@@ -50,3 +50,17 @@ def test_planted_recovery_and_init():
     o = Oracle(T, dev)
     s, G, moves = o.swap_search(3, init=[0, 1, 2], max_moves=0)
     assert s == (0, 1, 2) and moves == 0
+
+
+def test_tied_best_move_takes_smallest_tuple():
+    """S:L258-266 + reading c5: among equally good swaps the lexicographically
+    smallest resulting sorted tuple wins.  Hand fixture (log2 slowdowns, 2 envs):
+        c0 = [0, 3], c1 = [3, 0], c2 = [5, 5], c3 = [0, 3]   (c3 duplicates c0)
+    From {0, 3} (s = 3) the swaps reach {1,3}: 0, {2,3}: 3, {0,1}: 0, {0,2}: 3, in
+    that enumeration order; {1,3} and {0,1} tie at the optimum s = 0, so the move
+    is to (0, 1) -- a first-encountered rule would stop at (1, 3).  One move, G = 1."""
+    o = Oracle(pow2_matrix(np.array([[0, 3, 5, 0], [3, 0, 5, 3]])))
+    s, G, moves = o.swap_search(2, init=[0, 3])
+    assert s == (0, 1) and G == 1.0 and moves == 1
+    s, G, moves = o.swap_search(2, init=[3, 0])        # init order is irrelevant
+    assert s == (0, 1) and moves == 1
