@@ -8,7 +8,7 @@ LIB := paper_2507_15277_b200/libpt.so
 all: $(LIB) oracle/liboracle.so
 
 $(LIB): $(SRC) paper_2507_15277_b200/csrc/pt_internal.cuh include/pt.h
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -ldl
 
 oracle/liboracle.so: oracle/oracle.c
 	gcc -O2 -std=c99 -D_POSIX_C_SOURCE=200809L -fPIC -shared -o $@ $< -lm -lpthread

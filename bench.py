@@ -124,18 +124,20 @@ def oracle_sample_rate(T, dev, target_s=12.0, threads=None):
     def n_sets(n0):
         return sum(math.comb(C - 1 - a, 2) for a in range(n0))
 
-    n1 = max(1, threads // 4)
+    # the oracle deals first indices to its threads round-robin, so the sample
+    # always spans a multiple of `threads` first indices (every thread busy)
+    n1 = threads
     for _ in range(5):
         t0 = time.perf_counter()
         o.exhaustive(3, lo=0, hi=n1, threads=threads)
         dt = time.perf_counter() - t0
         rate = n_sets(n1) / dt
-        if dt >= 0.6 * target_s or n1 >= C - 3:
+        if dt >= 0.6 * target_s or n1 + threads > C - 3:
             break
         n2 = n1
-        while n2 < C - 3 and n_sets(n2 + 1) / rate < target_s:
-            n2 += 1
-        n1 = max(n2, n1 + 1)
+        while n2 + threads <= C - 3 and n_sets(n2 + threads) / rate < target_s:
+            n2 += threads
+        n1 = max(n2, n1 + threads)
     return rate, threads, (f"exhaustive k=3 over the paper-shaped matrix restricted to first index "
                            f"in [0,{n1}): {n_sets(n1)} triples x 320 envs, {dt:.1f} s, {threads} threads")
 
@@ -152,14 +154,18 @@ def run_reference(args):
     o = Oracle(T, dev)
     C = T.shape[1]
     per_step_target = max(1.0, 150.0 / max(1, args.steps + args.warmup))
-    # calibrate a first-index range so one step takes ~per_step_target seconds
+    # calibrate a first-index range so one step takes ~per_step_target seconds; the
+    # oracle deals first indices to its threads round-robin, so the range is a multiple
+    # of `threads` (every thread busy -- calibrating on one index left all but one idle)
+    def n_sets(n):
+        return sum(math.comb(C - 1 - a, 2) for a in range(n))
     t0 = time.perf_counter()
-    o.exhaustive(3, lo=0, hi=1, threads=threads)
-    r = math.comb(C - 1, 2) / (time.perf_counter() - t0)
-    n0 = 1
-    while n0 < C - 3 and sum(math.comb(C - 1 - a, 2) for a in range(n0 + 1)) / r < per_step_target:
-        n0 += 1
-    nsets = sum(math.comb(C - 1 - a, 2) for a in range(n0))
+    o.exhaustive(3, lo=0, hi=threads, threads=threads)
+    r = n_sets(threads) / (time.perf_counter() - t0)
+    n0 = threads
+    while n0 + threads <= C - 3 and n_sets(n0 + threads) / r < per_step_target:
+        n0 += threads
+    nsets = n_sets(n0)
     for _ in range(args.warmup):
         o.exhaustive(3, lo=0, hi=n0, threads=threads)
     t0 = time.perf_counter()
@@ -227,6 +233,56 @@ def measure_scaled(pt, synth, local, pk, steps=3, world=1):
                                   "(scan + window pick), MEASURED_PEAKS hbm_gbs (x world for sharded runs)"},
             "fp64_refined_candidates": st["greedy_candidates"]}
 
+
+
+def measure_per_config(pt, dT, dev, local, pk, reps=5):
+    """One sub-line per BASELINE config on the paper-shaped matrix (each
+    config has its own bounding roofline): the call alone, inputs resident, CUDA
+    events on the library's stream around it (median of `reps` after a warm-up), and
+    for the exhaustive searches the main kernel's own CUDA-event time."""
+    import torch
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    alu_peak = nsm * 128 * pk.get("sm_max_mhz", 1965.0) * 1e6
+    ctx = pt.pt_load_perf(dT, dev, device=local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def dev_ms(fn, stat=None):
+        fn()
+        ms, kms = [], []
+        for _ in range(reps):
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            if stat:
+                kms.append(pt.pt_get_stats(ctx)[stat])
+        return float(np.median(ms)), (float(np.median(kms)) if kms else None)
+
+    out = {}
+    ms, _ = dev_ms(lambda: pt.pt_greedy_select(ctx, K_GREEDY))
+    out["paper_greedy_k24"] = {
+        "config": "BASELINE configs[1]: greedy k=1..24 over 1,775 x 320", "ms": ms,
+        "us_per_step": ms * 1e3 / K_GREEDY, "sets_per_s": SETS["greedy24"] / (ms * 1e-3),
+        "roofline": {"bound": "latency", "basis": "24 dependent steps, each a grid barrier + a merge of "
+                     "per-CTA records (DESIGN.md 6.4); ALU work per step ~0.03 us at the ALU ceiling",
+                     "alu_frac": SETS["greedy24"] * E_PAPER / (ms * 1e-3) / alu_peak}}
+    for k, name in ((2, "paper_exhaustive_k2"), (3, "paper_exhaustive_k3")):
+        ms, kms = dev_ms(lambda: pt.pt_exhaustive_best(ctx, k), "exh_main_ms")
+        sets = SETS[f"exh{k}"]
+        out[name] = {"config": f"BASELINE configs[2]: exhaustive k={k} over 1,775 x 320", "ms": ms,
+                     "kernel_ms": kms, "sets_per_s": sets / (ms * 1e-3),
+                     "roofline": {"bound": "alu", "kernel": "k_exh_tiled", "unit": "T(set,env)/s",
+                                  "achieved": sets * E_PAPER / (kms * 1e-3) / 1e12, "peak": alu_peak / 1e12,
+                                  "frac": sets * E_PAPER / (kms * 1e-3) / alu_peak}}
+    ms, _ = dev_ms(lambda: pt.pt_eval_holdout_all(ctx, K_HOLDOUT, 5))
+    out["holdout_5fold_greedy_k5"] = {
+        "config": "BASELINE configs[3]: leave-one-device-out, 5 folds, greedy k=5 (one batched launch)",
+        "ms": ms, "sets_per_s": SETS["holdout"] / (ms * 1e-3),
+        "roofline": {"bound": "latency", "basis": "5 dependent greedy steps over 10 problems at once",
+                     "alu_frac": SETS["holdout"] * E_PAPER / (ms * 1e-3) / alu_peak}}
+    pt.pt_free(ctx)
+    return out
 
 
 FP64_PEAK_TFLOPS = 2 * 16.96   # tools/ubench_fp64.cu on this pool's B200: 58.3 DFMA/clk/SM (2 flops each)
@@ -416,6 +472,7 @@ def main():
         d2h_e2e, launches = int(agg[0].item()), int(agg[1].item())
     # secondary config-5 line: every rank takes part (sharded greedy for world > 1)
     scaled = None if args.no_scaled else measure_scaled(pt, synth, local, peaks(), world=world)
+    per_config = measure_per_config(pt, dT, dev, local, peaks()) if world == 1 else None
     next_rows = None
     if world == 1 and not args.no_next:
         next_rows = measure_next_rows(pt, T, dev, local, cpu=not args.no_cpu_baseline)
@@ -515,6 +572,7 @@ def main():
         "clocks_e2e": clocks_e2e,
         "parity": {"k3_best": list(res["r3"]["best"]), "k3_matches_oracle_golden": gold,
                    "k3_candidates_refined": res["k3_cand"]},
+        "per_config": per_config,
         "scaled_greedy": scaled,
         "k3_shard_balance": shard_bal,
         "next_rows": next_rows,

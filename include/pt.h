@@ -44,7 +44,7 @@ typedef enum {
     PT_EINVAL = -1,   /* bad argument (k < 1, k > #configs, bad index, bad shard) */
     PT_ENOMEM = -2,   /* host or device allocation failed */
     PT_ECUDA = -3,    /* CUDA runtime / driver error (message has details) */
-    PT_ENCCL = -4,    /* reserved: collective failure */
+    PT_ENCCL = -4,    /* collective failure (NCCL or the caller's exchange callback) */
     PT_ECAP = -5,     /* C(n,k) exceeds the enumeration cap (1e13) */
     PT_EEMPTY = -6,   /* empty scope (mask selects no environment) or empty set */
     PT_EDATA = -7     /* runtime <= 0, or an environment with no measured cell */
@@ -77,8 +77,9 @@ enum {
  *              runtime (ms) of configuration c in environment e.  NaN/+inf =
  *              missing.  Environments are device-major then input.
  *   n_env, n_cfg, ld   E >= 1, C >= 1, ld >= C (elements).
- *   env_device host, int32[n_env] device id per environment (>= 0), or NULL
- *              (then every env is device 0; pt_eval_holdout needs it).
+ *   env_device host, int32[n_env] device id per environment (>= 0, else
+ *              PT_EINVAL), or NULL (then every env is device 0; pt_eval_holdout
+ *              needs it).
  *   flags      PT_* flags above.
  *   cuda_device  device ordinal; cuda_stream: cudaStream_t borrowed (NULL =
  *              the legacy default stream), not owned.
@@ -191,6 +192,63 @@ pt_status pt_greedy_sharded_dev(pt_ctx *ctx, int32_t k, const uint8_t *env_mask,
                                 int32_t *out_idx, double *out_G_trace, double *out_gap_trace);
 
 /*
+ * ---- the cross-GPU reduction of the sharded exhaustive search ----
+ * "returns the variant combination with the highest ranking" over ranks:
+ * every rank searches shard `shard_rank` of `shard_count` (pt_exhaustive_best's
+ * partition), the ranks all-gather one record each -- [plan fingerprint, s1, s2,
+ * tuple1[k], tuple2[k]] as pt_record_len(k) doubles, on the device -- and every rank
+ * merges them on the device in (s asc, tuple asc) order and maps s to the objective
+ * (G = exp(-s/|scope|), Eq. 1; R = 1/cost, Eq. 2).  Identical results on every rank,
+ * equal to the unsharded pt_exhaustive_best for any shard_count.
+ *
+ * The exchange is either an NCCL all-gather over a communicator the LIBRARY builds
+ * (pt_comm_init; NVLink/NVSwitch between the GPUs of a node) or a caller's stream-
+ * ordered all-gather (pt_dev_allgather_fn, e.g. gloo with host staging in tests).
+ * NCCL is loaded at run time (libnccl.so.2; in a PyTorch process the one torch
+ * loaded).  All ranks must load the same matrix and set the same shard weights; a
+ * different shard plan on some rank is detected (the fingerprints disagree) and
+ * reported as PT_EINVAL instead of a wrong answer.
+ */
+typedef struct pt_comm pt_comm;        /* opaque; owns an ncclComm_t */
+#define PT_COMM_ID_BYTES 128           /* sizeof(ncclUniqueId) */
+
+/* pt_comm_unique_id -- one rank (e.g. rank 0) creates the id (host buffer of
+ * PT_COMM_ID_BYTES bytes) and broadcasts it to the others by any means.
+ * Errors: PT_EINVAL (NULL), PT_ENCCL (NCCL missing or failing). */
+pt_status pt_comm_unique_id(void *out_id);
+
+/* pt_comm_init -- collective over `world` ranks: every rank calls it with the same id
+ * and its own rank (0 <= rank < world); one GPU (cuda_device) per rank.
+ * *out is freed with pt_comm_free.  Errors: PT_EINVAL, PT_ENCCL, PT_ECUDA. */
+pt_status pt_comm_init(pt_comm **out, const void *id, int32_t rank, int32_t world, int cuda_device);
+void pt_comm_free(pt_comm *comm);
+
+/* pt_exhaustive_best_sharded -- the sharded search end to end.  Give exactly one of
+ *   comm       a communicator whose (rank, world) is (shard_rank, shard_count) and
+ *              whose device is the context's, or
+ *   allgather  a stream-ordered all-gather (pt_dev_allgather_fn above): mine =
+ *              pt_record_len(k) doubles on the device, all = shard_count times that,
+ *              in rank order; called once, on the calling thread.
+ * Outputs as pt_exhaustive_best (host).  Errors: those of pt_exhaustive_best,
+ * PT_ENCCL (the exchange failed), PT_EINVAL (bad shard, mismatched communicator, or
+ * ranks with different shard plans), PT_EEMPTY (no subset in any shard). */
+pt_status pt_exhaustive_best_sharded(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t objective,
+                                     int32_t shard_rank, int32_t shard_count, pt_comm *comm,
+                                     pt_dev_allgather_fn allgather, void *user, int32_t *out_idx,
+                                     double *out_G, int32_t *out_runner_idx, double *out_G_runner,
+                                     double *out_s);
+
+/* pt_record_len -- doubles per rank record for k (3 + 2k), or -1 if k is out of range. */
+int32_t pt_record_len(int32_t k);
+
+/* pt_merge_records -- host-only form of the merge above over n_rank gathered records
+ * (host double[n_rank * pt_record_len(k)]), for callers that exchange records
+ * themselves; n_env = the scope size (|scope| of Eq. 1).  Same outputs and errors. */
+pt_status pt_merge_records(const double *records, int32_t n_rank, int32_t k, int64_t n_env,
+                           int32_t objective, int32_t *out_idx, double *out_G,
+                           int32_t *out_runner_idx, double *out_G_runner, double *out_s);
+
+/*
  * pt_merge_top2 -- host-only: merge n_rec (s, sorted k-tuple) records (e.g.
  * gathered from every shard/rank) into the best two in (s asc, tuple asc)
  * order.  s = +inf marks an absent record.
@@ -223,10 +281,12 @@ pt_status pt_eval_holdout(pt_ctx *ctx, int32_t heldout_device, int32_t k, int32_
  * pt_eval_holdout_all -- pt_eval_holdout (method 0, greedy) for every device
  * d = 0..D-1 at once (D = 1 + the largest env_device id), computed in one
  * batched launch.  Outputs are [D][k] / [D] host arrays in the same meaning as
- * pt_eval_holdout; *out_n_device (host, or NULL) receives D.
- * Errors: as pt_eval_holdout; PT_EEMPTY if some device has no environment.
+ * pt_eval_holdout, with room for n_device_cap devices (nothing is written past
+ * it); *out_n_device (host, or NULL) receives D.
+ * Errors: as pt_eval_holdout; PT_EINVAL if D > n_device_cap (*out_n_device
+ * still set); PT_EEMPTY if some device has no environment.
  */
-pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t *out_idx, double *out_G_train,
+pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t n_device_cap, int32_t *out_idx, double *out_G_train,
                               double *out_G_unseen, double *out_G_known, int32_t *out_known_idx,
                               int32_t *out_n_device);
 

@@ -171,6 +171,7 @@ static pt_status shard_plan(pt_tasks *T, int N, const std::vector<double> &w, co
 
 extern "C" pt_status pt_set_shard_weights(pt_ctx *ctx, const double *weights, int32_t n)
 {
+    PT_NVTX();
     if (!ctx || n < 0) return pt_fail(PT_EINVAL, "bad argument");
     if (!weights || n == 0) {
         ctx->shard_w.clear();
@@ -183,8 +184,10 @@ extern "C" pt_status pt_set_shard_weights(pt_ctx *ctx, const double *weights, in
     return PT_OK;
 }
 
-// The work list depends only on (device, C, m, #SMs): built once per process
-// and shared by every context (a fresh pt_load_perf does not rebuild it).
+// The work list depends only on (C, m, tile shape): built once per process and
+// shared by every context (a fresh pt_load_perf does not rebuild it).  It must not
+// depend on the local GPU: the ranks of a sharded search each deal the SAME list
+// (ADVICE r1), so the task granularity is sized for a 148-SM B200 on every device.
 static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, int cols, pt_tasks **out)
 {
     static std::mutex mu;
@@ -213,7 +216,7 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, int
         if (mem[m - 1] + 1 >= C) continue;
         total_ct += (C - tile_lo(mem[m - 1]) + cols - 1) / cols;
     }
-    const int64_t umax = std::max<int64_t>(1, std::min<int64_t>(XT_UMAX, total_ct / (8 * std::max(ctx->num_sms, 1))));
+    const int64_t umax = std::max<int64_t>(1, std::min<int64_t>(XT_UMAX, total_ct / (8 * 148)));
     for (int64_t t = 0; t < n_rt; t++) {
         const int64_t R0 = t * rows, R1 = std::min(n_rows, R0 + rows);
         int32_t mem[PT_MAXK];
@@ -1911,6 +1914,7 @@ static pt_status run_generic(pt_ctx *ctx, const pt_view *v, int k, int64_t r0, i
     PT_CK(cudaEventRecord(ctx->ev1, s));
     k_top2<<<1, 256, 0, s>>>(bs, bt, 2 * nblk, nullptr, 0, k, os, ot);
     ctx->stats.launches += 2;
+    pt_pack_record(ctx, os, ot, k);
     PT_CK(cudaGetLastError());
     pt_hostio io(ctx);
     PT_TRY(io.d2h(s_out, os, sizeof(double) * 2));
@@ -2165,6 +2169,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
                                                                   v->l64, v->E_pad, rs, rt);
         k_top2<<<1, 256, 0, s>>>(rs, rt, 0, cn, cap, k, os, ot);
         ctx->stats.launches += 2;
+        pt_pack_record(ctx, os, ot, k);   // sharded search: this rank's record stays on the device
         PT_CK(cudaGetLastError());
         unsigned hU = 0;
         PT_TRY(io.d2h(&n_cand, cn, sizeof(unsigned)));
@@ -2263,6 +2268,7 @@ extern "C" pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *e
                                         int32_t *out_idx, double *out_G, int32_t *out_runner_idx,
                                         double *out_G_runner, double *out_s)
 {
+    PT_NVTX();
     if (!ctx || !out_idx || !out_G) return pt_fail(PT_EINVAL, "NULL argument");
     if (objective != PT_OBJ_GEOMEAN && objective != PT_OBJ_FLEET)
         return pt_fail(PT_EINVAL, "unknown objective %d", objective);
@@ -2304,6 +2310,7 @@ extern "C" pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *e
 extern "C" pt_status pt_merge_top2(const double *s, const int32_t *tuples, int32_t n_rec, int32_t k,
                                    int32_t *out_idx, int32_t *out_runner_idx, double *out_s)
 {
+    PT_NVTX();
     if (!s || !tuples || !out_idx || !out_s || k < 1 || k > PT_MAXK || n_rec < 0)
         return pt_fail(PT_EINVAL, "bad argument");
     double s1 = INFINITY, s2 = INFINITY;

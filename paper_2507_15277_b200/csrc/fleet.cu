@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(128) k_fleet_exh(const double *__restrict__ te
 extern "C" pt_status pt_set_fleet(pt_ctx *ctx, const double *q_device, int32_t n_device,
                                   const double *q_env)
 {
+    PT_NVTX();
     if (!ctx || !q_device || !q_env || n_device < 1) return pt_fail(PT_EINVAL, "bad argument");
     if (n_device > FL_MAXDEV) return pt_fail(PT_EINVAL, "at most %d devices", FL_MAXDEV);
     for (int32_t d = 0; d < n_device; d++)

@@ -816,6 +816,7 @@ extern "C" pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env
                                       int32_t objective, int32_t *out_idx, double *out_G_trace,
                                       double *out_gap_trace)
 {
+    PT_NVTX();
     if (!ctx || !out_idx) return pt_fail(PT_EINVAL, "NULL argument");
     if (objective != PT_OBJ_GEOMEAN && objective != PT_OBJ_FLEET)
         return pt_fail(PT_EINVAL, "unknown objective %d", objective);
@@ -990,6 +991,7 @@ extern "C" pt_status pt_greedy_sharded(pt_ctx *ctx, int32_t k, const uint8_t *en
                                        int32_t shard_count, pt_allgather_fn allgather, void *user,
                                        int32_t *out_idx, double *out_G_trace, double *out_gap_trace)
 {
+    PT_NVTX();
     if (!allgather) return pt_fail(PT_EINVAL, "NULL argument");
     return greedy_sharded_impl(ctx, k, env_mask, shard_rank, shard_count, allgather, nullptr, user, out_idx,
                                out_G_trace, out_gap_trace);
@@ -999,6 +1001,7 @@ extern "C" pt_status pt_greedy_sharded_dev(pt_ctx *ctx, int32_t k, const uint8_t
                                            int32_t shard_count, pt_dev_allgather_fn allgather, void *user,
                                            int32_t *out_idx, double *out_G_trace, double *out_gap_trace)
 {
+    PT_NVTX();
     if (!allgather) return pt_fail(PT_EINVAL, "NULL argument");
     return greedy_sharded_impl(ctx, k, env_mask, shard_rank, shard_count, nullptr, allgather, user, out_idx,
                                out_G_trace, out_gap_trace);

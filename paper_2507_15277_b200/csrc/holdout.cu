@@ -28,6 +28,7 @@ extern "C" pt_status pt_eval_holdout(pt_ctx *ctx, int32_t heldout_device, int32_
                                      int32_t *out_idx, double *out_G_train, double *out_G_unseen,
                                      double *out_G_known, int32_t *out_known_idx)
 {
+    PT_NVTX();
     if (!ctx || !out_idx || !out_G_train || !out_G_unseen || !out_G_known)
         return pt_fail(PT_EINVAL, "NULL argument");
     if (!ctx->have_device) return pt_fail(PT_EINVAL, "pt_load_perf was given no env_device");
@@ -202,10 +203,11 @@ __global__ void k_holdout_unseen(const double *__restrict__ l64, int64_t E_pad, 
     if (lane == 0) out_s[f] = acc;
 }
 
-extern "C" pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t *out_idx, double *out_G_train,
-                                         double *out_G_unseen, double *out_G_known,
+extern "C" pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t n_device_cap, int32_t *out_idx,
+                                         double *out_G_train, double *out_G_unseen, double *out_G_known,
                                          int32_t *out_known_idx, int32_t *out_n_device)
 {
+    PT_NVTX();
     if (!ctx || !out_idx || !out_G_train || !out_G_unseen || !out_G_known)
         return pt_fail(PT_EINVAL, "NULL argument");
     if (!ctx->have_device) return pt_fail(PT_EINVAL, "pt_load_perf was given no env_device");
@@ -214,6 +216,9 @@ extern "C" pt_status pt_eval_holdout_all(pt_ctx *ctx, int32_t k, int32_t *out_id
     if (k < 1 || k > C) return pt_fail(PT_EINVAL, "k=%d outside [1, %lld]", k, (long long)C);
     int32_t D = 0;
     for (int32_t d : ctx->env_device) D = std::max(D, d + 1);
+    if (out_n_device) *out_n_device = D;
+    if (D > n_device_cap)
+        return pt_fail(PT_EINVAL, "%d devices but output room for %d (n_device_cap)", D, n_device_cap);
     std::vector<int64_t> cnt(D, 0);
     for (int32_t d : ctx->env_device) cnt[d]++;
     for (int32_t d = 0; d < D; d++)

@@ -208,6 +208,7 @@ __global__ void k_km_select(const double *__restrict__ M, int64_t C, int32_t *__
 extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t max_iter,
                                       int32_t *out_idx, int32_t *out_n, double *out_G, int32_t *out_iters)
 {
+    PT_NVTX();
     if (!ctx || !out_idx || !out_n) return pt_fail(PT_EINVAL, "NULL argument");
     if (k < 1 || k > KM_MAXK) return pt_fail(PT_EINVAL, "k=%d outside [1, %d]", k, KM_MAXK);
     if (max_iter < 1) return pt_fail(PT_EINVAL, "max_iter must be >= 1");

@@ -39,6 +39,7 @@ extern "C" const char *pt_last_error(void) { return g_err.c_str(); }
 
 bool pt_is_device_ptr(const void *p)
 {
+    PT_NVTX();
     if (!p) return false;
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -372,6 +373,7 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
                                   int64_t n_cfg, int64_t ld, const int32_t *env_device,
                                   uint32_t flags, int cuda_device, void *cuda_stream)
 {
+    PT_NVTX();
     if (!out) return pt_fail(PT_EINVAL, "out is NULL");
     *out = nullptr;
     if (!times_ms || n_env < 1 || n_cfg < 1 || ld < n_cfg)
@@ -379,6 +381,10 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
                        (long long)n_env, (long long)n_cfg, (long long)ld);
     if (n_cfg >= (1 << 21))
         return pt_fail(PT_EINVAL, "n_cfg must be < 2^21 (subset keys pack 21-bit indices)");
+    if (env_device)
+        for (int64_t e = 0; e < n_env; e++)
+            if (env_device[e] < 0)
+                return pt_fail(PT_EINVAL, "env_device[%lld] = %d is negative", (long long)e, env_device[e]);
     PT_CK(cudaSetDevice(cuda_device));
     pt_ctx *ctx = new pt_ctx();
     ctx->dev = cuda_device;
@@ -473,6 +479,7 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
 
 extern "C" pt_status pt_get_stats(const pt_ctx *ctx, pt_stats *out)
 {
+    PT_NVTX();
     if (!ctx || !out) return pt_fail(PT_EINVAL, "NULL argument");
     *out = ctx->stats;
     return PT_OK;
@@ -480,6 +487,7 @@ extern "C" pt_status pt_get_stats(const pt_ctx *ctx, pt_stats *out)
 
 extern "C" void pt_free(pt_ctx *ctx)
 {
+    PT_NVTX();
     if (!ctx) return;
     cudaSetDevice(ctx->dev);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);

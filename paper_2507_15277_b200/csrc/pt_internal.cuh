@@ -11,6 +11,15 @@
 
 #include "pt.h"
 
+// NVTX ranges (header-only nvtx3; no-ops unless a tool is attached): every pt_* entry
+// point opens one named range for its whole duration (nsys / ncu --nvtx)
+#include <nvtx3/nvToolsExt.h>
+struct pt_nvtx_range {
+    explicit pt_nvtx_range(const char *name) { nvtxRangePushA(name); }
+    ~pt_nvtx_range() { nvtxRangePop(); }
+};
+#define PT_NVTX() pt_nvtx_range pt_nvtx_range_(__func__)
+
 // ---------------------------------------------------------------------------
 // errors
 // ---------------------------------------------------------------------------
@@ -107,6 +116,10 @@ struct pt_ctx {
     size_t scratch_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     pt_stats stats{};
+    // sharded search (dist.cu): where the exhaustive search packs this rank's record
+    double *rec_out = nullptr;
+    double rec_fp = 0.0;
+    bool rec_written = false;
 };
 
 // Small host<->device transfers of one API call through a pinned staging buffer
@@ -147,6 +160,8 @@ pt_status pt_exhaustive_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t s
                              double *s_out, int *n_found);
 pt_status pt_score_view(pt_ctx *ctx, const pt_view *v, const int32_t *d_sets, int64_t n_sets,
                         int32_t k, double *d_s);
+// sharded search (dist.cu): pack the local top-2 (device os[2], ot[2k]) into ctx->rec_out
+void pt_pack_record(pt_ctx *ctx, const double *d_os, const int32_t *d_ot, int k);
 // fleet objective (fleet.cu): rates of sets / greedy / exhaustive, env_mask may be NULL
 pt_status pt_fleet_score(pt_ctx *ctx, const int32_t *d_sets, int64_t n_sets, int32_t k,
                          const uint8_t *env_mask, double *d_R);

@@ -65,6 +65,7 @@ pt_status pt_score_view(pt_ctx *ctx, const pt_view *v, const int32_t *d_sets, in
 extern "C" pt_status pt_score_sets(pt_ctx *ctx, const int32_t *sets, int64_t n_sets, int32_t k,
                                    const uint8_t *env_mask, int32_t objective, double *out_G)
 {
+    PT_NVTX();
     if (!ctx || (!sets && n_sets > 0) || (!out_G && n_sets > 0) || n_sets < 0)
         return pt_fail(PT_EINVAL, "NULL argument");
     if (objective != PT_OBJ_GEOMEAN && objective != PT_OBJ_FLEET)

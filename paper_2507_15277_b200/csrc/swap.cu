@@ -131,6 +131,7 @@ extern "C" pt_status pt_swap_search(pt_ctx *ctx, int32_t k, const uint8_t *env_m
                                     int32_t max_moves, const int32_t *init, int32_t *out_idx,
                                     double *out_G, int32_t *out_moves)
 {
+    PT_NVTX();
     if (!ctx || !out_idx || !out_G) return pt_fail(PT_EINVAL, "NULL argument");
     if (objective != PT_OBJ_GEOMEAN)
         return pt_fail(PT_EINVAL, "swap search supports PT_OBJ_GEOMEAN only");

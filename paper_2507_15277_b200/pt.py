@@ -2,8 +2,9 @@
 
 Every step of the hot path runs in the CUDA kernels behind the C ABI; this
 module only converts numpy arrays / torch tensors to pointers, picks the
-current CUDA stream, and (for the multi-GPU search) moves the 8-byte-class
-(score, index) records between ranks with torch.distributed.  There is no CPU
+current CUDA stream, and hands the library a process group's ncclUniqueId (or, for
+gloo test groups, a host-staged all-gather callback); the record exchange, merge and
+objective transform of the multi-GPU search run inside the library.  There is no CPU
 fallback: if libpt.so is missing or cannot initialise a GPU, calls raise.
 
 Names follow the C ABI: pt_load_perf, pt_score_sets, pt_greedy_select,
@@ -26,8 +27,10 @@ PT_MISSING_PENALTY_MAX, PT_EXACT_FP64, PT_GREEDY_STREAM, PT_GREEDY_LAZY = 0x1, 0
 EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
            "pt_merge_top2", "pt_eval_holdout", "pt_eval_holdout_all", "pt_swap_search",
            "pt_kmeans_select", "pt_set_fleet", "pt_get_stats", "pt_greedy_sharded",
-           "pt_greedy_sharded_dev", "pt_set_shard_weights",
+           "pt_greedy_sharded_dev", "pt_set_shard_weights", "pt_comm_unique_id", "pt_comm_init",
+           "pt_comm_free", "pt_exhaustive_best_sharded", "pt_record_len", "pt_merge_records",
            "pt_free", "pt_last_error")
+PT_COMM_ID_BYTES = 128
 
 
 # int (*)(void *user, const double *mine, int32_t n, double *all)
@@ -82,17 +85,27 @@ def lib():
         L.pt_get_stats.argtypes = [P, ct.POINTER(pt_stats)]
         L.pt_set_fleet.argtypes = [P, P, i32, P]
         L.pt_swap_search.argtypes = [P, i32, P, i32, i32, P, P, P, P]
-        L.pt_eval_holdout_all.argtypes = [P, i32, P, P, P, P, P, P]
+        L.pt_eval_holdout_all.argtypes = [P, i32, i32, P, P, P, P, P, P]
         L.pt_kmeans_select.argtypes = [P, i32, P, i32, P, P, P, P]
         L.pt_greedy_sharded.argtypes = [P, i32, P, i32, i32, ALLGATHER_FN, P, P, P, P]
         L.pt_greedy_sharded_dev.argtypes = [P, i32, P, i32, i32, DEV_ALLGATHER_FN, P, P, P, P]
+        L.pt_comm_unique_id.argtypes = [P]
+        L.pt_comm_init.argtypes = [ct.POINTER(P), P, i32, i32, ct.c_int]
+        L.pt_comm_free.argtypes = [P]
+        L.pt_comm_free.restype = None
+        L.pt_exhaustive_best_sharded.argtypes = [P, i32, P, i32, i32, i32, P, DEV_ALLGATHER_FN, P,
+                                                 P, P, P, P, P]
+        L.pt_record_len.argtypes = [i32]
+        L.pt_record_len.restype = i32
+        L.pt_merge_records.argtypes = [P, i32, i32, i64, i32, P, P, P, P, P]
         L.pt_free.argtypes = [P]
         L.pt_free.restype = None
         L.pt_last_error.argtypes = []
         L.pt_last_error.restype = ct.c_char_p
         for f in ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
                   "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_set_fleet",
-                  "pt_swap_search", "pt_eval_holdout_all", "pt_kmeans_select"):
+                  "pt_swap_search", "pt_eval_holdout_all", "pt_kmeans_select", "pt_comm_unique_id",
+                  "pt_comm_init", "pt_exhaustive_best_sharded", "pt_merge_records"):
             getattr(L, f).restype = ct.c_int
         _lib = L
     return _lib
@@ -120,13 +133,13 @@ def _mask(m):
     return None if m is None else _np(m, np.uint8)
 
 
-def _stream(stream):
+def _stream(stream, device=None):
     if stream is not None:
-        return ct.c_void_p(int(stream))
+        return stream if isinstance(stream, ct.c_void_p) else ct.c_void_p(int(stream))
     try:
         import torch
         if torch.cuda.is_available():
-            return ct.c_void_p(torch.cuda.current_stream().cuda_stream)
+            return ct.c_void_p(torch.cuda.current_stream(device).cuda_stream)
     except ImportError:
         pass
     return None
@@ -151,8 +164,22 @@ class PtContext:
             pass
 
 
-def pt_load_perf(times_ms, env_device=None, flags=0, device=0, stream=None) -> PtContext:
-    """times_ms: [E][C] float32 numpy array (host) or torch tensor (host or cuda)."""
+def pt_load_perf(times_ms, env_device=None, flags=0, device=None, stream=None) -> PtContext:
+    """times_ms: [E][C] float32 numpy array (host) or torch tensor (host or cuda).
+    device: CUDA ordinal (default: a cuda tensor's own device, else torch's current
+    device); stream: a cudaStream_t handle (default: torch's current stream OF THAT
+    device)."""
+    if device is None:
+        if hasattr(times_ms, "is_cuda") and times_ms.is_cuda:
+            device = times_ms.device.index
+        else:
+            try:
+                import torch
+                device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+            except ImportError:
+                device = 0
+    if stream is None:
+        stream = _stream(None, device)
     if hasattr(times_ms, "data_ptr"):
         assert times_ms.dtype.__str__() == "torch.float32" and times_ms.is_contiguous()
         E, C = times_ms.shape
@@ -393,9 +420,9 @@ def pt_eval_holdout_all(ctx, k, n_device):
     kidx = np.zeros((D, k), np.int32)
     gtr, gun, gkn = np.zeros(D), np.zeros(D), np.zeros(D)
     nd = np.zeros(1, np.int32)
-    _chk(lib().pt_eval_holdout_all(ctx.handle, k, _ptr(idx), _ptr(gtr), _ptr(gun), _ptr(gkn),
+    _chk(lib().pt_eval_holdout_all(ctx.handle, k, D, _ptr(idx), _ptr(gtr), _ptr(gun), _ptr(gkn),
                                    _ptr(kidx), _ptr(nd)), "pt_eval_holdout_all")
-    assert int(nd[0]) == D, (int(nd[0]), D)
+    D = int(nd[0])   # the library writes D <= n_device rows
     return [{"idx": [int(x) for x in idx[d]], "G_train": float(gtr[d]), "G_unseen": float(gun[d]),
              "G_known": float(gkn[d]), "known_idx": [int(x) for x in kidx[d]]} for d in range(D)]
 
@@ -410,39 +437,159 @@ def pt_free(ctx):
     ctx.close()
 
 
-def exhaustive_best_distributed(ctx, k, env_mask=None, group=None, local_search=None,
-                                n_env=None):
-    """Sharded exhaustive search: rank r of world W searches shard r of W, then
-    the (s, tuple) top-2 records of every rank are all-gathered (NCCL over
-    NVLink for a cuda group, gloo on CPU) and merged identically on every rank
-    with pt_merge_top2.  `local_search(shard_rank, shard_count)` may replace the
-    GPU shard search (tests drive the protocol on CPU with it)."""
+class PtComm:
+    """Owner of a library-built NCCL communicator (pt_comm_init)."""
+
+    def __init__(self, handle, rank, world, device):
+        self.handle, self.rank, self.world, self.device = handle, rank, world, device
+
+    def close(self):
+        if self.handle:
+            lib().pt_comm_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pt_comm_unique_id():
+    """A fresh ncclUniqueId (bytes) for pt_comm_init; create on one rank, broadcast."""
+    buf = (ct.c_uint8 * PT_COMM_ID_BYTES)()
+    _chk(lib().pt_comm_unique_id(ct.cast(buf, ct.c_void_p)), "pt_comm_unique_id")
+    return bytes(buf)
+
+
+def pt_comm_init(uid, rank, world, device=None):
+    """Collective: every rank passes the same id bytes and its rank -> PtComm."""
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    buf = (ct.c_uint8 * PT_COMM_ID_BYTES).from_buffer_copy(uid)
+    h = ct.c_void_p()
+    _chk(lib().pt_comm_init(ct.byref(h), ct.cast(buf, ct.c_void_p), rank, world, device), "pt_comm_init")
+    return PtComm(h, rank, world, device)
+
+
+def pt_record_len(k):
+    return int(lib().pt_record_len(k))
+
+
+def _result(b, g, r, s):
+    has1, has2 = np.isfinite(s[0]), np.isfinite(s[1])
+    return {"best": tuple(int(x) for x in b) if has1 else None, "G": float(g[0]),
+            "runner": tuple(int(x) for x in r) if has2 else None, "G_runner": float(g[1]),
+            "s": (float(s[0]), float(s[1]))}
+
+
+def pt_exhaustive_best_sharded(ctx, k, shard_rank, shard_count, comm=None, allgather=None,
+                               env_mask=None, objective=PT_OBJ_GEOMEAN):
+    """The sharded search end to end in the library: shard search, record exchange over
+    `comm` (PtComm, NCCL) or `allgather(mine, out, stream)` (torch CUDA views of this
+    rank's record and of the gathered records, the library's stream; must enqueue the
+    gather in that stream's order), device merge, G.  Returns the pt_exhaustive_best dict."""
+    import torch
+    err = []
+    cb = None
+    if allgather is not None:
+        def _cb(_user, mine, n, all_out, stream):
+            try:
+                mt = torch.as_tensor(_DevView(mine, n), device="cuda")
+                at = torch.as_tensor(_DevView(all_out, n * shard_count), device="cuda")
+                st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+                allgather(mt, at, st)
+                return 0
+            except BaseException as ex:   # reported after the C call returns
+                err.append(ex)
+                return 1
+        cb = DEV_ALLGATHER_FN(_cb)
+    else:
+        cb = ct.cast(None, DEV_ALLGATHER_FN)
+    b = np.zeros(k, np.int32)
+    r = np.zeros(k, np.int32)
+    g = np.zeros(2, np.float64)
+    s = np.zeros(2, np.float64)
+    rc = lib().pt_exhaustive_best_sharded(ctx.handle, k, _ptr(_mask(env_mask)), objective, shard_rank,
+                                          shard_count, comm.handle if comm is not None else None, cb, None,
+                                          _ptr(b), _ptr(g[0:1]), _ptr(r), _ptr(g[1:2]), _ptr(s))
+    if err:
+        raise err[0]
+    _chk(rc, "pt_exhaustive_best_sharded")
+    return _result(b, g, r, s)
+
+
+def pt_merge_records(records, k, n_env, objective=PT_OBJ_GEOMEAN):
+    """Host merge of gathered rank records ([n_rank][pt_record_len(k)] float64)."""
+    rec = _np(records, np.float64).reshape(-1)
+    L = pt_record_len(k)
+    b = np.zeros(k, np.int32)
+    r = np.zeros(k, np.int32)
+    g = np.zeros(2, np.float64)
+    s = np.zeros(2, np.float64)
+    _chk(lib().pt_merge_records(_ptr(rec), rec.size // L, k, n_env, objective, _ptr(b), _ptr(g[0:1]), _ptr(r),
+                                _ptr(g[1:2]), _ptr(s)), "pt_merge_records")
+    return _result(b, g, r, s)
+
+
+_COMMS = {}
+
+
+def _library_comm(group, rank, world):
+    """One library-built NCCL communicator per (process group, device), created on
+    first use: rank 0 makes the ncclUniqueId, the group broadcasts it."""
     import torch
     import torch.distributed as dist
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    if local_search is None:
-        res = pt_exhaustive_best(ctx, k, env_mask, rank, world)
-        recs = [(res["s"][0], res["best"]), (res["s"][1], res["runner"])]
-    else:
-        recs = local_search(rank, world)
-    buf = torch.full((2, k + 1), float("inf"), dtype=torch.float64)
-    for q, (sv, tup) in enumerate(recs):
-        if tup is not None and np.isfinite(sv):
-            buf[q, 0] = sv
-            buf[q, 1:] = torch.tensor(tup, dtype=torch.float64)
-    if world > 1:
-        backend = dist.get_backend(group)
-        dev_buf = buf.cuda() if backend == "nccl" else buf
-        out = [torch.empty_like(dev_buf) for _ in range(world)]
-        dist.all_gather(out, dev_buf, group=group)
-        allr = torch.cat([o.cpu() for o in out]).numpy()
-    else:
-        allr = buf.numpy()
-    s = allr[:, 0]
-    t = np.where(np.isfinite(allr[:, 1:]), allr[:, 1:], -1).astype(np.int32)
-    best, runner, (s1, s2) = pt_merge_top2(s, t, k)
-    E = (ctx.E if ctx is not None else n_env) if env_mask is None else int(np.count_nonzero(env_mask))
-    return {"best": best, "G": float(np.exp(-s1 / E)), "runner": runner,
-            "G_runner": float(np.exp(-s2 / E)) if np.isfinite(s2) else float("nan"),
-            "s": (s1, s2)}
+    key = (id(group), world, torch.cuda.current_device())
+    if key not in _COMMS:
+        obj = [pt_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0 if group is None else dist.get_global_rank(group, 0),
+                                   group=group)
+        _COMMS[key] = pt_comm_init(obj[0], rank, world)
+    return _COMMS[key]
+
+
+def exhaustive_best_distributed(ctx, k, env_mask=None, group=None, objective=PT_OBJ_GEOMEAN,
+                                local_search=None, n_env=None):
+    """Sharded exhaustive search over a torch.distributed group: rank r of W searches
+    shard r, and the library exchanges and merges the (s, tuple) records --
+    over its own NCCL communicator for an nccl group (built once per group from a
+    broadcast ncclUniqueId), or through a host-staged gloo all-gather (tests).
+    `local_search(shard_rank, shard_count) -> [(s, tuple), ...]` replaces the GPU shard
+    search (CPU protocol tests); its records are merged by pt_merge_records."""
+    import torch
+    import torch.distributed as dist
+    init = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank(group) if init else 0
+    world = dist.get_world_size(group) if init else 1
+    if local_search is not None:        # CPU: marshal the records, gather, merge in C
+        L = pt_record_len(k)
+        rec = np.full(L, np.inf)
+        rec[0] = 0.0
+        for q, (sv, tup) in enumerate(local_search(rank, world)[:2]):
+            rec[1 + q] = sv
+            rec[3 + q * k:3 + (q + 1) * k] = tup
+        allr = [torch.empty(L, dtype=torch.float64) for _ in range(world)]
+        if world > 1:
+            dist.all_gather(allr, torch.from_numpy(rec), group=group)
+        else:
+            allr = [torch.from_numpy(rec)]
+        E = n_env if env_mask is None else int(np.count_nonzero(env_mask))
+        return pt_merge_records(torch.cat(allr).numpy(), k, E, objective)
+    if init and dist.get_backend(group) == "nccl":
+        return pt_exhaustive_best_sharded(ctx, k, rank, world, comm=_library_comm(group, rank, world),
+                                          env_mask=env_mask, objective=objective)
+
+    def host_allgather(mine, out, stream):      # gloo (or no group): host-staged
+        if world == 1:
+            with torch.cuda.stream(stream):
+                out.copy_(mine)
+            return
+        stream.synchronize()
+        parts = [torch.empty(mine.numel(), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, mine.cpu(), group=group)
+        with torch.cuda.stream(stream):
+            out.copy_(torch.cat(parts))
+    return pt_exhaustive_best_sharded(ctx, k, rank, world, allgather=host_allgather, env_mask=env_mask,
+                                      objective=objective)

@@ -14,7 +14,7 @@ from paper_2507_15277_b200 import pt
 
 def header_functions():
     src = open(os.path.join(ROOT, "include", "pt.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:pt_status|void|const char \*)\s*\**\s*(pt_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:pt_status|void|int32_t|const char \*)\s*\**\s*(pt_\w+)\s*\(",
                                  src, flags=re.M)))
 
 

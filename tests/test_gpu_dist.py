@@ -1,8 +1,10 @@
-"""The multi-GPU exhaustive path on a real GPU: a world-size-1 NCCL process
-group (all this box has) drives exhaustive_best_distributed end to end --
-shard search on the device, NCCL all-gather of the (s, tuple) records, merge
-with pt_merge_top2 -- and must equal the unsharded search.  The 2-rank protocol
-is covered by tests/test_dist.py (gloo, CPU)."""
+"""The multi-GPU exhaustive path on a real GPU, all through the C ABI:
+shard search on the device, the record exchange (NCCL over a communicator the
+library builds, or a caller's stream-ordered all-gather), the device merge and the
+objective transform in libpt.  A world-size-1 NCCL group (all this box has), two
+gloo processes sharing the GPU, and 8 thread-emulated ranks must each equal the
+unsharded search and the oracle.  The 2-rank protocol on CPU: tests/test_dist.py."""
+import threading
 import os
 import socket
 
@@ -111,3 +113,111 @@ def test_two_process_gloo_on_one_gpu():
         assert G == pytest.approx(want3["G"], rel=1e-12)
         assert idx == widx
         np.testing.assert_array_equal(np.array(gt), wgt)
+
+
+class _Gather:
+    """An in-process all-gather for thread-emulated ranks (one GPU): each rank's
+    device record is copied into every rank's output at its slot."""
+
+    def __init__(self, world):
+        self.world, self.bar, self.parts = world, threading.Barrier(world), [None] * world
+
+    def fn(self, r):
+        def gather(mine, out, stream):
+            stream.synchronize()
+            self.parts[r] = mine.clone()
+            self.bar.wait()
+            with torch.cuda.stream(stream):
+                out.copy_(torch.cat(self.parts))
+            self.bar.wait()
+        return gather
+
+
+def _emulate(T, dev, k, world, weights=None, objective=pt.PT_OBJ_GEOMEAN, fleet=None):
+    ctxs = [pt.pt_load_perf(T, dev) for _ in range(world)]
+    for r, c in enumerate(ctxs):
+        if weights is not None:
+            pt.pt_set_shard_weights(c, weights[r])
+        if fleet is not None:
+            pt.pt_set_fleet(c, *fleet)
+    g = _Gather(world)
+    res, errs = [None] * world, []
+
+    def body(r):
+        try:
+            res[r] = pt.pt_exhaustive_best_sharded(ctxs[r], k, r, world, allgather=g.fn(r), objective=objective)
+        except BaseException as e:
+            errs.append(e)
+            g.bar.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return res, errs
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_library_exchange_emulated_ranks(world):
+    """pt_exhaustive_best_sharded with `world` thread-emulated ranks: the device merge
+    and G = exp(-s/E) in the library equal the oracle on every rank."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    T, dev = synth.small_matrix(12, n_cfg=300, n_dev=3, n_inputs=16)
+    o = Oracle(T, dev)
+    for k in (2, 3):
+        b, gb, ru, gr = o.exhaustive(k)
+        res, errs = _emulate(T, dev, k, world)
+        assert not errs, errs
+        for r in res:
+            assert r["best"] == b and r["runner"] == ru
+            assert r["G"] == pytest.approx(gb, rel=1e-12) and r["G_runner"] == pytest.approx(gr, rel=1e-12)
+
+
+def test_library_exchange_fleet_objective():
+    """The sharded Eq. 2 search: records carry the cost 1/R, the library returns R."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    T, dev = synth.small_matrix(13, n_cfg=90, n_dev=3, n_inputs=8)
+    qd, qe = np.array([1.0, 2.0, 3.0]), np.linspace(1.0, 2.0, T.shape[0])
+    o = Oracle(T, dev)
+    o.set_fleet(qd, qe)
+    b, rb, ru, rr = o.fleet_exhaustive(2)
+    res, errs = _emulate(T, dev, 2, 4, objective=pt.PT_OBJ_FLEET, fleet=(qd, qe))
+    assert not errs, errs
+    for r in res:
+        assert r["best"] == b and r["G"] == pytest.approx(rb, rel=1e-12)
+
+
+def test_mismatched_shard_plans_are_an_error():
+    """ranks that deal the task list with different weights would skip or
+    repeat subsets; the plan fingerprint in the records turns that into PT_EINVAL."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    T, dev = synth.small_matrix(14, n_cfg=200, n_dev=2, n_inputs=16)
+    res, errs = _emulate(T, dev, 3, 2, weights=[[1.0, 1.0], [1.0, 3.0]])
+    assert len(errs) == 2 and all(isinstance(e, pt.PTError) and e.code == pt.PT_EINVAL for e in errs)
+    res, errs = _emulate(T, dev, 3, 2, weights=[[1.0, 3.0], [1.0, 3.0]])   # same weights: fine
+    assert not errs and res[0]["best"] == res[1]["best"] == Oracle(T, dev).exhaustive(3)[0]
+
+
+def test_library_nccl_comm_world1():
+    """pt_comm_unique_id + pt_comm_init without torch.distributed: the library's own
+    NCCL communicator (world 1) carries the record exchange."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    T, dev = synth.small_matrix(15, n_cfg=260, n_dev=2, n_inputs=16)
+    o = Oracle(T, dev)
+    comm = pt.pt_comm_init(pt.pt_comm_unique_id(), 0, 1, 0)
+    ctx = pt.pt_load_perf(torch.from_numpy(T).cuda(), dev)
+    for k in (2, 3):
+        r = pt.pt_exhaustive_best_sharded(ctx, k, 0, 1, comm=comm)
+        b, gb, ru, gr = o.exhaustive(k)
+        assert r["best"] == b and r["runner"] == ru and r["G"] == pytest.approx(gb, rel=1e-12)
+    with pytest.raises(pt.PTError) as ei:                 # rank/world must match the comm
+        pt.pt_exhaustive_best_sharded(ctx, 2, 0, 2, comm=comm)
+    assert ei.value.code == pt.PT_EINVAL
+    comm.close()
