@@ -9,10 +9,11 @@ of the whole hot path over that matrix:
   + pt_exhaustive_best k=2                    (1,574,425 sets)
   + pt_exhaustive_best k=3                    (930,485,175 sets)
   + pt_eval_holdout_all, 5 folds, greedy k=5  (88,655 sets)
-With N GPUs the exhaustive searches are sharded across ranks and merged with an
-NCCL all-gather of the (score, tuple) records (strong scaling: the job is fixed);
-every rank loads the matrix, greedy k=24 runs on rank 0 and the (batched,
-one-launch) holdout on rank 1 (both on rank 0 at N=1).
+With N GPUs the k=3 search is sharded across ranks and the library exchanges and
+merges the (score, tuple) records over its own NCCL communicator (strong scaling:
+the job is fixed); every rank loads the matrix, greedy k=24 runs on rank 0, the
+(batched, one-launch) holdout on rank 1 and the latency-bound k=2 search on rank 2
+(all on rank 0 at N=1), and those ranks take a smaller share of the k=3 tasks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {pt,reference}]
 """
@@ -397,13 +398,19 @@ def main():
     # those ranks take a correspondingly smaller share of the k=3 task list
     # (pt_set_shard_weights; extra work from DESIGN.md 6.4/6.8: ~0.24 and ~0.16 ms
     # against a k=3 search of ~12 ms on one GPU)
+    # exhaustive k=2 is latency-bound (1.6 M pairs = 13 us of ALU work on one GPU, one
+    # 32 us wave of 128x64 tiles): sharding it would cost every rank a full call for
+    # ~2 us of work each, so with N > 1 it runs unsharded on rank 2 (mod N); only the
+    # k=3 search (930 M triples) is sharded
     do_greedy = rank == 0
     do_holdout = rank == 1 % world
+    do_k2 = world == 1 or rank == 2 % world
     shard_w = None
     if world > 1:
         extra = [0.0] * world
         extra[0] += 0.24
         extra[1 % world] += 0.16
+        extra[2 % world] += 0.18
         shard_w = [max(0.2, 1.0 - x * world / 12.0) for x in extra]
 
     def step(src):
@@ -416,11 +423,10 @@ def main():
         if do_greedy:
             idx, gt, gp = pt.pt_greedy_select(ctx, K_GREEDY)
             d2h += idx.__len__() * 4 + gt.nbytes + gp.nbytes
-        r2 = pt.exhaustive_best_distributed(ctx, 2) if world > 1 else pt.pt_exhaustive_best(ctx, 2)
-        st = pt.pt_get_stats(ctx)
+        r2 = pt.pt_exhaustive_best(ctx, 2) if do_k2 else None
         r3 = pt.exhaustive_best_distributed(ctx, 3) if world > 1 else pt.pt_exhaustive_best(ctx, 3)
         st3 = pt.pt_get_stats(ctx)
-        d2h += 2 * (2 * 3 * 4 + 4 * 8)
+        d2h += (2 * 2 * 4 + 4 * 8 if do_k2 else 0) + 2 * 3 * 4 + 4 * 8
         if do_holdout:
             hold = pt.pt_eval_holdout_all(ctx, K_HOLDOUT, 5)      # all 5 folds, one batched launch
             d2h += len(hold) * (2 * K_HOLDOUT * 4 + 3 * 8)

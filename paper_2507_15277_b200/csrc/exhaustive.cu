@@ -24,7 +24,10 @@
 // k_exh_generic is the plain thread-per-subset fp64 kernel (k = 1, k > 4,
 // scopes wider than 384 envs, and the PT_EXACT_FP64 debug mode).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -1730,43 +1733,6 @@ __global__ void __launch_bounds__(256) k_tile_pp(const uint16_t *__restrict__ hT
 }
 
 // ---------------------------------------------------------------------------
-// fp64 refine of the survivors: warp per candidate, fixed shuffle tree
-// ---------------------------------------------------------------------------
-__global__ void k_exh_refine(const unsigned long long *__restrict__ key,
-                             const float *__restrict__ cs, const unsigned *__restrict__ n_dev, unsigned cap,
-                             float tau_pass, const unsigned *__restrict__ U, int m, int64_t C,
-                             const double *__restrict__ l64, int64_t E_pad,
-                             double *__restrict__ out_s, int32_t *__restrict__ out_t)
-{
-    // survivors = min(count, cap); final threshold = min(tau_pass, U) (the kernel's U
-    // is complete once this launch starts: stream order)
-    const int64_t n = min(*n_dev, cap);
-    const float tau = fminf(tau_pass, __uint_as_float(*U));
-    const int lane = threadIdx.x & 31;
-    const int k = m + 1;
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        int32_t tup[PT_MAXK];
-        const unsigned long long kv = key[w];
-        pt_unrank_colex((int64_t)(kv >> KEY_BITS), m, C, tup);
-        tup[m] = (int32_t)(kv & ((1ull << KEY_BITS) - 1));
-        if (lane < k) out_t[w * k + lane] = tup[lane];
-        if (cs[w] > tau) {
-            if (lane == 0) out_s[w] = INFINITY;
-            continue;
-        }
-        double acc = 0.0;
-        for (int64_t e = lane; e < E_pad; e += 32) {
-            double v = l64[(int64_t)tup[0] * E_pad + e];
-            for (int u = 1; u < k; u++) v = fmin(v, l64[(int64_t)tup[u] * E_pad + e]);
-            acc += v;
-        }
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) out_s[w] = acc;
-    }
-}
-
-// ---------------------------------------------------------------------------
 // top-2 over (s, tuple) records -- one CTA
 // ---------------------------------------------------------------------------
 struct Rec2 {
@@ -1825,6 +1791,96 @@ __global__ void __launch_bounds__(256) k_top2(const double *__restrict__ s, cons
     }
 }
 
+// fp64 refine of the survivors fused with their top-2: every block re-scores its
+// share (warp per candidate, the same fixed shuffle tree as k_exh_refine), keeps a
+// block top-2 and publishes it; the last block to finish (a counter it then resets)
+// merges the block records.  One launch instead of refine + k_top2.
+__global__ void __launch_bounds__(256) k_exh_refine_top2(
+    const unsigned long long *__restrict__ key, const float *__restrict__ cs, const unsigned *__restrict__ n_dev,
+    unsigned cap, float tau_pass, const unsigned *__restrict__ U, int m, int64_t C, const double *__restrict__ l64,
+    int64_t E_pad, Rec2 *__restrict__ blk, unsigned *__restrict__ done, double *__restrict__ out_s,
+    int32_t *__restrict__ out_t)
+{
+    const int64_t n = min(*n_dev, cap);
+    const float tau = fminf(tau_pass, __uint_as_float(*U));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = m + 1;
+    __shared__ Rec2 sh[256];
+    Rec2 r;
+    r.s1 = r.s2 = INFINITY;
+    for (int u = 0; u < PT_MAXK; u++) r.t1[u] = r.t2[u] = 0x7fffffff;
+    for (int64_t w = (int64_t)blockIdx.x * 8 + warp; w < n; w += (int64_t)gridDim.x * 8) {
+        int32_t tup[PT_MAXK];
+        const unsigned long long kv = key[w];
+        pt_unrank_colex((int64_t)(kv >> KEY_BITS), m, C, tup);
+        tup[m] = (int32_t)(kv & ((1ull << KEY_BITS) - 1));
+        if (cs[w] > tau) continue;
+        double acc = 0.0;
+        for (int64_t e = lane; e < E_pad; e += 32) {
+            double v = l64[(int64_t)tup[0] * E_pad + e];
+            for (int u = 1; u < k; u++) v = fmin(v, l64[(int64_t)tup[u] * E_pad + e]);
+            acc += v;
+        }
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) rec_offer(r, acc, tup, k);
+    }
+    sh[threadIdx.x] = r;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            Rec2 o = sh[threadIdx.x + w];
+            Rec2 me = sh[threadIdx.x];
+            rec_offer(me, o.s1, o.t1, k);
+            rec_offer(me, o.s2, o.t2, k);
+            sh[threadIdx.x] = me;
+        }
+        __syncthreads();
+    }
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        blk[blockIdx.x] = sh[0];
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    r.s1 = r.s2 = INFINITY;
+    for (int u = 0; u < PT_MAXK; u++) r.t1[u] = r.t2[u] = 0x7fffffff;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+        Rec2 o;   // L2 reads (other blocks' records; L1 is not coherent)
+        o.s1 = __ldcg(&blk[b].s1);
+        o.s2 = __ldcg(&blk[b].s2);
+        for (int u = 0; u < k; u++) {
+            o.t1[u] = __ldcg(&blk[b].t1[u]);
+            o.t2[u] = __ldcg(&blk[b].t2[u]);
+        }
+        rec_offer(r, o.s1, o.t1, k);
+        rec_offer(r, o.s2, o.t2, k);
+    }
+    sh[threadIdx.x] = r;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            Rec2 o = sh[threadIdx.x + w];
+            Rec2 me = sh[threadIdx.x];
+            rec_offer(me, o.s1, o.t1, k);
+            rec_offer(me, o.s2, o.t2, k);
+            sh[threadIdx.x] = me;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out_s[0] = sh[0].s1;
+        out_s[1] = sh[0].s2;
+        for (int u = 0; u < k; u++) {
+            out_t[u] = sh[0].t1[u];
+            out_t[k + u] = sh[0].t2[u];
+        }
+        *done = 0;   // ready for the next launch
+    }
+}
+
 // ---------------------------------------------------------------------------
 // generic fp64 thread-per-subset kernel: block -> its top-2 records
 // ---------------------------------------------------------------------------
@@ -1869,6 +1925,13 @@ __global__ void __launch_bounds__(256) k_exh_generic(const double *__restrict__ 
             blk_t[(2 * blockIdx.x + 1) * k + u] = sh[0].t2[u];
         }
     }
+}
+
+// the exhaustive search's threshold seeded from a device-resident greedy runner-up score
+// (rounded up, as f_up on the host path)
+__global__ void k_seed_U(const double *__restrict__ s2, unsigned *__restrict__ U)
+{
+    *U = __float_as_uint(__double2float_ru(*s2 * (1.0 + 1e-9) + 1e-30));
 }
 
 // one-CTA (s, tuple) top-2 over n records on the device -> host
@@ -1935,6 +1998,14 @@ static pt_status run_generic(pt_ctx *ctx, const pt_view *v, int k, int64_t r0, i
 static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_rank,
                            int32_t shard_count, double *s_out, int32_t *t_out)
 {
+    // PT_TRACE=1 (development): host timestamps of the call's phases on stderr
+    static const bool trace = getenv("PT_TRACE") != nullptr;
+    const auto t_entry = std::chrono::steady_clock::now();
+    auto mark = [&](const char *what) {
+        if (trace)
+            fprintf(stderr, "[pt k=%d] %-12s %8.1f us\n", k, what,
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_entry).count());
+    };
     cudaStream_t s = ctx->stream;
     const int m = k - 1;
     pt_tasks *T = nullptr;
@@ -2013,13 +2084,30 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     // (reused from an earlier greedy run of >= k steps on this view when there is one)
     // (a missing trace is computed for 4 steps -- the tiled kernel's largest k -- at once,
     // so a k=2 search followed by a k=3 one seeds both from one cooperative greedy launch)
-    if (v->greedy_s2.size() < (size_t)k) {
-        const int kg = (int)std::min<int64_t>(std::max(k, 4), v->C);
-        std::vector<int32_t> gidx(kg);
-        std::vector<double> gs1(kg), gs2(kg);
-        PT_TRY(pt_greedy_view(ctx, v, kg, gidx.data(), gs1.data(), gs2.data()));
+    // (development knob PT_EXH_SEED=none: no seed, the window starts at +inf and
+    // tightens only through the kernel's own U)
+    // Without a host trace the seed greedy is only enqueued: its runner-up trace stays on
+    // the device and a one-thread kernel writes the rounded-up seed into U before the
+    // search (U is itself an upper bound of s_(2), so min(seed, U) is one), no host
+    // round trip between the two.
+    static const bool no_seed = getenv("PT_EXH_SEED") && !strcmp(getenv("PT_EXH_SEED"), "none");
+    float tau_seed = INFINITY;
+    const double *seed_dev = nullptr;
+    if (!no_seed) {
+        if (v->greedy_s2.size() >= (size_t)k) {
+            tau_seed = f_up(v->greedy_s2[k - 1] * (1.0 + 1e-9) + 1e-30);
+        } else {
+            const int kg = (int)std::min<int64_t>(std::max(k, 3), v->C);   // a k=2 search leaves k=3's seed
+            if (v->d_seed_k < k && pt_greedy_seed_enqueue(ctx, v, kg) != PT_OK) {
+                std::vector<int32_t> gidx(kg);
+                std::vector<double> gs1(kg), gs2(kg);
+                PT_TRY(pt_greedy_view(ctx, v, kg, gidx.data(), gs1.data(), gs2.data()));
+                tau_seed = f_up(v->greedy_s2[k - 1] * (1.0 + 1e-9) + 1e-30);
+            } else {
+                seed_dev = v->d_seed_s2 + (k - 1);
+            }
+        }
     }
-    const float tau_seed = f_up(v->greedy_s2[k - 1] * (1.0 + 1e-9) + 1e-30);
 #if XT_MMA
     // tensor-summed kernel: fp16 terms u16 (the mins are exact fp16 values), then
     // E_pad/8 chained MMA accumulations, each assumed within 2^-18 relative of
@@ -2054,6 +2142,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
 
     if (v->E_pad % XT_K != 0)   // a stage must not straddle the padded env range
         return pt_fail(PT_EINVAL, "E_pad=%lld is not a multiple of the stage depth %d", (long long)v->E_pad, XT_K);
+    mark("seeded");
     PT_TRY(pt_view_fp16(ctx, v));
     if (!v->hTile) {
         pt_view *mv = const_cast<pt_view *>(v);
@@ -2099,7 +2188,22 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
                  sizeof(int4) + 2 * sizeof(int) * XT_S;
 #endif
     const int threads = XT_MMA ? XT_THREADS : ws ? XW_THREADS : XT_TTHREADS;
-    PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // per (kernel, smem) once per process: the attribute and the occupancy query
+    static std::mutex attr_mu;
+    static std::map<std::pair<const void *, size_t>, int> attr_occ;
+    int occ = 1;
+    {
+        std::lock_guard<std::mutex> g(attr_mu);
+        auto key = std::make_pair((const void *)kern, smem);
+        auto it = attr_occ.find(key);
+        if (it == attr_occ.end()) {
+            PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+            attr_occ[key] = occ;
+        } else {
+            occ = it->second;
+        }
+    }
 
     unsigned cap = 1u << 20;
     unsigned n_cand = 0;
@@ -2109,9 +2213,9 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
         const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)),
                      o_n = take(sizeof(unsigned)), o_key = take(sizeof(unsigned long long) * cap),
-                     o_cq = take(sizeof(float) * cap), o_rs = take(sizeof(double) * cap),
-                     o_rt = take(sizeof(int32_t) * (size_t)cap * k), o_os = take(sizeof(double) * 2),
-                     o_ot = take(sizeof(int32_t) * 2 * k);
+                     o_cq = take(sizeof(float) * cap),
+                     o_os = take(sizeof(double) * 2), o_ot = take(sizeof(int32_t) * 2 * k),
+                     o_blk = take(sizeof(Rec2) * (size_t)ctx->num_sms * 2), o_done = take(sizeof(unsigned));
         void *scr = nullptr;
         PT_TRY(pt_scratch(ctx, off, &scr));
         char *b = (char *)scr;
@@ -2119,13 +2223,21 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         unsigned *U = (unsigned *)(b + o_U), *cn = (unsigned *)(b + o_n);
         unsigned long long *ckey = (unsigned long long *)(b + o_key);
         float *cq = (float *)(b + o_cq);
-        double *rs = (double *)(b + o_rs), *os = (double *)(b + o_os);
-        int32_t *rt = (int32_t *)(b + o_rt), *ot = (int32_t *)(b + o_ot);
+        double *os = (double *)(b + o_os);
+        int32_t *ot = (int32_t *)(b + o_ot);
+        Rec2 *blk = (Rec2 *)(b + o_blk);
+        unsigned *done = (unsigned *)(b + o_done);
         const unsigned u_init = 0x7f800000u;   // +inf
         pt_hostio io(ctx);
         PT_TRY(io.h2d(ctr, &ta, sizeof(int)));
-        PT_TRY(io.h2d(U, &u_init, sizeof(unsigned)));
+        if (seed_dev) {
+            k_seed_U<<<1, 1, 0, s>>>(seed_dev, U);
+            ctx->stats.launches++;
+        } else {
+            PT_TRY(io.h2d(U, &u_init, sizeof(unsigned)));
+        }
         PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned), s));
+        PT_CK(cudaMemsetAsync(done, 0, sizeof(unsigned), s));
         XParams p;
         p.C = v->C;
         p.C_pad = v->C_pad;
@@ -2152,12 +2264,11 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         p.n_ct = v->n_ct;
         p.hC = v->hC;
         p.hPair = v->hPair;
-        int occ = 1;
-        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
         const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
 #if XT_PROBE
         PT_CK(cudaMemsetAsync(cq + cap - 8, 0, 32, s));
 #endif
+        mark("pre-launch");
         PT_CK(cudaEventRecord(ctx->ev0, s));
         kern<<<grid, threads, smem, s>>>(p);
         PT_CK(cudaEventRecord(ctx->ev1, s));
@@ -2165,10 +2276,10 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         PT_CK(cudaGetLastError());
         // refine + top-2 run on the device-side survivor count (no host round trip);
         // one synchronisation returns the count, U and the exact top-2
-        k_exh_refine<<<(unsigned)(ctx->num_sms * 8), 256, 0, s>>>(ckey, cq, cn, cap, tau_pass, U, m, v->C,
-                                                                  v->l64, v->E_pad, rs, rt);
-        k_top2<<<1, 256, 0, s>>>(rs, rt, 0, cn, cap, k, os, ot);
-        ctx->stats.launches += 2;
+        k_exh_refine_top2<<<(unsigned)(ctx->num_sms * 2), 256, 0, s>>>(ckey, cq, cn, cap, tau_pass, U, m, v->C,
+                                                                        v->l64, v->E_pad, blk, done, os, ot);
+        ctx->stats.launches++;
+        mark("launched");
         pt_pack_record(ctx, os, ot, k);   // sharded search: this rank's record stays on the device
         PT_CK(cudaGetLastError());
         unsigned hU = 0;
@@ -2177,6 +2288,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         PT_TRY(io.d2h(s_out, os, sizeof(double) * 2));
         PT_TRY(io.d2h(t_out, ot, sizeof(int32_t) * 2 * k));
         PT_TRY(io.finish());
+        mark("synced");
 #if XT_PROBE
         {
             unsigned long long w[4];

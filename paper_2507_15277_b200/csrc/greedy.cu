@@ -23,6 +23,8 @@
 #include <cmath>
 #include <vector>
 
+#include <map>
+#include <mutex>
 #include "pt_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -661,6 +663,55 @@ static bool use_stream(const pt_ctx *ctx, const pt_view *v)
     if (ctx->flags & (PT_GREEDY_STREAM | PT_GREEDY_LAZY)) return true;
     const double bytes = (double)v->C * (double)v->E_pad * 8.0;
     return bytes > 64.0 * (1 << 20) || v->E_pad * 8 > 160 * 1024;
+}
+
+pt_status pt_greedy_seed_enqueue(pt_ctx *ctx, const pt_view *v, int32_t k)
+{
+    if (k < 1 || k > v->C || use_stream(ctx, v)) return PT_EINVAL;   // caller takes the host path
+    const int64_t C = v->C, E_pad = v->E_pad;
+    const int64_t nwords = (C + 31) / 32;
+    cudaStream_t s = ctx->stream;
+    const size_t smem = sizeof(double) * E_pad + sizeof(uint32_t) * nwords;
+    static std::mutex mu;
+    static std::map<size_t, int> occ_cache;   // dynamic smem -> blocks per SM
+    int occ = 0;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = occ_cache.find(smem);
+        if (it == occ_cache.end()) {
+            if (smem > 48 * 1024)
+                PT_CK(cudaFuncSetAttribute(k_greedy_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+            PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_resident, 256, smem));
+            occ_cache[smem] = occ;
+        } else {
+            occ = it->second;
+        }
+    }
+    if (occ < 1) return PT_EINVAL;
+    const int nblk = ctx->num_sms * std::min(occ, GR_BPS);
+    pt_view *mv = const_cast<pt_view *>(v);
+    if (mv->d_seed_s2) pt_dfree(ctx, mv->d_seed_s2);
+    mv->d_seed_s2 = nullptr;
+    mv->d_seed_k = 0;
+    PT_TRY(pt_dalloc(ctx, (void **)&mv->d_seed_s2, sizeof(double) * k));
+    char *tmp = nullptr;
+    const size_t o_idx = pt_round_up(sizeof(double4) * 2 * nblk, 256) + 256;
+    const size_t o_s1 = o_idx + pt_round_up(sizeof(int32_t) * k, 256);
+    PT_TRY(pt_dalloc(ctx, (void **)&tmp, o_s1 + pt_round_up(sizeof(double) * k, 256)));
+    double4 *blk = (double4 *)tmp;
+    int32_t *d_idx = (int32_t *)(tmp + o_idx);
+    double *d_s1 = (double *)(tmp + o_s1), *d_s2 = mv->d_seed_s2;
+    const double *l64 = v->l64;
+    int kk = k;
+    int64_t CC = C, EE = E_pad;
+    void *args[] = {(void *)&l64, (void *)&CC, (void *)&EE, (void *)&kk, (void *)&blk,
+                    (void *)&d_idx, (void *)&d_s1, (void *)&d_s2};
+    PT_CK(cudaLaunchCooperativeKernel((void *)k_greedy_resident, dim3(nblk), dim3(256), args, smem, s));
+    ctx->stats.launches++;
+    pt_dfree(ctx, tmp);   // stream-ordered: released after the kernel
+    mv->d_seed_k = k;
+    return PT_OK;
 }
 
 pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_idx,

@@ -20,6 +20,10 @@
 
 #include <cuda_fp16.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <climits>
 #include "pt_internal.cuh"
 
 static thread_local std::string g_err;
@@ -156,6 +160,7 @@ void pt_view_free(pt_ctx *ctx, pt_view &v)
         pt_dfree(ctx, v.hC);
         pt_dfree(ctx, v.hPair);
     }
+    pt_dfree(ctx, v.d_seed_s2);   // allocated per view object (owned or not)
     v = pt_view();
 }
 
@@ -215,11 +220,40 @@ __global__ void k_rowstats(const float *__restrict__ T, int64_t C, double *__res
 
 // 32x32 tiles: read T[e][c] coalesced along c, write l64/l32[c][e] through a
 // shared transpose (coalesced along e).
+// dataset penalty (the largest measured slowdown, >= 1) and the first
+// environment whose status is bad (bit 1: a runtime <= 0, bit 2: no measured cell),
+// computed on the device so the load needs one host round trip, at its end
+__global__ void k_penalty(const double *__restrict__ rowmax, const int *__restrict__ status, int64_t E,
+                          double *__restrict__ pen, long long *__restrict__ bad)
+{
+    __shared__ double smax[256];
+    __shared__ long long sbad;
+    if (threadIdx.x == 0) sbad = LLONG_MAX;
+    __syncthreads();
+    double m = 1.0;
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+        m = fmax(m, rowmax[e]);
+        if (status[e]) atomicMin(&sbad, (long long)e);
+    }
+    smax[threadIdx.x] = m;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *pen = smax[0];
+        bad[0] = sbad;
+        bad[1] = sbad == LLONG_MAX ? 0 : status[sbad];
+    }
+}
+
 __global__ void k_ell(const float *__restrict__ T, int64_t E, int64_t C,
-                      const double *__restrict__ best, double penalty, int64_t E_pad,
+                      const double *__restrict__ best, const double *__restrict__ pen, int64_t E_pad,
                       float *__restrict__ l32, double *__restrict__ l64)
 {
     __shared__ double tile[32][33];
+    const double penalty = *pen;
     const int64_t c0 = (int64_t)blockIdx.x * 32, e0 = (int64_t)blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
     for (int r = ty; r < 32; r += 8) {
@@ -374,6 +408,13 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
                                   uint32_t flags, int cuda_device, void *cuda_stream)
 {
     PT_NVTX();
+    static const bool trace = getenv("PT_TRACE") != nullptr;
+    const auto t_entry = std::chrono::steady_clock::now();
+    auto mark = [&](const char *what) {
+        if (trace)
+            fprintf(stderr, "[pt load] %-12s %8.1f us\n", what,
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_entry).count());
+    };
     if (!out) return pt_fail(PT_EINVAL, "out is NULL");
     *out = nullptr;
     if (!times_ms || n_env < 1 || n_cfg < 1 || ld < n_cfg)
@@ -406,6 +447,7 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
     if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess)
         return bail(pt_fail(PT_ECUDA, "cudaEventCreate failed"));
 
+    mark("ctx");
     const int64_t E = n_env, C = n_cfg;
     keep_pool(cuda_device);
     float *dT = nullptr;
@@ -434,45 +476,43 @@ extern "C" pt_status pt_load_perf(pt_ctx **out, const float *times_ms, int64_t n
         return bail(pt_fail(PT_ECUDA, "copy of the runtime matrix failed: %s",
                             cudaGetErrorString(cudaGetLastError())));
     }
+    mark("copied");
     k_rowstats<<<(unsigned)E, 256, 0, ctx->stream>>>(dT, C, ctx->best, rowmax, status);
-    ctx->stats.launches++;
-    std::vector<double> h_rowmax(E);
-    std::vector<int> h_status(E);
-    pt_hostio io(ctx);
-    if (io.d2h(h_rowmax.data(), rowmax, sizeof(double) * E) != PT_OK ||
-        io.d2h(h_status.data(), status, sizeof(int) * E) != PT_OK || io.finish() != PT_OK) {
+    double *d_pen = nullptr;
+    long long *d_bad = nullptr;
+    if (pt_dalloc(ctx, (void **)&d_pen, 256 + 2 * sizeof(long long)) != PT_OK) {
         cleanup();
-        return bail(pt_fail(PT_ECUDA, "load: %s", cudaGetErrorString(cudaGetLastError())));
+        return bail(pt_fail(PT_ENOMEM, "device allocation failed"));
     }
-    double pen = 1.0;
-    for (int64_t e = 0; e < E; e++) {
-        if (h_status[e] & 1) {
-            cleanup();
-            return bail(pt_fail(PT_EDATA, "environment %lld has a runtime <= 0", (long long)e));
-        }
-        if (h_status[e] & 2) {
-            cleanup();
-            return bail(pt_fail(PT_EDATA, "environment %lld has no measured cell", (long long)e));
-        }
-        pen = std::max(pen, h_rowmax[e]);
-    }
-    ctx->penalty = pen;
+    d_bad = (long long *)((char *)d_pen + 256);
+    k_penalty<<<1, 256, 0, ctx->stream>>>(rowmax, status, E, d_pen, d_bad);
+    ctx->stats.launches += 2;
     pt_status st = alloc_view(ctx, ctx->full, E, C);
     if (st != PT_OK) {
         cleanup();
+        pt_dfree(ctx, d_pen);
         return bail(st);
     }
     pt_view &v = ctx->full;
     dim3 grid((unsigned)((C + 31) / 32), (unsigned)((v.E_pad + 31) / 32));
-    k_ell<<<grid, dim3(32, 8), 0, ctx->stream>>>(dT, E, C, ctx->best, pen, v.E_pad, v.l32, v.l64);
+    k_ell<<<grid, dim3(32, 8), 0, ctx->stream>>>(dT, E, C, ctx->best, d_pen, v.E_pad, v.l32, v.l64);
     ctx->stats.launches++;
     // keep the runtimes (env-major fp32) for objectives on raw times (Eq. 2)
     ctx->T32 = dT;
     pt_dfree(ctx, rowmax);
     pt_dfree(ctx, status);
-    cudaError_t ce = cudaStreamSynchronize(ctx->stream);
-    if (ce != cudaSuccess || cudaGetLastError() != cudaSuccess)
-        return bail(pt_fail(PT_ECUDA, "normalise kernel failed: %s", cudaGetErrorString(ce)));
+    mark("launched");
+    double pen = 1.0;
+    long long bad[2] = {0, 0};
+    pt_hostio io(ctx);
+    if (io.d2h(&pen, d_pen, sizeof(double)) != PT_OK || io.d2h(bad, d_bad, sizeof bad) != PT_OK ||
+        io.finish() != PT_OK || cudaGetLastError() != cudaSuccess)
+        return bail(pt_fail(PT_ECUDA, "load: %s", cudaGetErrorString(cudaGetLastError())));
+    mark("synced");
+    pt_dfree(ctx, d_pen);
+    if (bad[1] & 1) return bail(pt_fail(PT_EDATA, "environment %lld has a runtime <= 0", bad[0]));
+    if (bad[1] & 2) return bail(pt_fail(PT_EDATA, "environment %lld has no measured cell", bad[0]));
+    ctx->penalty = pen;
     *out = ctx;
     return PT_OK;
 }

@@ -70,6 +70,11 @@ struct pt_view {
     // deterministic and prefix-consistent, so a k-step run answers every k' <= k):
     // the exhaustive search reads its seed (runner-up score at step k) from here
     mutable std::vector<double> greedy_s2;
+    // the same runner-up trace left on the device by a seed-only greedy launch
+    // (pt_greedy_seed_enqueue): the exhaustive search seeds its threshold from it
+    // without a host round trip.  d_seed_k = steps it holds (0 = none).
+    double *d_seed_s2 = nullptr;
+    int d_seed_k = 0;
 };
 
 struct pt_tasks;  // exhaustive work list (exhaustive.cu)
@@ -155,6 +160,9 @@ bool pt_is_device_ptr(const void *p);
 // selection entry points used across files
 pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_idx,
                          double *s1_trace, double *s2_trace);
+// enqueue a resident greedy of k steps on ctx->stream whose runner-up trace stays on the
+// device (v->d_seed_s2); PT_EINVAL if this view takes the streamed greedy instead
+pt_status pt_greedy_seed_enqueue(pt_ctx *ctx, const pt_view *v, int32_t k);
 pt_status pt_exhaustive_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t shard_rank,
                              int32_t shard_count, int32_t *best, int32_t *runner,
                              double *s_out, int *n_found);

@@ -1,0 +1,1 @@
+PT_TRACE=1 timeout 300 python tools/trace_rank.py > gpurun_out/r2j.txt 2>&1

@@ -25,10 +25,12 @@ for N in (1, 2, 4, 8):
                 extra = [0.0] * N
                 extra[0] += 0.24
                 extra[1 % N] += 0.16
+                extra[2 % N] += 0.18
                 pt.pt_set_shard_weights(ctx, [max(0.2, 1.0 - x * N / 12.0) for x in extra])
             if r == 0:
                 pt.pt_greedy_select(ctx, 24)
-            pt.pt_exhaustive_best(ctx, 2, shard_rank=r, shard_count=N)
+            if N == 1 or r == 2 % N:      # k=2 unsharded on one rank (bench.py)
+                pt.pt_exhaustive_best(ctx, 2)
             pt.pt_exhaustive_best(ctx, 3, shard_rank=r, shard_count=N)
             if r == 1 % N:
                 pt.pt_eval_holdout_all(ctx, 5, 5)
