@@ -1,6 +1,7 @@
-"""The opt-in kernel variants DESIGN.md reports measurements for still compile for
-sm_100a (no GPU needed: nvcc cross-compiles).  Each is built in its own process,
-in parallel, as an object file of exhaustive.cu only."""
+"""The kernel variants DESIGN.md reports measurements for (rejected, so archived in
+tools/r1_variants/ and tools/exh_tc/, not part of libpt.so) still compile for sm_100a
+against the library's headers (no GPU needed: nvcc cross-compiles).  Each is built in
+its own process, in parallel, as an object file."""
 import os
 import shutil
 import subprocess
@@ -10,7 +11,9 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SRC = os.path.join(ROOT, "paper_2507_15277_b200", "csrc", "exhaustive.cu")
+SRC = os.path.join(ROOT, "tools", "r1_variants", "exhaustive_variants.cu")
+TC_SRC = os.path.join(ROOT, "tools", "exh_tc", "exh_tc.cu")
+CSRC = os.path.join(ROOT, "paper_2507_15277_b200", "csrc")
 
 VARIANTS = {
     "tensor_summed_mma": ["-DXT_MMA=1"],
@@ -23,6 +26,7 @@ VARIANTS = {
     "wait_backoff": ["-DXT_WAITNS=256"],
     "probe": ["-DXT_PROBE=2"],
     "shape_4x8": ["-DXT_SHAPE48=1"],
+    "archived_default": [],
 }
 
 
@@ -33,9 +37,13 @@ def test_opt_in_variants_compile():
         procs = {}
         for name, flags in VARIANTS.items():
             cmd = [nvcc, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
-                   "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-c", SRC,
+                   "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr", "-c", SRC,
                    "-o", os.path.join(tmp, name + ".o")] + flags
             procs[name] = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+        procs["tcgen05_summed"] = subprocess.Popen(
+            [nvcc, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+             "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "--expt-relaxed-constexpr", "-c", TC_SRC,
+             "-o", os.path.join(tmp, "tc.o")], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
         failed = {}
         for name, p in procs.items():
             out, _ = p.communicate(timeout=600)

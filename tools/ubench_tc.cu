@@ -10,6 +10,9 @@
 #include <cstring>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
+#include <cmath>
+#include <vector>
+#include <algorithm>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e_)); exit(1); } } while (0)
 
@@ -357,6 +360,81 @@ static void run_mma3()
            M, N, NW, (double)mx / (8.0 * n_iter * NW), f, (double)M * 16 * 8.0 * n_iter * NW / mx);
 }
 
+// ---------------------------------------------------------------- accumulation accuracy
+// 160 chained M=128 N=8 K=16 MMAs (A from TMEM, f16 inputs, f32 accumulate, B = pair
+// selector B[k][n] = (k/2 == n)): D[m][n] = sum over steps of A[m][2n] + A[m][2n+1].
+// Host compares with the exact (double) sums.
+__global__ void k_acc(const uint16_t *A /*[steps][128][16]*/, int steps, float *D /*[128][8]*/, int *flag)
+{
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(128) uint16_t Bs[16 * 8];
+    const int t = threadIdx.x, w = t >> 5;
+    if (w == 0) tm_alloc(&tbase, 32);
+    if (t == 0) bar_init(&bar, 1);
+    for (int i = t; i < 16 * 8; i += 128) {
+        const int k = i / 8, n = i % 8;
+        Bs[((k >> 3) * 128 + n * 16 + (k & 7) * 2) / 2] = (k / 2 == n) ? 0x3C00 : 0;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    fence_before(); __syncthreads(); fence_after();
+    const uint32_t tb = tbase, lane_off = (uint32_t)(32 * (w & 3)) << 16;
+    const uint64_t bd = sdesc(su32(Bs), 128, 256);
+    for (int q = 0; q < steps; q++) {
+        uint32_t v[8];
+        for (int j = 0; j < 8; j++) v[j] = (uint32_t)A[(q * 128 + t) * 16 + 2 * j] | ((uint32_t)A[(q * 128 + t) * 16 + 2 * j + 1] << 16);
+        st8(tb + lane_off + 16, v);
+        wait_st();
+        fence_before(); __syncthreads(); fence_after();
+        if (t == 0) { mma_ts(tb, tb + 16, bd, idesc_f16(128, 8), q > 0); commit(&bar); }
+        __syncwarp();
+        if (!bar_wait(&bar, q & 1)) atomicExch(flag, 1);
+        fence_after();
+    }
+    uint32_t r[8];
+    ld8(tb + lane_off, r);
+    wait_ld();
+    for (int j = 0; j < 8; j++) D[t * 8 + j] = __uint_as_float(r[j]);
+    fence_before(); __syncthreads();
+    if (w == 0) tm_free(tb, 32);
+}
+
+static int run_acc()
+{
+    const int steps = 160;
+    std::vector<uint16_t> hA((size_t)steps * 128 * 16);
+    std::vector<double> exact(128 * 8, 0.0);
+    uint64_t x = 88172645463325252ull;
+    auto rnd = [&]() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; };
+    for (int q = 0; q < steps; q++)
+        for (int m = 0; m < 128; m++)
+            for (int k = 0; k < 16; k++) {
+                // log-uniform magnitudes over 2^-16 .. 2^4 (fp16 subnormals included)
+                const double u = (double)(rnd() >> 11) / 9007199254740992.0;
+                float f = (float)std::exp2(-16.0 + 20.0 * u);
+                uint16_t hb = h(f);
+                __half hh; memcpy(&hh, &hb, 2);
+                hA[((size_t)q * 128 + m) * 16 + k] = hb;
+                exact[m * 8 + k / 2] += (double)__half2float(hh);
+            }
+    uint16_t *dA; float *dD; int *flag, f;
+    float got[128 * 8];
+    CK(cudaMalloc(&dA, hA.size() * 2)); CK(cudaMalloc(&dD, sizeof got)); CK(cudaMalloc(&flag, 4));
+    CK(cudaMemcpy(dA, hA.data(), hA.size() * 2, cudaMemcpyHostToDevice)); CK(cudaMemset(flag, 0, 4));
+    k_acc<<<1, 128>>>(dA, steps, dD, flag);
+    CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(got, dD, sizeof got, cudaMemcpyDeviceToHost)); CK(cudaMemcpy(&f, flag, 4, cudaMemcpyDeviceToHost));
+    double worst = 0, bias = 0;
+    for (int i = 0; i < 128 * 8; i++) {
+        const double rel = ((double)got[i] - exact[i]) / exact[i];
+        worst = std::max(worst, std::fabs(rel));
+        bias += rel;
+    }
+    printf("acc: %d chained MMAs, worst relative error %.3e (= %.2f x 2^-24 per step), mean %.3e, timeout=%d\n",
+           steps, worst, worst / steps / std::ldexp(1.0, -24), bias / (128 * 8), f);
+    return 0;
+}
+
 int main(int argc, char **argv)
 {
     if (argc < 2) { printf("usage: check N | sttm W X | mma M N\n"); return 2; }
@@ -368,5 +446,6 @@ int main(int argc, char **argv)
         run_mma2<128, 8, 1>(); run_mma2<128, 8, 4>(); run_mma2<128, 8, 8>(); run_mma2<128, 16, 1>(); run_mma2<128, 16, 4>();
         run_mma2<128, 64, 4>(); run_mma2<128, 256, 1>(); run_mma2<64, 8, 8>(); run_mma2<64, 16, 8>(); return 0; }
     if (!strcmp(argv[1], "mma3")) { run_mma3<128, 8, 1>(); run_mma3<128, 8, 2>(); run_mma3<128, 8, 4>(); run_mma3<128, 16, 2>(); run_mma3<128, 32, 2>(); return 0; }
+    if (!strcmp(argv[1], "acc")) return run_acc();
     return 2;
 }
