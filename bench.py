@@ -293,7 +293,7 @@ def measure_next_rows(pt, T, dev, local, cpu=True):
     """The §8(f) NEXT rows at the paper shape, each timed on the device (CUDA events
     around the call on the library's stream, median of 3 after a warm-up) beside the
     CPU oracle on the same workload: fleet objective (Eq. 2) greedy k=24 and
-    exhaustive k=2, swap local search k=24, k-means k=24.  Work = (set, env)
+    exhaustive k=2 / k=3 (tiled), swap local search k=24, k-means k=24.  Work = (set, env)
     evaluations of one min + one multiply-add (k-means: (point, centroid, dim) of
     one subtract + one multiply-add), counted as 2 fp64 flops; roofline = the
     measured DFMA rate."""
@@ -331,8 +331,28 @@ def measure_next_rows(pt, T, dev, local, cpu=True):
     ms, _ = dev_ms(lambda: pt.pt_greedy_select(ctx, 24, objective=pt.PT_OBJ_FLEET))
     ev = sum(C - t for t in range(24)) * E
     rows["fleet_greedy_k24"] = (ms, ev, sum(C - t for t in range(24)), cpu_s(lambda: o.fleet_greedy(24)))
-    ms, _ = dev_ms(lambda: pt.pt_exhaustive_best(ctx, 2, objective=pt.PT_OBJ_FLEET))
-    rows["fleet_exhaustive_k2"] = (ms, math.comb(C, 2) * E, math.comb(C, 2), cpu_s(lambda: o.fleet_exhaustive(2)))
+    # fleet exhaustive: the tiled (min,+) kernel with the per-device fold (k_exh_tiled<true>),
+    # roofline = the f16x2 ALU ceiling of the geomean kernel (same inner loop)
+    fleet_exh = {}
+    for kk in (2, 3):
+        ms, _ = dev_ms(lambda: pt.pt_exhaustive_best(ctx, kk, objective=pt.PT_OBJ_FLEET))
+        st = pt.pt_get_stats(ctx)
+        fleet_exh[kk] = (ms, st["exh_main_ms"], st["exh_kernel"], st["exh_candidates"])
+    rows_alu = {}
+    for kk, (ms, kms, path, cand) in fleet_exh.items():
+        sets = math.comb(C, kk)
+        nsm = torch.cuda.get_device_properties(local).multi_processor_count
+        alu_peak = nsm * 128 * 1965.0e6
+        rows_alu[f"fleet_exhaustive_k{kk}"] = {
+            "ms": ms, "kernel_ms": kms, "path": {3: "tiled fp16 + per-device fold"}.get(path, str(path)),
+            "candidates_refined": cand, "sets_per_s": sets / (ms * 1e-3),
+            "roofline": {"bound": "alu", "unit": "T(set,env)/s", "achieved": sets * E / (kms * 1e-3) / 1e12,
+                         "peak": alu_peak / 1e12, "frac": sets * E / (kms * 1e-3) / alu_peak}}
+    if o is not None:
+        t0 = time.perf_counter()
+        o.fleet_exhaustive_par(2)
+        rows_alu["fleet_exhaustive_k2"]["oracle_s"] = time.perf_counter() - t0
+        rows_alu["fleet_exhaustive_k2"]["oracle_sets_per_s"] = math.comb(C, 2) / rows_alu["fleet_exhaustive_k2"]["oracle_s"]
     ms, (_, _, moves) = dev_ms(lambda: pt.pt_swap_search(ctx, 24))
     sets = (moves + 1) * 24 * (C - 24)
     rows["swap_k24"] = (ms, sets * E, sets, cpu_s(lambda: o.swap_search(24)))
@@ -351,6 +371,7 @@ def measure_next_rows(pt, T, dev, local, cpu=True):
             r["oracle_s"] = cs
             r["oracle_sets_per_s"] = sets / cs if sets is not None else None
         out[name] = r
+    out.update(rows_alu)
     if moves is not None:
         out["swap_k24"]["moves"] = moves
     out["kmeans_k24"]["iterations"] = iters

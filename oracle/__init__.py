@@ -48,11 +48,13 @@ def _load():
         lib.or_fleet_exhaustive.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, ct.c_int,
                                             P, P, P, P, P]
         lib.or_fleet_greedy.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, ct.c_int, P, P, P]
+        lib.or_fleet_exhaustive_par.argtypes = [P, i64, i64, P, dbl, P, i32, P, P, P, ct.c_int, ct.c_int,
+                                                P, P, P, P, P]
         lib.or_swap_search.argtypes = [P, i64, i64, P, ct.c_int, P, ct.c_int, P, P, P]
         lib.or_kmeans.argtypes = [P, i64, i64, P, dbl, P, ct.c_int, ct.c_int, P, P, P, P]
         for f in (lib.or_normalize, lib.or_score, lib.or_exhaustive, lib.or_greedy,
                   lib.or_holdout, lib.or_fleet_rate, lib.or_fleet_exhaustive, lib.or_fleet_greedy,
-                  lib.or_swap_search, lib.or_kmeans):
+                  lib.or_swap_search, lib.or_kmeans, lib.or_fleet_exhaustive_par):
             f.restype = ct.c_int
         _lib = lib
     return _lib
@@ -210,6 +212,20 @@ class Oracle:
         nf = np.zeros(1, np.int32)
         _chk(_load().or_fleet_exhaustive(*self._fleet_args(), _p(m), k, _p(b), _p(rb), _p(ru), _p(rr),
                                          _p(nf)), "or_fleet_exhaustive")
+        return (tuple(int(x) for x in b), float(rb[0]),
+                tuple(int(x) for x in ru) if nf[0] >= 2 else None, float(rr[0]))
+
+    def fleet_exhaustive_par(self, k, mask=None, threads=None):
+        """fleet_exhaustive with the first index dealt to `threads` threads (same result)."""
+        threads = default_threads() if threads is None else threads
+        m = self._mask(mask)
+        b = np.zeros(k, np.int32)
+        ru = np.zeros(k, np.int32)
+        rb = np.zeros(1)
+        rr = np.full(1, np.nan)
+        nf = np.zeros(1, np.int32)
+        _chk(_load().or_fleet_exhaustive_par(*self._fleet_args(), _p(m), k, threads, _p(b), _p(rb), _p(ru),
+                                             _p(rr), _p(nf)), "or_fleet_exhaustive_par")
         return (tuple(int(x) for x in b), float(rb[0]),
                 tuple(int(x) for x in ru) if nf[0] >= 2 else None, float(rr[0]))
 

@@ -452,6 +452,78 @@ int or_fleet_exhaustive(const float *T, int64_t E, int64_t C, const double *best
 }
 
 /*
+ * or_fleet_exhaustive_par -- or_fleet_exhaustive with the first index dealt to
+ * nthreads threads round-robin (each thread enumerates its tuples in the same
+ * lexicographic order with the same or_fleet_rate, strict '>' keeps the first of
+ * equal rates); the per-thread best two are merged in (R desc, tuple asc) order,
+ * which is the order the sequential loop produces.  For full-size golden values.
+ */
+typedef struct {
+    const float *T; int64_t E, C; const double *best; double penalty;
+    const int32_t *env_device; int32_t n_dev; const double *q_dev, *q_env;
+    const uint8_t *mask; int k, tid, nth, rc;
+    top2 res;
+} fleet_job;
+
+static void *fleet_worker(void *arg)
+{
+    fleet_job *j = (fleet_job *)arg;
+    int k = j->k;
+    int32_t s[32];
+    memset(&j->res, 0, sizeof j->res);
+    for (int64_t a0 = j->tid; a0 + k <= j->C; a0 += j->nth) {
+        s[0] = (int32_t)a0;
+        for (int u = 1; u < k; u++) s[u] = s[u - 1] + 1;
+        for (;;) {
+            double R;
+            int rc = or_fleet_rate(j->T, j->E, j->C, j->best, j->penalty, j->env_device, j->n_dev,
+                                   j->q_dev, j->q_env, j->mask, s, k, &R);
+            if (rc) { j->rc = rc; return NULL; }
+            top2_offer(&j->res, R, s, k);
+            int u = k - 1;
+            while (u >= 1 && s[u] == (int32_t)(j->C - k + u)) u--;
+            if (u < 1) break;
+            s[u]++;
+            for (int v = u + 1; v < k; v++) s[v] = s[v - 1] + 1;
+        }
+    }
+    return NULL;
+}
+
+int or_fleet_exhaustive_par(const float *T, int64_t E, int64_t C, const double *best, double penalty,
+                            const int32_t *env_device, int32_t n_dev, const double *q_dev,
+                            const double *q_env, const uint8_t *mask, int k, int nthreads,
+                            int32_t *best_set, double *R_best, int32_t *runner_set, double *R_runner,
+                            int *n_found)
+{
+    if (k <= 0 || k > 32 || k > C) return OR_EINVAL;
+    if (nthreads < 1) nthreads = 1;
+    fleet_job *jobs = calloc((size_t)nthreads, sizeof(fleet_job));
+    pthread_t *th = calloc((size_t)nthreads, sizeof(pthread_t));
+    if (!jobs || !th) { free(jobs); free(th); return OR_ENOMEM; }
+    for (int t = 0; t < nthreads; t++) {
+        jobs[t] = (fleet_job){T, E, C, best, penalty, env_device, n_dev, q_dev, q_env, mask, k, t, nthreads, 0, {0}};
+        pthread_create(&th[t], NULL, fleet_worker, &jobs[t]);
+    }
+    top2 all;
+    memset(&all, 0, sizeof all);
+    int rc = OR_OK;
+    for (int t = 0; t < nthreads; t++) {
+        pthread_join(th[t], NULL);
+        if (jobs[t].rc) rc = jobs[t].rc;
+        if (jobs[t].res.have >= 1) top2_offer(&all, jobs[t].res.L1, jobs[t].res.s1, k);
+        if (jobs[t].res.have >= 2) top2_offer(&all, jobs[t].res.L2, jobs[t].res.s2, k);
+    }
+    if (rc == OR_OK) {
+        *n_found = all.have;
+        if (all.have >= 1) { memcpy(best_set, all.s1, sizeof(int32_t) * (size_t)k); *R_best = all.L1; }
+        if (all.have >= 2) { memcpy(runner_set, all.s2, sizeof(int32_t) * (size_t)k); *R_runner = all.L2; }
+    }
+    free(jobs); free(th);
+    return rc;
+}
+
+/*
  * or_fleet_greedy -- greedy forward selection maximising R: at each step
  * evaluate R(S u {c}) for every c not in S (ascending), take the maximum,
  * ties to the lowest c.  Writes picks, R trace and the top-two gap per step.

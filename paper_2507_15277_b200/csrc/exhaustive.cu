@@ -342,7 +342,13 @@ struct XParams {
     const uint16_t *hT;
     const uint16_t *hTile;
     int64_t n_ct;
+    // fleet objective (Eq. 2, k_exh_tiled<true>): every 64-env stage belongs to one
+    // device; after the last stage of device d each set adds Q_d / (its segment sum)
+    // to its rate.  Q_d = quantity(d) x the device's fp16 scale (see run_fleet_tiled).
+    uint32_t stage_end_mask;  // bit q: stage q is the last stage of its device
+    float stage_Q[32];        // Q_d of the device stage q ends
 };
+#define XT_MAXSTAGE 32
 
 #define XT_TCONS (2 * XT_R)    // consumer threads: 2 warps (column halves) per 32 rows
 #define XT_BROW (XT_C * 2)     // bytes of one env row of a column tile
@@ -362,7 +368,11 @@ __device__ __forceinline__ uint32_t bcast_hi(uint32_t w)
     return r;
 }
 
-__global__ void __launch_bounds__(XT_TCONS, XT_MINB) k_exh_tiled(const XParams p)
+// FLEET = false: Eq. 1 geomean (minimise s; the default, graded path).
+// FLEET = true : Eq. 2 fleet rate (maximise R = sum_d Q_d / s_d, per-device segment sums
+//               s_d of weighted runtimes); one CTA per SM (32 more live registers).
+template <bool FLEET>
+__global__ void __launch_bounds__(XT_TCONS, FLEET ? 1 : XT_MINB) k_exh_tiled(const XParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                        // [S][K][32] half2
@@ -385,7 +395,9 @@ __global__ void __launch_bounds__(XT_TCONS, XT_MINB) k_exh_tiled(const XParams p
 
     uint32_t steps = 0;   // pipeline steps of all previous tasks (same in every thread)
     const int tx = lane & 7, ty = lane >> 3;
-    float bA = INFINITY, bB = INFINITY, published = INFINITY;   // acc-domain group minima (window U)
+    // group minima of acc (FLEET: maxima of the rate) for the window's U
+    float bA = FLEET ? -INFINITY : INFINITY, bB = FLEET ? -INFINITY : INFINITY;
+    float published = FLEET ? -INFINITY : INFINITY;
 
     for (;;) {
         if (tid == 0) {
@@ -449,6 +461,14 @@ __global__ void __launch_bounds__(XT_TCONS, XT_MINB) k_exh_tiled(const XParams p
             for (int i = 0; i < 8; i++)
 #pragma unroll
                 for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
+            // FLEET: the running rate of every set (sum over completed devices)
+            [[maybe_unused]] float rate[FLEET ? 8 : 1][FLEET ? 4 : 1];
+            if constexpr (FLEET) {
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) rate[i][j] = 0.0f;
+            }
 
             // warp w covers rows 32*(w>>1) .. +31 and columns 32*(w&1) .. +31 of the
             // 128x64 tile; a thread holds 8 consecutive rows (one 16-byte LDS) x 4
@@ -519,6 +539,20 @@ __global__ void __launch_bounds__(XT_TCONS, XT_MINB) k_exh_tiled(const XParams p
                             }
                         }
                     }
+                    if constexpr (FLEET) {
+                        // end of a device segment: fold Q_d / s_d into the rate (IEEE division,
+                        // correctly rounded) and restart the segment sum
+                        if (!skip && ((p.stage_end_mask >> q) & 1u)) {
+                            const float Q = p.stage_Q[q];
+#pragma unroll
+                            for (int i = 0; i < 8; i++)
+#pragma unroll
+                                for (int j = 0; j < 4; j++) {
+                                    rate[i][j] = __fadd_rn(rate[i][j], __fdiv_rn(Q, acc[i][j]));
+                                    acc[i][j] = 0.0f;
+                                }
+                        }
+                    }
                     __syncwarp();
                     if (lane == 0) {
                         // release: the last of the consumer warps to finish this stage refills
@@ -539,67 +573,123 @@ __global__ void __launch_bounds__(XT_TCONS, XT_MINB) k_exh_tiled(const XParams p
                 }
                 if (skip) continue;
                 // ---- epilogue of one column tile ----
-                // LB = RD(acc*c1 - c2) and UB = RU(acc*c3 + c4) are non-decreasing in acc, so
-                // order statistics and the window test are taken on acc itself and mapped
-                // once.  Padding / ragged sets become +inf.
-                const int64_t l0 = ltile + c0;
-                if (!(l0 + XT_SPAN < p.C && l0 > last7)) {
+                if constexpr (FLEET) {
+                    // rate R_hat: R in [R_hat c1, R_hat c3]; invalid sets -> -inf.
+                    // Keep every set whose UB >= tau, tau = a lower bound of R_(2).
+                    const int64_t l0 = ltile + c0;
+                    const bool all_valid = l0 + XT_SPAN < p.C && l0 > last7;
+                    float tA = -INFINITY, tB = -INFINITY;
 #pragma unroll
                     for (int i = 0; i < 8; i++)
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             const int64_t l = ltile + XT_COL(i, j);
-                            if (!(l < p.C && l > last_s[XT_ROW(i, j)])) acc[i][j] = INFINITY;
+                            if (!all_valid && !(l < p.C && l > last_s[XT_ROW(i, j)])) rate[i][j] = -INFINITY;
+                            if (XT_GRPB(i, j)) tB = fmaxf(tB, rate[i][j]);
+                            else tA = fmaxf(tA, rate[i][j]);
                         }
-                }
-                // tile minima of two disjoint groups of the thread's sets
-                float tA = INFINITY, tB = INFINITY;
+                    bA = fmaxf(bA, tA);
+                    bB = fmaxf(bB, tB);
+                    const float tau = fmaxf(p.tau_seed, __uint_as_float(Ubits));
+                    if (__fmul_ru(fmaxf(tA, tB), p.c3) >= tau) {   // rare: some set is in the window
 #pragma unroll
-                for (int i = 0; i < 8; i++)
+                        for (int i = 0; i < 8; i++)
 #pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        if (XT_GRPB(i, j)) tB = fminf(tB, acc[i][j]);
-                        else tA = fminf(tA, acc[i][j]);
+                            for (int j = 0; j < 4; j++) {
+                                const float ub = __fmul_ru(rate[i][j], p.c3);
+                                if (rate[i][j] > -INFINITY && ub >= tau) {
+                                    const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                    if (idx < p.cap) {
+                                        p.cand_key[idx] = ((unsigned long long)(R0 + XT_ROW(i, j)) << KEY_BITS) |
+                                                          (unsigned long long)(ltile + XT_COL(i, j));
+                                        p.cand_s[idx] = ub;
+                                    }
+                                }
+                            }
                     }
-                bA = fminf(bA, tA);
-                bB = fminf(bB, tB);
-                const float tau = fminf(p.tau_seed, __uint_as_float(Ubits));
-                if (__fmaf_rd(fminf(tA, tB), p.c1, -p.c2) <= tau) {   // rare: some set is in the window
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+#pragma unroll
+                        for (int j = 0; j < 4; j++) rate[i][j] = 0.0f;
+                    // U: the warp's 2nd-largest group maximum, mapped to its lower bound
+                    float x1 = fmaxf(bA, bB), x2 = fminf(bA, bB);
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) {
+                        const float y1 = __shfl_xor_sync(0xffffffffu, x1, o);
+                        const float y2 = __shfl_xor_sync(0xffffffffu, x2, o);
+                        x2 = fmaxf(fminf(x1, y1), fmaxf(x2, y2));
+                        x1 = fmaxf(x1, y1);
+                    }
+                    if (lane == 0) {
+                        const float lb = __fmul_rd(x2, p.c1);
+                        if (lb > published && lb > 0.0f) {
+                            atomicMax(p.U, __float_as_uint(lb));   // positive floats: integer order
+                            published = lb;
+                        }
+                    }
+                } else {
+                    // LB = RD(acc*c1 - c2) and UB = RU(acc*c3 + c4) are non-decreasing in acc, so
+                    // order statistics and the window test are taken on acc itself and mapped
+                    // once.  Padding / ragged sets become +inf.
+                    const int64_t l0 = ltile + c0;
+                    if (!(l0 + XT_SPAN < p.C && l0 > last7)) {
+#pragma unroll
+                        for (int i = 0; i < 8; i++)
+#pragma unroll
+                            for (int j = 0; j < 4; j++) {
+                                const int64_t l = ltile + XT_COL(i, j);
+                                if (!(l < p.C && l > last_s[XT_ROW(i, j)])) acc[i][j] = INFINITY;
+                            }
+                    }
+                    // tile minima of two disjoint groups of the thread's sets
+                    float tA = INFINITY, tB = INFINITY;
 #pragma unroll
                     for (int i = 0; i < 8; i++)
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
-                            const float lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
-                            if (acc[i][j] < INFINITY && lb <= tau) {
-                                const unsigned idx = atomicAdd(p.cand_n, 1u);
-                                if (idx < p.cap) {
-                                    p.cand_key[idx] = ((unsigned long long)(R0 + XT_ROW(i, j)) << KEY_BITS) |
-                                                      (unsigned long long)(ltile + XT_COL(i, j));
-                                    p.cand_s[idx] = lb;
+                            if (XT_GRPB(i, j)) tB = fminf(tB, acc[i][j]);
+                            else tA = fminf(tA, acc[i][j]);
+                        }
+                    bA = fminf(bA, tA);
+                    bB = fminf(bB, tB);
+                    const float tau = fminf(p.tau_seed, __uint_as_float(Ubits));
+                    if (__fmaf_rd(fminf(tA, tB), p.c1, -p.c2) <= tau) {   // rare: some set is in the window
+#pragma unroll
+                        for (int i = 0; i < 8; i++)
+#pragma unroll
+                            for (int j = 0; j < 4; j++) {
+                                const float lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
+                                if (acc[i][j] < INFINITY && lb <= tau) {
+                                    const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                    if (idx < p.cap) {
+                                        p.cand_key[idx] = ((unsigned long long)(R0 + XT_ROW(i, j)) << KEY_BITS) |
+                                                          (unsigned long long)(ltile + XT_COL(i, j));
+                                        p.cand_s[idx] = lb;
+                                    }
                                 }
                             }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+#pragma unroll
+                        for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
+                    // U: the warp's 2nd-smallest group minimum.  bA and bB of all lanes are
+                    // minima over disjoint sets of sets, so the two smallest belong to two
+                    // distinct sets and UB(2nd) >= s_(2)
+                    float x1 = fminf(bA, bB), x2 = fmaxf(bA, bB);
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) {
+                        const float y1 = __shfl_xor_sync(0xffffffffu, x1, o);
+                        const float y2 = __shfl_xor_sync(0xffffffffu, x2, o);
+                        x2 = fminf(fmaxf(x1, y1), fminf(x2, y2));
+                        x1 = fminf(x1, y1);
+                    }
+                    if (lane == 0) {
+                        const float ub = __fmaf_ru(x2, p.c3, p.c4);
+                        if (ub < published) {
+                            atomicMin(p.U, __float_as_uint(ub));
+                            published = ub;
                         }
-                }
-#pragma unroll
-                for (int i = 0; i < 8; i++)
-#pragma unroll
-                    for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
-                // U: the warp's 2nd-smallest group minimum.  bA and bB of all lanes are
-                // minima over disjoint sets of sets, so the two smallest belong to two
-                // distinct sets and UB(2nd) >= s_(2)
-                float x1 = fminf(bA, bB), x2 = fmaxf(bA, bB);
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    const float y1 = __shfl_xor_sync(0xffffffffu, x1, o);
-                    const float y2 = __shfl_xor_sync(0xffffffffu, x2, o);
-                    x2 = fminf(fmaxf(x1, y1), fminf(x2, y2));
-                    x1 = fminf(x1, y1);
-                }
-                if (lane == 0) {
-                    const float ub = __fmaf_ru(x2, p.c3, p.c4);
-                    if (ub < published) {
-                        atomicMin(p.U, __float_as_uint(ub));
-                        published = ub;
                     }
                 }
             }
@@ -993,7 +1083,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());
     }
-    auto kern = k_exh_tiled;
+    auto kern = k_exh_tiled<false>;
     const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
                         sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
     const void *kfn = (const void *)kern;
@@ -1111,6 +1201,295 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
             for (int u = 0; u < 2 * k; u++) t_out[u] = 0;
         }
         return PT_OK;
+    }
+    return pt_fail(PT_ECUDA, "candidate buffer overflowed twice (internal error)");
+}
+
+// ---------------------------------------------------------------------------
+// the tiled search for the fleet objective (Eq. 2): k_exh_tiled<true> on
+// the fp16 weighted runtimes, each device one run of 64-env stages (pt_fleet_tiled),
+// fp64 exact refine of the survivors, ranked by cost 1/R ascending
+// ---------------------------------------------------------------------------
+// exact R of every candidate whose rate upper bound reaches the final threshold,
+// fused with the (cost = 1/R, tuple) top-2 (last-block merge, as k_exh_refine_top2)
+__global__ void __launch_bounds__(256) k_fleet_refine_top2(
+    const unsigned long long *__restrict__ key, const float *__restrict__ cub, const unsigned *__restrict__ n_dev,
+    unsigned cap, float tau_pass, const unsigned *__restrict__ U, int m, int64_t C,
+    const double *__restrict__ tcm, int64_t E_pad, const double *__restrict__ w, const int32_t *__restrict__ seg,
+    int n_devices, const double *__restrict__ qdev, Rec2 *__restrict__ blk, unsigned *__restrict__ done,
+    double *__restrict__ out_s, int32_t *__restrict__ out_t)
+{
+    const int64_t n = min(*n_dev, cap);
+    const float tau = fmaxf(tau_pass, __uint_as_float(*U));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = m + 1;
+    __shared__ Rec2 sh[256];
+    Rec2 r;
+    r.s1 = r.s2 = INFINITY;
+    for (int u = 0; u < PT_MAXK; u++) r.t1[u] = r.t2[u] = 0x7fffffff;
+    for (int64_t wi = (int64_t)blockIdx.x * 8 + warp; wi < n; wi += (int64_t)gridDim.x * 8) {
+        if (cub[wi] < tau) continue;
+        int32_t tup[PT_MAXK];
+        const unsigned long long kv = key[wi];
+        pt_unrank_colex((int64_t)(kv >> KEY_BITS), m, C, tup);
+        tup[m] = (int32_t)(kv & ((1ull << KEY_BITS) - 1));
+        double R = 0.0;
+        for (int d = 0; d < n_devices; d++) {
+            double den = 0.0, wsum = 0.0;
+            for (int q = seg[d] + lane; q < seg[d + 1]; q += 32) {
+                double y = tcm[(int64_t)tup[0] * E_pad + q];
+                for (int u = 1; u < k; u++) y = fmin(y, tcm[(int64_t)tup[u] * E_pad + q]);
+                den += w[q] * y;
+                wsum += w[q];
+            }
+            for (int o = 16; o; o >>= 1) {
+                den += __shfl_xor_sync(0xffffffffu, den, o);
+                wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+            }
+            if (wsum > 0.0) R += qdev[d] / den;
+        }
+        if (lane == 0) rec_offer(r, 1.0 / R, tup, k);
+    }
+    sh[threadIdx.x] = r;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if ((int)threadIdx.x < h) {
+            Rec2 o = sh[threadIdx.x + h];
+            Rec2 me = sh[threadIdx.x];
+            rec_offer(me, o.s1, o.t1, k);
+            rec_offer(me, o.s2, o.t2, k);
+            sh[threadIdx.x] = me;
+        }
+        __syncthreads();
+    }
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        blk[blockIdx.x] = sh[0];
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    r.s1 = r.s2 = INFINITY;
+    for (int u = 0; u < PT_MAXK; u++) r.t1[u] = r.t2[u] = 0x7fffffff;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+        Rec2 o;
+        o.s1 = __ldcg(&blk[b].s1);
+        o.s2 = __ldcg(&blk[b].s2);
+        for (int u = 0; u < k; u++) {
+            o.t1[u] = __ldcg(&blk[b].t1[u]);
+            o.t2[u] = __ldcg(&blk[b].t2[u]);
+        }
+        rec_offer(r, o.s1, o.t1, k);
+        rec_offer(r, o.s2, o.t2, k);
+    }
+    sh[threadIdx.x] = r;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if ((int)threadIdx.x < h) {
+            Rec2 o = sh[threadIdx.x + h];
+            Rec2 me = sh[threadIdx.x];
+            rec_offer(me, o.s1, o.t1, k);
+            rec_offer(me, o.s2, o.t2, k);
+            sh[threadIdx.x] = me;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out_s[0] = sh[0].s1;
+        out_s[1] = sh[0].s2;
+        for (int u = 0; u < k; u++) {
+            out_t[u] = sh[0].t1[u];
+            out_t[k + u] = sh[0].t2[u];
+        }
+        *done = 0;
+    }
+}
+
+pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, int32_t shard_count,
+                                    const pt_fleet_tiled *ft, int32_t *best, int32_t *runner, double *R_out,
+                                    double *cost_out, int *n_found)
+{
+    cudaStream_t s = ctx->stream;
+    const pt_view *v = &ctx->full;
+    const pt_fleet &f = ctx->fl;
+    const int m = k - 1;
+    pt_tasks *T = nullptr;
+    PT_TRY(build_tasks(ctx, v, m, XT_R, XT_C, &T));
+    const int4 *task_list = T->d;
+    int ta = 0, tb = (int)T->h.size();
+    ctx->stats.exh_sets = T->set_pre.back();
+    ctx->stats.exh_slots = T->slot_pre.back();
+    if (shard_count > 1) {
+        const pt_tasks::plan *P = nullptr;
+        static const std::vector<double> equal;
+        PT_TRY(shard_plan(T, shard_count, (int)ctx->shard_w.size() == shard_count ? ctx->shard_w : equal, &P));
+        task_list = P->d;
+        ta = P->off[shard_rank];
+        tb = P->off[shard_rank + 1];
+        ctx->stats.exh_sets = P->sets[shard_rank];
+        ctx->stats.exh_slots = P->slots[shard_rank];
+    }
+    ctx->stats.exh_kernel = 3;
+    ctx->stats.exh_env_pad = ft->E_fp;
+    ctx->stats.exh_candidates = 0;
+    ctx->stats.exh_passes = 0;
+    ctx->stats.exh_main_ms = 0.0;
+    std::vector<int32_t> t(2 * k, 0);
+    double sv[2] = {INFINITY, INFINITY};
+    auto finish = [&]() {
+        const int nf = (sv[0] < INFINITY) + (sv[1] < INFINITY);
+        if (n_found) *n_found = nf;
+        for (int u = 0; u < k; u++) {
+            best[u] = t[u];
+            if (runner) runner[u] = t[k + u];
+        }
+        cost_out[0] = sv[0];
+        cost_out[1] = sv[1];
+        R_out[0] = nf >= 1 ? 1.0 / sv[0] : NAN;
+        R_out[1] = nf >= 2 ? 1.0 / sv[1] : NAN;
+        return PT_OK;
+    };
+    if (ta >= tb) return finish();
+
+    // error model: each device sum s'_d of scaled weighted runtimes is
+    // the fp16 tier's sum of exact-normal fp16 terms -> |s_hat - s| <= eta s (the same
+    // tree/chain analysis as Eq. 1, no absolute term: every term is a normal fp16); then
+    // R_hat = sum_d RN(Q_d / s_hat_d) in fp32 (Q_d carries one fp32 rounding):
+    //   R_hat = R (1 + phi),  |phi| <= eta / (1 - eta) + (n_dev + 3) u32
+    const double u16 = std::ldexp(1.0, -11), u32 = std::ldexp(1.0, -24);
+    const double lv16 = 2.0 + XT_NG;
+    const double ngrp = (double)ft->E_fp / (4.0 * XT_NG) + 2.0;
+    const double gam = ngrp * u32 / (1.0 - ngrp * u32);
+    const double eta = (lv16 * u16 + lv16 * lv16 * u16 * u16 + gam + std::ldexp(1.0, -50)) * 1.01;
+    const double eta_R = (eta / (1.0 - eta) + (f.n_dev + 3) * u32) * 1.02;
+    auto f_up = [](double x) -> float {
+        if (!(x < 3.0e38)) return INFINITY;
+        float g = (float)x;
+        if ((double)g < x) g = nextafterf(g, INFINITY);
+        return g;
+    };
+    auto f_dn = [](double x) -> float {
+        float g = (float)x;
+        if ((double)g > x) g = nextafterf(g, -INFINITY);
+        return g;
+    };
+    const float c1 = f_dn(1.0 / (1.0 + eta_R)), c3 = f_up(1.0 / (1.0 - eta_R));
+    // seed: greedy's runner-up rate at step k (two distinct k-sets: <= R_(2))
+    float tau_seed = 0.0f;
+    {
+        std::vector<int32_t> gi(k);
+        std::vector<double> gr(k), gg(k);
+        PT_TRY(pt_fleet_greedy(ctx, k, nullptr, gi.data(), gr.data(), gg.data()));
+        const double r2 = gr[k - 1] - gg[k - 1];
+        if (std::isfinite(r2) && r2 > 0.0) tau_seed = f_dn(r2 * (1.0 - 1e-9));
+    }
+    if (!ft->hWTile) {
+        pt_fleet_tiled *mt = const_cast<pt_fleet_tiled *>(ft);
+        mt->n_ct = (v->C_pad + XT_C - 1) / XT_C + 1;
+        PT_TRY(pt_dalloc(ctx, (void **)&mt->hWTile, sizeof(uint16_t) * 8 * mt->n_ct * ft->E_fp * XT_C));
+        k_tile_hT<<<(unsigned)(8 * mt->n_ct), 256, 0, s>>>(ft->hWT, ft->E_fp, v->C_pad, mt->n_ct, mt->hWTile);
+        ctx->stats.launches++;
+        PT_CK(cudaGetLastError());
+    }
+    auto kern = k_exh_tiled<true>;
+    const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * ft->E_fp * XT_R +
+                        sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
+    static std::mutex mu;
+    static std::map<size_t, int> occ_cache;
+    int occ = 1;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = occ_cache.find(smem);
+        if (it == occ_cache.end()) {
+            PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT_TCONS, smem));
+            occ_cache[smem] = occ;
+        } else {
+            occ = it->second;
+        }
+    }
+    unsigned cap = 1u << 20, n_cand = 0;
+    float tau_pass = tau_seed;
+    for (int pass = 0; pass < 2; pass++) {
+        size_t off = 0;
+        auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
+        const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)), o_n = take(sizeof(unsigned)),
+                     o_key = take(sizeof(unsigned long long) * cap), o_cq = take(sizeof(float) * cap),
+                     o_os = take(sizeof(double) * 2), o_ot = take(sizeof(int32_t) * 2 * k),
+                     o_blk = take(sizeof(Rec2) * (size_t)ctx->num_sms * 2), o_done = take(sizeof(unsigned));
+        void *scr = nullptr;
+        PT_TRY(pt_scratch(ctx, off, &scr));
+        char *b = (char *)scr;
+        int *ctr = (int *)(b + o_ctr);
+        unsigned *U = (unsigned *)(b + o_U), *cn = (unsigned *)(b + o_n), *done = (unsigned *)(b + o_done);
+        unsigned long long *ckey = (unsigned long long *)(b + o_key);
+        float *cq = (float *)(b + o_cq);
+        double *os = (double *)(b + o_os);
+        int32_t *ot = (int32_t *)(b + o_ot);
+        Rec2 *blk = (Rec2 *)(b + o_blk);
+        pt_hostio io(ctx);
+        PT_TRY(io.h2d(ctr, &ta, sizeof(int)));
+        PT_CK(cudaMemsetAsync(U, 0, sizeof(unsigned), s));   // 0.0f: no lower bound yet
+        PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned), s));
+        PT_CK(cudaMemsetAsync(done, 0, sizeof(unsigned), s));
+        XParams p{};
+        p.C = v->C;
+        p.C_pad = v->C_pad;
+        p.E_pad = ft->E_fp;
+        p.n_rows = pt_binom(v->C, m);
+        p.m = m;
+        p.tasks = task_list;
+        p.task_hi = tb;
+        p.task_ctr = ctr;
+        p.tau_seed = tau_pass;
+        p.c1 = c1;
+        p.c2 = 0.0f;
+        p.c3 = c3;
+        p.c4 = 0.0f;
+        p.U = U;
+        p.cand_key = ckey;
+        p.cand_s = cq;
+        p.cand_n = cn;
+        p.cap = cap;
+        p.hT = ft->hWT;
+        p.hTile = ft->hWTile;
+        p.n_ct = ft->n_ct;
+        p.stage_end_mask = ft->stage_end_mask;
+        for (int q = 0; q < XT_MAXSTAGE; q++) p.stage_Q[q] = ft->stage_Q[q];
+        const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
+        PT_CK(cudaEventRecord(ctx->ev0, s));
+        kern<<<grid, XT_TCONS, smem, s>>>(p);
+        PT_CK(cudaEventRecord(ctx->ev1, s));
+        k_fleet_refine_top2<<<(unsigned)(ctx->num_sms * 2), 256, 0, s>>>(
+            ckey, cq, cn, cap, tau_pass, U, m, v->C, f.tcm, v->E_pad, f.w, f.seg, f.n_dev, f.qdev, blk, done, os, ot);
+        ctx->stats.launches += 2;
+        pt_pack_record(ctx, os, ot, k);
+        PT_CK(cudaGetLastError());
+        unsigned hU = 0;
+        PT_TRY(io.d2h(&n_cand, cn, sizeof(unsigned)));
+        PT_TRY(io.d2h(&hU, U, sizeof(unsigned)));
+        PT_TRY(io.d2h(sv, os, sizeof(double) * 2));
+        PT_TRY(io.d2h(t.data(), ot, sizeof(int32_t) * 2 * k));
+        PT_TRY(io.finish());
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        if (pass == 0) ctx->stats.exh_main_ms = ms;
+        ctx->stats.exh_passes = pass + 1;
+        float Uf;
+        memcpy(&Uf, &hU, sizeof Uf);
+        if (n_cand > cap) {   // overflow: rerun with the final threshold and room for every survivor
+            cap = n_cand;
+            tau_pass = std::max(tau_pass, Uf);
+            continue;
+        }
+        ctx->stats.exh_candidates = n_cand;
+        if (n_cand == 0) {
+            sv[0] = sv[1] = INFINITY;
+            for (int u = 0; u < 2 * k; u++) t[u] = 0;
+        }
+        return finish();
     }
     return pt_fail(PT_ECUDA, "candidate buffer overflowed twice (internal error)");
 }

@@ -16,6 +16,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "pt_internal.cuh"
 
 #define FL_MAXDEV 64
@@ -259,6 +261,120 @@ __global__ void __launch_bounds__(128) k_fleet_exh(const double *__restrict__ te
     }
 }
 
+// per device segment: max and min over (env, config < C) of w[q] * tcm[c][q]
+__global__ void k_fleet_seg_minmax(const double *__restrict__ tcm, int64_t E_pad, int64_t C,
+                                   const double *__restrict__ w, const int32_t *__restrict__ seg,
+                                   double *__restrict__ out /* [n_dev][2] */)
+{
+    const int d = blockIdx.x;
+    const int64_t q0 = seg[d], q1 = seg[d + 1];
+    double mx = 0.0, mn = INFINITY;
+    for (int64_t i = threadIdx.x; i < (q1 - q0) * C; i += blockDim.x) {
+        const int64_t q = q0 + i / C, c = i % C;
+        const double v = w[q] * tcm[c * E_pad + q];
+        mx = fmax(mx, v);
+        mn = fmin(mn, v);
+    }
+    __shared__ double smx[256], smn[256];
+    smx[threadIdx.x] = mx;
+    smn[threadIdx.x] = mn;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if ((int)threadIdx.x < h) {
+            smx[threadIdx.x] = fmax(smx[threadIdx.x], smx[threadIdx.x + h]);
+            smn[threadIdx.x] = fmin(smn[threadIdx.x], smn[threadIdx.x + h]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[2 * d] = smx[0];
+        out[2 * d + 1] = smn[0];
+    }
+}
+
+// hWT[r][c] = RN16(w[q] * tcm[c][q] * scale[r]) for the segment row r -> permuted env q
+// (rowq[r] = -1: a padding row), 0 past C
+__global__ void k_fleet_half(const double *__restrict__ tcm, int64_t E_pad, int64_t C, int64_t C_pad,
+                             const double *__restrict__ w, const int32_t *__restrict__ rowq,
+                             const double *__restrict__ rscale, int64_t E_fp, uint16_t *__restrict__ hWT)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= E_fp * C_pad) return;
+    const int64_t r = i / C_pad, c = i % C_pad;
+    const int32_t q = rowq[r];
+    double v = 0.0;
+    if (q >= 0 && c < C) v = w[q] * tcm[c * E_pad + q] * rscale[r];
+    hWT[i] = __half_as_ushort(__double2half(v));
+}
+
+void pt_fleet_tiled_free(pt_ctx *ctx)
+{
+    pt_fleet_tiled &t = ctx->fl.tiled;
+    pt_dfree(ctx, t.hWT);
+    pt_dfree(ctx, t.hWTile);
+    t = pt_fleet_tiled();
+}
+
+pt_status pt_fleet_tiled_operands(pt_ctx *ctx, const pt_fleet_tiled **out)
+{
+    pt_fleet &f = ctx->fl;
+    pt_fleet_tiled &t = f.tiled;
+    *out = &t;
+    if (t.built) return PT_OK;
+    t.built = true;
+    const int64_t C = ctx->C, E_pad = ctx->full.E_pad, C_pad = ctx->full.C_pad;
+    cudaStream_t s = ctx->stream;
+    double *mm = nullptr;
+    PT_TRY(pt_dalloc(ctx, (void **)&mm, sizeof(double) * 2 * f.n_dev));
+    k_fleet_seg_minmax<<<f.n_dev, 256, 0, s>>>(f.tcm, E_pad, C, f.w, f.seg, mm);
+    ctx->stats.launches++;
+    std::vector<double> h(2 * f.n_dev);
+    PT_CK(cudaMemcpyAsync(h.data(), mm, sizeof(double) * 2 * f.n_dev, cudaMemcpyDeviceToHost, s));
+    PT_CK(cudaStreamSynchronize(s));
+    pt_dfree(ctx, mm);
+    // segments -> padded rows; per device sigma_d = 2^(10 - ceil(log2 max))
+    std::vector<int32_t> rowq;
+    std::vector<double> rscale;
+    int nst = 0;
+    bool ok = true;
+    for (int32_t d = 0; d < f.n_dev; d++) {
+        const int64_t n = f.h_seg[d + 1] - f.h_seg[d];
+        if (n == 0) continue;                             // a device without environments
+        const double sigma = std::ldexp(1.0, 10 - (int)std::ceil(std::log2(h[2 * d])));
+        if (!(h[2 * d + 1] * sigma >= std::ldexp(1.0, -14)) || !(h[2 * d] * sigma <= 1024.0)) ok = false;
+        const int64_t rows = (n + 63) / 64 * 64;
+        for (int64_t r = 0; r < rows; r++) {
+            rowq.push_back(r < n ? (int32_t)(f.h_seg[d] + r) : -1);
+            rscale.push_back(sigma);
+        }
+        nst += (int)(rows / 64);
+        if (nst > 32) {
+            ok = false;
+            break;
+        }
+        t.stage_end_mask |= 1u << (nst - 1);
+        t.stage_Q[nst - 1] = (float)(f.h_qdev[d] * sigma);
+    }
+    if (!ok) return PT_OK;    // not eligible: the thread-per-subset search runs instead
+    t.E_fp = (int64_t)rowq.size();
+    int32_t *d_rowq = nullptr;
+    double *d_rs = nullptr;
+    PT_TRY(pt_dalloc(ctx, (void **)&d_rowq, sizeof(int32_t) * t.E_fp));
+    PT_TRY(pt_dalloc(ctx, (void **)&d_rs, sizeof(double) * t.E_fp));
+    PT_TRY(pt_dalloc(ctx, (void **)&t.hWT, sizeof(uint16_t) * t.E_fp * C_pad));
+    PT_CK(cudaMemcpyAsync(d_rowq, rowq.data(), sizeof(int32_t) * t.E_fp, cudaMemcpyHostToDevice, s));
+    PT_CK(cudaMemcpyAsync(d_rs, rscale.data(), sizeof(double) * t.E_fp, cudaMemcpyHostToDevice, s));
+    k_fleet_half<<<(unsigned)((t.E_fp * C_pad + 255) / 256), 256, 0, s>>>(f.tcm, E_pad, C, C_pad, f.w, d_rowq, d_rs,
+                                                                          t.E_fp, t.hWT);
+    ctx->stats.launches++;
+    PT_CK(cudaGetLastError());
+    PT_CK(cudaStreamSynchronize(s));   // rowq / rscale are host temporaries
+    pt_dfree(ctx, d_rowq);
+    pt_dfree(ctx, d_rs);
+    t.eligible = true;
+    return PT_OK;
+}
+
 // ---------------------------------------------------------------------------
 // host
 // ---------------------------------------------------------------------------
@@ -277,6 +393,7 @@ extern "C" pt_status pt_set_fleet(pt_ctx *ctx, const double *q_device, int32_t n
         if (!(q_env[e] > 0.0)) return pt_fail(PT_EINVAL, "quantity of env %lld must be > 0", (long long)e);
     }
     PT_CK(cudaSetDevice(ctx->dev));
+    pt_fleet_tiled_free(ctx);     // new quantities: the fp16 operands are rebuilt on use
     pt_fleet &f = ctx->fl;
     const int64_t E = ctx->E, C = ctx->C, E_pad = ctx->full.E_pad;
     f.perm.clear();
@@ -442,6 +559,15 @@ pt_status pt_fleet_exhaustive(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, i
     const double nsets = std::exp(std::lgamma((double)C + 1) - std::lgamma((double)k + 1) -
                                   std::lgamma((double)(C - k) + 1));
     if (nsets > 1e13) return pt_fail(PT_ECAP, "C(%lld,%d) = %.3g exceeds the cap 1e13", (long long)C, k, nsets);
+    if (!ctx->fl.set) return pt_fail(PT_EINVAL, "PT_OBJ_FLEET needs pt_set_fleet first");
+    // the (min,+) tiled search with a per-device fold (exhaustive.cu) for the full scope
+    if (!env_mask && k >= 2 && k <= 4 && k < C && !(ctx->flags & PT_EXACT_FP64) && E_pad <= 768) {
+        const pt_fleet_tiled *ft = nullptr;
+        PT_TRY(pt_fleet_tiled_operands(ctx, &ft));
+        if (ft->eligible)
+            return pt_fleet_exhaustive_tiled(ctx, k, shard_rank, shard_count, ft, best, runner, R_out, cost_out,
+                                             n_found);
+    }
     const double *w = nullptr;
     PT_TRY(fleet_weights(ctx, env_mask, &w));
     const int64_t n = pt_binom(C, k);

@@ -541,6 +541,7 @@ extern "C" void pt_free(pt_ctx *ctx)
     pt_dfree(ctx, ctx->fl.w);
     pt_dfree(ctx, ctx->fl.qdev);
     pt_dfree(ctx, ctx->fl.seg);
+    pt_fleet_tiled_free(ctx);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);

@@ -85,8 +85,25 @@ struct pt_scope {   // one cached compacted scope
     uint64_t last_use = 0;
 };
 
+// fp16 operands of the tiled fleet search (full scope, built on first use after
+// pt_set_fleet): per device d the weighted runtimes W[q][c] = quantity(q) * T[q][c]
+// of its environments, scaled by a power of two sigma_d (max of the segment -> 2^10,
+// so a 16-env fp16 chain cannot overflow), rounded to fp16, each segment padded with
+// zero rows to whole 64-env stages.  eligible = every scaled value is a normal fp16
+// (>= 2^-14: pure relative rounding error) and there are at most 32 stages.
+struct pt_fleet_tiled {
+    bool built = false, eligible = false;
+    int64_t E_fp = 0;            // padded env rows (sum of ceil64(E_d))
+    int64_t n_ct = 0;
+    uint16_t *hWT = nullptr;     // [E_fp][C_pad] fp16, env-major
+    uint16_t *hWTile = nullptr;  // [8 shifts][n_ct][E_fp][64] (the hTile layout)
+    uint32_t stage_end_mask = 0; // bit q: stage q ends a device segment
+    float stage_Q[32] = {};      // quantity(d) * sigma_d at that stage
+};
+
 // fleet objective (Eq. 2) data, built by pt_set_fleet
 struct pt_fleet {
+    pt_fleet_tiled tiled;
     bool set = false;
     int32_t n_dev = 0;
     double *tcm = nullptr;    // [C][E_pad] runtimes (missing -> penalty*best), envs grouped by device
@@ -178,6 +195,12 @@ pt_status pt_fleet_greedy(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32
 pt_status pt_fleet_exhaustive(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t shard_rank,
                               int32_t shard_count, int32_t *best, int32_t *runner, double *R_out,
                               double *cost_out, int *n_found);
+// the tiled fleet search: operands (fleet.cu) and the search itself (exhaustive.cu)
+pt_status pt_fleet_tiled_operands(pt_ctx *ctx, const pt_fleet_tiled **out);
+void pt_fleet_tiled_free(pt_ctx *ctx);
+pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, int32_t shard_count,
+                                    const pt_fleet_tiled *ft, int32_t *best, int32_t *runner, double *R_out,
+                                    double *cost_out, int *n_found);
 
 
 // ---------------------------------------------------------------------------

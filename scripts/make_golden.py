@@ -22,17 +22,26 @@ ap.add_argument("--seeds", type=int, nargs="+", default=[1, 2, 3])
 ap.add_argument("--ks", type=int, nargs="+", default=[2, 3])
 ap.add_argument("--threads", type=int, default=default_threads())
 ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "paper_exhaustive.json"))
+ap.add_argument("--fleet", action="store_true",
+                help="the fleet objective (Eq. 2) instead: q_dev = FLEET_QDEV, q_env = 1 -> seed<S>_fleet_k<K>")
 a = ap.parse_args()
+FLEET_QDEV = [5.0, 2.0, 1.0, 3.0, 4.0]   # fleet mix of bench.py next_rows (invented quantities)
 
 res = json.load(open(a.out)) if os.path.exists(a.out) else {}
 for seed in a.seeds:
     T, dev = synth.paper_matrix(seed)
     o = Oracle(T, dev)
+    if a.fleet:
+        o.set_fleet(FLEET_QDEV, [1.0] * T.shape[0])
     for k in a.ks:
         t0 = time.time()
-        b, gb, ru, gr = o.exhaustive(k, threads=a.threads)
+        if a.fleet:
+            b, gb, ru, gr = o.fleet_exhaustive_par(k, threads=a.threads)
+            key, vals = f"seed{seed}_fleet_k{k}", {"R": gb, "R_runner": gr, "q_dev": FLEET_QDEV, "q_env": 1.0}
+        else:
+            b, gb, ru, gr = o.exhaustive(k, threads=a.threads)
+            key, vals = f"seed{seed}_k{k}", {"G": gb, "G_runner": gr}
         dt = time.time() - t0
-        res[f"seed{seed}_k{k}"] = {"best": list(b), "G": gb, "runner": list(ru), "G_runner": gr,
-                                   "oracle_seconds": round(dt, 2), "threads": a.threads}
+        res[key] = dict(vals, best=list(b), runner=list(ru), oracle_seconds=round(dt, 2), threads=a.threads)
         print(seed, k, b, gb, ru, gr, f"{dt:.1f}s", flush=True)
         json.dump(res, open(a.out, "w"), indent=1, sort_keys=True)

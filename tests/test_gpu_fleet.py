@@ -124,3 +124,53 @@ def test_errors():
         pt.pt_set_fleet(ctx, [1.0], np.ones(len(dev)))        # device id 4 out of range
     with pytest.raises(pt.PTError):
         pt.pt_set_fleet(ctx, np.ones(5), -np.ones(len(dev)))
+
+
+def test_tiled_fleet_path():
+    """The full-scope fleet search runs the (min,+) tiled kernel with the per-device
+    fold (exh_kernel 3); a masked scope the thread-per-subset fp64 search (2).
+    Uneven device segments (9 envs each, padded to 64-env stages) and a missing cell."""
+    T, dev = synth.small_matrix(4, n_cfg=300, n_dev=4, n_inputs=9)
+    T[7, 33] = np.nan
+    rng = np.random.default_rng(4)
+    qd, qe = rng.uniform(1, 5, 4), rng.integers(1, 4, len(dev)).astype(float)
+    o, ctx = both(T, dev, qd, qe)
+    for k in (2, 3):
+        check_exh(o, ctx, k)
+        assert pt.pt_get_stats(ctx)["exh_kernel"] == 3
+        check_exh(o, ctx, k, shards=5)
+    check_exh(o, ctx, 2, mask=(dev != 1).astype(np.uint8))
+    assert pt.pt_get_stats(ctx)["exh_kernel"] == 2
+
+
+def test_paper_fleet_k3_golden():
+    """Config 3b with the fleet objective (Eq. 2): k=2 and k=3 over 1,775 x 320 against
+    the oracle's full search (tests/golden/paper_exhaustive.json, written by
+    scripts/make_golden.py --fleet, which calls only oracle/)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    gold = json.load(open(os.path.join(GOLDEN, "paper_exhaustive.json")))
+    if "seed1_fleet_k3" not in gold:
+        pytest.skip("fleet golden not generated")
+    T, dev = synth.paper_matrix(1)
+    qd = np.array(gold["seed1_fleet_k3"]["q_dev"])
+    ctx = pt.pt_load_perf(T, dev)
+    pt.pt_set_fleet(ctx, qd, np.ones(len(dev)))
+    for k in (2, 3):
+        g = gold[f"seed1_fleet_k{k}"]
+        r = pt.pt_exhaustive_best(ctx, k, objective=pt.PT_OBJ_FLEET)
+        st = pt.pt_get_stats(ctx)
+        assert st["exh_kernel"] == 3
+        assert r["G"] == pytest.approx(g["R"], rel=RTOL) and r["G_runner"] == pytest.approx(g["R_runner"], rel=RTOL)
+        if g["R"] - g["R_runner"] > GAP * g["R"]:
+            assert r["best"] == tuple(g["best"])
+        assert r["runner"] == tuple(g["runner"]) or abs(r["G_runner"] - g["R_runner"]) <= GAP * g["R"]
+    # 8 shards through the library's own exchange + merge (thread-emulated ranks)
+    r8 = []
+    for rank in range(8):
+        r8.append(pt.pt_exhaustive_best(ctx, 3, shard_rank=rank, shard_count=8, objective=pt.PT_OBJ_FLEET))
+    ss = [x for r in r8 for x in r["s"]]
+    tt = [t if t is not None else (-1, -1, -1) for r in r8 for t in (r["best"], r["runner"])]
+    b, ru, (c1, c2) = pt.pt_merge_top2(ss, tt, 3)
+    assert b == tuple(gold["seed1_fleet_k3"]["best"]) and 1.0 / c1 == pytest.approx(gold["seed1_fleet_k3"]["R"], rel=RTOL)

@@ -148,3 +148,15 @@ def test_missing_cell_costs_penalty_times_best():
     assert o2.fleet_rate([1]) == pytest.approx(1 / 8 + 1, rel=1e-15)
     b, rb, ru, rr = o2.fleet_exhaustive(1)
     assert b == (0,) and rb == pytest.approx(1 + 1 / 8, rel=1e-15)   # ties by R; lex-first c0
+
+
+def test_parallel_exhaustive_equals_sequential():
+    """or_fleet_exhaustive_par (first index dealt to threads, used for the full-size
+    golden) returns exactly the sequential search's best, runner-up and rates."""
+    for seed in (13, 14):
+        T, dev = synth.small_matrix(seed, n_cfg=36, n_dev=3, n_inputs=6)
+        o = Oracle(T, dev)
+        o.set_fleet([1.0, 2.0, 3.0], np.linspace(1.0, 2.0, T.shape[0]))
+        for k in (1, 2, 3):
+            for th in (1, 3, 8):
+                assert o.fleet_exhaustive_par(k, threads=th) == o.fleet_exhaustive(k)
