@@ -212,6 +212,26 @@ def measure_scaled(pt, synth, local, pk, steps=3, world=1):
         run()
         ms.append(pt.pt_get_stats(ctx)["greedy_ms"])
     st = pt.pt_get_stats(ctx)
+    km = None
+    if world == 1:
+        # k-means selector at the same shape: 4,096 points x 65,536 dims, k = 32,
+        # bit-identical to the oracle's order of operations; fp64 CUDA cores
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pt.pt_kmeans_select(ctx, 32)
+        e0.record()
+        sel, _, iters = pt.pt_kmeans_select(ctx, 32)
+        e1.record()
+        torch.cuda.synchronize()
+        kms = e0.elapsed_time(e1)
+        nsm = torch.cuda.get_device_properties(local).multi_processor_count
+        dp_peak = nsm * 58.3 * pk.get("sm_max_mhz", 1965.0) * 1e6          # DP instructions / s (ubench_fp64)
+        dp_ops = 3.0 * 4096 * 65536 * (32 * iters + 32 + 1)                 # sub, mul, add per (point, centroid, dim)
+        km = {"workload": "k-means selector, 4,096 envs x 65,536 configs, k=32", "ms": kms, "iterations": iters,
+              "selected": len(sel),
+              "roofline": {"bound": "fp64", "achieved": dp_ops / (kms * 1e-3) / 1e12, "peak": dp_peak / 1e12,
+                           "unit": "T DP-instr/s", "frac": dp_ops / (kms * 1e-3) / dp_peak,
+                           "basis": "distance passes only (init + Lloyd), each (point, centroid, config) a "
+                                    "DSUB + DMUL + DADD in the oracle's order; peak 58.3 DP/clk/SM"}}
     pt.pt_free(ctx)
     del dT
     torch.cuda.empty_cache()
@@ -232,7 +252,7 @@ def measure_scaled(pt, synth, local, pk, steps=3, world=1):
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                          "basis": "4 B per (candidate, env) per step over the whole selection "
                                   "(scan + window pick), MEASURED_PEAKS hbm_gbs (x world for sharded runs)"},
-            "fp64_refined_candidates": st["greedy_candidates"]}
+            "fp64_refined_candidates": st["greedy_candidates"], "kmeans_scaled": km}
 
 
 
