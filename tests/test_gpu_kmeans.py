@@ -62,3 +62,19 @@ def test_many_points_per_pass_init():
         sel, G, it = pt.pt_kmeans_select(ctx, k)
         osel, oit, _ = o.kmeans(k)
         assert sel == osel and it == oit
+
+
+def test_k32_many_tiles_and_chunks():
+    """k = 32 (8 warps of 4 centroids), 2,048 points (64 point tiles), 2,050 configs
+    (33 staged chunks, the last one config wide: the bulk-copy padding double): the device
+    Lloyd loop stays bit-identical to the oracle (selection and iteration count)."""
+    T, dev = synth.scaled(5, n_cfg=2049, n_dev=32, n_inputs=64)
+    o = Oracle(T, dev)
+    ctx = pt.pt_load_perf(T, dev)
+    for k in (32, 5):
+        sel, G, it = pt.pt_kmeans_select(ctx, k)
+        osel, oit, _ = o.kmeans(k)
+        assert sel == osel and it == oit
+    sel, G, it = pt.pt_kmeans_select(ctx, 32, max_iter=3)    # stopped by max_iter, not convergence
+    osel, oit, _ = o.kmeans(32, max_iter=3)
+    assert sel == osel and it == oit == 3

@@ -36,6 +36,15 @@ pt.pt_set_fleet(ctx, qd, qe)
 print("fleet greedy", pt.pt_greedy_select(ctx, 3, objective=pt.PT_OBJ_FLEET)[0])
 print("fleet exh", pt.pt_exhaustive_best(ctx, 2, objective=pt.PT_OBJ_FLEET)["best"])
 print("fleet score", pt.pt_score_sets(ctx, np.array([[0, 1]], np.int32), objective=pt.PT_OBJ_FLEET))
+print("fleet exh tiled k3", pt.pt_exhaustive_best(ctx, 3, objective=pt.PT_OBJ_FLEET)["best"],
+      pt.pt_get_stats(ctx)["exh_kernel"])
+print("fleet exh tiled shard", pt.pt_exhaustive_best(ctx, 3, shard_rank=1, shard_count=2,
+                                                     objective=pt.PT_OBJ_FLEET)["best"])
+# the library-side record exchange + device merge (world 1, stream-ordered callback)
+print("sharded exhaustive", pt.pt_exhaustive_best_sharded(ctx, 3, 0, 1, allgather=lambda m, o, s: o.copy_(m))["best"])
+print("sharded fleet", pt.pt_exhaustive_best_sharded(ctx, 2, 0, 1, allgather=lambda m, o, s: o.copy_(m),
+                                                     objective=pt.PT_OBJ_FLEET)["best"])
+print("kmeans k8", pt.pt_kmeans_select(ctx, 8, max_iter=4))
 pt.pt_free(ctx)
 print("sanitize driver done")
 # multi-stage column tiles (E_pad = 192: three 64-env stages per tile, the ring wraps
