@@ -337,7 +337,7 @@ struct XParams {
     unsigned *U;              // float bits: min over warps of their 2nd-smallest upper bound
     unsigned long long *cand_key;
     float *cand_s;
-    unsigned *cand_n;
+    unsigned long long *cand_n;   // 64-bit: more than 2^32 survivors cannot wrap it
     unsigned cap;
     const uint16_t *hT;
     const uint16_t *hTile;
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(XT_TCONS, FLEET ? 1 : XT_MINB) k_exh_tiled(con
                             for (int j = 0; j < 4; j++) {
                                 const float ub = __fmul_ru(rate[i][j], p.c3);
                                 if (rate[i][j] > -INFINITY && ub >= tau) {
-                                    const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                    const unsigned long long idx = atomicAdd(p.cand_n, 1ull);
                                     if (idx < p.cap) {
                                         p.cand_key[idx] = ((unsigned long long)(R0 + XT_ROW(i, j)) << KEY_BITS) |
                                                           (unsigned long long)(ltile + XT_COL(i, j));
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(XT_TCONS, FLEET ? 1 : XT_MINB) k_exh_tiled(con
                             for (int j = 0; j < 4; j++) {
                                 const float lb = __fmaf_rd(acc[i][j], p.c1, -p.c2);
                                 if (acc[i][j] < INFINITY && lb <= tau) {
-                                    const unsigned idx = atomicAdd(p.cand_n, 1u);
+                                    const unsigned long long idx = atomicAdd(p.cand_n, 1ull);
                                     if (idx < p.cap) {
                                         p.cand_key[idx] = ((unsigned long long)(R0 + XT_ROW(i, j)) << KEY_BITS) |
                                                           (unsigned long long)(ltile + XT_COL(i, j));
@@ -781,12 +781,12 @@ __global__ void __launch_bounds__(256) k_top2(const double *__restrict__ s, cons
 // block top-2 and publishes it; the last block to finish (a counter it then resets)
 // merges the block records.  One launch instead of refine + k_top2.
 __global__ void __launch_bounds__(256) k_exh_refine_top2(
-    const unsigned long long *__restrict__ key, const float *__restrict__ cs, const unsigned *__restrict__ n_dev,
+    const unsigned long long *__restrict__ key, const float *__restrict__ cs, const unsigned long long *__restrict__ n_dev,
     unsigned cap, float tau_pass, const unsigned *__restrict__ U, int m, int64_t C, const double *__restrict__ l64,
     int64_t E_pad, Rec2 *__restrict__ blk, unsigned *__restrict__ done, double *__restrict__ out_s,
     int32_t *__restrict__ out_t)
 {
-    const int64_t n = min(*n_dev, cap);
+    const int64_t n = (int64_t)min(*n_dev, (unsigned long long)cap);
     const float tau = fminf(tau_pass, __uint_as_float(*U));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int k = m + 1;
@@ -1107,13 +1107,13 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     }
 
     unsigned cap = 1u << 20;
-    unsigned n_cand = 0;
+    unsigned long long n_cand = 0;
     float tau_pass = tau_seed;
     for (int pass = 0; pass < 2; pass++) {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
         const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)),
-                     o_n = take(sizeof(unsigned)), o_key = take(sizeof(unsigned long long) * cap),
+                     o_n = take(sizeof(unsigned long long)), o_key = take(sizeof(unsigned long long) * cap),
                      o_cq = take(sizeof(float) * cap),
                      o_os = take(sizeof(double) * 2), o_ot = take(sizeof(int32_t) * 2 * k),
                      o_blk = take(sizeof(Rec2) * (size_t)ctx->num_sms * 2), o_done = take(sizeof(unsigned));
@@ -1121,7 +1121,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         PT_TRY(pt_scratch(ctx, off, &scr));
         char *b = (char *)scr;
         int *ctr = (int *)(b + o_ctr);
-        unsigned *U = (unsigned *)(b + o_U), *cn = (unsigned *)(b + o_n);
+        unsigned *U = (unsigned *)(b + o_U);
+        unsigned long long *cn = (unsigned long long *)(b + o_n);
         unsigned long long *ckey = (unsigned long long *)(b + o_key);
         float *cq = (float *)(b + o_cq);
         double *os = (double *)(b + o_os);
@@ -1137,7 +1138,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         } else {
             PT_TRY(io.h2d(U, &u_init, sizeof(unsigned)));
         }
-        PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned), s));
+        PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned long long), s));
         PT_CK(cudaMemsetAsync(done, 0, sizeof(unsigned), s));
         XParams p;
         p.C = v->C;
@@ -1177,7 +1178,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         pt_pack_record(ctx, os, ot, k);   // sharded search: this rank's record stays on the device
         PT_CK(cudaGetLastError());
         unsigned hU = 0;
-        PT_TRY(io.d2h(&n_cand, cn, sizeof(unsigned)));
+        PT_TRY(io.d2h(&n_cand, cn, sizeof(unsigned long long)));
         PT_TRY(io.d2h(&hU, U, sizeof(unsigned)));
         PT_TRY(io.d2h(s_out, os, sizeof(double) * 2));
         PT_TRY(io.d2h(t_out, ot, sizeof(int32_t) * 2 * k));
@@ -1191,7 +1192,10 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         memcpy(&Uf, &hU, sizeof Uf);
         if (n_cand > cap) {
             // overflow: rerun with the final threshold and room for every survivor
-            cap = n_cand;
+            if (n_cand > (1ull << 28))
+                return pt_fail(PT_ECAP, "%llu fp16-tier survivors (massively tied data): above the 2^28 buffer limit",
+                               n_cand);
+            cap = (unsigned)n_cand;
             tau_pass = std::min(tau_pass, Uf);
             continue;
         }
@@ -1213,13 +1217,13 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
 // exact R of every candidate whose rate upper bound reaches the final threshold,
 // fused with the (cost = 1/R, tuple) top-2 (last-block merge, as k_exh_refine_top2)
 __global__ void __launch_bounds__(256) k_fleet_refine_top2(
-    const unsigned long long *__restrict__ key, const float *__restrict__ cub, const unsigned *__restrict__ n_dev,
+    const unsigned long long *__restrict__ key, const float *__restrict__ cub, const unsigned long long *__restrict__ n_dev,
     unsigned cap, float tau_pass, const unsigned *__restrict__ U, int m, int64_t C,
     const double *__restrict__ tcm, int64_t E_pad, const double *__restrict__ w, const int32_t *__restrict__ seg,
     int n_devices, const double *__restrict__ qdev, Rec2 *__restrict__ blk, unsigned *__restrict__ done,
     double *__restrict__ out_s, int32_t *__restrict__ out_t)
 {
-    const int64_t n = min(*n_dev, cap);
+    const int64_t n = (int64_t)min(*n_dev, (unsigned long long)cap);
     const float tau = fmaxf(tau_pass, __uint_as_float(*U));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int k = m + 1;
@@ -1410,12 +1414,13 @@ pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, 
             occ = it->second;
         }
     }
-    unsigned cap = 1u << 20, n_cand = 0;
+    unsigned cap = 1u << 20;
+    unsigned long long n_cand = 0;
     float tau_pass = tau_seed;
     for (int pass = 0; pass < 2; pass++) {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
-        const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)), o_n = take(sizeof(unsigned)),
+        const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)), o_n = take(sizeof(unsigned long long)),
                      o_key = take(sizeof(unsigned long long) * cap), o_cq = take(sizeof(float) * cap),
                      o_os = take(sizeof(double) * 2), o_ot = take(sizeof(int32_t) * 2 * k),
                      o_blk = take(sizeof(Rec2) * (size_t)ctx->num_sms * 2), o_done = take(sizeof(unsigned));
@@ -1423,7 +1428,8 @@ pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, 
         PT_TRY(pt_scratch(ctx, off, &scr));
         char *b = (char *)scr;
         int *ctr = (int *)(b + o_ctr);
-        unsigned *U = (unsigned *)(b + o_U), *cn = (unsigned *)(b + o_n), *done = (unsigned *)(b + o_done);
+        unsigned *U = (unsigned *)(b + o_U), *done = (unsigned *)(b + o_done);
+        unsigned long long *cn = (unsigned long long *)(b + o_n);
         unsigned long long *ckey = (unsigned long long *)(b + o_key);
         float *cq = (float *)(b + o_cq);
         double *os = (double *)(b + o_os);
@@ -1432,7 +1438,7 @@ pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, 
         pt_hostio io(ctx);
         PT_TRY(io.h2d(ctr, &ta, sizeof(int)));
         PT_CK(cudaMemsetAsync(U, 0, sizeof(unsigned), s));   // 0.0f: no lower bound yet
-        PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned), s));
+        PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned long long), s));
         PT_CK(cudaMemsetAsync(done, 0, sizeof(unsigned), s));
         XParams p{};
         p.C = v->C;
@@ -1468,7 +1474,7 @@ pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, 
         pt_pack_record(ctx, os, ot, k);
         PT_CK(cudaGetLastError());
         unsigned hU = 0;
-        PT_TRY(io.d2h(&n_cand, cn, sizeof(unsigned)));
+        PT_TRY(io.d2h(&n_cand, cn, sizeof(unsigned long long)));
         PT_TRY(io.d2h(&hU, U, sizeof(unsigned)));
         PT_TRY(io.d2h(sv, os, sizeof(double) * 2));
         PT_TRY(io.d2h(t.data(), ot, sizeof(int32_t) * 2 * k));
@@ -1480,7 +1486,10 @@ pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, 
         float Uf;
         memcpy(&Uf, &hU, sizeof Uf);
         if (n_cand > cap) {   // overflow: rerun with the final threshold and room for every survivor
-            cap = n_cand;
+            if (n_cand > (1ull << 28))
+                return pt_fail(PT_ECAP, "%llu fp16-tier survivors (massively tied data): above the 2^28 buffer limit",
+                               n_cand);
+            cap = (unsigned)n_cand;
             tau_pass = std::max(tau_pass, Uf);
             continue;
         }
