@@ -217,6 +217,51 @@ __global__ void __launch_bounds__(1024) k_km_pick(const double *__restrict__ v, 
         }
 }
 
+// small scopes (ne <= KM_PAIR_MAX): every point's distance to every point and to the mean
+// (column ne) in one pass -- P[q][r] is exactly what k_km_dist returns for point q and a
+// centroid that is a copy of point r (same c-ascending sum) -- so the maximin init needs
+// no further distance pass
+#define KM_PAIR_MAX 1024
+__global__ void __launch_bounds__(128) k_km_pair(const double *__restrict__ Xt, int64_t ne, int64_t C,
+                                                const double *__restrict__ mean, double *__restrict__ P)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ne * (ne + 1)) return;
+    const int64_t q = i % ne, r = i / ne;
+    const double *xq = Xt + (q >> 5) * C * 32 + (q & 31);
+    const double *xr = r < ne ? Xt + (r >> 5) * C * 32 + (r & 31) : nullptr;
+    double acc = 0.0;
+    int64_t c = 0;
+    for (; c + 8 <= C; c += 8) {   // 8 operand pairs in flight, then the sums in c order
+        double x[8], y[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            x[u] = xq[(c + u) * 32];
+            y[u] = xr ? xr[(c + u) * 32] : mean[c + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const double d = __dsub_rn(x[u], y[u]);
+            acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
+    }
+    for (; c < C; c++) {
+        const double d = __dsub_rn(xq[c * 32], xr ? xr[c * 32] : mean[c]);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    P[q * (ne + 1) + r] = acc;
+}
+
+// init helper (pairwise path): dmin[q] = P[q][*col] (first) or min(dmin[q], P[q][*col])
+__global__ void k_km_dmin_col(const double *__restrict__ P, int64_t ne, const int64_t *__restrict__ col, int first,
+                              double *__restrict__ dmin)
+{
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= ne) return;
+    const double d = P[q * (ne + 1) + *col];
+    dmin[q] = first ? d : fmin(dmin[q], d);
+}
+
 // init helper: dmin[q] = D[q][0] (first) or min(dmin[q], D[q][0])
 __global__ void k_km_dmin(const double *__restrict__ D, int64_t ne, int first, double *__restrict__ dmin)
 {
@@ -409,18 +454,39 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
             k_km_dist<KM_JW><<<(unsigned)nt, 32 * ((nc + KM_JW - 1) / KM_JW), smem_of(nc), s>>>(X, ne, C, cent, nc, D, c);
     };
     const unsigned gc = (unsigned)((C + 127) / 128), gq = (unsigned)((ne + 255) / 256);
-    // init: the point nearest the mean, then successive farthest points (maximin)
+    // init: the point nearest the mean, then successive farthest points (maximin).  Every
+    // init centroid is a copy of a point, so small scopes read one pairwise pass; larger
+    // ones run one single-centroid distance pass per centroid.
     k_km_mean<<<gc, 128, 0, s>>>(X, ne, C, mean);
-    dist(mean, 1, nullptr);
-    k_km_pick<<<1, 1024, 0, s>>>(D, KM_MAXK, ne, 0, X, C, 0, k, M, cent1, nullptr);
-    dist(cent1, 1, nullptr);
-    k_km_dmin<<<gq, 256, 0, s>>>(D, ne, 1, dmin);
-    ctx->stats.launches += 6;
-    for (int j = 1; j < k; j++) {
-        k_km_pick<<<1, 1024, 0, s>>>(dmin, 1, ne, 1, X, C, j, k, M, cent1, nullptr);
-        dist(cent1, 1, nullptr);
-        k_km_dmin<<<gq, 256, 0, s>>>(D, ne, 0, dmin);
+    ctx->stats.launches++;
+    if (ne <= KM_PAIR_MAX) {
+        double *P = nullptr;
+        int64_t *pq = nullptr;
+        PT_TRY(pt_dalloc(ctx, (void **)&P, sizeof(double) * ne * (ne + 1)));
+        PT_TRY(pt_dalloc(ctx, (void **)&pq, sizeof(int64_t)));
+        k_km_pair<<<(unsigned)((ne * (ne + 1) + 127) / 128), 128, 0, s>>>(X, ne, C, mean, P);
+        k_km_pick<<<1, 1024, 0, s>>>(P + ne, ne + 1, ne, 0, X, C, 0, k, M, cent1, pq);
+        k_km_dmin_col<<<gq, 256, 0, s>>>(P, ne, pq, 1, dmin);
         ctx->stats.launches += 3;
+        for (int j = 1; j < k; j++) {
+            k_km_pick<<<1, 1024, 0, s>>>(dmin, 1, ne, 1, X, C, j, k, M, cent1, pq);
+            k_km_dmin_col<<<gq, 256, 0, s>>>(P, ne, pq, 0, dmin);
+            ctx->stats.launches += 2;
+        }
+        pt_dfree(ctx, P);
+        pt_dfree(ctx, pq);
+    } else {
+        dist(mean, 1, nullptr);
+        k_km_pick<<<1, 1024, 0, s>>>(D, KM_MAXK, ne, 0, X, C, 0, k, M, cent1, nullptr);
+        dist(cent1, 1, nullptr);
+        k_km_dmin<<<gq, 256, 0, s>>>(D, ne, 1, dmin);
+        ctx->stats.launches += 5;
+        for (int j = 1; j < k; j++) {
+            k_km_pick<<<1, 1024, 0, s>>>(dmin, 1, ne, 1, X, C, j, k, M, cent1, nullptr);
+            dist(cent1, 1, nullptr);
+            k_km_dmin<<<gq, 256, 0, s>>>(D, ne, 0, dmin);
+            ctx->stats.launches += 3;
+        }
     }
     PT_CK(cudaGetLastError());
     // Lloyd, enqueued in batches of passes; a pass after the stop flag returns at once

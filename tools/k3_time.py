@@ -1,0 +1,15 @@
+"""k=3 kernel time at the paper shape, 5 reps (development aid; PT_LIB selects a variant)."""
+import os
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+from paper_2507_15277_b200 import pt, synth  # noqa: E402
+T, dev = synth.paper_matrix(1)
+ctx = pt.pt_load_perf(torch.from_numpy(T).cuda(), dev)
+ms = []
+for rep in range(6):
+    r = pt.pt_exhaustive_best(ctx, 3)
+    ms.append(pt.pt_get_stats(ctx)["exh_main_ms"])
+print(os.environ.get("PT_LIB", "default"), r["best"], "k3 kernel ms", [round(x, 3) for x in ms[1:]],
+      "median", round(float(np.median(ms[1:])), 3), flush=True)

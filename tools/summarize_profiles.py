@@ -24,7 +24,7 @@ for r in rows:
     cnt[n] += 1
 S = sum(tot.values())
 lines = [f"# ncu launch list ({launches}): ncu --metrics gpu__time_duration.sum --clock-control none",
-         "#   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-scaled",
+         "#   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-scaled [--no-next]",
          "# (3 device-resident + 3 e2e steps).  Per-launch times are cold-cache and serialised:",
          "# compare SHARES, not absolutes.",
          f"{'kernel':60s} {'launches':>8s} {'total_ms':>10s} {'share':>7s}"]
