@@ -16,6 +16,7 @@
 #include <cmath>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <cuda_fp16.h>
 
 #include "pt_internal.cuh"
@@ -182,6 +183,85 @@ __global__ void __launch_bounds__(1024) k_fleet_greedy_pick(const double *__rest
     __syncthreads();
     const double *col = tcm + (int64_t)cstar * E_pad;
     for (int64_t q = threadIdx.x; q < E_pad; q += blockDim.x) cur[q] = fmin(cur[q], col[q]);
+}
+
+// the whole fleet greedy in one cooperative launch (as k_greedy_resident for Eq. 1): the
+// current per-env minima live in every CTA's shared memory; per step every warp scores
+// its candidates (fleet_rate_warp, fp64, the scan kernel's order), each CTA keeps its
+// (R desc, c asc) top-2, one grid barrier, every CTA merges the same block records and
+// commits the same winner.  One launch for k steps instead of 2 k.
+namespace cgf = cooperative_groups;
+__global__ void __launch_bounds__(256) k_fleet_greedy_resident(
+    const double *__restrict__ tcm, int64_t E_pad, int64_t C, int k, const double *__restrict__ w,
+    const int32_t *__restrict__ seg, int n_dev, const double *__restrict__ qdev, double4 *__restrict__ blk,
+    int32_t *__restrict__ out_idx, double *__restrict__ r1_tr, double *__restrict__ r2_tr)
+{
+    extern __shared__ double fsm[];
+    double *cur = fsm;
+    uint32_t *taken = reinterpret_cast<uint32_t *>(cur + E_pad);
+    __shared__ double wr1[8], wr2[8];
+    __shared__ int wc1[8], wc2[8];
+    __shared__ int cstar;
+    cgf::grid_group grid = cgf::this_grid();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nwords = (C + 31) / 32;
+    for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) cur[e] = INFINITY;
+    for (int64_t q = threadIdx.x; q < nwords; q += blockDim.x) taken[q] = 0u;
+    __syncthreads();
+    const int64_t gw = (int64_t)blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
+    for (int t = 0; t < k; t++) {
+        double r1 = -INFINITY, r2 = -INFINITY;
+        int c1 = FL_BIGI, c2 = FL_BIGI;
+        for (int64_t c = gw; c < C; c += nw) {
+            if (taken[c >> 5] >> (c & 31) & 1u) continue;
+            const double r = fleet_rate_warp(cur, tcm + c * E_pad, w, seg, n_dev, qdev, lane);
+            top2_max(r1, c1, r2, c2, r, (int)c);
+        }
+        if (lane == 0) {
+            wr1[warp] = r1;
+            wr2[warp] = r2;
+            wc1[warp] = c1;
+            wc2[warp] = c2;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 1; q < 8; q++) {
+                top2_max(r1, c1, r2, c2, wr1[q], wc1[q]);
+                top2_max(r1, c1, r2, c2, wr2[q], wc2[q]);
+            }
+            blk[(t & 1) * gridDim.x + blockIdx.x] = make_double4(r1, r2, (double)c1, (double)c2);
+        }
+        grid.sync();
+        if (warp == 0) {
+            r1 = r2 = -INFINITY;
+            c1 = c2 = FL_BIGI;
+            for (int b = lane; b < (int)gridDim.x; b += 32) {
+                const double4 rec = blk[(t & 1) * gridDim.x + b];
+                top2_max(r1, c1, r2, c2, rec.x, (int)rec.z);
+                top2_max(r1, c1, r2, c2, rec.y, (int)rec.w);
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double a1 = __shfl_xor_sync(0xffffffffu, r1, o), a2 = __shfl_xor_sync(0xffffffffu, r2, o);
+                const int b1 = __shfl_xor_sync(0xffffffffu, c1, o), b2 = __shfl_xor_sync(0xffffffffu, c2, o);
+                top2_max(r1, c1, r2, c2, a1, b1);
+                top2_max(r1, c1, r2, c2, a2, b2);
+            }
+            if (lane == 0) {
+                cstar = c1;
+                if (blockIdx.x == 0) {
+                    out_idx[t] = c1;
+                    r1_tr[t] = r1;
+                    r2_tr[t] = r2;
+                }
+            }
+        }
+        __syncthreads();
+        const int cs = cstar;
+        if (threadIdx.x == 0) taken[cs >> 5] |= 1u << (cs & 31);
+        const double *col = tcm + (int64_t)cs * E_pad;
+        for (int64_t e = threadIdx.x; e < E_pad; e += blockDim.x) cur[e] = fmin(cur[e], col[e]);
+        __syncthreads();
+    }
 }
 
 // exhaustive: thread per subset (colex rank), per-device accumulators in
@@ -516,12 +596,36 @@ pt_status pt_fleet_greedy(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32
     k_fill_inf<<<(unsigned)((E_pad + 255) / 256), 256, 0, s>>>(cur, E_pad);
     ctx->stats.launches++;
     const int grid = (int)std::min<int64_t>((C * 32 + 255) / 256, (int64_t)ctx->num_sms * 8);
+    // one cooperative launch for all k steps when the current minima fit in shared memory
+    const size_t rsmem = sizeof(double) * E_pad + sizeof(uint32_t) * nwords;
+    int occ = 0;
+    if (rsmem <= 200 * 1024) {
+        if (rsmem > 48 * 1024)
+            PT_CK(cudaFuncSetAttribute(k_fleet_greedy_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)rsmem));
+        PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fleet_greedy_resident, 256, rsmem));
+    }
     PT_CK(cudaEventRecord(ctx->ev0, s));
-    for (int t = 0; t < k; t++) {
-        k_fleet_greedy_scan<<<grid, 256, 0, s>>>(ctx->fl.tcm, E_pad, C, cur, taken, w, ctx->fl.seg,
-                                                 ctx->fl.n_dev, ctx->fl.qdev, R);
-        k_fleet_greedy_pick<<<1, 1024, 0, s>>>(R, C, ctx->fl.tcm, E_pad, cur, taken, t, d_idx, r1, r2);
-        ctx->stats.launches += 2;
+    if (occ >= 1) {
+        const int nblk = ctx->num_sms * std::min(occ, 2);
+        double4 *blk = nullptr;
+        PT_TRY(pt_dalloc(ctx, (void **)&blk, sizeof(double4) * 2 * nblk));
+        const double *tcm = ctx->fl.tcm, *qd = ctx->fl.qdev;
+        const int32_t *sg = ctx->fl.seg;
+        int nd = ctx->fl.n_dev, kk = k;
+        int64_t EE = E_pad, CC = C;
+        void *args[] = {(void *)&tcm, (void *)&EE, (void *)&CC, (void *)&kk, (void *)&w, (void *)&sg,
+                        (void *)&nd, (void *)&qd, (void *)&blk, (void *)&d_idx, (void *)&r1, (void *)&r2};
+        PT_CK(cudaLaunchCooperativeKernel((void *)k_fleet_greedy_resident, dim3(nblk), dim3(256), args, rsmem, s));
+        ctx->stats.launches++;
+        pt_dfree(ctx, blk);
+    } else {
+        for (int t = 0; t < k; t++) {
+            k_fleet_greedy_scan<<<grid, 256, 0, s>>>(ctx->fl.tcm, E_pad, C, cur, taken, w, ctx->fl.seg,
+                                                     ctx->fl.n_dev, ctx->fl.qdev, R);
+            k_fleet_greedy_pick<<<1, 1024, 0, s>>>(R, C, ctx->fl.tcm, E_pad, cur, taken, t, d_idx, r1, r2);
+            ctx->stats.launches += 2;
+        }
     }
     PT_CK(cudaEventRecord(ctx->ev1, s));
     PT_CK(cudaGetLastError());
