@@ -451,7 +451,7 @@ def main():
         extra = [0.0] * world
         extra[0] += 0.24
         extra[1 % world] += 0.16
-        extra[2 % world] += 0.18
+        extra[2 % world] += 0.12
         shard_w = [max(0.2, 1.0 - x * world / 12.0) for x in extra]
 
     def step(src):

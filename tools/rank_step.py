@@ -25,7 +25,7 @@ for N in (1, 2, 4, 8):
                 extra = [0.0] * N
                 extra[0] += 0.24
                 extra[1 % N] += 0.16
-                extra[2 % N] += 0.18
+                extra[2 % N] += 0.12
                 pt.pt_set_shard_weights(ctx, [max(0.2, 1.0 - x * N / 12.0) for x in extra])
             if r == 0:
                 pt.pt_greedy_select(ctx, 24)
