@@ -540,10 +540,22 @@ def _library_comm(group, rank, world):
     import torch.distributed as dist
     key = (id(group), world, torch.cuda.current_device())
     if key not in _COMMS:
-        obj = [pt_comm_unique_id() if rank == 0 else None]
+        # rank 0 makes the id (or reports why it cannot); every rank sees the same outcome,
+        # so either all ranks build the communicator or all take the fallback
+        obj = [None]
+        if rank == 0:
+            try:
+                obj = [pt_comm_unique_id()]
+            except PTError as ex:
+                obj = [f"error: {ex}"]
         dist.broadcast_object_list(obj, src=0 if group is None else dist.get_global_rank(group, 0),
                                    group=group)
-        _COMMS[key] = pt_comm_init(obj[0], rank, world)
+        if isinstance(obj[0], str):
+            _COMMS[key] = None
+        else:
+            _COMMS[key] = pt_comm_init(obj[0], rank, world)
+    if _COMMS[key] is None:
+        raise PTError(PT_ENCCL, "pt_comm_unique_id", "NCCL unavailable on rank 0")
     return _COMMS[key]
 
 
@@ -575,8 +587,22 @@ def exhaustive_best_distributed(ctx, k, env_mask=None, group=None, objective=PT_
         E = n_env if env_mask is None else int(np.count_nonzero(env_mask))
         return pt_merge_records(torch.cat(allr).numpy(), k, E, objective)
     if init and dist.get_backend(group) == "nccl":
-        return pt_exhaustive_best_sharded(ctx, k, rank, world, comm=_library_comm(group, rank, world),
-                                          env_mask=env_mask, objective=objective)
+        comm = None
+        try:
+            comm = _library_comm(group, rank, world)
+        except PTError as ex:   # e.g. no libnccl.so.2 visible to dlopen: same exchange via torch's NCCL
+            import warnings
+            warnings.warn(f"library NCCL communicator unavailable ({ex}); exchanging records through "
+                          "torch.distributed on the library's stream")
+        if comm is not None:
+            return pt_exhaustive_best_sharded(ctx, k, rank, world, comm=comm, env_mask=env_mask,
+                                              objective=objective)
+
+        def nccl_allgather(mine, out, stream):
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(out, mine, group=group)
+        return pt_exhaustive_best_sharded(ctx, k, rank, world, allgather=nccl_allgather, env_mask=env_mask,
+                                          objective=objective)
 
     def host_allgather(mine, out, stream):      # gloo (or no group): host-staged
         if world == 1:
