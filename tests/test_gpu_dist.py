@@ -221,3 +221,29 @@ def test_library_nccl_comm_world1():
         pt.pt_exhaustive_best_sharded(ctx, 2, 0, 2, comm=comm)
     assert ei.value.code == pt.PT_EINVAL
     comm.close()
+
+
+def test_library_exchange_callback_failure():
+    """A failing exchange is reported as PT_ENCCL (pt.h) -- the caller's exception is
+    re-raised by the binding after the C call returns."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    T, dev = synth.small_matrix(16, n_cfg=120, n_dev=2, n_inputs=8)
+    ctx = pt.pt_load_perf(T, dev)
+
+    def broken(mine, out, stream):
+        raise RuntimeError("link down")
+    with pytest.raises(RuntimeError, match="link down"):
+        pt.pt_exhaustive_best_sharded(ctx, 2, 0, 1, allgather=broken)
+    # the context stays usable afterwards
+    assert pt.pt_exhaustive_best_sharded(ctx, 2, 0, 1, allgather=lambda m, o, s: o.copy_(m))["best"] == \
+        pt.pt_exhaustive_best(ctx, 2)["best"]
+    with pytest.raises(pt.PTError) as ei:               # neither comm nor callback
+        lib = pt.lib()
+        import ctypes as ct
+        b = (ct.c_int32 * 2)()
+        g = (ct.c_double * 2)()
+        rc = lib.pt_exhaustive_best_sharded(ctx.handle, 2, None, 0, 0, 1, None, ct.cast(None, pt.DEV_ALLGATHER_FN),
+                                            None, b, ct.byref(g, 0), None, None, None)
+        pt._chk(rc, "pt_exhaustive_best_sharded")
+    assert ei.value.code == pt.PT_EINVAL
