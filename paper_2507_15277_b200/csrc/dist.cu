@@ -314,7 +314,10 @@ extern "C" pt_status pt_exhaustive_best_sharded(pt_ctx *ctx, int32_t k, const ui
     // 2. the exchange, stream-ordered on the context's stream
     if (comm) {
         const nccl_api *n = nullptr;
-        PT_TRY(nccl_load(&n));
+        if (const pt_status ls = nccl_load(&n); ls != PT_OK) {
+            pt_dfree(ctx, b);
+            return ls;
+        }
         const ncclResult_t r = n->all_gather(mine, all, (size_t)L, ncclFloat64, comm->comm, s);
         if (r != ncclSuccess) {
             pt_dfree(ctx, b);
@@ -331,10 +334,11 @@ extern "C" pt_status pt_exhaustive_best_sharded(pt_ctx *ctx, int32_t k, const ui
     std::vector<double> out(4 + 2 * k);
     int hst = 0;
     pt_hostio io(ctx);
-    PT_TRY(io.d2h(out.data(), dout, sizeof(double) * out.size()));
-    PT_TRY(io.d2h(&hst, dst, sizeof(int)));
-    PT_TRY(io.finish());
+    pt_status ios = io.d2h(out.data(), dout, sizeof(double) * out.size());
+    if (ios == PT_OK) ios = io.d2h(&hst, dst, sizeof(int));
+    if (ios == PT_OK) ios = io.finish();
     pt_dfree(ctx, b);
+    if (ios != PT_OK) return ios;
     if (hst == 1) return pt_fail(PT_EINVAL, "shard plans differ across ranks (record fingerprints disagree)");
     if (hst == 2) return pt_fail(PT_EEMPTY, "no k-subset in any shard");
     for (int u = 0; u < k; u++) {
