@@ -1091,11 +1091,11 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const int threads = XT_TCONS;
     // per (kernel, smem) once per process: the attribute and the occupancy query
     static std::mutex attr_mu;
-    static std::map<std::pair<const void *, size_t>, int> attr_occ;
+    static std::map<std::tuple<int, const void *, size_t>, int> attr_occ;   // per device
     int occ = 1;
     {
         std::lock_guard<std::mutex> g(attr_mu);
-        auto key = std::make_pair(kfn, smem_k);
+        auto key = std::make_tuple(ctx->dev, kfn, smem_k);
         auto it = attr_occ.find(key);
         if (it == attr_occ.end()) {
             PT_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k));
@@ -1401,15 +1401,15 @@ pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, 
     const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * ft->E_fp * XT_R +
                         sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
     static std::mutex mu;
-    static std::map<size_t, int> occ_cache;
+    static std::map<std::pair<int, size_t>, int> occ_cache;   // (device, smem) -> blocks per SM
     int occ = 1;
     {
         std::lock_guard<std::mutex> g(mu);
-        auto it = occ_cache.find(smem);
+        auto it = occ_cache.find(std::make_pair(ctx->dev, smem));
         if (it == occ_cache.end()) {
             PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT_TCONS, smem));
-            occ_cache[smem] = occ;
+            occ_cache[std::make_pair(ctx->dev, smem)] = occ;
         } else {
             occ = it->second;
         }

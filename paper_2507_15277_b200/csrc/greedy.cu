@@ -673,17 +673,17 @@ pt_status pt_greedy_seed_enqueue(pt_ctx *ctx, const pt_view *v, int32_t k)
     cudaStream_t s = ctx->stream;
     const size_t smem = sizeof(double) * E_pad + sizeof(uint32_t) * nwords;
     static std::mutex mu;
-    static std::map<size_t, int> occ_cache;   // dynamic smem -> blocks per SM
+    static std::map<std::pair<int, size_t>, int> occ_cache;   // (device, dynamic smem) -> blocks per SM
     int occ = 0;
     {
         std::lock_guard<std::mutex> g(mu);
-        auto it = occ_cache.find(smem);
+        auto it = occ_cache.find(std::make_pair(ctx->dev, smem));
         if (it == occ_cache.end()) {
             if (smem > 48 * 1024)
                 PT_CK(cudaFuncSetAttribute(k_greedy_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
             PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_resident, 256, smem));
-            occ_cache[smem] = occ;
+            occ_cache[std::make_pair(ctx->dev, smem)] = occ;
         } else {
             occ = it->second;
         }

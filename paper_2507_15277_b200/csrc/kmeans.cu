@@ -16,6 +16,7 @@
 // every few passes (no round trip per pass).
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "pt_internal.cuh"
@@ -440,12 +441,14 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
     k_km_build<<<dim3((unsigned)C, (unsigned)nt), 32, 0, s>>>(ctx->T32, C, ctx->best, ctx->penalty, d_envs, ne, X);
     // M is config-major, Mt[c][k]: a chunk of all centroids is one contiguous block
     auto smem_of = [](int nc) { return sizeof(double) * KM_NS * KM_CB * (32 + nc) + sizeof(uint64_t) * KM_NS; };
-    static bool attr = false;
-    if (!attr) {
+    static std::mutex attr_mu;
+    static uint64_t attr_done = 0;   // bit d: attributes set on device d
+    std::lock_guard<std::mutex> attr_g(attr_mu);
+    if (!(attr_done >> (ctx->dev & 63) & 1ull)) {
         PT_CK(cudaFuncSetAttribute(k_km_dist<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(1)));
         PT_CK(cudaFuncSetAttribute(k_km_dist<KM_JW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem_of(KM_MAXK)));
-        attr = true;
+        attr_done |= 1ull << (ctx->dev & 63);
     }
     auto dist = [&](const double *cent, int nc, const KmCtl *c) {
         if (nc == 1)
