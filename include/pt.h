@@ -323,6 +323,17 @@ pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int3
                            int32_t *out_idx, int32_t *out_n, double *out_G, int32_t *out_iters);
 
 /*
+ * pt_kmeans_select_from -- pt_kmeans_select from a given start instead of the maximin
+ * initialisation: init host double[k][C] (row j = centroid j in the slowdown space of
+ * the points, T/best per configuration), copied.  Same Lloyd loop, re-seed rule and
+ * selection; bit-identical to the oracle's or_kmeans_from.
+ * Errors: as pt_kmeans_select; PT_EINVAL if init is NULL.
+ */
+pt_status pt_kmeans_select_from(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t max_iter,
+                                const double *init, int32_t *out_idx, int32_t *out_n, double *out_G,
+                                int32_t *out_iters);
+
+/*
  * pt_set_fleet -- quantities for the fleet objective, Eq. 2:
  *   R(S) = sum_d quantity(d) / sum_{i} y'_{d,i}(S) * quantity(i),
  *   y'_{d,i}(S) = min_{c in S} T[(d,i)][c]  (best member; a missing cell costs

@@ -52,9 +52,10 @@ def _load():
                                                 P, P, P, P, P]
         lib.or_swap_search.argtypes = [P, i64, i64, P, ct.c_int, P, ct.c_int, P, P, P]
         lib.or_kmeans.argtypes = [P, i64, i64, P, dbl, P, ct.c_int, ct.c_int, P, P, P, P]
+        lib.or_kmeans_from.argtypes = [P, i64, i64, P, dbl, P, ct.c_int, ct.c_int, P, P, P, P, P]
         for f in (lib.or_normalize, lib.or_score, lib.or_exhaustive, lib.or_greedy,
                   lib.or_holdout, lib.or_fleet_rate, lib.or_fleet_exhaustive, lib.or_fleet_greedy,
-                  lib.or_swap_search, lib.or_kmeans, lib.or_fleet_exhaustive_par):
+                  lib.or_swap_search, lib.or_kmeans, lib.or_fleet_exhaustive_par, lib.or_kmeans_from):
             f.restype = ct.c_int
         _lib = lib
     return _lib
@@ -177,6 +178,19 @@ class Oracle:
         w = np.zeros(max_iter)
         _chk(_load().or_kmeans(_p(self.T), self.E, self.C, _p(self.best), self.penalty, _p(m), k,
                                max_iter, _p(sel), _p(n), _p(it), _p(w)), "or_kmeans")
+        return tuple(int(x) for x in sel[:n[0]]), int(it[0]), w[:it[0]]
+
+    def kmeans_from(self, init, mask=None, max_iter=100):
+        """k-means from given initial centroids (init: [k][C] slowdowns): (selection, iterations, wcss)."""
+        m = self._mask(mask)
+        init = np.ascontiguousarray(init, dtype=np.float64)
+        k = init.shape[0]
+        sel = np.zeros(k, np.int32)
+        n = np.zeros(1, np.int32)
+        it = np.zeros(1, np.int32)
+        w = np.zeros(max_iter)
+        _chk(_load().or_kmeans_from(_p(self.T), self.E, self.C, _p(self.best), self.penalty, _p(m), k, max_iter,
+                                    _p(init), _p(sel), _p(n), _p(it), _p(w)), "or_kmeans_from")
         return tuple(int(x) for x in sel[:n[0]]), int(it[0]), w[:it[0]]
 
     # ---- fleet objective (Eq. 2) --------------------------------------------

@@ -17,11 +17,9 @@
  *
  * Parity status of each function: see DESIGN.md "Oracle pins".  All
  * functions below are pinned (tests/test_oracle*.py, mutation-checked by
- * tools/oracle_mutants.py).  One branch is "parity unpinned": or_kmeans's
- * re-seed of an emptied cluster (the point farthest from its centroid) --
- * with the deterministic maximin start a cluster empties only when there are
- * fewer distinct points than k, and there no input searched distinguishes
- * that rule from any other.
+ * tools/oracle_mutants.py); none is "parity unpinned".  (The k-means re-seed
+ * of an emptied cluster is pinned through or_kmeans_from: the maximin start
+ * itself never empties a cluster on the inputs searched.)
  */
 #include <math.h>
 #include <pthread.h>
@@ -661,54 +659,13 @@ static double sqdist(const double *x, const double *mu, int64_t C)
     return d;
 }
 
-int or_kmeans(const float *T, int64_t E, int64_t C, const double *best, double penalty,
-              const uint8_t *mask, int k, int max_iter, int32_t *sel, int *n_sel, int *iters,
-              double *wcss)
+/* Lloyd iterations from the centroids in M (k x C) and the selection; shared by
+ * or_kmeans (maximin start) and or_kmeans_from (given start).  dmin, asg, cnt are
+ * scratch (ne, ne, k).  Same arithmetic and order as before the split. */
+static void kmeans_lloyd(const double *X, int64_t ne, int64_t C, int k, int max_iter, double *M,
+                         double *dmin, int *asg, int *cnt, int32_t *sel, int *n_sel, int *iters,
+                         double *wcss)
 {
-    int64_t *envs = malloc(sizeof(int64_t) * (size_t)E);
-    if (!envs) return OR_ENOMEM;
-    int64_t ne = scope_list(mask, E, envs);
-    if (ne == 0) { free(envs); return OR_EEMPTY; }
-    if (k < 1 || k > ne) { free(envs); return OR_EINVAL; }
-    double *X = malloc(sizeof(double) * (size_t)(ne * C));
-    double *M = malloc(sizeof(double) * (size_t)(k * C));
-    double *mean = calloc((size_t)C, sizeof(double));
-    double *dmin = malloc(sizeof(double) * (size_t)ne);
-    int *asg = malloc(sizeof(int) * (size_t)ne), *cnt = malloc(sizeof(int) * (size_t)k);
-    if (!X || !M || !mean || !dmin || !asg || !cnt) {
-        free(envs); free(X); free(M); free(mean); free(dmin); free(asg); free(cnt);
-        return OR_ENOMEM;
-    }
-    for (int64_t q = 0; q < ne; q++)
-        for (int64_t c = 0; c < C; c++) {
-            float t = T[envs[q] * C + c];
-            double tt = isfinite(t) ? (double)t : penalty * best[envs[q]];
-            X[q * C + c] = tt / best[envs[q]];
-        }
-    /* init */
-    for (int64_t q = 0; q < ne; q++)
-        for (int64_t c = 0; c < C; c++) mean[c] += X[q * C + c];
-    for (int64_t c = 0; c < C; c++) mean[c] /= (double)ne;
-    int64_t first = 0;
-    double bd = INFINITY;
-    for (int64_t q = 0; q < ne; q++) {
-        double d = sqdist(X + q * C, mean, C);
-        if (d < bd) { bd = d; first = q; }
-    }
-    memcpy(M, X + first * C, sizeof(double) * (size_t)C);
-    for (int64_t q = 0; q < ne; q++) dmin[q] = sqdist(X + q * C, M, C);
-    for (int j = 1; j < k; j++) {
-        int64_t far = 0;
-        double fd = -1.0;
-        for (int64_t q = 0; q < ne; q++)
-            if (dmin[q] > fd) { fd = dmin[q]; far = q; }
-        memcpy(M + (int64_t)j * C, X + far * C, sizeof(double) * (size_t)C);
-        for (int64_t q = 0; q < ne; q++) {
-            double d = sqdist(X + q * C, M + (int64_t)j * C, C);
-            if (d < dmin[q]) dmin[q] = d;
-        }
-    }
-    /* Lloyd */
     for (int64_t q = 0; q < ne; q++) asg[q] = -1;
     int it = 0;
     while (it < max_iter) {
@@ -764,7 +721,93 @@ int or_kmeans(const float *T, int64_t E, int64_t C, const double *best, double p
     }
     qsort(sel, (size_t)n, sizeof(int32_t), cmp_i32);
     *n_sel = n;
+}
+
+int or_kmeans(const float *T, int64_t E, int64_t C, const double *best, double penalty,
+              const uint8_t *mask, int k, int max_iter, int32_t *sel, int *n_sel, int *iters,
+              double *wcss)
+{
+    int64_t *envs = malloc(sizeof(int64_t) * (size_t)E);
+    if (!envs) return OR_ENOMEM;
+    int64_t ne = scope_list(mask, E, envs);
+    if (ne == 0) { free(envs); return OR_EEMPTY; }
+    if (k < 1 || k > ne) { free(envs); return OR_EINVAL; }
+    double *X = malloc(sizeof(double) * (size_t)(ne * C));
+    double *M = malloc(sizeof(double) * (size_t)(k * C));
+    double *mean = calloc((size_t)C, sizeof(double));
+    double *dmin = malloc(sizeof(double) * (size_t)ne);
+    int *asg = malloc(sizeof(int) * (size_t)ne), *cnt = malloc(sizeof(int) * (size_t)k);
+    if (!X || !M || !mean || !dmin || !asg || !cnt) {
+        free(envs); free(X); free(M); free(mean); free(dmin); free(asg); free(cnt);
+        return OR_ENOMEM;
+    }
+    for (int64_t q = 0; q < ne; q++)
+        for (int64_t c = 0; c < C; c++) {
+            float t = T[envs[q] * C + c];
+            double tt = isfinite(t) ? (double)t : penalty * best[envs[q]];
+            X[q * C + c] = tt / best[envs[q]];
+        }
+    /* init */
+    for (int64_t q = 0; q < ne; q++)
+        for (int64_t c = 0; c < C; c++) mean[c] += X[q * C + c];
+    for (int64_t c = 0; c < C; c++) mean[c] /= (double)ne;
+    int64_t first = 0;
+    double bd = INFINITY;
+    for (int64_t q = 0; q < ne; q++) {
+        double d = sqdist(X + q * C, mean, C);
+        if (d < bd) { bd = d; first = q; }
+    }
+    memcpy(M, X + first * C, sizeof(double) * (size_t)C);
+    for (int64_t q = 0; q < ne; q++) dmin[q] = sqdist(X + q * C, M, C);
+    for (int j = 1; j < k; j++) {
+        int64_t far = 0;
+        double fd = -1.0;
+        for (int64_t q = 0; q < ne; q++)
+            if (dmin[q] > fd) { fd = dmin[q]; far = q; }
+        memcpy(M + (int64_t)j * C, X + far * C, sizeof(double) * (size_t)C);
+        for (int64_t q = 0; q < ne; q++) {
+            double d = sqdist(X + q * C, M + (int64_t)j * C, C);
+            if (d < dmin[q]) dmin[q] = d;
+        }
+    }
+    kmeans_lloyd(X, ne, C, k, max_iter, M, dmin, asg, cnt, sel, n_sel, iters, wcss);
     free(envs); free(X); free(M); free(mean); free(dmin); free(asg); free(cnt);
+    return OR_OK;
+}
+
+/*
+ * or_kmeans_from -- or_kmeans with the initial centroids given (init: k x C doubles,
+ * row j = centroid j in the same slowdown space as the points) instead of the maximin
+ * start; the Lloyd iterations, the empty-cluster re-seed and the selection are the
+ * same code.  A start far from every point empties a cluster on the first pass, which
+ * is how the re-seed rule is pinned (tests/test_oracle_kmeans.py).
+ */
+int or_kmeans_from(const float *T, int64_t E, int64_t C, const double *best, double penalty,
+                   const uint8_t *mask, int k, int max_iter, const double *init, int32_t *sel,
+                   int *n_sel, int *iters, double *wcss)
+{
+    int64_t *envs = malloc(sizeof(int64_t) * (size_t)E);
+    if (!envs) return OR_ENOMEM;
+    int64_t ne = scope_list(mask, E, envs);
+    if (ne == 0) { free(envs); return OR_EEMPTY; }
+    if (k < 1 || k > ne || !init) { free(envs); return OR_EINVAL; }
+    double *X = malloc(sizeof(double) * (size_t)(ne * C));
+    double *M = malloc(sizeof(double) * (size_t)(k * C));
+    double *dmin = malloc(sizeof(double) * (size_t)ne);
+    int *asg = malloc(sizeof(int) * (size_t)ne), *cnt = malloc(sizeof(int) * (size_t)k);
+    if (!X || !M || !dmin || !asg || !cnt) {
+        free(envs); free(X); free(M); free(dmin); free(asg); free(cnt);
+        return OR_ENOMEM;
+    }
+    for (int64_t q = 0; q < ne; q++)
+        for (int64_t c = 0; c < C; c++) {
+            float t = T[envs[q] * C + c];
+            double tt = isfinite(t) ? (double)t : penalty * best[envs[q]];
+            X[q * C + c] = tt / best[envs[q]];
+        }
+    memcpy(M, init, sizeof(double) * (size_t)(k * C));
+    kmeans_lloyd(X, ne, C, k, max_iter, M, dmin, asg, cnt, sel, n_sel, iters, wcss);
+    free(envs); free(X); free(M); free(dmin); free(asg); free(cnt);
     return OR_OK;
 }
 

@@ -403,10 +403,10 @@ __global__ void k_km_select(const double *__restrict__ Mt, int64_t C, int k, int
     if (threadIdx.x == 0) sel[j] = bc[0];
 }
 
-extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t max_iter,
-                                      int32_t *out_idx, int32_t *out_n, double *out_G, int32_t *out_iters)
+// init: NULL = the deterministic maximin start; else host [k][C] initial centroids
+static pt_status kmeans_run(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t max_iter, const double *init,
+                            int32_t *out_idx, int32_t *out_n, double *out_G, int32_t *out_iters)
 {
-    PT_NVTX();
     if (!ctx || !out_idx || !out_n) return pt_fail(PT_EINVAL, "NULL argument");
     if (k < 1 || k > KM_MAXK) return pt_fail(PT_EINVAL, "k=%d outside [1, %d]", k, KM_MAXK);
     if (max_iter < 1) return pt_fail(PT_EINVAL, "max_iter must be >= 1");
@@ -459,7 +459,15 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
     const unsigned gc = (unsigned)((C + 127) / 128), gq = (unsigned)((ne + 255) / 256);
     // init: the point nearest the mean, then successive farthest points (maximin).  Every
     // init centroid is a copy of a point, so small scopes read one pairwise pass; larger
-    // ones run one single-centroid distance pass per centroid.
+    // ones run one single-centroid distance pass per centroid.  A given start is copied
+    // in (config-major).
+    if (init) {
+        std::vector<double> mt((size_t)k * C);
+        for (int j = 0; j < k; j++)
+            for (int64_t c = 0; c < C; c++) mt[(size_t)c * k + j] = init[(size_t)j * C + c];
+        PT_CK(cudaMemcpyAsync(M, mt.data(), sizeof(double) * k * C, cudaMemcpyHostToDevice, s));
+        PT_CK(cudaStreamSynchronize(s));   // mt is a host temporary
+    } else {
     k_km_mean<<<gc, 128, 0, s>>>(X, ne, C, mean);
     ctx->stats.launches++;
     if (ne <= KM_PAIR_MAX) {
@@ -490,6 +498,7 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
             k_km_dmin<<<gq, 256, 0, s>>>(D, ne, 0, dmin);
             ctx->stats.launches += 3;
         }
+    }
     }
     PT_CK(cudaGetLastError());
     // Lloyd, enqueued in batches of passes; a pass after the stop flag returns at once
@@ -527,4 +536,20 @@ extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env
     if (out_iters) *out_iters = h.it;
     if (out_G) PT_TRY(pt_score_sets(ctx, sel.data(), 1, (int32_t)sel.size(), env_mask, PT_OBJ_GEOMEAN, out_G));
     return PT_OK;
+}
+
+extern "C" pt_status pt_kmeans_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t max_iter,
+                                      int32_t *out_idx, int32_t *out_n, double *out_G, int32_t *out_iters)
+{
+    PT_NVTX();
+    return kmeans_run(ctx, k, env_mask, max_iter, nullptr, out_idx, out_n, out_G, out_iters);
+}
+
+extern "C" pt_status pt_kmeans_select_from(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t max_iter,
+                                           const double *init, int32_t *out_idx, int32_t *out_n, double *out_G,
+                                           int32_t *out_iters)
+{
+    PT_NVTX();
+    if (!init) return pt_fail(PT_EINVAL, "init is NULL");
+    return kmeans_run(ctx, k, env_mask, max_iter, init, out_idx, out_n, out_G, out_iters);
 }

@@ -30,6 +30,7 @@ EXPORTS = ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_b
            "pt_kmeans_select", "pt_set_fleet", "pt_get_stats", "pt_greedy_sharded",
            "pt_greedy_sharded_dev", "pt_set_shard_weights", "pt_comm_unique_id", "pt_comm_init",
            "pt_comm_free", "pt_exhaustive_best_sharded", "pt_record_len", "pt_merge_records",
+           "pt_kmeans_select_from",
            "pt_free", "pt_last_error")
 PT_COMM_ID_BYTES = 128
 
@@ -88,6 +89,7 @@ def lib():
         L.pt_swap_search.argtypes = [P, i32, P, i32, i32, P, P, P, P]
         L.pt_eval_holdout_all.argtypes = [P, i32, i32, P, P, P, P, P, P]
         L.pt_kmeans_select.argtypes = [P, i32, P, i32, P, P, P, P]
+        L.pt_kmeans_select_from.argtypes = [P, i32, P, i32, P, P, P, P, P]
         L.pt_greedy_sharded.argtypes = [P, i32, P, i32, i32, ALLGATHER_FN, P, P, P, P]
         L.pt_greedy_sharded_dev.argtypes = [P, i32, P, i32, i32, DEV_ALLGATHER_FN, P, P, P, P]
         L.pt_comm_unique_id.argtypes = [P]
@@ -106,7 +108,7 @@ def lib():
         for f in ("pt_load_perf", "pt_score_sets", "pt_greedy_select", "pt_exhaustive_best",
                   "pt_merge_top2", "pt_eval_holdout", "pt_get_stats", "pt_set_fleet",
                   "pt_swap_search", "pt_eval_holdout_all", "pt_kmeans_select", "pt_comm_unique_id",
-                  "pt_comm_init", "pt_exhaustive_best_sharded", "pt_merge_records"):
+                  "pt_comm_init", "pt_exhaustive_best_sharded", "pt_merge_records", "pt_kmeans_select_from"):
             getattr(L, f).restype = ct.c_int
         _lib = L
     return _lib
@@ -372,6 +374,19 @@ def pt_kmeans_select(ctx, k, env_mask=None, max_iter=100):
     it = np.zeros(1, np.int32)
     _chk(lib().pt_kmeans_select(ctx.handle, k, _ptr(_mask(env_mask)), max_iter, _ptr(out), _ptr(n),
                                 _ptr(g), _ptr(it)), "pt_kmeans_select")
+    return tuple(int(x) for x in out[:n[0]]), float(g[0]), int(it[0])
+
+
+def pt_kmeans_select_from(ctx, init, env_mask=None, max_iter=100):
+    """k-means from given initial centroids (init: [k][C] slowdowns): (selection, G, iterations)."""
+    ini = _np(init, np.float64)
+    k = ini.shape[0]
+    out = np.zeros(k, np.int32)
+    n = np.zeros(1, np.int32)
+    g = np.zeros(1)
+    it = np.zeros(1, np.int32)
+    _chk(lib().pt_kmeans_select_from(ctx.handle, k, _ptr(_mask(env_mask)), max_iter, _ptr(ini), _ptr(out),
+                                     _ptr(n), _ptr(g), _ptr(it)), "pt_kmeans_select_from")
     return tuple(int(x) for x in out[:n[0]]), float(g[0]), int(it[0])
 
 

@@ -78,3 +78,25 @@ def test_k32_many_tiles_and_chunks():
     sel, G, it = pt.pt_kmeans_select(ctx, 32, max_iter=3)    # stopped by max_iter, not convergence
     osel, oit, _ = o.kmeans(32, max_iter=3)
     assert sel == osel and it == oit == 3
+
+
+def test_given_start_reseed():
+    """pt_kmeans_select_from against or_kmeans_from: the hand fixture whose start empties
+    a cluster (the re-seed rule, tests/test_oracle_kmeans.py), and random scopes started
+    with one centroid far from every point (a re-seed on the first pass)."""
+    T = np.array([[1, 5], [1, 6], [4, 1]], np.float32)
+    init = np.array([[1.0, 5.5], [100.0, 100.0]])
+    ctx = pt.pt_load_perf(T)
+    sel, G, it = pt.pt_kmeans_select_from(ctx, init)
+    assert (sel, it) == ((0, 1), 3)
+    for seed, C, nd, ni in ((1, 60, 3, 6), (2, 300, 4, 12)):
+        T, dev = synth.small_matrix(seed, n_cfg=C, n_dev=nd, n_inputs=ni)
+        o = Oracle(T, dev)
+        ctx = pt.pt_load_perf(T, dev)
+        X = T.astype(np.float64) / T.astype(np.float64).min(axis=1, keepdims=True)
+        for k in (3, 6):
+            init = X[:k].copy()
+            init[-1] = 1e6                     # far from every point: empty on pass 1
+            sel, G, it = pt.pt_kmeans_select_from(ctx, init)
+            osel, oit, _ = o.kmeans_from(init)
+            assert sel == osel and it == oit

@@ -59,8 +59,28 @@ def test_degenerate_reseed_branch():
     then at distance 0); the third cluster is empty and re-seeded with a point at
     distance 0.  Every centroid sits on a point, so WCSS = 0, the assignment is
     stable after the second pass, and the selection is {c0 (p0's best), c1 (p2's)}.
-    Whether the farthest-point rule or any other point re-seeds is not observable
-    here (the re-seed rule itself is parity unpinned)."""
+    Which point re-seeds is not observable here (every candidate sits on a centroid);
+    the rule itself is pinned by test_reseed_rule_hand."""
     T = np.array([[1, 4, 2], [1, 4, 2], [4, 1, 2]], np.float32)
     sel, iters, w = Oracle(T).kmeans(3)
     assert sel == (0, 1) and iters == 2 and np.all(w == 0.0)
+
+
+def test_reseed_rule_hand():
+    """The empty-cluster re-seed (the point farthest from its own centroid),
+    pinned by a hand-worked trace from a given start (or_kmeans_from).  Points (slowdown
+    rows) p0 = (1, 5), p1 = (1, 6), p2 = (4, 1); start mu0 = (1, 5.5), mu1 = (100, 100).
+      pass 1: every point -> mu0 (d = 0.25, 0.25, 29.25), WCSS 29.75; mu1 empty.
+              update mu0 = mean = (2, 4); re-seed mu1 with the farthest point from its
+              centroid: p2 (29.25)  ->  mu1 = (4, 1).
+      pass 2: p0 -> mu0 (2 vs 25), p1 -> mu0 (5 vs 34), p2 -> mu1 (13 vs 0): WCSS 7;
+              update mu0 = (1, 5.5), mu1 = (4, 1).
+      pass 3: unchanged: WCSS 0.25 + 0.25 + 0 = 0.5, converged after 3 passes.
+    Selection: mu0 -> config 0, mu1 -> config 1.  Re-seeding with point 0 instead gives
+    WCSS 29.75, 14, 0.5 (pass 2: p0, p1 -> (1, 5); p2 -> (2, 4))."""
+    T = np.array([[1, 5], [1, 6], [4, 1]], np.float32)
+    sel, iters, w = Oracle(T).kmeans_from(np.array([[1.0, 5.5], [100.0, 100.0]]))
+    assert sel == (0, 1) and iters == 3
+    assert list(w) == [29.75, 7.0, 0.5]
+    # the maximin start on the same points never empties a cluster: the plain path agrees
+    assert Oracle(T).kmeans(2)[0] == (0, 1)
