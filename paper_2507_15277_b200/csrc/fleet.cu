@@ -435,6 +435,8 @@ pt_status pt_fleet_tiled_operands(pt_ctx *ctx, const pt_fleet_tiled **out)
         t.stage_end_mask |= 1u << (nst - 1);
         t.stage_Q[nst - 1] = (float)(f.h_qdev[d] * sigma);
     }
+    // the tiled kernel keeps the row tile's A operand for all E_fp rows in shared memory
+    if ((int64_t)rowq.size() > 768) ok = false;
     if (!ok) return PT_OK;    // not eligible: the thread-per-subset search runs instead
     t.E_fp = (int64_t)rowq.size();
     int32_t *d_rowq = nullptr;

@@ -174,3 +174,15 @@ def test_paper_fleet_k3_golden():
     tt = [t if t is not None else (-1, -1, -1) for r in r8 for t in (r["best"], r["runner"])]
     b, ru, (c1, c2) = pt.pt_merge_top2(ss, tt, 3)
     assert b == tuple(gold["seed1_fleet_k3"]["best"]) and 1.0 / c1 == pytest.approx(gold["seed1_fleet_k3"]["R"], rel=RTOL)
+
+
+def test_fleet_many_small_devices_falls_back():
+    """12 devices of 5 environments: each segment padded to a 64-env stage gives 768+ rows,
+    beyond the tiled kernel's shared-memory A tile -> the fp64 thread-per-subset search,
+    still equal to the oracle."""
+    T, dev = synth.small_matrix(17, n_cfg=80, n_dev=13, n_inputs=5)
+    rng = np.random.default_rng(17)
+    qd, qe = rng.uniform(1, 3, 13), np.ones(len(dev))
+    o, ctx = both(T, dev, qd, qe)
+    check_exh(o, ctx, 2)
+    assert pt.pt_get_stats(ctx)["exh_kernel"] == 2
