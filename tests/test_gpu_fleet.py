@@ -180,7 +180,8 @@ def test_fleet_many_small_devices_falls_back():
     """12 devices of 5 environments: each segment padded to a 64-env stage gives 768+ rows,
     beyond the tiled kernel's shared-memory A tile -> the fp64 thread-per-subset search,
     still equal to the oracle."""
-    T, dev = synth.small_matrix(17, n_cfg=80, n_dev=13, n_inputs=5)
+    T, _ = synth.small_matrix(17, n_cfg=80, n_dev=13, n_inputs=5)
+    dev = np.repeat(np.arange(13, dtype=np.int32), 5)        # 13 device ids, 5 envs each
     rng = np.random.default_rng(17)
     qd, qe = rng.uniform(1, 3, 13), np.ones(len(dev))
     o, ctx = both(T, dev, qd, qe)
