@@ -291,11 +291,14 @@ def measure_per_config(pt, dT, dev, local, pk, reps=5):
     for k, name in ((2, "paper_exhaustive_k2"), (3, "paper_exhaustive_k3")):
         ms, kms = dev_ms(lambda: pt.pt_exhaustive_best(ctx, k), "exh_main_ms")
         sets = SETS[f"exh{k}"]
+        q8 = pt.pt_get_stats(ctx)["exh_kernel"] == 4
+        pk_k = alu_peak * (2 if q8 else 1)   # u8 tier: 4 (set,env) per VABSDIFF4
         out[name] = {"config": f"BASELINE configs[2]: exhaustive k={k} over 1,775 x 320", "ms": ms,
                      "kernel_ms": kms, "sets_per_s": sets / (ms * 1e-3),
-                     "roofline": {"bound": "alu", "kernel": "k_exh_tiled", "unit": "T(set,env)/s",
-                                  "achieved": sets * E_PAPER / (kms * 1e-3) / 1e12, "peak": alu_peak / 1e12,
-                                  "frac": sets * E_PAPER / (kms * 1e-3) / alu_peak}}
+                     "roofline": {"bound": "alu", "kernel": "k_exh_q8" if q8 else "k_exh_tiled",
+                                  "unit": "T(set,env)/s",
+                                  "achieved": sets * E_PAPER / (kms * 1e-3) / 1e12, "peak": pk_k / 1e12,
+                                  "frac": sets * E_PAPER / (kms * 1e-3) / pk_k}}
     ms, _ = dev_ms(lambda: pt.pt_eval_holdout_all(ctx, K_HOLDOUT, 5))
     out["holdout_5fold_greedy_k5"] = {
         "config": "BASELINE configs[3]: leave-one-device-out, 5 folds, greedy k=5 (one batched launch)",
@@ -474,7 +477,7 @@ def main():
         st_end = pt.pt_get_stats(ctx)
         pt.pt_free(ctx)
         return {"greedy": idx, "r2": r2, "r3": r3, "k3_ms": st3["exh_main_ms"],
-                "k3_sets": st3["exh_sets"], "k3_slots": st3["exh_slots"],
+                "k3_sets": st3["exh_sets"], "k3_slots": st3["exh_slots"], "k3_kernel": st3["exh_kernel"],
                 "k3_cand": st3["exh_candidates"], "launches": st_end["launches"]}, d2h
 
     def timed(src, steps, warmup):
@@ -550,16 +553,21 @@ def main():
     pk = peaks()
     sm_max = pk.get("sm_max_mhz", 1965.0)
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    # roofline of the dominant kernel (k_exh_tiled, k=3).  Algorithmic work: one
-    # min + one add per (set, env), E = 320 envs per set.  Peak = the ALU-pipe
-    # ceiling for the mins (the only pipe with a min): 16 lanes/clk/SMSP x 4 SMSP
-    # x 2 mins per packed f16x2 HMNMX2 = 128 (set,env)/clk/SM (DESIGN.md
-    # "Roofline").  The FP32 roofline of the north star (one FMNMX at 16
-    # lanes/clk/SMSP + one FADD per (set, env)) is 64 (set,env)/clk/SM.
+    # roofline of the dominant kernel (k=3).  Algorithmic work: one min + one add per
+    # (set, env), E = 320 envs per set.  Default tier (exh_kernel 4, k_exh_q8): the
+    # quantised set score is 4 (set, env) evaluations per VABSDIFF4.U8.ACC, which
+    # issues at 16 lanes/clk/SMSP (tools/ubench.cu: 2.06 warp-instr/clk/SM) -> 16 x 4
+    # SMSP x 4 = 256 (set,env)/clk/SM.  fp16 tier (exh_kernel 0, k_exh_tiled): the
+    # ALU-pipe min ceiling, 16 lanes/clk/SMSP x 4 SMSP x 2 mins per HMNMX2 = 128.
+    # The FP32 roofline of the north star (one FMNMX at 16 lanes/clk/SMSP + one FADD
+    # per (set, env)) is 64 (set,env)/clk/SM.
+    tier_q8 = res.get("k3_kernel") == 4
+    per_clk = 256 if tier_q8 else 128
     evals = float(E_PAPER) * res["k3_sets"]
     k3_avg = float(np.mean(k3_ms))
     achieved = evals / (k3_avg * 1e-3) / 1e12
-    peak = nsm * 128 * sm_max * 1e6 / 1e12
+    peak = nsm * per_clk * sm_max * 1e6 / 1e12
+    peak_f16 = nsm * 128 * sm_max * 1e6 / 1e12
     peak_fp32 = nsm * 64 * sm_max * 1e6 / 1e12
     traffic, l2 = None, None
     try:
@@ -595,7 +603,8 @@ def main():
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f16x2 min + f32 sum filter, f64 exact refine",
+        "dtype": ("u8 (exact integer |a-b| score of the quantised matrix) filter, f64 exact refine" if tier_q8
+                  else "f16x2 min + f32 sum filter, f64 exact refine"),
         "data": "synthetic (seeded generator, paper shape; private dataset unavailable)",
         "config": {"workload": WORKLOAD, "sets_per_step": SETS_PER_STEP, "seed": args.seed,
                    "l2": "flushed between steps (256 MiB write, inside the timed region)",
@@ -603,13 +612,20 @@ def main():
         "e2e": {"value": SETS_PER_STEP * args.steps / (ms_e2e * 1e-3), "unit": "sets/s",
                 "h2d_bytes_per_step": h2d_e2e, "d2h_bytes_per_step": int(d2h_e2e)},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "alu", "kernel": "k_exh_tiled (k=3)", "achieved": achieved,
+        "roofline": {"bound": "alu", "kernel": ("k_exh_q8" if tier_q8 else "k_exh_tiled") + " (k=3)",
+                     "achieved": achieved,
                      "peak": peak, "unit": "T(set,env)/s", "frac": achieved / peak, "traffic": traffic,
                      "work_per_set": f"{E_PAPER} (set,env) evaluations = {E_PAPER} min + {E_PAPER} add",
-                     "peak_basis": f"ALU-pipe min ceiling: {nsm} SMs x 4 SMSP x 16 lanes/clk x 2 mins "
-                                   f"(f16x2 HMNMX2) x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); "
-                                   "the packed adds (HADD2, half rate on the FMA pipe) and the issue "
-                                   "port have the same ceiling (DESIGN.md 6.1)",
+                     "peak_basis": (f"VABSDIFF4.U8.ACC ceiling: {nsm} SMs x 4 SMSP x 16 lanes/clk x 4 (set,env) "
+                                    f"per instruction x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); issue rate "
+                                    "measured by tools/ubench.cu, the inner loop alone reaches 245/clk/SM "
+                                    "(tools/ubench_sad.cu, DESIGN.md 6.2b)") if tier_q8 else
+                                   (f"ALU-pipe min ceiling: {nsm} SMs x 4 SMSP x 16 lanes/clk x 2 mins "
+                                    f"(f16x2 HMNMX2) x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); "
+                                    "the packed adds (HADD2, half rate on the FMA pipe) and the issue "
+                                    "port have the same ceiling (DESIGN.md 6.1)"),
+                     "f16x2_roofline": {"peak": peak_f16, "frac": achieved / peak_f16,
+                                        "basis": "the fp16 tier's HMNMX2 ceiling (128 (set,env)/clk/SM)"},
                      "fp32_roofline": {"peak": peak_fp32, "frac": achieved / peak_fp32,
                                        "basis": "one FMNMX (16 lanes/clk/SMSP) + one FADD per (set, env)"},
                      "kernel_ms": k3_avg, "kernel_share_of_step": k3_avg / (ms / args.steps),

@@ -137,8 +137,13 @@ pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int3
  *   out_s          host double[2] or NULL: the exact fp64 log-slowdown sums
  *                  s = -|scope| log G of best and runner-up (+inf if absent) --
  *                  the keys pt_merge_top2 orders by.
- * Errors: PT_EINVAL (k < 1, k > C, bad shard), PT_ECAP (C(n,k) > 1e13),
- *         PT_EEMPTY.
+ * Method (k = 2..4, scopes <= 768 envs): a filter scores every set -- by default
+ * the exact integer score of the matrix quantised to bytes (q = rint(l / Delta),
+ * Delta = scope max / 255), else fp16 -- keeps every set whose rigorous lower
+ * bound reaches the best two, and re-scores those in fp64; the result is the
+ * same as scoring every set in fp64.
+ * Errors: PT_EINVAL (k < 1, k > C, bad shard), PT_ECAP (C(n,k) > 1e13, or more
+ *         than 2^28 fp16-tier survivors), PT_EEMPTY.
  */
 pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t objective,
                              int32_t shard_rank, int32_t shard_count,
@@ -354,9 +359,12 @@ typedef struct {
     int64_t exh_sets;        /* k-subsets that launch scored (its shard) */
     int64_t exh_slots;       /* (row, column) slots it computed, incl. masked waste */
     int64_t exh_env_pad;     /* padded env count of its scope (K-loop length) */
-    int64_t exh_candidates;  /* fp32-tier candidates re-scored in fp64 */
-    int32_t exh_passes;      /* 1, or 2 after a candidate-buffer overflow */
-    int32_t exh_kernel;      /* 0 = tiled fp32 (min,+), 1 = generic fp64 */
+    int64_t exh_candidates;  /* filter-tier candidates re-scored in fp64 */
+    int32_t exh_passes;      /* 1; +1 per candidate-buffer overflow rerun or u8 -> fp16 hand-over */
+    int32_t exh_kernel;      /* 4 = tiled u8 filter (k_exh_q8, the default), 0 = tiled fp16 filter
+                                (k_exh_tiled; environment PT_EXH_TIER=fp16, or the u8 tier left
+                                more than 2^24 candidates), 1 = generic fp64, 2 = fleet fp64,
+                                3 = fleet tiled fp16 */
     double greedy_ms;        /* CUDA-event time of the last greedy selection */
     int64_t greedy_candidates; /* streamed greedy: configs re-scored in fp64 (all steps) */
 } pt_stats;

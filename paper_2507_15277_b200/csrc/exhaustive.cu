@@ -720,6 +720,326 @@ __global__ void __launch_bounds__(256) k_tile_hT(const uint16_t *__restrict__ hT
 // ---------------------------------------------------------------------------
 // top-2 over (s, tuple) records -- one CTA
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// u8 tier (k_exh_q8): the default filter of the tiled search since round 2.
+//
+// Quantise every value of the scope to q(l) = rint(l / Delta) in 0..255 with
+// Delta = (scope max of l) / 255.  q is non-decreasing, so the quantised best
+// member of a set is the quantisation of its best member, and the quantised set
+// score S_q = sum_e min_c q(l[c][e]) is an exact integer with
+//     |Delta * S_q - s| <= E * Delta / 2   (+ the fp64 slack of DESIGN.md 6.3)
+// For bytes, min(a, b) = (a + b - |a - b|) / 2, so with SA_rho = sum_e A_q[e] and
+// SB_l = sum_e q[l][e]
+//     2 S_q = SA_rho + SB_l - sum_e |A_q[e] - q[l][e]|
+// and the sum of absolute differences of four environments (one 32-bit word of
+// bytes) plus the running sum is ONE instruction, VABSDIFF4.U8.ACC: 4 (set, env)
+// evaluations per instruction, against 2 per HMNMX2 and 2 per HADD2 in the fp16
+// tier.  Measured alone (tools/ubench_sad.cu, 8 rows x 4 columns per thread,
+// operands from shared memory): 245 (set, env)/clk/SM, against 83 for the fp16
+// tree.  The integer score is exact, so the only error is the quantisation's,
+// bounded per term; the window test and the U bookkeeping are those of the fp16
+// tier with X = 2 S_q in place of the fp32 accumulator.
+// ---------------------------------------------------------------------------
+#define XQ_R 128   // rows per CTA tile
+#define XQ_C 64    // columns per CTA tile
+
+// qmax: scope max of l (non-negative doubles order as their bit patterns)
+__global__ void __launch_bounds__(256) k_q8_max(const double *__restrict__ l64, int64_t C, int64_t E,
+                                               int64_t E_pad, unsigned long long *__restrict__ qmax)
+{
+    double m = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < C * E; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / E, e = i - c * E;
+        m = fmax(m, l64[c * E_pad + e]);
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(qmax, (unsigned long long)__double_as_longlong(m));
+}
+
+// Delta, 1/Delta and the window constants (one thread; no host round trip).
+// Per term |Delta q(l) - l| <= Delta (1/2 + 1e-12) (1/Delta and l/Delta rounded in
+// fp64); the refine's fp64 sum differs from the exact s by <= E_pad^2 qmax 2^-52.
+__global__ void k_q8_const(const unsigned long long *__restrict__ qmax_bits, int64_t E_pad, float *__restrict__ qc)
+{
+    const double qmax = __longlong_as_double((long long)*qmax_bits);
+    const double delta = qmax > 0.0 ? qmax / 255.0 : 1.0;
+    const double Ed = (double)E_pad;
+    const double slack = Ed * delta * (0.5 + 1e-12) + Ed * Ed * qmax * 0x1p-52 + 1e-300;
+    qc[0] = __double2float_rd(delta * 0.5);
+    qc[1] = __double2float_ru(slack);
+    qc[2] = __double2float_ru(delta * 0.5);
+    qc[3] = __double2float_ru(slack);
+    *reinterpret_cast<double *>(qc + 4) = 1.0 / delta;
+}
+
+// qC[c][g] = bytes q(l[c][4g + 0..3]) (0 past E and past C), qSum[c] = sum of them:
+// one warp per config
+__global__ void __launch_bounds__(256) k_q8_build(const double *__restrict__ l64, int64_t C, int64_t E, int64_t E_pad,
+                                                 int64_t C_pad, const float *__restrict__ qc,
+                                                 uint32_t *__restrict__ qC, int32_t *__restrict__ qSum)
+{
+    const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= C_pad) return;
+    const double inv = *reinterpret_cast<const double *>(qc + 4);
+    const int64_t G = E_pad / 4;
+    int sum = 0;
+    for (int64_t g = lane; g < G; g += 32) {
+        uint32_t w = 0;
+        for (int b = 0; b < 4; b++) {
+            const int64_t e = 4 * g + b;
+            uint32_t q = 0;
+            if (c < C && e < E) q = (uint32_t)fmin(fmax(rint(l64[c * E_pad + e] * inv), 0.0), 255.0);
+            w |= q << (8 * b);
+            sum += (int)q;
+        }
+        qC[c * G + g] = w;
+    }
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) qSum[c] = sum;
+}
+
+// qTile[sh][ct][g][j] = qC[64 ct + 8 sh + j][g] (0 past C_pad)
+__global__ void __launch_bounds__(256) k_q8_tile(const uint32_t *__restrict__ qC, int64_t G, int64_t C_pad,
+                                                int64_t n_ct, uint32_t *__restrict__ qTile)
+{
+    const int64_t sct = blockIdx.x, ct = sct % n_ct, sh = sct / n_ct;
+    const int64_t c0 = 64 * ct + 8 * sh;
+    uint32_t *dst = qTile + sct * G * 64;
+    for (int64_t i = threadIdx.x; i < G * 64; i += blockDim.x) {
+        const int64_t g = i >> 6, c = c0 + (i & 63);
+        dst[i] = c < C_pad ? qC[c * G + g] : 0u;
+    }
+}
+
+struct QParams {
+    int64_t C, E_pad, n_rows, n_ct;
+    int m, G, S;              // G = E_pad / 4 words per config; S = ring depth
+    const int4 *tasks;
+    int task_hi;
+    int *task_ctr;
+    float tau_seed;
+    const float *qc;          // c1..c4 (k_q8_const)
+    unsigned *U;
+    unsigned long long *cand_key;
+    float *cand_s;
+    unsigned long long *cand_n;
+    unsigned cap;
+    const uint32_t *qC, *qTile;
+    const int32_t *qSum;
+};
+
+__device__ __forceinline__ uint32_t sad4(uint32_t a, uint32_t b, uint32_t acc)
+{
+    uint32_t r;
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(acc));
+    return r;
+}
+
+// 256 threads, 8 rows x 4 columns per thread (the k_exh_tiled mapping); a task's A
+// (128 rows x all envs, bytes) is staged once; each column tile (all envs x 64
+// configs, E_pad * 64 bytes) is one bulk copy into an S-deep ring.
+__global__ void __launch_bounds__(256, 2) k_exh_q8(const QParams p)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int G = p.G, S = p.S;
+    uint32_t *Bs = reinterpret_cast<uint32_t *>(smem);                 // [S][G][64]
+    uint32_t *As = Bs + (size_t)S * G * XQ_C;                           // [G][128]
+    int *sap = reinterpret_cast<int *>(As + (size_t)G * XQ_R);          // [256] partial row sums
+    int *last_s = sap + 256;                                            // [128]
+    uint64_t *full = reinterpret_cast<uint64_t *>(last_s + XQ_R);       // [4]
+    int4 *task_s = reinterpret_cast<int4 *>(full + 4);
+    int *relcnt = reinterpret_cast<int *>(task_s + 1);                  // [4]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 1);
+            relcnt[s] = 0;
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const float c1 = p.qc[0], c2 = p.qc[1], c3 = p.qc[2], c4 = p.qc[3];
+    const uint32_t stage_bytes = (uint32_t)G * XQ_C * 4u;
+
+    uint32_t steps = 0;
+    const int tx = lane & 7, ty = lane >> 3;
+    int bA = INT_MAX, bB = INT_MAX;      // group minima of X for U
+    float published = INFINITY;
+
+    for (;;) {
+        if (tid == 0) {
+            int ti = atomicAdd(p.task_ctr, 1);
+            *task_s = ti < p.task_hi ? p.tasks[ti] : make_int4(-1, 0, 0, 0);
+        }
+        __syncthreads();
+        const int4 tk = *task_s;
+        if (tk.x < 0) break;
+        const int64_t R0 = (int64_t)tk.x * XQ_R;
+        int32_t mem0[PT_MAXK];
+        pt_unrank_colex(R0, p.m, p.C, mem0);
+        const int64_t lo = tile_lo(mem0[p.m - 1]);
+        const int nsteps = tk.z - tk.y;
+        auto issue = [&](int g) {
+            const int sl = (int)((steps + (uint32_t)g) % (uint32_t)S);
+            const int64_t col = lo + (int64_t)(tk.y + g) * XQ_C;
+            const int64_t sh = (col >> 3) & 7, ct = (col - 8 * sh) >> 6;
+            mbar_expect_tx(&full[sl], stage_bytes);
+            bulk_g2s(Bs + (size_t)sl * G * XQ_C, p.qTile + (sh * p.n_ct + ct) * (int64_t)G * XQ_C, stage_bytes, &full[sl]);
+        };
+        if (tid == 0)
+            for (int g = 0; g < S && g < nsteps; g++) issue(g);
+
+        // ---- stage A: byte-wise min over the row's members, and its row sum ----
+        {
+            const int r = tid & (XQ_R - 1), half = tid >> 7;
+            const int64_t R = R0 + r;
+            int32_t mem[PT_MAXK];
+            const bool valid = R < p.n_rows;
+            if (valid) pt_unrank_colex(R, p.m, p.C, mem);
+            else for (int u = 0; u < p.m; u++) mem[u] = 0;
+            if (tid < XQ_R) last_s[r] = valid ? mem[p.m - 1] : 0x7fffffff;
+            uint32_t part = 0;
+            // 16-byte loads (4 words = 16 envs); the two threads of a row take alternate ones
+            for (int g4 = half; g4 < G / 4; g4 += 2) {
+                uint4 v = *reinterpret_cast<const uint4 *>(p.qC + (int64_t)mem[0] * G + 4 * g4);
+                for (int u = 1; u < p.m; u++) {
+                    const uint4 w = *reinterpret_cast<const uint4 *>(p.qC + (int64_t)mem[u] * G + 4 * g4);
+                    v.x = __vminu4(v.x, w.x);
+                    v.y = __vminu4(v.y, w.y);
+                    v.z = __vminu4(v.z, w.z);
+                    v.w = __vminu4(v.w, w.w);
+                }
+                if (!valid) v = make_uint4(0, 0, 0, 0);
+                As[(4 * g4 + 0) * XQ_R + r] = v.x;
+                As[(4 * g4 + 1) * XQ_R + r] = v.y;
+                As[(4 * g4 + 2) * XQ_R + r] = v.z;
+                As[(4 * g4 + 3) * XQ_R + r] = v.w;
+                part = sad4(v.x, 0u, part);
+                part = sad4(v.y, 0u, part);
+                part = sad4(v.z, 0u, part);
+                part = sad4(v.w, 0u, part);
+            }
+            sap[tid] = (int)part;
+        }
+        __syncthreads();
+
+        const int r0 = 32 * (warp >> 1) + 8 * ty;
+        const int c0 = 32 * (warp & 1) + 4 * tx;
+        int SA[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) SA[i] = sap[r0 + i] + sap[XQ_R + r0 + i];
+        const int last7 = last_s[r0 + 7];
+        uint32_t slot = steps % (uint32_t)S, phase = (steps / (uint32_t)S) & 1u;
+        int64_t ltile = lo + (int64_t)tk.y * XQ_C;
+        for (int ct = tk.y; ct < tk.z; ct++, ltile += XQ_C) {
+            const bool skip = ltile + 32 * (warp & 1) >= p.C;
+            const unsigned Ubits = *(volatile unsigned *)p.U;
+            uint32_t acc[8][4];
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = 0u;
+            mbar_wait(&full[slot], phase);
+            if (!skip) {
+                const uint32_t *B = Bs + (size_t)slot * G * XQ_C + c0;
+                const uint32_t *A = As + r0;
+#pragma unroll 4
+                for (int g = 0; g < G; g++) {
+                    const uint4 a0 = *reinterpret_cast<const uint4 *>(A + g * XQ_R);
+                    const uint4 a1 = *reinterpret_cast<const uint4 *>(A + g * XQ_R + 4);
+                    const uint4 b = *reinterpret_cast<const uint4 *>(B + g * XQ_C);
+                    const uint32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+#pragma unroll
+                        for (int j = 0; j < 4; j++) acc[i][j] = sad4(av[i], bv[j], acc[i][j]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                if (atomicAdd(&relcnt[slot], 1) == 256 / 32 - 1) {
+                    relcnt[slot] = 0;
+                    __threadfence_block();
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const int gn = ct - tk.y + S;
+                    if (gn < nsteps) issue(gn);
+                }
+            }
+            if (++slot == (uint32_t)S) {
+                slot = 0;
+                phase ^= 1u;
+            }
+            if (skip) continue;
+            // ---- epilogue: X = 2 S_q = SA + SB - D; invalid sets -> INT_MAX ----
+            int SB[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) SB[j] = __ldg(p.qSum + ltile + c0 + j);
+            int X[8][4];
+            const int64_t l0 = ltile + c0;
+            const bool all_valid = l0 + 3 < p.C && l0 > last7;
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    X[i][j] = SA[i] + SB[j] - (int)acc[i][j];
+                    if (!all_valid) {
+                        const int64_t l = l0 + j;
+                        if (!(l < p.C && l > last_s[r0 + i])) X[i][j] = INT_MAX;
+                    }
+                }
+            int tA = INT_MAX, tB = INT_MAX;
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    if (j >= 2) tB = min(tB, X[i][j]);
+                    else tA = min(tA, X[i][j]);
+                }
+            bA = min(bA, tA);
+            bB = min(bB, tB);
+            const float tau = fminf(p.tau_seed, __uint_as_float(Ubits));
+            const int tmin = min(tA, tB);
+            if (tmin != INT_MAX && __fmaf_rd((float)tmin, c1, -c2) <= tau) {   // rare
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const float lb = __fmaf_rd((float)X[i][j], c1, -c2);
+                        if (X[i][j] != INT_MAX && lb <= tau) {
+                            const unsigned long long idx = atomicAdd(p.cand_n, 1ull);
+                            if (idx < p.cap) {
+                                p.cand_key[idx] = ((unsigned long long)(R0 + r0 + i) << KEY_BITS) |
+                                                  (unsigned long long)(l0 + j);
+                                p.cand_s[idx] = lb;
+                            }
+                        }
+                    }
+            }
+            // U: the warp's 2nd-smallest group minimum (two distinct sets), as an upper bound
+            int x1 = min(bA, bB), x2 = max(bA, bB);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const int y1 = __shfl_xor_sync(0xffffffffu, x1, o);
+                const int y2 = __shfl_xor_sync(0xffffffffu, x2, o);
+                x2 = min(max(x1, y1), min(x2, y2));
+                x1 = min(x1, y1);
+            }
+            if (lane == 0 && x2 != INT_MAX) {
+                const float ub = __fmaf_ru((float)x2, c3, c4);
+                if (ub < published) {
+                    atomicMin(p.U, __float_as_uint(ub));
+                    published = ub;
+                }
+            }
+        }
+        steps += nsteps;
+    }
+}
+
 struct Rec2 {
     double s1, s2;
     int32_t t1[PT_MAXK], t2[PT_MAXK];
@@ -980,6 +1300,50 @@ static pt_status run_generic(pt_ctx *ctx, const pt_view *v, int k, int64_t r0, i
     return PT_OK;
 }
 
+// 64-config column tiles of a view (one extra zero tile past the end), shared by both tiers
+static int64_t view_n_ct(const pt_view *v) { return (v->C_pad + XT_C - 1) / XT_C + 1; }
+
+// fp16 tier operands: hT (pt_view_fp16) re-cut into hTile, built on first use
+static pt_status tile_fp16(pt_ctx *ctx, const pt_view *v)
+{
+    if (v->hTile) return PT_OK;
+    pt_view *mv = const_cast<pt_view *>(v);
+    mv->n_ct = view_n_ct(v);
+    PT_TRY(pt_dalloc(ctx, (void **)&mv->hTile, sizeof(uint16_t) * 8 * mv->n_ct * v->E_pad * XT_C));
+    k_tile_hT<<<(unsigned)(8 * mv->n_ct), 256, 0, ctx->stream>>>(v->hT, v->E_pad, v->C_pad, mv->n_ct, mv->hTile);
+    ctx->stats.launches++;
+    PT_CK(cudaGetLastError());
+    return PT_OK;
+}
+
+// u8 tier operands (qC, qTile, qSum, qConst), built on first use: four launches,
+// stream-ordered, no host round trip (Delta stays on the device)
+static pt_status pt_view_q8(pt_ctx *ctx, const pt_view *v)
+{
+    if (v->qTile) return PT_OK;
+    pt_view *mv = const_cast<pt_view *>(v);
+    cudaStream_t s = ctx->stream;
+    mv->n_ct = view_n_ct(v);
+    const int64_t G = v->E_pad / 4, nsum = (mv->n_ct + 1) * XQ_C + XQ_C;
+    PT_TRY(pt_dalloc(ctx, (void **)&mv->qConst, sizeof(float) * 8 + sizeof(unsigned long long)));
+    PT_TRY(pt_dalloc(ctx, (void **)&mv->qC, sizeof(uint32_t) * v->C_pad * G));
+    PT_TRY(pt_dalloc(ctx, (void **)&mv->qSum, sizeof(int32_t) * nsum));
+    PT_TRY(pt_dalloc(ctx, (void **)&mv->qTile, sizeof(uint32_t) * 8 * mv->n_ct * G * XQ_C));
+    unsigned long long *qmax = reinterpret_cast<unsigned long long *>(mv->qConst + 8);
+    PT_CK(cudaMemsetAsync(qmax, 0, sizeof(unsigned long long), s));
+    PT_CK(cudaMemsetAsync(mv->qSum, 0, sizeof(int32_t) * nsum, s));
+    const int64_t n = v->C * v->E;
+    const unsigned gmax = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4L * ctx->num_sms));
+    k_q8_max<<<gmax, 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, qmax);
+    k_q8_const<<<1, 1, 0, s>>>(qmax, v->E_pad, mv->qConst);
+    k_q8_build<<<(unsigned)((v->C_pad + 7) / 8), 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, v->C_pad, mv->qConst,
+                                                              mv->qC, mv->qSum);
+    k_q8_tile<<<(unsigned)(8 * mv->n_ct), 256, 0, s>>>(mv->qC, G, v->C_pad, mv->n_ct, mv->qTile);
+    ctx->stats.launches += 4;
+    PT_CK(cudaGetLastError());
+    return PT_OK;
+}
+
 static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_rank,
                            int32_t shard_count, double *s_out, int32_t *t_out)
 {
@@ -1073,43 +1437,53 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     if (v->E_pad % XT_K != 0)   // a stage must not straddle the padded env range
         return pt_fail(PT_EINVAL, "E_pad=%lld is not a multiple of the stage depth %d", (long long)v->E_pad, XT_K);
     mark("seeded");
-    PT_TRY(pt_view_fp16(ctx, v));
-    if (!v->hTile) {
-        pt_view *mv = const_cast<pt_view *>(v);
-        // 64-config tiles (one extra zero tile past the end)
-        mv->n_ct = (v->C_pad + XT_C - 1) / XT_C + 1;
-        PT_TRY(pt_dalloc(ctx, (void **)&mv->hTile, sizeof(uint16_t) * 8 * mv->n_ct * v->E_pad * XT_C));
-        k_tile_hT<<<(unsigned)(8 * mv->n_ct), 256, 0, s>>>(v->hT, v->E_pad, v->C_pad, mv->n_ct, mv->hTile);
-        ctx->stats.launches++;
-        PT_CK(cudaGetLastError());
-    }
-    auto kern = k_exh_tiled<false>;
-    const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
-                        sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
-    const void *kfn = (const void *)kern;
-    const size_t smem_k = smem;
-    const int threads = XT_TCONS;
     // per (kernel, smem) once per process: the attribute and the occupancy query
     static std::mutex attr_mu;
     static std::map<std::tuple<int, const void *, size_t>, int> attr_occ;   // per device
-    int occ = 1;
-    {
+    auto occupancy = [&](const void *kfn, size_t smem_k, int threads, int *occ) -> pt_status {
         std::lock_guard<std::mutex> g(attr_mu);
         auto key = std::make_tuple(ctx->dev, kfn, smem_k);
         auto it = attr_occ.find(key);
         if (it == attr_occ.end()) {
-            PT_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k));
-            PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, smem_k));
-            attr_occ[key] = occ;
+            PT_TRY(pt_smem_optin(ctx, kfn));
+            PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kfn, threads, smem_k));
+            attr_occ[key] = *occ;
         } else {
-            occ = it->second;
+            *occ = it->second;
         }
+        return PT_OK;
+    };
+    // fp16 tier (k_exh_tiled)
+    auto kern = k_exh_tiled<false>;
+    const size_t smem = sizeof(uint32_t) * XT_S * XT_K * (XT_C / 2) + sizeof(uint16_t) * v->E_pad * XT_R +
+                        sizeof(int) * XT_R + 2 * sizeof(uint64_t) * XT_S + sizeof(int4) + sizeof(int) * XT_S;
+    const int threads = XT_TCONS;
+    int occ = 1;
+    PT_TRY(occupancy((const void *)kern, smem, threads, &occ));
+    // u8 tier (k_exh_q8): the default; PT_EXH_TIER=fp16 keeps the fp16 tier (read per call,
+    // so the tests can exercise both tiers in one process)
+    const char *tier_env = getenv("PT_EXH_TIER");
+    const bool force_fp16 = tier_env && !strcmp(tier_env, "fp16");
+    bool q8 = !force_fp16;
+    const int G = (int)(v->E_pad / 4);
+    auto q8_smem = [&](int S) {
+        return (size_t)4 * S * G * XQ_C + (size_t)4 * G * XQ_R + sizeof(int) * (256 + XQ_R) +
+               sizeof(uint64_t) * 4 + sizeof(int4) + sizeof(int) * 4;
+    };
+    const size_t smem_budget = 227 * 1024;
+    const int q8_S = 2 * q8_smem(3) <= smem_budget ? 3 : 2;
+    const size_t smem_q8 = q8_smem(q8_S);
+    int occ_q8 = 0;
+    if (q8) {
+        PT_TRY(pt_view_q8(ctx, v));
+        PT_TRY(occupancy((const void *)k_exh_q8, smem_q8, 256, &occ_q8));
+        if (occ_q8 < 1) q8 = false;
     }
 
     unsigned cap = 1u << 20;
     unsigned long long n_cand = 0;
     float tau_pass = tau_seed;
-    for (int pass = 0; pass < 2; pass++) {
+    for (int pass = 0; pass < 4; pass++) {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
         const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)),
@@ -1140,32 +1514,62 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         }
         PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned long long), s));
         PT_CK(cudaMemsetAsync(done, 0, sizeof(unsigned), s));
-        XParams p;
-        p.C = v->C;
-        p.C_pad = v->C_pad;
-        p.E_pad = v->E_pad;
-        p.n_rows = pt_binom(v->C, m);
-        p.m = m;
-        p.tasks = task_list;
-        p.task_hi = tb;
-        p.task_ctr = ctr;
-        p.tau_seed = tau_pass;
-        p.c1 = c1;
-        p.c2 = c2;
-        p.c3 = c3;
-        p.c4 = c4;
-        p.U = U;
-        p.cand_key = ckey;
-        p.cand_s = cq;
-        p.cand_n = cn;
-        p.cap = cap;
-        p.hT = v->hT;
-        p.hTile = v->hTile;
-        p.n_ct = v->n_ct;
-        const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
-        mark("pre-launch");
-        PT_CK(cudaEventRecord(ctx->ev0, s));
-        kern<<<grid, threads, smem, s>>>(p);
+        if (q8) {
+            QParams p;
+            p.C = v->C;
+            p.E_pad = v->E_pad;
+            p.n_rows = pt_binom(v->C, m);
+            p.n_ct = v->n_ct;
+            p.m = m;
+            p.G = G;
+            p.S = q8_S;
+            p.tasks = task_list;
+            p.task_hi = tb;
+            p.task_ctr = ctr;
+            p.tau_seed = tau_pass;
+            p.qc = v->qConst;
+            p.U = U;
+            p.cand_key = ckey;
+            p.cand_s = cq;
+            p.cand_n = cn;
+            p.cap = cap;
+            p.qC = v->qC;
+            p.qTile = v->qTile;
+            p.qSum = v->qSum;
+            const int grid = std::min(ctx->num_sms * occ_q8, tb - ta);
+            mark("pre-launch");
+            PT_CK(cudaEventRecord(ctx->ev0, s));
+            k_exh_q8<<<grid, 256, smem_q8, s>>>(p);
+        } else {
+            PT_TRY(pt_view_fp16(ctx, v));
+            PT_TRY(tile_fp16(ctx, v));
+            XParams p;
+            p.C = v->C;
+            p.C_pad = v->C_pad;
+            p.E_pad = v->E_pad;
+            p.n_rows = pt_binom(v->C, m);
+            p.m = m;
+            p.tasks = task_list;
+            p.task_hi = tb;
+            p.task_ctr = ctr;
+            p.tau_seed = tau_pass;
+            p.c1 = c1;
+            p.c2 = c2;
+            p.c3 = c3;
+            p.c4 = c4;
+            p.U = U;
+            p.cand_key = ckey;
+            p.cand_s = cq;
+            p.cand_n = cn;
+            p.cap = cap;
+            p.hT = v->hT;
+            p.hTile = v->hTile;
+            p.n_ct = v->n_ct;
+            const int grid = std::min(ctx->num_sms * std::max(occ, 1), tb - ta);
+            mark("pre-launch");
+            PT_CK(cudaEventRecord(ctx->ev0, s));
+            kern<<<grid, threads, smem, s>>>(p);
+        }
         PT_CK(cudaEventRecord(ctx->ev1, s));
         ctx->stats.launches++;
         PT_CK(cudaGetLastError());
@@ -1191,14 +1595,22 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         float Uf;
         memcpy(&Uf, &hU, sizeof Uf);
         if (n_cand > cap) {
-            // overflow: rerun with the final threshold and room for every survivor
+            // overflow: rerun with the final threshold (U is an upper bound of s_(2) in
+            // either tier) and room for every survivor; a u8 tier that leaves more than
+            // 2^24 survivors hands over to the finer fp16 tier
+            tau_pass = std::min(tau_pass, Uf);
+            if (q8 && n_cand > (1ull << 24)) {
+                q8 = false;
+                cap = 1u << 20;
+                continue;
+            }
             if (n_cand > (1ull << 28))
                 return pt_fail(PT_ECAP, "%llu fp16-tier survivors (massively tied data): above the 2^28 buffer limit",
                                n_cand);
             cap = (unsigned)n_cand;
-            tau_pass = std::min(tau_pass, Uf);
             continue;
         }
+        ctx->stats.exh_kernel = q8 ? 4 : 0;
         ctx->stats.exh_candidates = n_cand;
         if (n_cand == 0) {
             s_out[0] = s_out[1] = INFINITY;
@@ -1407,7 +1819,7 @@ pt_status pt_fleet_exhaustive_tiled(pt_ctx *ctx, int32_t k, int32_t shard_rank, 
         std::lock_guard<std::mutex> g(mu);
         auto it = occ_cache.find(std::make_pair(ctx->dev, smem));
         if (it == occ_cache.end()) {
-            PT_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            PT_TRY(pt_smem_optin(ctx, (const void *)kern));
             PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT_TCONS, smem));
             occ_cache[std::make_pair(ctx->dev, smem)] = occ;
         } else {

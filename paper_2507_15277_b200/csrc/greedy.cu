@@ -679,9 +679,7 @@ pt_status pt_greedy_seed_enqueue(pt_ctx *ctx, const pt_view *v, int32_t k)
         std::lock_guard<std::mutex> g(mu);
         auto it = occ_cache.find(std::make_pair(ctx->dev, smem));
         if (it == occ_cache.end()) {
-            if (smem > 48 * 1024)
-                PT_CK(cudaFuncSetAttribute(k_greedy_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_greedy_resident));
             PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_resident, 256, smem));
             occ_cache[std::make_pair(ctx->dev, smem)] = occ;
         } else {

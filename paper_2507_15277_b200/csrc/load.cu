@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <mutex>
 #include <cmath>
+#include <set>
 #include <vector>
 
 #include <cuda_fp16.h>
@@ -157,6 +158,10 @@ void pt_view_free(pt_ctx *ctx, pt_view &v)
         pt_dfree(ctx, v.l64);
         pt_dfree(ctx, v.hT);
         pt_dfree(ctx, v.hTile);
+        pt_dfree(ctx, v.qC);
+        pt_dfree(ctx, v.qTile);
+        pt_dfree(ctx, v.qSum);
+        pt_dfree(ctx, v.qConst);
         pt_dfree(ctx, v.hC);
         pt_dfree(ctx, v.hPair);
     }
@@ -332,6 +337,22 @@ static pt_status alloc_view(pt_ctx *ctx, pt_view &v, int64_t E, int64_t C)
         return pt_fail(PT_ENOMEM, "device allocation for a %lld x %lld view failed",
                        (long long)E, (long long)C);
     }
+    return PT_OK;
+}
+
+pt_status pt_smem_optin(pt_ctx *ctx, const void *kfn)
+{
+    static std::mutex mu;
+    static std::set<std::pair<int, const void *>> done;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(std::make_pair(ctx->dev, kfn))) return PT_OK;
+    int optin = 0;
+    PT_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->dev));
+    cudaFuncAttributes fa;
+    PT_CK(cudaFuncGetAttributes(&fa, kfn));
+    // static + dynamic shared memory of a block must fit the opt-in maximum
+    PT_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+    done.insert(std::make_pair(ctx->dev, kfn));
     return PT_OK;
 }
 

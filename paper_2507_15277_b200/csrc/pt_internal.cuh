@@ -59,10 +59,20 @@ struct pt_view {
     // one contiguous 4 KB block (one bulk copy).  Built on first exhaustive use.
     uint16_t *hTile = nullptr;
     int64_t n_ct = 0;
-    // tensor-summed exhaustive kernel (k_exh_mma) operands:
-    //   hC    [C_pad][E_pad] fp16, config-major: the same RN16(l64) values as hT
-    //   hPair [8][n_ct][E_pad/2][64] u32: hTile with env pairs (2p, 2p+1) packed
-    //         into one f16x2 word per config (low half = env 2p)
+    // u8 tier of the exhaustive search (k_exh_q8), built on first use: every value
+    // quantised to q = rint(l / Delta) in 0..255, Delta = (scope max of l) / 255;
+    //   qC    [C_pad][E_pad/4] u32, config-major, 4 consecutive envs per word (low byte first)
+    //   qTile [8][n_ct][E_pad/4][64] u32: qC re-laid out in 64-config column tiles
+    //         starting at config 64*ct + 8*s (one contiguous block per tile: one bulk copy)
+    //   qSum  [(n_ct + 1) * 64] int32: sum over envs of q per config (0 past C)
+    //   qConst[0..3] float: c1, c2, c3, c4 of the window (LB = RD(X c1 - c2), UB = RU(X c3 + c4),
+    //         X = twice the quantised set score); qConst + 4 (as double): 1 / Delta
+    uint32_t *qC = nullptr;
+    uint32_t *qTile = nullptr;
+    int32_t *qSum = nullptr;
+    float *qConst = nullptr;
+    // operands of the archived tensor-summed variants (tools/r1_variants, tools/exh_tc):
+    //   hC [C_pad][E_pad] fp16 config-major; hPair [8][n_ct][E_pad/2][64] env-pair words
     uint16_t *hC = nullptr;
     uint32_t *hPair = nullptr;
     bool owned = false;
@@ -170,6 +180,10 @@ pt_status pt_scratch(pt_ctx *ctx, size_t bytes, void **p);
 pt_status pt_get_view(pt_ctx *ctx, const uint8_t *env_mask, const pt_view **out);
 void pt_view_free(pt_ctx *ctx, pt_view &v);
 // build the view's fp16 tier (hT) if it does not exist yet
+// raise a kernel's dynamic shared-memory limit to the device's opt-in maximum, once per
+// (device, kernel).  A per-call limit cached by smem size can be left below a later
+// launch's smem when a smaller size was set in between (a launch error).
+pt_status pt_smem_optin(pt_ctx *ctx, const void *kfn);
 pt_status pt_view_fp16(pt_ctx *ctx, const pt_view *v);
 // true if p is device (or managed) memory
 bool pt_is_device_ptr(const void *p);

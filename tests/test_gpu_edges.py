@@ -81,19 +81,22 @@ def test_single_env_scope():
         check_exh(o, pt.pt_exhaustive_best(ctx, k, env_mask=mask), k, mask=mask)
 
 
+@pytest.mark.parametrize("tier", ["u8", "fp16"])
 @pytest.mark.parametrize("C", [9, 61, 64, 65, 71, 72, 127, 130])
 @pytest.mark.parametrize("k", [2, 3, 4])
-def test_every_subset_is_evaluated(C, k):
+def test_every_subset_is_evaluated(C, k, tier, monkeypatch):
     """All-tied data: every k-subset lands in the candidate window, so the count
     of refined candidates must equal C(C, k) -- a direct coverage check of the
     tiling (row tiles, column tiles, the 8-config column alignment, masks) --
     and the shards must partition the subset space."""
     if math.comb(C, k) > 900_000:
         pytest.skip("stays under the 1 M candidate buffer")
+    monkeypatch.setenv("PT_EXH_TIER", tier)
     T = np.ones((37, C), np.float32)
     ctx = pt.pt_load_perf(T)
     r = pt.pt_exhaustive_best(ctx, k)
     st = pt.pt_get_stats(ctx)
+    assert st["exh_kernel"] == (4 if tier == "u8" else 0)
     assert r["best"] == tuple(range(k))
     assert st["exh_candidates"] == math.comb(C, k) == st["exh_sets"]
     tot = 0

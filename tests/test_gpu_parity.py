@@ -92,15 +92,18 @@ def test_planted():
 
 
 # ------------------------------------------------------- medium (several tiles)
+@pytest.mark.parametrize("tier", ["u8", "fp16"])
 @pytest.mark.parametrize("seed,C,ndev,nin", [(1, 300, 3, 16), (2, 257, 2, 19), (3, 129, 5, 7)])
-def test_medium_exhaustive(seed, C, ndev, nin):
+def test_medium_exhaustive(seed, C, ndev, nin, tier, monkeypatch):
+    """Both filter tiers of the tiled search (u8 default, fp16 by PT_EXH_TIER)."""
+    monkeypatch.setenv("PT_EXH_TIER", tier)
     T, dev = synth.small_matrix(seed, n_cfg=C, n_dev=ndev, n_inputs=nin)
     o = Oracle(T, dev)
     ctx = pt.pt_load_perf(T, dev)
     for k in (2, 3):
         check_exh(o, pt.pt_exhaustive_best(ctx, k), k)
         st = pt.pt_get_stats(ctx)
-        assert st["exh_kernel"] == 0 and st["exh_sets"] == math.comb(C, k)
+        assert st["exh_kernel"] == (4 if tier == "u8" else 0) and st["exh_sets"] == math.comb(C, k)
     # sharded on one GPU (fake multi-GPU): merged shards == unsharded
     for k in (2, 3):
         want = o.exhaustive(k)
@@ -207,10 +210,13 @@ def test_paper_exhaustive_k2(paper1):
     check_exh(o, pt.pt_exhaustive_best(ctx, 2), 2)
 
 
+@pytest.mark.parametrize("tier", ["u8", "fp16"])
 @pytest.mark.parametrize("seed", [1, 2, 3])
-def test_paper_exhaustive_k3_golden(seed):
+def test_paper_exhaustive_k3_golden(seed, tier, monkeypatch):
     """Full size: 930,485,175 triples vs the oracle's stored result
-    (tests/golden/paper_exhaustive.json, written by scripts/make_golden.py)."""
+    (tests/golden/paper_exhaustive.json, written by scripts/make_golden.py), with
+    either filter tier."""
+    monkeypatch.setenv("PT_EXH_TIER", tier)
     gold = json.load(open(os.path.join(GOLDEN, "paper_exhaustive.json")))[f"seed{seed}_k3"]
     T, dev = synth.paper_matrix(seed)
     o = Oracle(T, dev)
@@ -220,7 +226,7 @@ def test_paper_exhaustive_k3_golden(seed):
     check_exh(o, res, 3, want=want)
     assert res["runner"] == want[2]
     st = pt.pt_get_stats(ctx)
-    assert st["exh_sets"] == 930_485_175
+    assert st["exh_sets"] == 930_485_175 and st["exh_kernel"] == (4 if tier == "u8" else 0)
     # the oracle re-scores the GPU's pick one by one
     assert o.score(list(res["best"])) == pytest.approx(res["G"], rel=1e-12)
     # 8-way sharded on one device (the multi-GPU partition), merged

@@ -11,5 +11,13 @@ ms = []
 for rep in range(6):
     r = pt.pt_exhaustive_best(ctx, 3)
     ms.append(pt.pt_get_stats(ctx)["exh_main_ms"])
-print(os.environ.get("PT_LIB", "default"), r["best"], "k3 kernel ms", [round(x, 3) for x in ms[1:]],
-      "median", round(float(np.median(ms[1:])), 3), flush=True)
+st = pt.pt_get_stats(ctx)
+print(os.environ.get("PT_LIB", "default"), os.environ.get("PT_EXH_TIER", "u8"), r["best"], r["runner"], r["G"],
+      "k3 kernel ms", [round(x, 3) for x in ms[1:]], "median", round(float(np.median(ms[1:])), 3),
+      "kernel", st["exh_kernel"], "candidates", st["exh_candidates"], "passes", st["exh_passes"], flush=True)
+for k in (2, 4):
+    r = pt.pt_exhaustive_best(ctx, k)
+    r = pt.pt_exhaustive_best(ctx, k)
+    st = pt.pt_get_stats(ctx)
+    print("k", k, r["best"], r["runner"], "ms", round(st["exh_main_ms"], 3), "kernel", st["exh_kernel"],
+          "candidates", st["exh_candidates"], flush=True)

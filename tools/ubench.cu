@@ -59,6 +59,16 @@ __global__ void __launch_bounds__(256) kern(float *out, const float *in, unsigne
                 if (i & 1) asm volatile("add.rn.f16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));
                 else asm volatile("min.f16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));
             }
+            if (OP == 16) asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]), "r"(*(unsigned *)&b[(i + 1) % CH]));  // VABSDIFF4.ACC
+            if (OP == 17) asm volatile("dp4a.u32.u32 %0, %1, %2, %0;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]), "r"(*(unsigned *)&b[(i + 1) % CH]));  // IDP.4A
+            if (OP == 18) {   // alternate VABSDIFF4 / HMNMX2: do they share a pipe?
+                if (i & 1) asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]), "r"(*(unsigned *)&b[(i + 1) % CH]));
+                else asm volatile("min.f16x2 %0, %0, %1;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]));
+            }
+            if (OP == 19) {   // alternate VABSDIFF4 / IMAD (FMA pipe)
+                if (i & 1) asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]), "r"(*(unsigned *)&b[(i + 1) % CH]));
+                else asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(*(unsigned *)&a[i]) : "r"(*(unsigned *)&b[i]), "r"(*(unsigned *)&b[(i + 1) % CH]));
+            }
             if (OP == 10) {  // |a-b| accumulate: FADD + FADD(|.|)
                 float d;
                 asm volatile("sub.f32 %0, %1, %2;" : "=f"(d) : "f"(a[i]), "f"(b[i]));
@@ -133,5 +143,9 @@ int main()
     run<13>("HMNMX2|VIMNMX.U16x2 alt", 1, nsm);
     run<14>("FMNMX3", 1, nsm);
     run<15>("HMNMX2|HADD2 alt", 1, nsm);
+    run<16>("VABSDIFF4.ACC (words)", 1, nsm);
+    run<17>("IDP.4A (words)", 1, nsm);
+    run<18>("VABSDIFF4|HMNMX2 alt", 1, nsm);
+    run<19>("VABSDIFF4|IMAD alt", 1, nsm);
     return 0;
 }
