@@ -9,7 +9,9 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-rnd, launches, k3rep, scanrep = sys.argv[1:5]
+rnd, launches, k3rep = sys.argv[1:4]
+scanrep = sys.argv[4] if len(sys.argv) > 4 and sys.argv[4] != "-" else None
+k3name = sys.argv[5] if len(sys.argv) > 5 else "k_exh_tiled"
 out = os.path.join(ROOT, "profiles", rnd)
 os.makedirs(out, exist_ok=True)
 src = os.path.join(ROOT, "gpurun_out")
@@ -73,7 +75,7 @@ def summary(rep, title):
     return res, vals
 
 
-k3, vals = summary(k3rep, "k_exh_tiled, exhaustive k=3, paper shape 1775 x 320, seed 1")
+k3, vals = summary(k3rep, f"{k3name}, exhaustive k=3, paper shape 1775 x 320, seed 1")
 open(os.path.join(out, "k3_ncu_summary.txt"), "w").write("\n".join(k3) + "\n")
 unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 b = sum(float(vals[k][0].replace(",", "")) * unit.get(vals[k][1], 1)
@@ -81,13 +83,15 @@ b = sum(float(vals[k][0].replace(",", "")) * unit.get(vals[k][1], 1)
 l2 = float(vals["lts__t_sectors.sum"][0].replace(",", "")) * 32 if "lts__t_sectors.sum" in vals else None
 l2pct = float(vals["lts__throughput.avg.pct_of_peak_sustained_elapsed"][0]) \
     if "lts__throughput.avg.pct_of_peak_sustained_elapsed" in vals else None
-json.dump({"kernel": "k_exh_tiled k=3 paper shape", "bytes_per_launch": b,
+json.dump({"kernel": f"{k3name} k=3 paper shape", "bytes_per_launch": b,
            "l2_bytes_per_launch": l2, "l2_throughput_pct_of_peak": l2pct,
            "source": f"profiles/{rnd}/k3_ncu_summary.txt (dram__bytes_read.sum + dram__bytes_write.sum; "
                      "lts__t_sectors.sum x 32 B; lts__throughput)"},
           open(os.path.join(ROOT, "profiles", "k3_dram_bytes.json"), "w"), indent=1)
-sc, _ = summary(scanrep, "k_greedy_scan, scaled greedy step (65,536 configs x 4,096 envs, 1 GiB fp32 stream)")
-open(os.path.join(out, "scan_ncu_summary.txt"), "w").write("\n".join(sc) + "\n")
+sc = []
+if scanrep:
+    sc, _ = summary(scanrep, "k_greedy_scan, scaled greedy step (65,536 configs x 4,096 envs, 1 GiB fp32 stream)")
+    open(os.path.join(out, "scan_ncu_summary.txt"), "w").write("\n".join(sc) + "\n")
 print("\n".join(lines[-6:]))
 print("\n".join(k3[:8]))
 print("\n".join(sc[:12]))
