@@ -291,14 +291,19 @@ def measure_per_config(pt, dT, dev, local, pk, reps=5):
     for k, name in ((2, "paper_exhaustive_k2"), (3, "paper_exhaustive_k3")):
         ms, kms = dev_ms(lambda: pt.pt_exhaustive_best(ctx, k), "exh_main_ms")
         sets = SETS[f"exh{k}"]
-        q8 = pt.pt_get_stats(ctx)["exh_kernel"] == 4
+        stk = pt.pt_get_stats(ctx)
+        q8 = stk["exh_kernel"] == 4
         pk_k = alu_peak * (2 if q8 else 1)   # u8 tier: 4 (set,env) per VABSDIFF4
+        roof = {"bound": "alu", "kernel": "k_exh_q8" if q8 else "k_exh_tiled", "unit": "T(set,env)/s",
+                "achieved": sets * E_PAPER / (kms * 1e-3) / 1e12, "peak": pk_k / 1e12,
+                "frac": sets * E_PAPER / (kms * 1e-3) / pk_k}
+        if stk["exh_kernel"] == 5:   # tc tier: tensor-bound
+            fp8 = 2.0 * float(peaks().get("bf16_tflops", 1590.0))
+            tf = 2.0 * stk["exh_tc_nt"] * stk["exh_env_pad"] * sets / (kms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "kernel": "k_exh_tc", "unit": "TFLOP/s", "achieved": tf, "peak": fp8,
+                    "frac": tf / fp8, "survivors": stk["exh_tc_survivors"], "nt": stk["exh_tc_nt"]}
         out[name] = {"config": f"BASELINE configs[2]: exhaustive k={k} over 1,775 x 320", "ms": ms,
-                     "kernel_ms": kms, "sets_per_s": sets / (ms * 1e-3),
-                     "roofline": {"bound": "alu", "kernel": "k_exh_q8" if q8 else "k_exh_tiled",
-                                  "unit": "T(set,env)/s",
-                                  "achieved": sets * E_PAPER / (kms * 1e-3) / 1e12, "peak": pk_k / 1e12,
-                                  "frac": sets * E_PAPER / (kms * 1e-3) / pk_k}}
+                     "kernel_ms": kms, "sets_per_s": sets / (ms * 1e-3), "roofline": roof}
     ms, _ = dev_ms(lambda: pt.pt_eval_holdout_all(ctx, K_HOLDOUT, 5))
     out["holdout_5fold_greedy_k5"] = {
         "config": "BASELINE configs[3]: leave-one-device-out, 5 folds, greedy k=5 (one batched launch)",
@@ -478,7 +483,8 @@ def main():
         pt.pt_free(ctx)
         return {"greedy": idx, "r2": r2, "r3": r3, "k3_ms": st3["exh_main_ms"],
                 "k3_sets": st3["exh_sets"], "k3_slots": st3["exh_slots"], "k3_kernel": st3["exh_kernel"],
-                "k3_cand": st3["exh_candidates"], "launches": st_end["launches"]}, d2h
+                "k3_cand": st3["exh_candidates"], "k3_nt": st3["exh_tc_nt"], "k3_env_pad": st3["exh_env_pad"],
+                "launches": st_end["launches"]}, d2h
 
     def timed(src, steps, warmup):
         for _ in range(warmup):
@@ -561,14 +567,31 @@ def main():
     # ALU-pipe min ceiling, 16 lanes/clk/SMSP x 4 SMSP x 2 mins per HMNMX2 = 128.
     # The FP32 roofline of the north star (one FMNMX at 16 lanes/clk/SMSP + one FADD
     # per (set, env)) is 64 (set,env)/clk/SM.
+    # Threshold-count tier (exh_kernel 5, k_exh_tc, the default): a tensor-core
+    # contraction; algorithmic work = 2 x K flops per set, K = nt x E_pad (the 0/1
+    # vectors' length), against the dense fp8 peak = the MEASURED bf16 peak x 2 (the
+    # guide's nominal fp8/bf16 ratio; burst figure: the kernel runs ~1 ms inside the step).
+    tier_tc = res.get("k3_kernel") == 5
     tier_q8 = res.get("k3_kernel") == 4
     per_clk = 256 if tier_q8 else 128
     evals = float(E_PAPER) * res["k3_sets"]
     k3_avg = float(np.mean(k3_ms))
     achieved = evals / (k3_avg * 1e-3) / 1e12
     peak = nsm * per_clk * sm_max * 1e6 / 1e12
+    peak_q8 = nsm * 256 * sm_max * 1e6 / 1e12
     peak_f16 = nsm * 128 * sm_max * 1e6 / 1e12
     peak_fp32 = nsm * 64 * sm_max * 1e6 / 1e12
+    tc_roof = None
+    if tier_tc:
+        K_tc = int(res["k3_nt"]) * int(res["k3_env_pad"])
+        tflops = 2.0 * K_tc * res["k3_sets"] / (k3_avg * 1e-3) / 1e12
+        fp8_peak = 2.0 * float(pk.get("bf16_tflops", 1590.0))   # fallback: B200_PROFILING.md's 1.59 PF bf16
+        tc_roof = {"bound": "tensor", "kernel": "k_exh_tc (k=3)", "achieved": tflops, "peak": fp8_peak,
+                   "unit": "TFLOP/s", "frac": tflops / fp8_peak,
+                   "work_per_set": f"2 x K = {2 * K_tc} flops (K = nt {res['k3_nt']} x E_pad {res['k3_env_pad']}: "
+                                   "the 0/1 threshold vectors' dot product, DESIGN.md 6.2c)",
+                   "peak_basis": "dense fp8 (E4M3, kind::f8f6f4) = MEASURED_PEAKS bf16_tflops (burst) x 2, "
+                                 "the guide's nominal fp8/bf16 ratio"}
     traffic, l2 = None, None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "k3_dram_bytes.json")))
@@ -603,7 +626,9 @@ def main():
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": ("u8 (exact integer |a-b| score of the quantised matrix) filter, f64 exact refine" if tier_q8
+        "dtype": ("e4m3 0/1 threshold-count filter on tcgen05 (exact integer counts, fp32 accumulate), "
+                  "f64 exact refine" if tier_tc else
+                  "u8 (exact integer |a-b| score of the quantised matrix) filter, f64 exact refine" if tier_q8
                   else "f16x2 min + f32 sum filter, f64 exact refine"),
         "data": "synthetic (seeded generator, paper shape; private dataset unavailable)",
         "config": {"workload": WORKLOAD, "sets_per_step": SETS_PER_STEP, "seed": args.seed,
@@ -612,7 +637,11 @@ def main():
         "e2e": {"value": SETS_PER_STEP * args.steps / (ms_e2e * 1e-3), "unit": "sets/s",
                 "h2d_bytes_per_step": h2d_e2e, "d2h_bytes_per_step": int(d2h_e2e)},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "alu", "kernel": ("k_exh_q8" if tier_q8 else "k_exh_tiled") + " (k=3)",
+        "roofline": dict(tc_roof, traffic=traffic, kernel_ms=k3_avg, kernel_share_of_step=k3_avg / (ms / args.steps),
+                         l2=l2, set_env_rate={"achieved": achieved, "unit": "T(set,env)/s",
+                                              "vs_u8_alu_ceiling": achieved / peak_q8,
+                                              "vs_fp32_alu_ceiling": achieved / peak_fp32}) if tier_tc else
+                    {"bound": "alu", "kernel": ("k_exh_q8" if tier_q8 else "k_exh_tiled") + " (k=3)",
                      "achieved": achieved,
                      "peak": peak, "unit": "T(set,env)/s", "frac": achieved / peak, "traffic": traffic,
                      "work_per_set": f"{E_PAPER} (set,env) evaluations = {E_PAPER} min + {E_PAPER} add",

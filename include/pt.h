@@ -361,12 +361,16 @@ typedef struct {
     int64_t exh_env_pad;     /* padded env count of its scope (K-loop length) */
     int64_t exh_candidates;  /* filter-tier candidates re-scored in fp64 */
     int32_t exh_passes;      /* 1; +1 per candidate-buffer overflow rerun or u8 -> fp16 hand-over */
-    int32_t exh_kernel;      /* 4 = tiled u8 filter (k_exh_q8, the default), 0 = tiled fp16 filter
-                                (k_exh_tiled; environment PT_EXH_TIER=fp16, or the u8 tier left
-                                more than 2^24 candidates), 1 = generic fp64, 2 = fleet fp64,
-                                3 = fleet tiled fp16 */
+    int32_t exh_kernel;      /* 5 = tiled threshold-count filter on tcgen05 (k_exh_tc, the default
+                                for k = 2..4), 4 = tiled u8 filter (k_exh_q8; PT_EXH_TIER=u8, or
+                                the fall-back of the tc tier), 0 = tiled fp16 filter (k_exh_tiled;
+                                PT_EXH_TIER=fp16, or the u8 tier left more than 2^24 candidates),
+                                1 = generic fp64, 2 = fleet fp64, 3 = fleet tiled fp16 */
     double greedy_ms;        /* CUDA-event time of the last greedy selection */
     int64_t greedy_candidates; /* streamed greedy: configs re-scored in fp64 (all steps) */
+    int32_t exh_tc_nt;       /* tc tier: thresholds per environment of the last search */
+    int32_t exh_tc_pad;
+    int64_t exh_tc_survivors; /* tc tier: survivors of its last pass (-1: tau unusable, fell back) */
 } pt_stats;
 
 pt_status pt_get_stats(const pt_ctx *ctx, pt_stats *out);

@@ -1,0 +1,649 @@
+// exh_tc.cu -- the threshold-count filter tier of the tiled exhaustive search
+// (k_exh_tc): the (min,+) filter of P:L271-276 / Eq. 1
+// rewritten as a dense 0/1 contraction on the 5th-generation tensor cores.
+//
+// Floor quantisation with nt uniform levels below a cap.  With thresholds
+// t_j = j u (j = 1..nt) and Q(x) = u #{j : x >= t_j}:  0 <= Q(x) <= x, Q is
+// non-decreasing, so Q(min_c l_c) = min_c Q(l_c), and [min_c l_c >= t] is the AND of
+// the members' [l_c >= t].  For a set S = rho u {l} (rho = a (k-1)-subset "row",
+// l a larger "column" index, as in k_exh_tiled):
+//     s(S) = sum_e min_{c in S} l[c][e]  >=  u P(S),
+//     P(S) = sum_e sum_j [A_rho[e] >= t_j] [l[l][e] >= t_j]
+// a dot product of two 0/1 vectors of length K = nt E_pad.  Over a task (128 rows x
+// every column above the rows) that is a GEMM: E4M3 0/1 operands (exact), fp32
+// accumulation of integers (exact below 2^24), tcgen05.mma kind::f8f6f4 into tensor
+// memory.  A set survives iff u P - slack <= tau, tau = an upper bound of the second
+// best score (two distinct k-sets scored exactly: the local optimum of a device-side
+// swap search started from greedy's k-set and its best neighbour);
+// survivors are re-scored in fp64 by the common refine (k_exh_refine_top2).  u is
+// chosen from tau (u = 1.5 tau / E): the filter's strength is a property of the data,
+// its correctness is not -- a weak filter overflows the candidate buffer and the
+// search falls back to the u8 tier.
+//
+// k_exh_tc: one CTA per SM (persistent, dynamic task queue), 10 warps:
+//   warps 0-3  epilogue: TMEM lane quarter w, thread = row; tcgen05.ld 32 columns at
+//              a time, keep the (row, column) pairs with P <= Pthr, l > last member of
+//              the row, l < C (the rare survivor path appends (key, lower bound));
+//   warps 4-7  A builders: row r of the task = AND of its members' bit rows (16-byte
+//              loads from tcA), stored in the UMMA K-major core-matrix layout of one
+//              of two A buffers (the next task's A is built during this task's MMAs);
+//   warp 8     B producer: 256-column x 64-byte K stages of tcB, one 16 KB bulk copy
+//              (cp.async.bulk, the TMA engine) per stage into an S-deep ring;
+//   warp 9     MMA issuer (one thread): per 256-column tile, K/32 MMAs of 128 x 256 x 32
+//              into one of two TMEM accumulators (2 x 256 of the 512 columns), so the
+//              epilogue of a tile overlaps the MMAs of the next.
+// Shared-memory layouts (no swizzle; core matrix = 8 rows x 16 bytes):
+//   A: offset(r, k) = (k/16) 2048 + (r/8) 128 + (r%8) 16 + k%16   (LBO 2048, SBO 128)
+//   B stage: offset(n, kk) = (n/8) 512 + (kk/16) 128 + (n%8) 16 + kk%16 (LBO 128, SBO 512)
+// (layouts and the instruction descriptor verified by tools/ubench_tc8.cu).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include <cooperative_groups.h>
+
+#include "pt_internal.cuh"
+
+namespace cgt = cooperative_groups;
+
+#define TC_R 128        // rows per task (TMEM lanes)
+#define TC_N 256        // columns per accumulator tile
+#define TC_KC 64        // K bytes per B stage
+#define TC_KMAX 640     // widest K (nt E_pad) with two A buffers in shared memory
+#define TC_THREADS 320
+
+namespace {
+
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t *b, uint32_t n)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t *b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity)
+{
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(su32(b)), "r"(parity), "r"(1000000u)
+            : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// shared-memory matrix descriptor: K-major, no swizzle, LBO = byte step between core
+// matrices along K, SBO = byte step between 8-row groups, bit 46 = sm_100 version
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo)
+{
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+// instruction descriptor, kind::f8f6f4: D f32 (bits 4-5 = 1), A = B = E4M3 (0), both
+// K-major, N >> 3 at bit 17, M >> 4 at bit 24
+constexpr uint32_t kTcIdesc = (1u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_R >> 4) << 24);
+__device__ __forceinline__ void tc_mma(uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc)
+{
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p; }" ::"r"(d),
+                 "l"(ad), "l"(bd), "r"(kTcIdesc), "r"(acc)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_ld32(uint32_t a, uint32_t (&v)[32])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"   // same asm: no use of v[] can be scheduled before the wait
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(a)
+        : "memory");
+}
+
+}  // namespace
+
+// device constants of one search (k_tc_const)
+struct TcConst {
+    double u;            // threshold step (a float value: j u is exact in fp64)
+    double tau;          // upper bound of s_(2) (fp64, exact scores of two distinct sets)
+    float pthr;          // survivor iff P <= pthr
+    float u_dn;          // u as a float
+    float slack;         // fp64 rounding slack of the refine's sums (rounded up)
+    int ok;              // 0: tau is not finite / u underflows -> the caller falls back
+    unsigned long long lmax_bits;   // scope max of l (atomicMax on the bit pattern)
+};
+
+// ---------------------------------------------------------------------------
+// tau: best-improvement swap search from greedy's k-set, entirely on the device (one
+// cooperative launch, one grid barrier per move).  Every move scores all k (C - k)
+// neighbours S - S[a] + b exactly in fp64 (leave-one-out minima, as swap.cu); the
+// larger score of two distinct sets bounds s_(2) from above, so
+//     tau = min( greedy's runner-up at step k, min over moves max(s(S), s(best neighbour)) ).
+// Every CTA merges the per-CTA bests itself (same order: same move everywhere), so the
+// loop needs one grid barrier per move.  Ties and the move rule only affect tau's
+// tightness, never correctness.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_swap_tau(const double *__restrict__ l64, int64_t C, int64_t E_pad, int k,
+                                                  const int32_t *__restrict__ S0, const double *__restrict__ seed_s2,
+                                                  int iters, double *__restrict__ rs, long long *__restrict__ rw,
+                                                  double *__restrict__ tau_out)
+{
+    cgt::grid_group grid = cgt::this_grid();
+    extern __shared__ double M[];   // [k][E_pad] leave-one-out minima
+    __shared__ int32_t S[PT_MAXK];
+    __shared__ double red[8];
+    __shared__ long long redw[8];
+    __shared__ double tau_s;
+    __shared__ int stop_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < k) S[tid] = S0[tid];
+    if (tid == 0) {
+        tau_s = seed_s2 ? *seed_s2 : INFINITY;
+        stop_s = 0;
+    }
+    __syncthreads();
+    for (int it = 0; it < iters; it++) {
+        // leave-one-out minima and the current score (same order in every CTA)
+        double part = 0.0;
+        for (int64_t e = tid; e < E_pad; e += blockDim.x) {
+            double v[PT_MAXK], suf[PT_MAXK + 1];
+            for (int u = 0; u < k; u++) v[u] = l64[(int64_t)S[u] * E_pad + e];
+            suf[k] = INFINITY;
+            for (int u = k - 1; u >= 0; u--) suf[u] = fmin(suf[u + 1], v[u]);
+            double pre = INFINITY;
+            for (int a = 0; a < k; a++) {
+                M[(int64_t)a * E_pad + e] = fmin(pre, suf[a + 1]);
+                pre = fmin(pre, v[a]);
+            }
+            part += pre;
+        }
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) red[warp] = part;
+        __syncthreads();
+        double cur = 0.0;
+        for (int w = 0; w < 8; w++) cur += red[w];
+        // this CTA's best neighbour (warp per (a, b); ties -> smallest a C + b)
+        double bs = INFINITY;
+        long long bw = LLONG_MAX;
+        const int64_t nw = (int64_t)k * C;
+        for (int64_t w = (int64_t)blockIdx.x * 8 + warp; w < nw; w += (int64_t)gridDim.x * 8) {
+            const int a = (int)(w / C);
+            const int64_t b = w - (int64_t)a * C;
+            bool in = false;
+            for (int u = 0; u < k; u++) in |= (S[u] == b);
+            if (in) continue;
+            const double *mr = M + (int64_t)a * E_pad, *col = l64 + b * E_pad;
+            double acc = 0.0;
+            for (int64_t e = lane; e < E_pad; e += 32) acc += fmin(mr[e], col[e]);
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (acc < bs) {
+                bs = acc;
+                bw = w;
+            }
+        }
+        __syncthreads();   // red[] reused below
+        if (lane == 0) {
+            red[warp] = bs;
+            redw[warp] = bw;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < 8; w++)
+                if (red[w] < bs || (red[w] == bs && redw[w] < bw)) {
+                    bs = red[w];
+                    bw = redw[w];
+                }
+            rs[(it & 1) * gridDim.x + blockIdx.x] = bs;
+            rw[(it & 1) * gridDim.x + blockIdx.x] = bw;
+        }
+        grid.sync();
+        // merge every CTA's record (identically in every CTA) and apply the move
+        double ms = INFINITY;
+        long long mw = LLONG_MAX;
+        for (int b = tid; b < (int)gridDim.x; b += blockDim.x) {
+            const double x = __ldcg(&rs[(it & 1) * gridDim.x + b]);
+            const long long y = __ldcg(&rw[(it & 1) * gridDim.x + b]);
+            if (x < ms || (x == ms && y < mw)) {
+                ms = x;
+                mw = y;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double x = __shfl_xor_sync(0xffffffffu, ms, o);
+            const long long y = __shfl_xor_sync(0xffffffffu, mw, o);
+            if (x < ms || (x == ms && y < mw)) {
+                ms = x;
+                mw = y;
+            }
+        }
+        __syncthreads();
+        if (lane == 0) {
+            red[warp] = ms;
+            redw[warp] = mw;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < 8; w++)
+                if (red[w] < ms || (red[w] == ms && redw[w] < mw)) {
+                    ms = red[w];
+                    mw = redw[w];
+                }
+            if (ms < INFINITY) tau_s = fmin(tau_s, fmax(cur, ms));
+            if (ms < cur) {
+                S[mw / C] = (int32_t)(mw % C);
+            } else {
+                stop_s = 1;
+            }
+        }
+        __syncthreads();
+        if (stop_s) break;
+    }
+    if (blockIdx.x == 0 && tid == 0) *tau_out = tau_s;
+}
+
+// scope max of l (non-negative doubles order as their bit patterns)
+__global__ void __launch_bounds__(256) k_tc_lmax(const double *__restrict__ l64, int64_t C, int64_t E, int64_t E_pad,
+                                                TcConst *__restrict__ cst)
+{
+    double m = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < C * E; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / E, e = i - c * E;
+        m = fmax(m, l64[c * E_pad + e]);
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&cst->lmax_bits, (unsigned long long)__double_as_longlong(m));
+}
+
+// u, the survivor threshold and the refine's tau (one thread, no host round trip).
+// The refine's fp64 sum of E_pad terms in [0, lmax] differs from the exact score by
+// <= E_pad^2 lmax 2^-53 (any order); two such sums (tau's sets and the refine's) and the
+// lower bound give 3 of them: slack = 4 E_pad^2 lmax 2^-52.
+__global__ void k_tc_const(const double *__restrict__ tau_dev, int64_t E, int64_t E_pad, double alpha,
+                           TcConst *__restrict__ cst, unsigned *__restrict__ U, unsigned long long *__restrict__ cand_n)
+{
+    const double tau = *tau_dev;
+    const double lmax = __longlong_as_double((long long)cst->lmax_bits);
+    const double slack = 4.0 * (double)E_pad * (double)E_pad * lmax * 0x1p-52 + 1e-300;
+    const float uf = (float)(alpha * tau / (double)E);
+    const double u = (double)uf;
+    const bool ok = isfinite(tau) && u > 1e-30 && isfinite(u);
+    cst->u = u;
+    cst->tau = tau;
+    cst->ok = ok ? 1 : 0;
+    cst->u_dn = uf;
+    cst->slack = __double2float_ru(slack);
+    cst->pthr = ok ? __double2float_ru((tau + slack) / u * (1.0 + 1e-12)) : -1.0f;
+    *U = __float_as_uint(ok ? __double2float_ru(tau + slack) : 0.0f);
+    if (!ok) *cand_n = 1ull << 63;   // "not run": the refine skips, the host falls back
+}
+
+// the bit operands: tcA[c][k] and tcB in the B-stage layout; k = j E_pad + e,
+// bit = [l[c][e] >= (j+1) u] for real configs and environments (0 elsewhere)
+__global__ void __launch_bounds__(256) k_tc_build(const double *__restrict__ l64, int64_t C, int64_t E, int64_t E_pad,
+                                                 int K, int64_t n_cfg, const TcConst *__restrict__ cst,
+                                                 uint8_t *__restrict__ A, uint8_t *__restrict__ B)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_cfg * K) return;
+    const int64_t c = i / K;
+    const int k = (int)(i - c * K);
+    const int j = k / (int)E_pad, e = k - j * (int)E_pad;
+    uint8_t bit = 0;
+    if (cst->ok && c < C && e < E && l64[c * E_pad + e] >= (double)(j + 1) * cst->u) bit = 0x38;   // E4M3 1.0
+    A[i] = bit;
+    const int64_t n_grp = n_cfg / 8;
+    const int kc = k / TC_KC, kk = k % TC_KC;
+    B[((int64_t)kc * n_grp + c / 8) * (8 * TC_KC) + (kk / 16) * 128 + (c % 8) * 16 + kk % 16] = bit;
+}
+
+struct TcParams {
+    int64_t C, n_rows, n_grp;
+    int m, K, S;
+    const int4 *tasks;
+    int task_hi;
+    int *task_ctr;
+    const uint8_t *A, *B;
+    const TcConst *cst;
+    unsigned long long *cand_key;
+    float *cand_s;
+    unsigned long long *cand_n;
+    unsigned cap;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int K = p.K, S = p.S;
+    uint8_t *Abuf = smem;                                     // [2][128 K]
+    uint8_t *Bbuf = smem + 2 * TC_R * K;                      // [S][256 x 64]
+    int *last = reinterpret_cast<int *>(Bbuf + S * TC_N * TC_KC);   // [2][128]
+    int4 *tinfo = reinterpret_cast<int4 *>(last + 2 * TC_R);        // [2] (row tile, u0, u1, lo)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tinfo + 2);
+    uint64_t *a_full = bars, *a_empty = bars + 2, *t_full = bars + 4, *acc_full = bars + 6, *acc_empty = bars + 8;
+    uint64_t *b_full = bars + 10, *b_empty = bars + 10 + S;
+    uint32_t *tmem_s = reinterpret_cast<uint32_t *>(bars + 10 + 2 * S);
+    int *bcast = reinterpret_cast<int *>(tmem_s + 1);          // [2]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (!p.cst->ok) return;   // tau unusable (k_tc_const flagged the search as not run)
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) {
+            bar_init(&a_full[i], TC_R);
+            bar_init(&a_empty[i], 1 + 4);
+            bar_init(&t_full[i], 1);
+            bar_init(&acc_full[i], 1);
+            bar_init(&acc_empty[i], 4);
+        }
+        for (int s = 0; s < S; s++) {
+            bar_init(&b_full[s], 1);
+            bar_init(&b_empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_s)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_s;
+    const int m = p.m;
+
+    if (warp < 4) {
+        // ---------------- epilogue ----------------
+        const int r = 32 * warp + lane;
+        const float pthr = p.cst->pthr, u_dn = p.cst->u_dn, slk = p.cst->slack;
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
+        uint32_t tcnt = 0;
+        for (int t = 0;; t++) {
+            const int slot = t & 1;
+            bar_wait(&a_full[slot], (t >> 1) & 1);
+            const int4 ti = tinfo[slot];
+            const int lastr = last[slot * TC_R + r];
+            __syncwarp();
+            if (lane == 0) bar_arrive(&a_empty[slot]);
+            if (ti.x < 0) break;
+            const int64_t R = (int64_t)ti.x * TC_R + r;
+            for (int u = ti.y; u < ti.z; u++, tcnt++) {
+                const int buf = tcnt & 1;
+                bar_wait(&acc_full[buf], (tcnt >> 1) & 1);
+                tc_fence_after();
+                const int64_t col0 = (int64_t)ti.w + (int64_t)u * TC_N;
+#pragma unroll 1
+                for (int q = 0; q < TC_N / 32; q++) {
+                    uint32_t v[32];
+                    tc_ld32(lane_base + buf * TC_N + q * 32, v);
+                    float mn = __uint_as_float(v[0]);
+#pragma unroll
+                    for (int j = 1; j < 32; j++) mn = fminf(mn, __uint_as_float(v[j]));
+                    if (mn <= pthr) {   // rare: the window, then validity
+                        const int64_t cb = col0 + q * 32;
+                        for (int j = 0; j < 32; j++) {
+                            const float P = __uint_as_float(v[j]);
+                            const int64_t l = cb + j;
+                            if (P <= pthr && l > lastr && l < p.C) {
+                                const unsigned long long idx = atomicAdd(p.cand_n, 1ull);
+                                if (idx < p.cap) {
+                                    p.cand_key[idx] = ((unsigned long long)R << KEY_BITS) | (unsigned long long)l;
+                                    p.cand_s[idx] = __fmaf_rd(P, u_dn, -slk);
+                                }
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&acc_empty[buf]);
+            }
+        }
+    } else if (warp < 8) {
+        // ---------------- A builders ----------------
+        const int bt = tid - 128;
+        for (int t = 0;; t++) {
+            const int slot = t & 1;
+            bar_wait(&a_empty[slot], ((t >> 1) & 1) ^ 1);
+            if (bt == 0) bcast[slot] = atomicAdd(p.task_ctr, 1);
+            named_sync(1, 128);
+            const int ti = bcast[slot];
+            if (ti >= p.task_hi) {
+                if (bt == 0) {
+                    tinfo[slot] = make_int4(-1, 0, 0, 0);
+                    bar_arrive(&t_full[slot]);
+                }
+                bar_arrive(&a_full[slot]);
+                break;
+            }
+            const int4 tk = p.tasks[ti];
+            const int64_t R0 = (int64_t)tk.x * TC_R;
+            if (bt == 0) {
+                int32_t mem0[PT_MAXK];
+                pt_unrank_colex(R0, m, p.C, mem0);
+                tinfo[slot] = make_int4(tk.x, tk.y, tk.z, (int)tile_lo(mem0[m - 1]));
+                bar_arrive(&t_full[slot]);
+            }
+            const int64_t R = R0 + bt;
+            const bool valid = R < p.n_rows;
+            int32_t mem[PT_MAXK];
+            if (valid) pt_unrank_colex(R, m, p.C, mem);
+            else for (int u = 0; u < m; u++) mem[u] = 0;
+            last[slot * TC_R + bt] = valid ? mem[m - 1] : 0x7fffffff;
+            uint8_t *As = Abuf + (size_t)slot * TC_R * K + (bt >> 3) * 128 + (bt & 7) * 16;
+            const uint4 *src0 = reinterpret_cast<const uint4 *>(p.A + (int64_t)mem[0] * K);
+            const uint4 *src1 = reinterpret_cast<const uint4 *>(p.A + (int64_t)mem[m > 1 ? 1 : 0] * K);
+            const uint4 *src2 = reinterpret_cast<const uint4 *>(p.A + (int64_t)mem[m > 2 ? 2 : 0] * K);
+#pragma unroll 4
+            for (int kq = 0; kq < K / 16; kq++) {
+                uint4 v = src0[kq];
+                if (m > 1) {
+                    const uint4 w = src1[kq];
+                    v.x &= w.x; v.y &= w.y; v.z &= w.z; v.w &= w.w;
+                }
+                if (m > 2) {
+                    const uint4 w = src2[kq];
+                    v.x &= w.x; v.y &= w.y; v.z &= w.z; v.w &= w.w;
+                }
+                if (!valid) v = make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4 *>(As + kq * (TC_R * 16)) = v;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+            bar_arrive(&a_full[slot]);
+        }
+    } else if (warp == 8) {
+        // ---------------- B producer ----------------
+        if (lane == 0) {
+            uint32_t sc = 0;
+            const int nkc = K / TC_KC;
+            for (int t = 0;; t++) {
+                const int slot = t & 1;
+                bar_wait(&t_full[slot], (t >> 1) & 1);
+                const int4 ti = tinfo[slot];
+                if (ti.x < 0) break;
+                for (int u = ti.y; u < ti.z; u++) {
+                    const int64_t grp0 = ((int64_t)ti.w + (int64_t)u * TC_N) >> 3;
+                    for (int kc = 0; kc < nkc; kc++, sc++) {
+                        const int st = (int)(sc % (uint32_t)S);
+                        bar_wait(&b_empty[st], ((sc / (uint32_t)S) & 1) ^ 1);
+                        bar_expect_tx(&b_full[st], TC_N * TC_KC);
+                        bulk_g2s(Bbuf + (size_t)st * TC_N * TC_KC, p.B + ((int64_t)kc * p.n_grp + grp0) * (8 * TC_KC),
+                                 TC_N * TC_KC, &b_full[st]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            uint32_t sc = 0, tcnt = 0;
+            const int nkc = K / TC_KC;
+            for (int t = 0;; t++) {
+                const int slot = t & 1;
+                bar_wait(&a_full[slot], (t >> 1) & 1);
+                const int4 ti = tinfo[slot];
+                if (ti.x < 0) break;
+                tc_fence_after();
+                const uint32_t abase = su32(Abuf + (size_t)slot * TC_R * K);
+                for (int u = ti.y; u < ti.z; u++, tcnt++) {
+                    const int buf = tcnt & 1;
+                    bar_wait(&acc_empty[buf], ((tcnt >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem + buf * TC_N;
+                    for (int kc = 0; kc < nkc; kc++, sc++) {
+                        const int st = (int)(sc % (uint32_t)S);
+                        bar_wait(&b_full[st], (sc / (uint32_t)S) & 1);
+                        tc_fence_after();
+                        const uint32_t bbase = su32(Bbuf + (size_t)st * TC_N * TC_KC);
+#pragma unroll
+                        for (int i = 0; i < TC_KC / 32; i++) {
+                            const int kk = kc * TC_KC + i * 32;
+                            tc_mma(d, sdesc(abase + (kk / 16) * (TC_R * 16), TC_R * 16, 128),
+                                   sdesc(bbase + i * 256, 128, 8 * TC_KC), (kc | i) ? 1u : 0u);
+                        }
+                        tc_commit(&b_empty[st]);
+                    }
+                    tc_commit(&acc_full[buf]);
+                }
+                tc_commit(&a_empty[slot]);
+            }
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static size_t tc_smem(int K, int S)
+{
+    return (size_t)2 * TC_R * K + (size_t)S * TC_N * TC_KC + sizeof(int) * 2 * TC_R + sizeof(int4) * 2 +
+           sizeof(uint64_t) * (10 + 2 * S) + 16;
+}
+
+pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, int *nt_out)
+{
+    cudaStream_t s = ctx->stream;
+    const int m = a.k - 1;
+    if (m < 1 || m > 3 || v->C >= (1 << KEY_BITS) || v->E_pad % TC_KC != 0) return PT_EINVAL;
+    // nt thresholds (PT_TC_NT, default 2), as many as fit TC_KMAX
+    // (read per call: the tests vary them in one process)
+    const int nt_env = getenv("PT_TC_NT") ? atoi(getenv("PT_TC_NT")) : 2;
+    const double alpha = getenv("PT_TC_ALPHA") ? atof(getenv("PT_TC_ALPHA")) : 1.5;
+    const int nt = (int)std::min<int64_t>(std::max(nt_env, 1), TC_KMAX / v->E_pad);
+    if (nt < 1) return PT_EINVAL;
+    const int K = nt * (int)v->E_pad;
+    const size_t smem_limit = 227 * 1024 - 1024;   // margin for static shared memory
+    int S = 4;
+    while (S > 2 && tc_smem(K, S) > smem_limit) S--;
+    if (tc_smem(K, S) > smem_limit) return PT_EINVAL;
+    // per-call operands (the thresholds follow tau)
+    pt_view *mv = const_cast<pt_view *>(v);
+    const int64_t n_cfg = pt_round_up(v->C + TC_N + 8, 8);
+    if (!mv->tcConst) PT_TRY(pt_dalloc(ctx, &mv->tcConst, sizeof(TcConst)));
+    if (mv->tc_ncfg != n_cfg || mv->tc_K != K) {
+        pt_dfree(ctx, mv->tcA);
+        pt_dfree(ctx, mv->tcB);
+        mv->tcA = mv->tcB = nullptr;
+        PT_TRY(pt_dalloc(ctx, (void **)&mv->tcA, (size_t)n_cfg * K));
+        PT_TRY(pt_dalloc(ctx, (void **)&mv->tcB, (size_t)n_cfg * K));
+        mv->tc_ncfg = n_cfg;
+        mv->tc_K = K;
+    }
+    TcConst *cst = (TcConst *)mv->tcConst;
+    // tau: device swap search from greedy's k-set
+    static std::mutex mu;
+    static std::map<std::tuple<int, size_t>, int> occ_cache;
+    const size_t sw_smem = sizeof(double) * a.k * v->E_pad;
+    int occ = 0;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto key = std::make_tuple(ctx->dev, sw_smem);
+        auto it = occ_cache.find(key);
+        if (it == occ_cache.end()) {
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_swap_tau));
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc));
+            PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_swap_tau, 256, sw_smem));
+            occ_cache[key] = occ;
+        } else {
+            occ = it->second;
+        }
+    }
+    if (occ < 1) return PT_EINVAL;
+    const int nblk = ctx->num_sms;
+    double *rs = a.swap_rs;
+    long long *rw = a.swap_rw;
+    double *tau_dev = a.tau_dev;
+    {
+        const double *l64 = v->l64;
+        int64_t CC = v->C, EE = v->E_pad;
+        int kk = a.k, iters = 16;
+        const int32_t *S0 = a.d_S0;
+        const double *seed = a.d_seed_s2;
+        void *args[] = {(void *)&l64, (void *)&CC, (void *)&EE, (void *)&kk, (void *)&S0, (void *)&seed,
+                        (void *)&iters, (void *)&rs, (void *)&rw, (void *)&tau_dev};
+        PT_CK(cudaLaunchCooperativeKernel((void *)k_swap_tau, dim3(nblk), dim3(256), args, sw_smem, s));
+    }
+    PT_CK(cudaMemsetAsync(&cst->lmax_bits, 0, sizeof(unsigned long long), s));
+    const int64_t ne = v->C * v->E;
+    const unsigned gmax = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ne + 255) / 256, 4L * ctx->num_sms));
+    k_tc_lmax<<<gmax, 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, cst);
+    k_tc_const<<<1, 1, 0, s>>>(tau_dev, v->E, v->E_pad, alpha, cst, a.U, a.cand_n);
+    const int64_t nb = n_cfg * K;
+    k_tc_build<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, K, n_cfg, cst, mv->tcA,
+                                                             mv->tcB);
+    ctx->stats.launches += 4;
+    PT_CK(cudaGetLastError());
+    TcParams p;
+    p.C = v->C;
+    p.n_rows = pt_binom(v->C, m);
+    p.n_grp = n_cfg / 8;
+    p.m = m;
+    p.K = K;
+    p.S = S;
+    p.tasks = a.tasks;
+    p.task_hi = a.tb;
+    p.task_ctr = a.ctr;
+    p.A = mv->tcA;
+    p.B = mv->tcB;
+    p.cst = cst;
+    p.cand_key = a.cand_key;
+    p.cand_s = a.cand_s;
+    p.cand_n = a.cand_n;
+    p.cap = a.cap;
+    const int grid = std::min(ctx->num_sms, a.tb - a.ta);
+    PT_CK(cudaEventRecord(ctx->ev0, s));
+    k_exh_tc<<<grid, TC_THREADS, tc_smem(K, S), s>>>(p);
+    PT_CK(cudaEventRecord(ctx->ev1, s));
+    ctx->stats.launches++;
+    PT_CK(cudaGetLastError());
+    if (nt_out) *nt_out = nt;
+    return PT_OK;
+}

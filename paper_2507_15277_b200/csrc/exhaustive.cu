@@ -61,16 +61,10 @@ static constexpr int kXtPUnroll = XT_PUNROLL;
 static_assert(XT_K % (4 * XT_NG) == 0, "a pipeline stage must hold whole fp16 chains");
 #define XT_EMAX 768 // widest scope the resident-A kernel takes (smem)
 #define XT_UMAX 1024 // column tiles per task (a whole row tile: A staged once)
-#define KEY_BITS 21
 
 // ---------------------------------------------------------------------------
 // work list
 // ---------------------------------------------------------------------------
-// first column of a row tile whose first row's largest member is j0: j0 + 1
-// rounded down to 8 configs (16-byte aligned fp16 rows); the extra columns are
-// <= every row's largest member and masked.  Used by the task builder AND the
-// kernel so both cover exactly [tile_lo, tile_lo + 64 * n_ct) >= [j0+1, C).
-__host__ __device__ static inline int64_t tile_lo(int64_t j0) { return (j0 + 1) & ~(int64_t)7; }
 
 struct pt_tasks {
     int m = 0;
@@ -1106,7 +1100,8 @@ __global__ void __launch_bounds__(256) k_exh_refine_top2(
     int64_t E_pad, Rec2 *__restrict__ blk, unsigned *__restrict__ done, double *__restrict__ out_s,
     int32_t *__restrict__ out_t)
 {
-    const int64_t n = (int64_t)min(*n_dev, (unsigned long long)cap);
+    const unsigned long long nd = *n_dev;   // bit 63: the filter did not run (tc tier)
+    const int64_t n = (nd >> 63) ? 0 : (int64_t)min(nd, (unsigned long long)cap);
     const float tau = fminf(tau_pass, __uint_as_float(*U));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int k = m + 1;
@@ -1464,7 +1459,34 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     // so the tests can exercise both tiers in one process)
     const char *tier_env = getenv("PT_EXH_TIER");
     const bool force_fp16 = tier_env && !strcmp(tier_env, "fp16");
+    const bool force_u8 = tier_env && !strcmp(tier_env, "u8");
     bool q8 = !force_fp16;
+    // threshold-count tier (k_exh_tc, exh_tc.cu): the default for k = 2..4; its own task
+    // list (256-column tiles); on an unusable tau or a buffer overflow the search falls
+    // back to the u8 tier in the next pass
+    bool tc = !force_fp16 && !force_u8 && k >= 2 && k <= 4;
+    const int4 *tc_list = nullptr;
+    int tc_ta = 0, tc_tb = 0;
+    int64_t tc_sets = 0, tc_slots = 0;
+    if (tc) {
+        pt_tasks *TT = nullptr;
+        PT_TRY(build_tasks(ctx, v, m, XT_R, PT_TC_COLS, &TT));
+        tc_list = TT->d;
+        tc_tb = (int)TT->h.size();
+        tc_sets = TT->set_pre.back();
+        tc_slots = TT->slot_pre.back();
+        if (shard_count > 1) {
+            const pt_tasks::plan *P = nullptr;
+            static const std::vector<double> equal;
+            PT_TRY(shard_plan(TT, shard_count, (int)ctx->shard_w.size() == shard_count ? ctx->shard_w : equal, &P));
+            tc_list = P->d;
+            tc_ta = P->off[shard_rank];
+            tc_tb = P->off[shard_rank + 1];
+            tc_sets = P->sets[shard_rank];
+            tc_slots = P->slots[shard_rank];
+        }
+        if (tc_sets != ctx->stats.exh_sets) tc = false;   // both lists cover the same sets (always)
+    }
     const int G = (int)(v->E_pad / 4);
     auto q8_smem = [&](int S) {
         return (size_t)4 * S * G * XQ_C + (size_t)4 * G * XQ_R + sizeof(int) * (256 + XQ_R) +
@@ -1474,23 +1496,37 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const int q8_S = 2 * q8_smem(3) <= smem_budget ? 3 : 2;
     const size_t smem_q8 = q8_smem(q8_S);
     int occ_q8 = 0;
-    if (q8) {
-        PT_TRY(pt_view_q8(ctx, v));
-        PT_TRY(occupancy((const void *)k_exh_q8, smem_q8, 256, &occ_q8));
-        if (occ_q8 < 1) q8 = false;
+    bool q8_ready = false;
+    auto prepare_q8 = [&]() -> pt_status {
+        if (q8 && !q8_ready) {
+            PT_TRY(pt_view_q8(ctx, v));
+            PT_TRY(occupancy((const void *)k_exh_q8, smem_q8, 256, &occ_q8));
+            if (occ_q8 < 1) q8 = false;
+            q8_ready = true;
+        }
+        return PT_OK;
+    };
+    if (!tc) PT_TRY(prepare_q8());
+    // the tc tier starts its swap search from greedy's k-set: the host trace's picks, or
+    // the device trace (enqueued above when there is no host trace)
+    if (tc && v->greedy_idx.size() < (size_t)k && v->d_seed_k < k) {
+        if (pt_greedy_seed_enqueue(ctx, v, (int)std::min<int64_t>(std::max(k, 3), v->C)) != PT_OK) tc = false;
     }
 
     unsigned cap = 1u << 20;
     unsigned long long n_cand = 0;
     float tau_pass = tau_seed;
-    for (int pass = 0; pass < 4; pass++) {
+    int tier_pass0 = -1;   // first pass of the filter tier whose answer is returned (its time is exh_main_ms)
+    for (int pass = 0; pass < 6; pass++) {
         size_t off = 0;
         auto take = [&](size_t b) { size_t o = off; off += pt_round_up(b, 256); return o; };
         const size_t o_ctr = take(sizeof(int)), o_U = take(sizeof(unsigned)),
                      o_n = take(sizeof(unsigned long long)), o_key = take(sizeof(unsigned long long) * cap),
                      o_cq = take(sizeof(float) * cap),
                      o_os = take(sizeof(double) * 2), o_ot = take(sizeof(int32_t) * 2 * k),
-                     o_blk = take(sizeof(Rec2) * (size_t)ctx->num_sms * 2), o_done = take(sizeof(unsigned));
+                     o_blk = take(sizeof(Rec2) * (size_t)ctx->num_sms * 2), o_done = take(sizeof(unsigned)),
+                     o_S0 = take(sizeof(int32_t) * k), o_sd = take(sizeof(double)), o_tau = take(sizeof(double)),
+                     o_rs = take(sizeof(double) * 2 * ctx->num_sms), o_rw = take(sizeof(long long) * 2 * ctx->num_sms);
         void *scr = nullptr;
         PT_TRY(pt_scratch(ctx, off, &scr));
         char *b = (char *)scr;
@@ -1505,8 +1541,11 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         unsigned *done = (unsigned *)(b + o_done);
         const unsigned u_init = 0x7f800000u;   // +inf
         pt_hostio io(ctx);
-        PT_TRY(io.h2d(ctr, &ta, sizeof(int)));
-        if (seed_dev) {
+        if (!tc) PT_TRY(prepare_q8());
+        PT_TRY(io.h2d(ctr, tc ? &tc_ta : &ta, sizeof(int)));
+        if (tc) {
+            // (U is written by the tc tier's constants kernel)
+        } else if (seed_dev) {
             k_seed_U<<<1, 1, 0, s>>>(seed_dev, U);
             ctx->stats.launches++;
         } else {
@@ -1514,7 +1553,57 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         }
         PT_CK(cudaMemsetAsync(cn, 0, sizeof(unsigned long long), s));
         PT_CK(cudaMemsetAsync(done, 0, sizeof(unsigned), s));
-        if (q8) {
+        bool tc_launched = false;
+        if (!tc && tier_pass0 < 0) tier_pass0 = pass;
+        if (tc) {
+            pt_tc_args a;
+            a.k = k;
+            a.tasks = tc_list;
+            a.ta = tc_ta;
+            a.tb = tc_tb;
+            a.ctr = ctr;
+            a.U = U;
+            a.cand_n = cn;
+            a.cand_key = ckey;
+            a.cand_s = cq;
+            a.cap = cap;
+            if (v->greedy_idx.size() >= (size_t)k) {
+                const double sd = v->greedy_s2[k - 1];
+                PT_TRY(io.h2d(b + o_S0, v->greedy_idx.data(), sizeof(int32_t) * k));
+                PT_TRY(io.h2d(b + o_sd, &sd, sizeof(double)));
+                a.d_S0 = (const int32_t *)(b + o_S0);
+                a.d_seed_s2 = (const double *)(b + o_sd);
+            } else {
+                a.d_S0 = v->d_seed_idx;
+                a.d_seed_s2 = v->d_seed_s2 + (k - 1);
+            }
+            a.swap_rs = (double *)(b + o_rs);
+            a.swap_rw = (long long *)(b + o_rw);
+            a.tau_dev = (double *)(b + o_tau);
+            mark("pre-launch");
+            int nt = 0;
+            const pt_status st = pt_exh_tc_enqueue(ctx, v, a, &nt);
+            if (st == PT_OK) {
+                tc_launched = true;
+                ctx->stats.exh_tc_nt = nt;
+            } else if (st == PT_EINVAL) {
+                tc = false;   // not eligible: this pass runs the u8 tier
+                tier_pass0 = pass;
+                PT_TRY(prepare_q8());
+                PT_TRY(io.h2d(ctr, &ta, sizeof(int)));
+                if (seed_dev) {
+                    k_seed_U<<<1, 1, 0, s>>>(seed_dev, U);
+                    ctx->stats.launches++;
+                } else {
+                    PT_TRY(io.h2d(U, &u_init, sizeof(unsigned)));
+                }
+            } else {
+                return st;
+            }
+        }
+        if (tc_launched) {
+            tau_pass = INFINITY;   // the refine's threshold is U (k_tc_const)
+        } else if (q8) {
             QParams p;
             p.C = v->C;
             p.E_pad = v->E_pad;
@@ -1590,10 +1679,29 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         mark("synced");
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
-        if (pass == 0) ctx->stats.exh_main_ms = ms;
+        if (pass == tier_pass0 || tc_launched) ctx->stats.exh_main_ms = ms;
         ctx->stats.exh_passes = pass + 1;
         float Uf;
         memcpy(&Uf, &hU, sizeof Uf);
+        if (tc_launched) {
+            ctx->stats.exh_tc_survivors = (n_cand >> 63) ? -1 : (int64_t)n_cand;
+            if ((n_cand >> 63) || n_cand > cap) {
+                // tau unusable or too weak a filter: the u8 tier, seeded as before
+                tc = false;
+                tau_pass = tau_seed;
+                cap = 1u << 20;
+                continue;
+            }
+            ctx->stats.exh_kernel = 5;
+            ctx->stats.exh_candidates = n_cand;
+            ctx->stats.exh_sets = tc_sets;
+            ctx->stats.exh_slots = tc_slots;
+            if (n_cand == 0) {
+                s_out[0] = s_out[1] = INFINITY;
+                for (int u = 0; u < 2 * k; u++) t_out[u] = 0;
+            }
+            return PT_OK;
+        }
         if (n_cand > cap) {
             // overflow: rerun with the final threshold (U is an upper bound of s_(2) in
             // either tier) and room for every survivor; a u8 tier that leaves more than

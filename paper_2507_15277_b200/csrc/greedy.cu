@@ -690,15 +690,17 @@ pt_status pt_greedy_seed_enqueue(pt_ctx *ctx, const pt_view *v, int32_t k)
     const int nblk = ctx->num_sms * std::min(occ, GR_BPS);
     pt_view *mv = const_cast<pt_view *>(v);
     if (mv->d_seed_s2) pt_dfree(ctx, mv->d_seed_s2);
+    if (mv->d_seed_idx) pt_dfree(ctx, mv->d_seed_idx);
     mv->d_seed_s2 = nullptr;
+    mv->d_seed_idx = nullptr;
     mv->d_seed_k = 0;
     PT_TRY(pt_dalloc(ctx, (void **)&mv->d_seed_s2, sizeof(double) * k));
+    PT_TRY(pt_dalloc(ctx, (void **)&mv->d_seed_idx, sizeof(int32_t) * k));
     char *tmp = nullptr;
-    const size_t o_idx = pt_round_up(sizeof(double4) * 2 * nblk, 256) + 256;
-    const size_t o_s1 = o_idx + pt_round_up(sizeof(int32_t) * k, 256);
+    const size_t o_s1 = pt_round_up(sizeof(double4) * 2 * nblk, 256) + 256;
     PT_TRY(pt_dalloc(ctx, (void **)&tmp, o_s1 + pt_round_up(sizeof(double) * k, 256)));
     double4 *blk = (double4 *)tmp;
-    int32_t *d_idx = (int32_t *)(tmp + o_idx);
+    int32_t *d_idx = mv->d_seed_idx;
     double *d_s1 = (double *)(tmp + o_s1), *d_s2 = mv->d_seed_s2;
     const double *l64 = v->l64;
     int kk = k;
@@ -849,7 +851,10 @@ pt_status pt_greedy_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t *out_
     }
     PT_CK(cudaEventRecord(ctx->ev1, s));
     PT_TRY(io.finish());
-    if ((size_t)k > v->greedy_s2.size()) v->greedy_s2.assign(s2_trace, s2_trace + k);
+    if ((size_t)k > v->greedy_s2.size()) {
+        v->greedy_s2.assign(s2_trace, s2_trace + k);
+        v->greedy_idx.assign(out_idx, out_idx + k);
+    }
     if (!nc.empty()) {
         int64_t tot = 0;
         for (int t = 0; t < k; t++) tot += nc[t];

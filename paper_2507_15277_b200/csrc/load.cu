@@ -165,7 +165,12 @@ void pt_view_free(pt_ctx *ctx, pt_view &v)
         pt_dfree(ctx, v.hC);
         pt_dfree(ctx, v.hPair);
     }
-    pt_dfree(ctx, v.d_seed_s2);   // allocated per view object (owned or not)
+    // allocated per view object (owned or not)
+    pt_dfree(ctx, v.d_seed_s2);
+    pt_dfree(ctx, v.d_seed_idx);
+    pt_dfree(ctx, v.tcA);
+    pt_dfree(ctx, v.tcB);
+    pt_dfree(ctx, v.tcConst);
     v = pt_view();
 }
 

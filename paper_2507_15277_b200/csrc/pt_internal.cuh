@@ -84,7 +84,17 @@ struct pt_view {
     // (pt_greedy_seed_enqueue): the exhaustive search seeds its threshold from it
     // without a host round trip.  d_seed_k = steps it holds (0 = none).
     double *d_seed_s2 = nullptr;
+    int32_t *d_seed_idx = nullptr;   // the picks of that run (the swap search's start)
     int d_seed_k = 0;
+    mutable std::vector<int32_t> greedy_idx;   // picks of the host-traced greedy run
+    // threshold-count tier (exh_tc.cu), rebuilt per search (the thresholds follow tau):
+    //   tcA [tc_ncfg][tc_K] bytes, config-major: E4M3 1.0 where l[c][e] >= j u (k = j E_pad + e)
+    //   tcB the same bits in the B-stage layout of k_exh_tc ([K/64][tc_ncfg/8][512 B])
+    //   tcConst device constants (u, survivor threshold, slack, the scope max of l)
+    uint8_t *tcA = nullptr, *tcB = nullptr;
+    void *tcConst = nullptr;
+    int64_t tc_ncfg = 0;
+    int tc_K = 0;
 };
 
 struct pt_tasks;  // exhaustive work list (exhaustive.cu)
@@ -199,6 +209,27 @@ pt_status pt_exhaustive_view(pt_ctx *ctx, const pt_view *v, int32_t k, int32_t s
                              double *s_out, int *n_found);
 pt_status pt_score_view(pt_ctx *ctx, const pt_view *v, const int32_t *d_sets, int64_t n_sets,
                         int32_t k, double *d_s);
+// threshold-count tier of the exhaustive search (exh_tc.cu): enqueue the device swap
+// search for tau, the bit operands and k_exh_tc on ctx->stream (no host round trip).
+// PT_EINVAL = not eligible for this view / k (the caller takes the u8 tier); a tau that
+// turns out unusable on the device sets *cand_n = 2^63 (the refine then skips).
+struct pt_tc_args {
+    int k = 0;
+    const int4 *tasks = nullptr;   // this shard's task list [ta, tb) (rows 128, columns 256)
+    int ta = 0, tb = 0;
+    int *ctr = nullptr;
+    unsigned *U = nullptr;         // written: the refine's threshold (float bits)
+    unsigned long long *cand_n = nullptr, *cand_key = nullptr;
+    float *cand_s = nullptr;
+    unsigned cap = 0;
+    const int32_t *d_S0 = nullptr;     // greedy's k-set (device)
+    const double *d_seed_s2 = nullptr; // greedy's runner-up score at step k (device) or NULL
+    double *swap_rs = nullptr;         // [2 num_sms] scratch
+    long long *swap_rw = nullptr;      // [2 num_sms] scratch
+    double *tau_dev = nullptr;         // [1] scratch
+};
+pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, int *nt_out);
+#define PT_TC_COLS 256   // the tc tier's column-tile width (its task list)
 // sharded search (dist.cu): pack the local top-2 (device os[2], ot[2k]) into ctx->rec_out
 void pt_pack_record(pt_ctx *ctx, const double *d_os, const int32_t *d_ot, int k);
 // fleet objective (fleet.cu): rates of sets / greedy / exhaustive, env_mask may be NULL
@@ -271,4 +302,13 @@ __host__ __device__ static inline bool pt_key_less(double sa, const int32_t *a, 
 }
 
 #define PT_MAXK 8
+
+// exhaustive search (exhaustive.cu, exh_tc.cu): first column of a row tile whose first
+// row's largest member is j0: j0 + 1 rounded down to 8 configs (16-byte aligned rows);
+// the extra columns are <= every row's largest member and masked.  Used by the task
+// builder AND every tiled kernel so all cover exactly [tile_lo, tile_lo + W * n_ct) >=
+// [j0+1, C) for their column-tile width W.
+__host__ __device__ static inline int64_t tile_lo(int64_t j0) { return (j0 + 1) & ~(int64_t)7; }
+// survivor key = (row colex rank << KEY_BITS) | column
+#define KEY_BITS 21
 #define PT_SWAP_MAXK 32

@@ -57,7 +57,8 @@ class pt_stats(ct.Structure):
                 ("exh_slots", ct.c_int64), ("exh_env_pad", ct.c_int64),
                 ("exh_candidates", ct.c_int64), ("exh_passes", ct.c_int32),
                 ("exh_kernel", ct.c_int32), ("greedy_ms", ct.c_double),
-                ("greedy_candidates", ct.c_int64)]
+                ("greedy_candidates", ct.c_int64), ("exh_tc_nt", ct.c_int32), ("exh_tc_pad", ct.c_int32),
+                ("exh_tc_survivors", ct.c_int64)]
 
 
 class PTError(RuntimeError):

@@ -46,7 +46,10 @@ def test_all_tied_overflow_second_pass():
     st = pt.pt_get_stats(ctx)
     assert r["best"] == (0, 1, 2) and r["runner"] == (0, 1, 3)
     assert r["G"] == 1.0
-    assert st["exh_passes"] == 2 and st["exh_candidates"] == math.comb(300, 3)
+    # pass 1: the tc tier finds tau = 0 (every score is 0) and does not run; pass 2:
+    # the u8 tier overflows; pass 3: its rerun with room for every survivor
+    assert st["exh_tc_survivors"] == -1 and st["exh_kernel"] == 4
+    assert st["exh_passes"] == 3 and st["exh_candidates"] == math.comb(300, 3)
 
 
 def test_near_ties_duplicates():
@@ -81,7 +84,7 @@ def test_single_env_scope():
         check_exh(o, pt.pt_exhaustive_best(ctx, k, env_mask=mask), k, mask=mask)
 
 
-@pytest.mark.parametrize("tier", ["u8", "fp16"])
+@pytest.mark.parametrize("tier", ["tc", "u8", "fp16"])
 @pytest.mark.parametrize("C", [9, 61, 64, 65, 71, 72, 127, 130])
 @pytest.mark.parametrize("k", [2, 3, 4])
 def test_every_subset_is_evaluated(C, k, tier, monkeypatch):
@@ -96,7 +99,8 @@ def test_every_subset_is_evaluated(C, k, tier, monkeypatch):
     ctx = pt.pt_load_perf(T)
     r = pt.pt_exhaustive_best(ctx, k)
     st = pt.pt_get_stats(ctx)
-    assert st["exh_kernel"] == (4 if tier == "u8" else 0)
+    # tc: every score is 0, so tau = 0 gives no threshold step -> the u8 tier runs
+    assert st["exh_kernel"] == {"tc": 4, "u8": 4, "fp16": 0}[tier]
     assert r["best"] == tuple(range(k))
     assert st["exh_candidates"] == math.comb(C, k) == st["exh_sets"]
     tot = 0

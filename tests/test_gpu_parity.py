@@ -19,6 +19,9 @@ from paper_2507_15277_b200 import pt, synth
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
+# exh_kernel values a PT_EXH_TIER setting may report (the tc tier falls back to u8
+# when its threshold is unusable or its filter leaves more than 2^20 survivors)
+TIER_KERNELS = {"tc": (5, 4), "u8": (4,), "fp16": (0,)}
 
 RTOL = 1e-6
 GAP = 1e-9
@@ -92,10 +95,11 @@ def test_planted():
 
 
 # ------------------------------------------------------- medium (several tiles)
-@pytest.mark.parametrize("tier", ["u8", "fp16"])
+@pytest.mark.parametrize("tier", ["tc", "u8", "fp16"])
 @pytest.mark.parametrize("seed,C,ndev,nin", [(1, 300, 3, 16), (2, 257, 2, 19), (3, 129, 5, 7)])
 def test_medium_exhaustive(seed, C, ndev, nin, tier, monkeypatch):
-    """Both filter tiers of the tiled search (u8 default, fp16 by PT_EXH_TIER)."""
+    """Every filter tier of the tiled search (tc default, u8 / fp16 by PT_EXH_TIER; the
+    tc tier may fall back to u8 when its filter is too weak for the data)."""
     monkeypatch.setenv("PT_EXH_TIER", tier)
     T, dev = synth.small_matrix(seed, n_cfg=C, n_dev=ndev, n_inputs=nin)
     o = Oracle(T, dev)
@@ -103,7 +107,7 @@ def test_medium_exhaustive(seed, C, ndev, nin, tier, monkeypatch):
     for k in (2, 3):
         check_exh(o, pt.pt_exhaustive_best(ctx, k), k)
         st = pt.pt_get_stats(ctx)
-        assert st["exh_kernel"] == (4 if tier == "u8" else 0) and st["exh_sets"] == math.comb(C, k)
+        assert st["exh_kernel"] in TIER_KERNELS[tier] and st["exh_sets"] == math.comb(C, k)
     # sharded on one GPU (fake multi-GPU): merged shards == unsharded
     for k in (2, 3):
         want = o.exhaustive(k)
@@ -210,7 +214,7 @@ def test_paper_exhaustive_k2(paper1):
     check_exh(o, pt.pt_exhaustive_best(ctx, 2), 2)
 
 
-@pytest.mark.parametrize("tier", ["u8", "fp16"])
+@pytest.mark.parametrize("tier", ["tc", "u8", "fp16"])
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_paper_exhaustive_k3_golden(seed, tier, monkeypatch):
     """Full size: 930,485,175 triples vs the oracle's stored result
@@ -226,7 +230,7 @@ def test_paper_exhaustive_k3_golden(seed, tier, monkeypatch):
     check_exh(o, res, 3, want=want)
     assert res["runner"] == want[2]
     st = pt.pt_get_stats(ctx)
-    assert st["exh_sets"] == 930_485_175 and st["exh_kernel"] == (4 if tier == "u8" else 0)
+    assert st["exh_sets"] == 930_485_175 and st["exh_kernel"] == {"tc": 5, "u8": 4, "fp16": 0}[tier]
     # the oracle re-scores the GPU's pick one by one
     assert o.score(list(res["best"])) == pytest.approx(res["G"], rel=1e-12)
     # 8-way sharded on one device (the multi-GPU partition), merged

@@ -7,7 +7,7 @@
 // first column of a row tile whose first row's largest member is j0: j0 + 1 rounded
 // down to 8 configs (16-byte aligned tiles); the extra columns are <= every row's
 // largest member and masked.  The task builder AND the kernels use this one function.
-__host__ __device__ static inline int64_t tile_lo(int64_t j0) { return (j0 + 1) & ~(int64_t)7; }
+// (tile_lo: pt_internal.cuh)
 
 #define TC_R 128   // rows per task = threads per CTA = TMEM lanes
 #define TC_C 64    // columns per tile

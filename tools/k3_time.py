@@ -14,7 +14,19 @@ for rep in range(6):
 st = pt.pt_get_stats(ctx)
 print(os.environ.get("PT_LIB", "default"), os.environ.get("PT_EXH_TIER", "u8"), r["best"], r["runner"], r["G"],
       "k3 kernel ms", [round(x, 3) for x in ms[1:]], "median", round(float(np.median(ms[1:])), 3),
-      "kernel", st["exh_kernel"], "candidates", st["exh_candidates"], "passes", st["exh_passes"], flush=True)
+      "kernel", st["exh_kernel"], "candidates", st["exh_candidates"], "passes", st["exh_passes"],
+      "nt", st["exh_tc_nt"], "tc_survivors", st["exh_tc_survivors"], flush=True)
+# whole call (swap search + operands + kernel + refine), CUDA events around it
+s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+calls = []
+for rep in range(5):
+    torch.cuda.synchronize()
+    s_.record()
+    pt.pt_exhaustive_best(ctx, 3)
+    e_.record()
+    torch.cuda.synchronize()
+    calls.append(s_.elapsed_time(e_))
+print("k3 whole call ms", [round(x, 3) for x in calls], flush=True)
 for k in (2, 4):
     r = pt.pt_exhaustive_best(ctx, k)
     r = pt.pt_exhaustive_best(ctx, k)

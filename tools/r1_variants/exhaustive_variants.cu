@@ -88,7 +88,6 @@
 static_assert(XT_K % (4 * XT_NG) == 0, "a pipeline stage must hold whole fp16 chains");
 #define XT_EMAX 768 // widest scope the resident-A kernel takes (smem)
 #define XT_UMAX 1024 // column tiles per task (a whole row tile: A staged once)
-#define KEY_BITS 21
 
 // ---------------------------------------------------------------------------
 // work list
@@ -97,7 +96,7 @@ static_assert(XT_K % (4 * XT_NG) == 0, "a pipeline stage must hold whole fp16 ch
 // rounded down to 8 configs (16-byte aligned fp16 rows); the extra columns are
 // <= every row's largest member and masked.  Used by the task builder AND the
 // kernel so both cover exactly [tile_lo, tile_lo + 64 * n_ct) >= [j0+1, C).
-__host__ __device__ static inline int64_t tile_lo(int64_t j0) { return (j0 + 1) & ~(int64_t)7; }
+// (tile_lo and KEY_BITS: pt_internal.cuh)
 
 struct pt_tasks {
     int m = 0;
