@@ -110,6 +110,36 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar)
 {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar)) : "memory");
 }
+// cluster helpers (the multicast variant, CL > 1)
+__device__ __forceinline__ uint32_t cluster_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// one bulk copy global -> the same shared-memory offset of every CTA in cta_mask;
+// complete_tx on the mbarrier at the same offset in each of them
+__device__ __forceinline__ void bulk_g2s_mc(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint16_t mask)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(bar)), "h"(mask)
+        : "memory");
+}
+// arrive (once each) on the mbarrier at this offset in every CTA of cta_mask when the
+// previously issued MMAs complete
+__device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     su32(bar)),
+                 "h"(mask)
+                 : "memory");
+}
 __device__ __forceinline__ void tc_ld32(uint32_t a, uint32_t (&v)[32])
 {
     asm volatile(
@@ -332,8 +362,15 @@ struct TcParams {
     float *cand_s;
     unsigned long long *cand_n;
     unsigned cap;
+    unsigned long long *mbox;   // CL > 1: [clusters][4] task mailbox ((t + 1) << 32 | task), zeroed
 };
 
+// CL = CTAs per cluster sharing every B stage: the cluster's tasks are CL x 128 rows
+// (CTA rank r takes rows [128 r, 128 r + 128)) over the same column tiles; CTA 0 alone
+// streams B, multicast into every CTA's ring (L2 reads / CL), and every CTA's MMA
+// completion releases the stage in CTA 0 (multicast commit).  CTA 0 fetches the tasks
+// and posts them in a global mailbox.
+template <int CL>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -350,6 +387,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (!p.cst->ok) return;   // tau unusable (k_tc_const flagged the search as not run)
+    const uint32_t crank = CL > 1 ? cluster_rank() : 0;
     if (tid == 0) {
         for (int i = 0; i < 2; i++) {
             bar_init(&a_full[i], TC_R);
@@ -360,7 +398,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
         }
         for (int s = 0; s < S; s++) {
             bar_init(&b_full[s], 1);
-            bar_init(&b_empty[s], 1);
+            bar_init(&b_empty[s], crank == 0 ? CL : 1);   // CTA 0's: every CTA's MMA
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -370,6 +408,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     }
     tc_fence_before();
     __syncthreads();
+    if (CL > 1) cluster_sync_all();   // every CTA's barriers exist before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_s;
     const int m = p.m;
@@ -427,7 +466,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
         for (int t = 0;; t++) {
             const int slot = t & 1;
             bar_wait(&a_empty[slot], ((t >> 1) & 1) ^ 1);
-            if (bt == 0) bcast[slot] = atomicAdd(p.task_ctr, 1);
+            if (bt == 0) {
+                if (CL == 1) {
+                    bcast[slot] = atomicAdd(p.task_ctr, 1);
+                } else {
+                    // the cluster's CTAs are at most 2 tasks apart (B stages are shared),
+                    // so a 4-entry mailbox tagged with t + 1 cannot be overwritten early
+                    unsigned long long *box = p.mbox + (size_t)(blockIdx.x / CL) * 4 + (t & 3);
+                    if (crank == 0) {
+                        const unsigned long long v = ((unsigned long long)(t + 1) << 32) |
+                                                     (unsigned)atomicAdd(p.task_ctr, 1);
+                        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(box), "l"(v) : "memory");
+                        bcast[slot] = (int)(unsigned)v;
+                    } else {
+                        unsigned long long v = 0;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(box) : "memory");
+                        } while ((v >> 32) != (unsigned long long)(t + 1));
+                        bcast[slot] = (int)(unsigned)v;
+                    }
+                }
+            }
             named_sync(1, 128);
             const int ti = bcast[slot];
             if (ti >= p.task_hi) {
@@ -439,11 +498,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                 break;
             }
             const int4 tk = p.tasks[ti];
-            const int64_t R0 = (int64_t)tk.x * TC_R;
+            const int64_t G0 = (int64_t)tk.x * (TC_R * CL);      // the cluster's first row
+            const int64_t R0 = G0 + (int64_t)crank * TC_R;        // this CTA's
             if (bt == 0) {
                 int32_t mem0[PT_MAXK];
-                pt_unrank_colex(R0, m, p.C, mem0);
-                tinfo[slot] = make_int4(tk.x, tk.y, tk.z, (int)tile_lo(mem0[m - 1]));
+                pt_unrank_colex(G0, m, p.C, mem0);
+                tinfo[slot] = make_int4((int)(R0 / TC_R), tk.y, tk.z, (int)tile_lo(mem0[m - 1]));
                 bar_arrive(&t_full[slot]);
             }
             const int64_t R = R0 + bt;
@@ -489,8 +549,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                         const int st = (int)(sc % (uint32_t)S);
                         bar_wait(&b_empty[st], ((sc / (uint32_t)S) & 1) ^ 1);
                         bar_expect_tx(&b_full[st], TC_N * TC_KC);
-                        bulk_g2s(Bbuf + (size_t)st * TC_N * TC_KC, p.B + ((int64_t)kc * p.n_grp + grp0) * (8 * TC_KC),
-                                 TC_N * TC_KC, &b_full[st]);
+                        if (CL == 1) {
+                            bulk_g2s(Bbuf + (size_t)st * TC_N * TC_KC,
+                                     p.B + ((int64_t)kc * p.n_grp + grp0) * (8 * TC_KC), TC_N * TC_KC, &b_full[st]);
+                        } else if (crank == 0) {
+                            bulk_g2s_mc(Bbuf + (size_t)st * TC_N * TC_KC,
+                                        p.B + ((int64_t)kc * p.n_grp + grp0) * (8 * TC_KC), TC_N * TC_KC, &b_full[st],
+                                        (uint16_t)((1u << CL) - 1));
+                        }
                     }
                 }
             }
@@ -524,7 +590,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                             tc_mma(d, sdesc(abase + (kk / 16) * (TC_R * 16), TC_R * 16, 128),
                                    sdesc(bbase + i * 256, 128, 8 * TC_KC), (kc | i) ? 1u : 0u);
                         }
-                        tc_commit(&b_empty[st]);
+                        if (CL == 1 || crank == 0) tc_commit(&b_empty[st]);
+                        else tc_commit_mc(&b_empty[st], (uint16_t)(1u | (1u << crank)));   // CTA 0's and own
                     }
                     tc_commit(&acc_full[buf]);
                 }
@@ -535,6 +602,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     }
     tc_fence_before();
     __syncthreads();
+    if (CL > 1) cluster_sync_all();   // no CTA leaves while a peer may still signal it
     tc_fence_after();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
@@ -553,6 +621,7 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     cudaStream_t s = ctx->stream;
     const int m = a.k - 1;
     if (m < 1 || m > 3 || v->C >= (1 << KEY_BITS) || v->E_pad % TC_KC != 0) return PT_EINVAL;
+    if (a.cl != 1 && a.cl != 2 && a.cl != 4) return PT_EINVAL;
     // nt thresholds (PT_TC_NT, default 2), as many as fit TC_KMAX
     // (read per call: the tests vary them in one process)
     const int nt_env = getenv("PT_TC_NT") ? atoi(getenv("PT_TC_NT")) : 2;
@@ -589,7 +658,9 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
         auto it = occ_cache.find(key);
         if (it == occ_cache.end()) {
             PT_TRY(pt_smem_optin(ctx, (const void *)k_swap_tau));
-            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc));
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc<1>));
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc<2>));
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc<4>));
             PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_swap_tau, 256, sw_smem));
             occ_cache[key] = occ;
         } else {
@@ -638,12 +709,68 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     p.cand_s = a.cand_s;
     p.cand_n = a.cand_n;
     p.cap = a.cap;
-    const int grid = std::min(ctx->num_sms, a.tb - a.ta);
+    p.mbox = a.mbox;
+    const int CL = a.cl;
+    const void *kfn = CL == 4 ? (const void *)k_exh_tc<4> : CL == 2 ? (const void *)k_exh_tc<2> : (const void *)k_exh_tc<1>;
+    const size_t smem = tc_smem(K, S);
+    int grid = std::min(ctx->num_sms, (a.tb - a.ta) * CL);
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute attr[1];
+    lc.blockDim = dim3(TC_THREADS);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    if (CL > 1) {
+        static std::mutex cmu;
+        static std::map<std::tuple<int, int, size_t>, int> clusters;   // (device, CL, smem) -> co-resident clusters
+        int ncl = 0;
+        {
+            std::lock_guard<std::mutex> g(cmu);
+            auto key = std::make_tuple(ctx->dev, CL, smem);
+            auto it = clusters.find(key);
+            if (it == clusters.end()) {
+                PT_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+                cudaLaunchConfig_t q = lc;
+                q.gridDim = dim3(CL * ctx->num_sms);
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = CL;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                q.attrs = attr;
+                q.numAttrs = 1;
+                PT_CK(cudaOccupancyMaxActiveClusters(&ncl, kfn, &q));
+                clusters[key] = ncl;
+            } else {
+                ncl = it->second;
+            }
+        }
+        if (ncl < 1) return PT_EINVAL;
+        grid = std::min(ncl * CL, grid / CL * CL);
+        if (grid < CL) grid = CL;
+        PT_CK(cudaMemsetAsync(a.mbox, 0, sizeof(unsigned long long) * 4 * (grid / CL), s));
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+    }
+    lc.gridDim = dim3(grid);
     PT_CK(cudaEventRecord(ctx->ev0, s));
-    k_exh_tc<<<grid, TC_THREADS, tc_smem(K, S), s>>>(p);
+    if (CL == 4) PT_CK(cudaLaunchKernelEx(&lc, k_exh_tc<4>, p));
+    else if (CL == 2) PT_CK(cudaLaunchKernelEx(&lc, k_exh_tc<2>, p));
+    else PT_CK(cudaLaunchKernelEx(&lc, k_exh_tc<1>, p));
     PT_CK(cudaEventRecord(ctx->ev1, s));
     ctx->stats.launches++;
     PT_CK(cudaGetLastError());
     if (nt_out) *nt_out = nt;
     return PT_OK;
+}
+
+// CTAs per cluster sharing the B stream (PT_TC_CL = 1, 2 or 4; default 2 for k >= 3,
+// 1 for the small k = 2 search).  The caller builds its task list with 128 x CL rows.
+int pt_tc_cluster(int k)
+{
+    const char *e = getenv("PT_TC_CL");
+    int cl = e ? atoi(e) : (k >= 3 ? 2 : 1);
+    return (cl == 1 || cl == 2 || cl == 4) ? cl : 1;
 }

@@ -1468,9 +1468,11 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const int4 *tc_list = nullptr;
     int tc_ta = 0, tc_tb = 0;
     int64_t tc_sets = 0, tc_slots = 0;
+    int tc_cl = 1;
     if (tc) {
         pt_tasks *TT = nullptr;
-        PT_TRY(build_tasks(ctx, v, m, XT_R, PT_TC_COLS, &TT));
+        tc_cl = pt_tc_cluster(k);
+        PT_TRY(build_tasks(ctx, v, m, XT_R * tc_cl, PT_TC_COLS, &TT));
         tc_list = TT->d;
         tc_tb = (int)TT->h.size();
         tc_sets = TT->set_pre.back();
@@ -1514,6 +1516,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     }
 
     unsigned cap = 1u << 20;
+    if (tc && getenv("PT_TC_CAP")) cap = (unsigned)std::max(1, atoi(getenv("PT_TC_CAP")));   // (tests: overflow paths)
     unsigned long long n_cand = 0;
     float tau_pass = tau_seed;
     int tier_pass0 = -1;   // first pass of the filter tier whose answer is returned (its time is exh_main_ms)
@@ -1526,7 +1529,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
                      o_os = take(sizeof(double) * 2), o_ot = take(sizeof(int32_t) * 2 * k),
                      o_blk = take(sizeof(Rec2) * (size_t)ctx->num_sms * 2), o_done = take(sizeof(unsigned)),
                      o_S0 = take(sizeof(int32_t) * k), o_sd = take(sizeof(double)), o_tau = take(sizeof(double)),
-                     o_rs = take(sizeof(double) * 2 * ctx->num_sms), o_rw = take(sizeof(long long) * 2 * ctx->num_sms);
+                     o_rs = take(sizeof(double) * 2 * ctx->num_sms), o_rw = take(sizeof(long long) * 2 * ctx->num_sms),
+                     o_mbox = take(sizeof(unsigned long long) * 4 * ctx->num_sms);
         void *scr = nullptr;
         PT_TRY(pt_scratch(ctx, off, &scr));
         char *b = (char *)scr;
@@ -1580,6 +1584,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
             a.swap_rs = (double *)(b + o_rs);
             a.swap_rw = (long long *)(b + o_rw);
             a.tau_dev = (double *)(b + o_tau);
+            a.cl = tc_cl;
+            a.mbox = (unsigned long long *)(b + o_mbox);
             mark("pre-launch");
             int nt = 0;
             const pt_status st = pt_exh_tc_enqueue(ctx, v, a, &nt);
@@ -1685,8 +1691,20 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         memcpy(&Uf, &hU, sizeof Uf);
         if (tc_launched) {
             ctx->stats.exh_tc_survivors = (n_cand >> 63) ? -1 : (int64_t)n_cand;
+            if (!(n_cand >> 63) && n_cand > cap && shard_count > 1) {
+                // sharded: every rank must scan the SAME task list (the tiers' lists
+                // partition the subset space differently), and an overflow is a
+                // per-shard event -- so a sharded tc search reruns itself with room
+                // for every survivor instead of falling back
+                if (n_cand > (1ull << 28))
+                    return pt_fail(PT_ECAP, "%llu tc-tier survivors in this shard: above the 2^28 buffer limit",
+                                   n_cand);
+                cap = (unsigned)n_cand;
+                continue;
+            }
             if ((n_cand >> 63) || n_cand > cap) {
-                // tau unusable or too weak a filter: the u8 tier, seeded as before
+                // tau unusable (identical on every rank) or too weak a filter: the u8
+                // tier, seeded as before
                 tc = false;
                 tau_pass = tau_seed;
                 cap = 1u << 20;

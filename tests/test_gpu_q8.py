@@ -24,13 +24,19 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
+@pytest.fixture(autouse=True)
+def _u8_tier(monkeypatch):
+    """These tests are about the u8 tier: select it (the default is the tc tier)."""
+    monkeypatch.setenv("PT_EXH_TIER", "u8")
+
+
 def both_tiers(ctx, k, monkeypatch, **kw):
     out = {}
     for tier in ("u8", "fp16"):
         monkeypatch.setenv("PT_EXH_TIER", tier)
         r = pt.pt_exhaustive_best(ctx, k, **kw)
         out[tier] = (r, pt.pt_get_stats(ctx))
-    monkeypatch.delenv("PT_EXH_TIER")
+    monkeypatch.setenv("PT_EXH_TIER", "u8")
     return out
 
 

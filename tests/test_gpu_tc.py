@@ -149,3 +149,51 @@ def test_tc_sharded_partition():
                   [(r["s"][1], r["runner"]) for r in recs if r["runner"] is not None])
     assert cand[0][1] == full["best"] and cand[0][0] == full["s"][0]
     assert cand[1][1] == full["runner"] and cand[1][0] == full["s"][1]
+
+
+def test_tc_overflow_paths(monkeypatch):
+    """A tiny survivor buffer (PT_TC_CAP=16): unsharded, the search falls back to the
+    u8 tier; sharded, every shard must stay on the tc task list (the tiers partition
+    the subset space differently), so it reruns with room for every survivor -- and
+    the merged shards still equal the unsharded answer."""
+    T, dev = synth.small_matrix(40, n_cfg=500, n_dev=5, n_inputs=20)
+    o = Oracle(T, dev)
+    ctx = pt.pt_load_perf(T, dev)
+    want = pt.pt_exhaustive_best(ctx, 3)
+    assert pt.pt_get_stats(ctx)["exh_kernel"] == 5
+    check_exh(o, want, 3)
+    monkeypatch.setenv("PT_TC_CAP", "16")
+    r = pt.pt_exhaustive_best(ctx, 3)
+    st = pt.pt_get_stats(ctx)
+    assert st["exh_kernel"] == 4 and st["exh_tc_survivors"] > 16
+    assert r["best"] == want["best"] and r["s"] == want["s"]
+    recs, sets = [], 0
+    for s in range(3):
+        rr = pt.pt_exhaustive_best(ctx, 3, shard_rank=s, shard_count=3)
+        st = pt.pt_get_stats(ctx)
+        assert st["exh_kernel"] == 5
+        sets += st["exh_sets"]
+        recs.append(rr)
+    assert sets == math.comb(500, 3)
+    cand = sorted([(x["s"][0], x["best"]) for x in recs if x["best"] is not None] +
+                  [(x["s"][1], x["runner"]) for x in recs if x["runner"] is not None])
+    assert cand[0] == (want["s"][0], want["best"]) and cand[1] == (want["s"][1], want["runner"])
+
+
+@pytest.mark.parametrize("cl", ["1", "2", "4"])
+def test_tc_cluster_sizes(cl, monkeypatch):
+    """CTAs per cluster sharing the multicast B stream (PT_TC_CL): same answer and
+    the same survivor count for 1, 2 and 4, at the paper shape (k=3) and on a small
+    ragged matrix (k=2, 3, 4; the last cluster task has rows past the end)."""
+    monkeypatch.setenv("PT_TC_CL", cl)
+    T, dev = synth.small_matrix(41, n_cfg=333, n_dev=3, n_inputs=17)
+    o = Oracle(T, dev)
+    ctx = pt.pt_load_perf(T, dev)
+    for k in (2, 3, 4):
+        check_exh(o, pt.pt_exhaustive_best(ctx, k), k)
+    T, dev = synth.paper_matrix(1)
+    ctx = pt.pt_load_perf(T, dev)
+    r = pt.pt_exhaustive_best(ctx, 3)
+    st = pt.pt_get_stats(ctx)
+    assert st["exh_kernel"] == 5 and r["best"] == (295, 469, 825) and r["runner"] == (295, 455, 825)
+    assert st["exh_sets"] == math.comb(1775, 3)
