@@ -52,8 +52,8 @@ namespace cgt = cooperative_groups;
 #define TC_R 128        // rows per task (TMEM lanes)
 #define TC_N 256        // columns per accumulator tile
 #define TC_KC 64        // K bytes per B stage
-#define TC_KMAX 640     // widest K (nt E_pad) with two A buffers in shared memory
-#define TC_THREADS 320
+#define TC_KMAX 1024    // widest K (nt E_pad): the A buffer (128 K bytes) + a ring of >= 4 B stages
+#define TC_THREADS 576
 
 namespace {
 
@@ -97,48 +97,17 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
     return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
-// instruction descriptor, kind::f8f6f4: D f32 (bits 4-5 = 1), A = B = E4M3 (0), both
-// K-major, N >> 3 at bit 17, M >> 4 at bit 24
-constexpr uint32_t kTcIdesc = (1u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_R >> 4) << 24);
-__device__ __forceinline__ void tc_mma(uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc)
+// instruction descriptor (built per tile), kind::f8f6f4: D f32 (bits 4-5 = 1), A = B =
+// E4M3 (0), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+__device__ __forceinline__ void tc_mma(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc)
 {
     asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p; }" ::"r"(d),
-                 "l"(ad), "l"(bd), "r"(kTcIdesc), "r"(acc)
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
                  : "memory");
 }
 __device__ __forceinline__ void tc_commit(uint64_t *bar)
 {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar)) : "memory");
-}
-// cluster helpers (the multicast variant, CL > 1)
-__device__ __forceinline__ uint32_t cluster_rank()
-{
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all()
-{
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// one bulk copy global -> the same shared-memory offset of every CTA in cta_mask;
-// complete_tx on the mbarrier at the same offset in each of them
-__device__ __forceinline__ void bulk_g2s_mc(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint16_t mask)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
-            su32(dst)),
-        "l"(src), "r"(bytes), "r"(su32(bar)), "h"(mask)
-        : "memory");
-}
-// arrive (once each) on the mbarrier at this offset in every CTA of cta_mask when the
-// previously issued MMAs complete
-__device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask)
-{
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                     su32(bar)),
-                 "h"(mask)
-                 : "memory");
 }
 __device__ __forceinline__ void tc_ld32(uint32_t a, uint32_t (&v)[32])
 {
@@ -331,23 +300,43 @@ __global__ void k_tc_const(const double *__restrict__ tau_dev, int64_t E, int64_
     if (!ok) *cand_n = 1ull << 63;   // "not run": the refine skips, the host falls back
 }
 
-// the bit operands: tcA[c][k] and tcB in the B-stage layout; k = j E_pad + e,
-// bit = [l[c][e] >= (j+1) u] for real configs and environments (0 elsewhere)
+// the bit operands, k = j E_pad + e, bit = [l[c][e] >= (j+1) u] for real configs and
+// environments (0 elsewhere): tcA[c][k/32] packed bits (the builders AND and expand them),
+// tcB bytes (E4M3 1.0 = 0x38) in the B-stage layout.  Thread = (config, 32-bit word).
 __global__ void __launch_bounds__(256) k_tc_build(const double *__restrict__ l64, int64_t C, int64_t E, int64_t E_pad,
                                                  int K, int64_t n_cfg, const TcConst *__restrict__ cst,
-                                                 uint8_t *__restrict__ A, uint8_t *__restrict__ B)
+                                                 uint32_t *__restrict__ A, uint8_t *__restrict__ B)
 {
+    const int W = K / 32;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_cfg * K) return;
-    const int64_t c = i / K;
-    const int k = (int)(i - c * K);
-    const int j = k / (int)E_pad, e = k - j * (int)E_pad;
-    uint8_t bit = 0;
-    if (cst->ok && c < C && e < E && l64[c * E_pad + e] >= (double)(j + 1) * cst->u) bit = 0x38;   // E4M3 1.0
-    A[i] = bit;
+    if (i >= n_cfg * W) return;
+    const int64_t c = i / W;
+    const int w = (int)(i - c * W);
     const int64_t n_grp = n_cfg / 8;
-    const int kc = k / TC_KC, kk = k % TC_KC;
-    B[((int64_t)kc * n_grp + c / 8) * (8 * TC_KC) + (kk / 16) * 128 + (c % 8) * 16 + kk % 16] = bit;
+    const bool ok = cst->ok && c < C;
+    const double u = cst->u;
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; b++) {
+        const int k = 32 * w + b;
+        const int j = k / (int)E_pad, e = k - j * (int)E_pad;
+        const bool on = ok && e < E && l64[c * E_pad + e] >= (double)(j + 1) * u;
+        bits |= (uint32_t)on << b;
+        const int kc = k / TC_KC, kk = k % TC_KC;
+        B[((int64_t)kc * n_grp + c / 8) * (8 * TC_KC) + (kk / 16) * 128 + (c % 8) * 16 + kk % 16] = on ? 0x38 : 0;
+    }
+    A[i] = bits;
+}
+
+// 8 packed bits -> 8 bytes of E4M3 (1.0 = 0x38 where the bit is set): per nibble, the
+// multiply by 0x00204081 places bit j at bit 8j with no overlapping partial products
+__device__ __forceinline__ uint32_t expand4(uint32_t nib)
+{
+    return ((nib * 0x00204081u) & 0x01010101u) * 0x38u;
+}
+__device__ __forceinline__ uint4 expand16(uint32_t bits16)
+{
+    return make_uint4(expand4(bits16 & 15u), expand4((bits16 >> 4) & 15u), expand4((bits16 >> 8) & 15u),
+                      expand4((bits16 >> 12) & 15u));
 }
 
 struct TcParams {
@@ -356,49 +345,60 @@ struct TcParams {
     const int4 *tasks;
     int task_hi;
     int *task_ctr;
-    const uint8_t *A, *B;
+    const uint32_t *A;   // packed bits [n_cfg][K/32]
+    const uint8_t *B;
     const TcConst *cst;
     unsigned long long *cand_key;
     float *cand_s;
     unsigned long long *cand_n;
     unsigned cap;
-    unsigned long long *mbox;   // CL > 1: [clusters][4] task mailbox ((t + 1) << 32 | task), zeroed
+    int dbg;   // development knob PT_TC_DBG (bit 0: the epilogue skips its TMEM reads, bit 1: no MMAs)
 };
 
-// CL = CTAs per cluster sharing every B stage: the cluster's tasks are CL x 128 rows
-// (CTA rank r takes rows [128 r, 128 r + 128)) over the same column tiles; CTA 0 alone
-// streams B, multicast into every CTA's ring (L2 reads / CL), and every CTA's MMA
-// completion releases the stage in CTA 0 (multicast commit).  CTA 0 fetches the tasks
-// and posts them in a global mailbox.
-template <int CL>
+// warp roles (TC_THREADS = 18 warps)
+#define TC_EPI_WARPS 8      // 0-7: epilogue (lane quarter w & 3, column half w >> 2)
+#define TC_BLD_WARPS 8      // 8-15: A builders (2 threads per row)
+#define TC_PROD_WARP 16
+#define TC_MMA_WARP 17
+
+// One CTA per SM (persistent, dynamic task queue).  A task = 128 rows x its column
+// tiles; the A operand is ONE buffer cut into K-chunks of 64 bytes (8 KB each): chunk kc
+// of task t+1 is built as soon as the last tile of task t has consumed chunk kc, so the
+// next task's A streams in behind the current task's last tile and the rest of shared
+// memory goes to a deep B ring (9 stages at K = 640) -- the ring depth is what hides the
+// latency of the bulk copies (a 4-stage ring with two whole A buffers kept the tensor
+// pipe ~30 % busy).  The last tile of a task is trimmed to N = round_up(columns, 16).
 __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    const int K = p.K, S = p.S;
-    uint8_t *Abuf = smem;                                     // [2][128 K]
-    uint8_t *Bbuf = smem + 2 * TC_R * K;                      // [S][256 x 64]
-    int *last = reinterpret_cast<int *>(Bbuf + S * TC_N * TC_KC);   // [2][128]
+    const int K = p.K, S = p.S, nkc = K / TC_KC;
+    uint8_t *Abuf = smem;                                           // [nkc][8 KB]
+    uint8_t *Bbuf = smem + (size_t)TC_R * K;                        // [S][256 x 64]
+    int *last = reinterpret_cast<int *>(Bbuf + (size_t)S * TC_N * TC_KC);   // [2][128]
     int4 *tinfo = reinterpret_cast<int4 *>(last + 2 * TC_R);        // [2] (row tile, u0, u1, lo)
     uint64_t *bars = reinterpret_cast<uint64_t *>(tinfo + 2);
-    uint64_t *a_full = bars, *a_empty = bars + 2, *t_full = bars + 4, *acc_full = bars + 6, *acc_empty = bars + 8;
-    uint64_t *b_full = bars + 10, *b_empty = bars + 10 + S;
-    uint32_t *tmem_s = reinterpret_cast<uint32_t *>(bars + 10 + 2 * S);
-    int *bcast = reinterpret_cast<int *>(tmem_s + 1);          // [2]
+    uint64_t *t_full = bars, *t_empty = bars + 2, *acc_full = bars + 4, *acc_empty = bars + 6;
+    uint64_t *a_full = bars + 8, *a_empty = a_full + nkc;
+    uint64_t *b_full = a_empty + nkc, *b_empty = b_full + S;
+    uint32_t *tmem_s = reinterpret_cast<uint32_t *>(b_empty + S);
+    int *bcast = reinterpret_cast<int *>(tmem_s + 1);               // [2]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (!p.cst->ok) return;   // tau unusable (k_tc_const flagged the search as not run)
-    const uint32_t crank = CL > 1 ? cluster_rank() : 0;
     if (tid == 0) {
         for (int i = 0; i < 2; i++) {
-            bar_init(&a_full[i], TC_R);
-            bar_init(&a_empty[i], 1 + 4);
-            bar_init(&t_full[i], 1);
+            bar_init(&t_full[i], TC_BLD_WARPS * 32);
+            bar_init(&t_empty[i], 1 + 1 + TC_EPI_WARPS);   // producer, MMA, epilogue warps
             bar_init(&acc_full[i], 1);
-            bar_init(&acc_empty[i], 4);
+            bar_init(&acc_empty[i], TC_EPI_WARPS);
         }
-        for (int s = 0; s < S; s++) {
-            bar_init(&b_full[s], 1);
-            bar_init(&b_empty[s], crank == 0 ? CL : 1);   // CTA 0's: every CTA's MMA
+        for (int c = 0; c < nkc; c++) {
+            bar_init(&a_full[c], TC_BLD_WARPS * 32);
+            bar_init(&a_empty[c], 1);
+        }
+        for (int q = 0; q < S; q++) {
+            bar_init(&b_full[q], 1);
+            bar_init(&b_empty[q], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -408,40 +408,55 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     }
     tc_fence_before();
     __syncthreads();
-    if (CL > 1) cluster_sync_all();   // every CTA's barriers exist before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_s;
     const int m = p.m;
 
-    if (warp < 4) {
+    if (warp < TC_EPI_WARPS) {
         // ---------------- epilogue ----------------
-        const int r = 32 * warp + lane;
+        const int quarter = warp & 3, half = warp >> 2;
+        const int r = 32 * quarter + lane;
         const float pthr = p.cst->pthr, u_dn = p.cst->u_dn, slk = p.cst->slack;
-        const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * quarter) << 16);
         uint32_t tcnt = 0;
         for (int t = 0;; t++) {
             const int slot = t & 1;
-            bar_wait(&a_full[slot], (t >> 1) & 1);
+            bar_wait(&t_full[slot], (t >> 1) & 1);
             const int4 ti = tinfo[slot];
             const int lastr = last[slot * TC_R + r];
             __syncwarp();
-            if (lane == 0) bar_arrive(&a_empty[slot]);
+            if (lane == 0) bar_arrive(&t_empty[slot]);
             if (ti.x < 0) break;
             const int64_t R = (int64_t)ti.x * TC_R + r;
             for (int u = ti.y; u < ti.z; u++, tcnt++) {
                 const int buf = tcnt & 1;
+                const int64_t col0 = (int64_t)ti.w + (int64_t)u * TC_N;
+                const int ncols = (int)min((int64_t)TC_N, p.C - col0);
                 bar_wait(&acc_full[buf], (tcnt >> 1) & 1);
                 tc_fence_after();
-                const int64_t col0 = (int64_t)ti.w + (int64_t)u * TC_N;
 #pragma unroll 1
-                for (int q = 0; q < TC_N / 32; q++) {
+                for (int q = half * 4; q < half * 4 + 4 && q * 32 < ncols && !(p.dbg & 1); q++) {
                     uint32_t v[32];
                     tc_ld32(lane_base + buf * TC_N + q * 32, v);
-                    float mn = __uint_as_float(v[0]);
+                    const int64_t cb = col0 + q * 32;
+                    float w[16];
+                    if (cb > lastr && cb + 31 < p.C) {   // every column valid: a 32-wide min tree
 #pragma unroll
-                    for (int j = 1; j < 32; j++) mn = fminf(mn, __uint_as_float(v[j]));
+                        for (int j = 0; j < 16; j++) w[j] = fminf(__uint_as_float(v[j]), __uint_as_float(v[j + 16]));
+                    } else {                             // row start / matrix end: mask first
+#pragma unroll
+                        for (int j = 0; j < 16; j++) {
+                            const float a = (cb + j > lastr && cb + j < p.C) ? __uint_as_float(v[j]) : INFINITY;
+                            const float b = (cb + j + 16 > lastr && cb + j + 16 < p.C) ? __uint_as_float(v[j + 16]) : INFINITY;
+                            w[j] = fminf(a, b);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; j++) w[j] = fminf(w[j], w[j + 8]);
+#pragma unroll
+                    for (int j = 0; j < 4; j++) w[j] = fminf(w[j], w[j + 4]);
+                    const float mn = fminf(fminf(w[0], w[2]), fminf(w[1], w[3]));
                     if (mn <= pthr) {   // rare: the window, then validity
-                        const int64_t cb = col0 + q * 32;
                         for (int j = 0; j < 32; j++) {
                             const float P = __uint_as_float(v[j]);
                             const int64_t l = cb + j;
@@ -460,102 +475,88 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                 if (lane == 0) bar_arrive(&acc_empty[buf]);
             }
         }
-    } else if (warp < 8) {
-        // ---------------- A builders ----------------
-        const int bt = tid - 128;
+    } else if (warp < TC_EPI_WARPS + TC_BLD_WARPS) {
+        // ---------------- A builders: thread = (row, half of each chunk) ----------------
+        const int bt = tid - TC_EPI_WARPS * 32;          // 0..255
+        const int row = bt & (TC_R - 1), part = bt >> 7;  // part: 16-byte pieces 2 part, 2 part + 1
         for (int t = 0;; t++) {
             const int slot = t & 1;
-            bar_wait(&a_empty[slot], ((t >> 1) & 1) ^ 1);
-            if (bt == 0) {
-                if (CL == 1) {
-                    bcast[slot] = atomicAdd(p.task_ctr, 1);
-                } else {
-                    // the cluster's CTAs are at most 2 tasks apart (B stages are shared),
-                    // so a 4-entry mailbox tagged with t + 1 cannot be overwritten early
-                    unsigned long long *box = p.mbox + (size_t)(blockIdx.x / CL) * 4 + (t & 3);
-                    if (crank == 0) {
-                        const unsigned long long v = ((unsigned long long)(t + 1) << 32) |
-                                                     (unsigned)atomicAdd(p.task_ctr, 1);
-                        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(box), "l"(v) : "memory");
-                        bcast[slot] = (int)(unsigned)v;
-                    } else {
-                        unsigned long long v = 0;
-                        do {
-                            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(box) : "memory");
-                        } while ((v >> 32) != (unsigned long long)(t + 1));
-                        bcast[slot] = (int)(unsigned)v;
-                    }
-                }
-            }
-            named_sync(1, 128);
+            bar_wait(&t_empty[slot], ((t >> 1) & 1) ^ 1);
+            if (bt == 0) bcast[slot] = atomicAdd(p.task_ctr, 1);
+            named_sync(1, TC_BLD_WARPS * 32);
             const int ti = bcast[slot];
             if (ti >= p.task_hi) {
-                if (bt == 0) {
-                    tinfo[slot] = make_int4(-1, 0, 0, 0);
-                    bar_arrive(&t_full[slot]);
-                }
-                bar_arrive(&a_full[slot]);
+                if (bt == 0) tinfo[slot] = make_int4(-1, 0, 0, 0);
+                bar_arrive(&t_full[slot]);
                 break;
             }
             const int4 tk = p.tasks[ti];
-            const int64_t G0 = (int64_t)tk.x * (TC_R * CL);      // the cluster's first row
-            const int64_t R0 = G0 + (int64_t)crank * TC_R;        // this CTA's
+            const int64_t R0 = (int64_t)tk.x * TC_R;
             if (bt == 0) {
                 int32_t mem0[PT_MAXK];
-                pt_unrank_colex(G0, m, p.C, mem0);
-                tinfo[slot] = make_int4((int)(R0 / TC_R), tk.y, tk.z, (int)tile_lo(mem0[m - 1]));
-                bar_arrive(&t_full[slot]);
+                pt_unrank_colex(R0, m, p.C, mem0);
+                tinfo[slot] = make_int4(tk.x, tk.y, tk.z, (int)tile_lo(mem0[m - 1]));
             }
-            const int64_t R = R0 + bt;
+            const int64_t R = R0 + row;
             const bool valid = R < p.n_rows;
             int32_t mem[PT_MAXK];
             if (valid) pt_unrank_colex(R, m, p.C, mem);
             else for (int u = 0; u < m; u++) mem[u] = 0;
-            last[slot * TC_R + bt] = valid ? mem[m - 1] : 0x7fffffff;
-            uint8_t *As = Abuf + (size_t)slot * TC_R * K + (bt >> 3) * 128 + (bt & 7) * 16;
-            const uint4 *src0 = reinterpret_cast<const uint4 *>(p.A + (int64_t)mem[0] * K);
-            const uint4 *src1 = reinterpret_cast<const uint4 *>(p.A + (int64_t)mem[m > 1 ? 1 : 0] * K);
-            const uint4 *src2 = reinterpret_cast<const uint4 *>(p.A + (int64_t)mem[m > 2 ? 2 : 0] * K);
-#pragma unroll 4
-            for (int kq = 0; kq < K / 16; kq++) {
-                uint4 v = src0[kq];
-                if (m > 1) {
-                    const uint4 w = src1[kq];
-                    v.x &= w.x; v.y &= w.y; v.z &= w.z; v.w &= w.w;
+            if (part == 0) last[slot * TC_R + row] = valid ? mem[m - 1] : 0x7fffffff;
+            bar_arrive(&t_full[slot]);
+            // this thread's 32-element halves of every chunk: words 2 c + part of the
+            // members' packed rows, ANDed (= the bits of the row's minimum), then expanded
+            const int W = K / 32;
+            const uint32_t *r0 = p.A + (int64_t)mem[0] * W + part;
+            const uint32_t *r1 = p.A + (int64_t)mem[m > 1 ? 1 : 0] * W + part;
+            const uint32_t *r2 = p.A + (int64_t)mem[m > 2 ? 2 : 0] * W + part;
+            uint32_t wv[TC_KMAX / TC_KC];
+#pragma unroll
+            for (int c = 0; c < TC_KMAX / TC_KC; c++) {
+                if (c < nkc) {
+                    uint32_t x = __ldg(r0 + 2 * c);
+                    if (m > 1) x &= __ldg(r1 + 2 * c);
+                    if (m > 2) x &= __ldg(r2 + 2 * c);
+                    wv[c] = valid ? x : 0u;
                 }
-                if (m > 2) {
-                    const uint4 w = src2[kq];
-                    v.x &= w.x; v.y &= w.y; v.z &= w.z; v.w &= w.w;
-                }
-                if (!valid) v = make_uint4(0, 0, 0, 0);
-                *reinterpret_cast<uint4 *>(As + kq * (TC_R * 16)) = v;
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
-            bar_arrive(&a_full[slot]);
+            uint8_t *dst = Abuf + (row >> 3) * 128 + (row & 7) * 16;
+#pragma unroll
+            for (int c = 0; c < TC_KMAX / TC_KC; c++) {
+                if (c >= nkc) break;
+                const uint4 lo = expand16(wv[c] & 0xffffu), hi = expand16(wv[c] >> 16);
+                bar_wait(&a_empty[c], (t & 1) ^ 1);   // the last tile of task t-1 is done with it
+                const int kq = c * (TC_KC / 16) + 2 * part;
+                *reinterpret_cast<uint4 *>(dst + kq * (TC_R * 16)) = lo;
+                *reinterpret_cast<uint4 *>(dst + (kq + 1) * (TC_R * 16)) = hi;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+                bar_arrive(&a_full[c]);
+            }
         }
-    } else if (warp == 8) {
+    } else if (warp == TC_PROD_WARP) {
         // ---------------- B producer ----------------
         if (lane == 0) {
-            uint32_t sc = 0;
-            const int nkc = K / TC_KC;
+            int st = 0;
+            uint32_t ph = 0;   // ring position and the phase parity of its current lap
+            const int64_t kstride = p.n_grp * (8 * TC_KC);
             for (int t = 0;; t++) {
                 const int slot = t & 1;
                 bar_wait(&t_full[slot], (t >> 1) & 1);
                 const int4 ti = tinfo[slot];
+                bar_arrive(&t_empty[slot]);
                 if (ti.x < 0) break;
                 for (int u = ti.y; u < ti.z; u++) {
-                    const int64_t grp0 = ((int64_t)ti.w + (int64_t)u * TC_N) >> 3;
-                    for (int kc = 0; kc < nkc; kc++, sc++) {
-                        const int st = (int)(sc % (uint32_t)S);
-                        bar_wait(&b_empty[st], ((sc / (uint32_t)S) & 1) ^ 1);
-                        bar_expect_tx(&b_full[st], TC_N * TC_KC);
-                        if (CL == 1) {
-                            bulk_g2s(Bbuf + (size_t)st * TC_N * TC_KC,
-                                     p.B + ((int64_t)kc * p.n_grp + grp0) * (8 * TC_KC), TC_N * TC_KC, &b_full[st]);
-                        } else if (crank == 0) {
-                            bulk_g2s_mc(Bbuf + (size_t)st * TC_N * TC_KC,
-                                        p.B + ((int64_t)kc * p.n_grp + grp0) * (8 * TC_KC), TC_N * TC_KC, &b_full[st],
-                                        (uint16_t)((1u << CL) - 1));
+                    const int64_t col0 = (int64_t)ti.w + (int64_t)u * TC_N;
+                    const int n_eff = (int)min((int64_t)TC_N, (p.C - col0 + 15) & ~(int64_t)15);
+                    const uint32_t bytes = (uint32_t)n_eff * TC_KC;
+                    const uint8_t *src = p.B + (col0 >> 3) * (8 * TC_KC);
+                    for (int kc = 0; kc < nkc; kc++, src += kstride) {
+                        bar_wait(&b_empty[st], ph ^ 1);
+                        bar_expect_tx(&b_full[st], bytes);
+                        bulk_g2s(Bbuf + (size_t)st * TC_N * TC_KC, src, bytes, &b_full[st]);
+                        if (++st == S) {
+                            st = 0;
+                            ph ^= 1;
                         }
                     }
                 }
@@ -565,44 +566,56 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     } else {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            uint32_t sc = 0, tcnt = 0;
-            const int nkc = K / TC_KC;
+            // one thread issues everything: keep its loop lean (no division, descriptors
+            // advanced by adding (byte offset >> 4) to their 14-bit address field)
+            int st = 0;
+            uint32_t ph = 0, tcnt = 0;
+            const uint64_t adesc0 = sdesc(su32(Abuf), TC_R * 16, 128);
+            const uint64_t bdesc0 = sdesc(su32(Bbuf), 128, 8 * TC_KC);
+            constexpr uint64_t A_KC = (uint64_t)(TC_KC / 16) * TC_R * 16 >> 4;   // one A chunk (8 KB)
+            constexpr uint64_t A_K32 = (uint64_t)2 * TC_R * 16 >> 4;              // 32 bytes of K in A
+            constexpr uint64_t B_ST = (uint64_t)TC_N * TC_KC >> 4;                // one B stage (16 KB)
+            constexpr uint64_t B_K32 = 256 >> 4;                                  // 32 bytes of K in B
             for (int t = 0;; t++) {
                 const int slot = t & 1;
-                bar_wait(&a_full[slot], (t >> 1) & 1);
+                bar_wait(&t_full[slot], (t >> 1) & 1);
                 const int4 ti = tinfo[slot];
+                bar_arrive(&t_empty[slot]);
                 if (ti.x < 0) break;
-                tc_fence_after();
-                const uint32_t abase = su32(Abuf + (size_t)slot * TC_R * K);
                 for (int u = ti.y; u < ti.z; u++, tcnt++) {
                     const int buf = tcnt & 1;
+                    const int64_t col0 = (int64_t)ti.w + (int64_t)u * TC_N;
+                    const int n_eff = (int)min((int64_t)TC_N, (p.C - col0 + 15) & ~(int64_t)15);
+                    const uint32_t idesc = (1u << 4) | ((uint32_t)(n_eff >> 3) << 17) | ((uint32_t)(TC_R >> 4) << 24);
+                    const bool first = u == ti.y, lastu = u == ti.z - 1;
                     bar_wait(&acc_empty[buf], ((tcnt >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t d = tmem + buf * TC_N;
-                    for (int kc = 0; kc < nkc; kc++, sc++) {
-                        const int st = (int)(sc % (uint32_t)S);
-                        bar_wait(&b_full[st], (sc / (uint32_t)S) & 1);
+                    uint64_t ad = adesc0;
+                    for (int kc = 0; kc < nkc; kc++, ad += A_KC) {
+                        if (first) bar_wait(&a_full[kc], t & 1);
+                        bar_wait(&b_full[st], ph);
                         tc_fence_after();
-                        const uint32_t bbase = su32(Bbuf + (size_t)st * TC_N * TC_KC);
-#pragma unroll
-                        for (int i = 0; i < TC_KC / 32; i++) {
-                            const int kk = kc * TC_KC + i * 32;
-                            tc_mma(d, sdesc(abase + (kk / 16) * (TC_R * 16), TC_R * 16, 128),
-                                   sdesc(bbase + i * 256, 128, 8 * TC_KC), (kc | i) ? 1u : 0u);
+                        const uint64_t bd = bdesc0 + (uint64_t)st * B_ST;
+                        if (!(p.dbg & 2)) {
+                            tc_mma(d, ad, bd, idesc, kc ? 1u : 0u);
+                            tc_mma(d, ad + A_K32, bd + B_K32, idesc, 1u);
                         }
-                        if (CL == 1 || crank == 0) tc_commit(&b_empty[st]);
-                        else tc_commit_mc(&b_empty[st], (uint16_t)(1u | (1u << crank)));   // CTA 0's and own
+                        tc_commit(&b_empty[st]);
+                        if (lastu) tc_commit(&a_empty[kc]);   // the task's last use of A chunk kc
+                        if (++st == S) {
+                            st = 0;
+                            ph ^= 1;
+                        }
                     }
                     tc_commit(&acc_full[buf]);
                 }
-                tc_commit(&a_empty[slot]);
             }
         }
         __syncwarp();
     }
     tc_fence_before();
     __syncthreads();
-    if (CL > 1) cluster_sync_all();   // no CTA leaves while a peer may still signal it
     tc_fence_after();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
@@ -612,8 +625,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 // ---------------------------------------------------------------------------
 static size_t tc_smem(int K, int S)
 {
-    return (size_t)2 * TC_R * K + (size_t)S * TC_N * TC_KC + sizeof(int) * 2 * TC_R + sizeof(int4) * 2 +
-           sizeof(uint64_t) * (10 + 2 * S) + 16;
+    return (size_t)TC_R * K + (size_t)S * TC_N * TC_KC + sizeof(int) * 2 * TC_R + sizeof(int4) * 2 +
+           sizeof(uint64_t) * (8 + 2 * (K / TC_KC) + 2 * S) + 16;
 }
 
 pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, int *nt_out)
@@ -621,7 +634,6 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     cudaStream_t s = ctx->stream;
     const int m = a.k - 1;
     if (m < 1 || m > 3 || v->C >= (1 << KEY_BITS) || v->E_pad % TC_KC != 0) return PT_EINVAL;
-    if (a.cl != 1 && a.cl != 2 && a.cl != 4) return PT_EINVAL;
     // nt thresholds (PT_TC_NT, default 2), as many as fit TC_KMAX
     // (read per call: the tests vary them in one process)
     const int nt_env = getenv("PT_TC_NT") ? atoi(getenv("PT_TC_NT")) : 2;
@@ -630,8 +642,8 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     if (nt < 1) return PT_EINVAL;
     const int K = nt * (int)v->E_pad;
     const size_t smem_limit = 227 * 1024 - 1024;   // margin for static shared memory
-    int S = 4;
-    while (S > 2 && tc_smem(K, S) > smem_limit) S--;
+    int S = 16;   // as deep a B ring as fits beside the A buffer
+    while (S > 4 && tc_smem(K, S) > smem_limit) S--;
     if (tc_smem(K, S) > smem_limit) return PT_EINVAL;
     // per-call operands (the thresholds follow tau)
     pt_view *mv = const_cast<pt_view *>(v);
@@ -641,7 +653,7 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
         pt_dfree(ctx, mv->tcA);
         pt_dfree(ctx, mv->tcB);
         mv->tcA = mv->tcB = nullptr;
-        PT_TRY(pt_dalloc(ctx, (void **)&mv->tcA, (size_t)n_cfg * K));
+        PT_TRY(pt_dalloc(ctx, (void **)&mv->tcA, (size_t)n_cfg * K / 8));
         PT_TRY(pt_dalloc(ctx, (void **)&mv->tcB, (size_t)n_cfg * K));
         mv->tc_ncfg = n_cfg;
         mv->tc_K = K;
@@ -658,9 +670,7 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
         auto it = occ_cache.find(key);
         if (it == occ_cache.end()) {
             PT_TRY(pt_smem_optin(ctx, (const void *)k_swap_tau));
-            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc<1>));
-            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc<2>));
-            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc<4>));
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc));
             PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_swap_tau, 256, sw_smem));
             occ_cache[key] = occ;
         } else {
@@ -687,9 +697,9 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     const unsigned gmax = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ne + 255) / 256, 4L * ctx->num_sms));
     k_tc_lmax<<<gmax, 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, cst);
     k_tc_const<<<1, 1, 0, s>>>(tau_dev, v->E, v->E_pad, alpha, cst, a.U, a.cand_n);
-    const int64_t nb = n_cfg * K;
-    k_tc_build<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, K, n_cfg, cst, mv->tcA,
-                                                             mv->tcB);
+    const int64_t nb = n_cfg * (K / 32);
+    k_tc_build<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, K, n_cfg, cst,
+                                                             (uint32_t *)mv->tcA, mv->tcB);
     ctx->stats.launches += 4;
     PT_CK(cudaGetLastError());
     TcParams p;
@@ -702,63 +712,17 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     p.tasks = a.tasks;
     p.task_hi = a.tb;
     p.task_ctr = a.ctr;
-    p.A = mv->tcA;
+    p.A = (const uint32_t *)mv->tcA;
     p.B = mv->tcB;
     p.cst = cst;
     p.cand_key = a.cand_key;
     p.cand_s = a.cand_s;
     p.cand_n = a.cand_n;
     p.cap = a.cap;
-    p.mbox = a.mbox;
-    const int CL = a.cl;
-    const void *kfn = CL == 4 ? (const void *)k_exh_tc<4> : CL == 2 ? (const void *)k_exh_tc<2> : (const void *)k_exh_tc<1>;
-    const size_t smem = tc_smem(K, S);
-    int grid = std::min(ctx->num_sms, (a.tb - a.ta) * CL);
-    cudaLaunchConfig_t lc = {};
-    cudaLaunchAttribute attr[1];
-    lc.blockDim = dim3(TC_THREADS);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = s;
-    if (CL > 1) {
-        static std::mutex cmu;
-        static std::map<std::tuple<int, int, size_t>, int> clusters;   // (device, CL, smem) -> co-resident clusters
-        int ncl = 0;
-        {
-            std::lock_guard<std::mutex> g(cmu);
-            auto key = std::make_tuple(ctx->dev, CL, smem);
-            auto it = clusters.find(key);
-            if (it == clusters.end()) {
-                PT_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-                cudaLaunchConfig_t q = lc;
-                q.gridDim = dim3(CL * ctx->num_sms);
-                attr[0].id = cudaLaunchAttributeClusterDimension;
-                attr[0].val.clusterDim.x = CL;
-                attr[0].val.clusterDim.y = 1;
-                attr[0].val.clusterDim.z = 1;
-                q.attrs = attr;
-                q.numAttrs = 1;
-                PT_CK(cudaOccupancyMaxActiveClusters(&ncl, kfn, &q));
-                clusters[key] = ncl;
-            } else {
-                ncl = it->second;
-            }
-        }
-        if (ncl < 1) return PT_EINVAL;
-        grid = std::min(ncl * CL, grid / CL * CL);
-        if (grid < CL) grid = CL;
-        PT_CK(cudaMemsetAsync(a.mbox, 0, sizeof(unsigned long long) * 4 * (grid / CL), s));
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CL;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        lc.attrs = attr;
-        lc.numAttrs = 1;
-    }
-    lc.gridDim = dim3(grid);
+    p.dbg = getenv("PT_TC_DBG") ? atoi(getenv("PT_TC_DBG")) : 0;
+    const int grid = std::min(ctx->num_sms, a.tb - a.ta);
     PT_CK(cudaEventRecord(ctx->ev0, s));
-    if (CL == 4) PT_CK(cudaLaunchKernelEx(&lc, k_exh_tc<4>, p));
-    else if (CL == 2) PT_CK(cudaLaunchKernelEx(&lc, k_exh_tc<2>, p));
-    else PT_CK(cudaLaunchKernelEx(&lc, k_exh_tc<1>, p));
+    k_exh_tc<<<grid, TC_THREADS, tc_smem(K, S), s>>>(p);
     PT_CK(cudaEventRecord(ctx->ev1, s));
     ctx->stats.launches++;
     PT_CK(cudaGetLastError());
@@ -766,11 +730,3 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     return PT_OK;
 }
 
-// CTAs per cluster sharing the B stream (PT_TC_CL = 1, 2 or 4; default 2 for k >= 3,
-// 1 for the small k = 2 search).  The caller builds its task list with 128 x CL rows.
-int pt_tc_cluster(int k)
-{
-    const char *e = getenv("PT_TC_CL");
-    int cl = e ? atoi(e) : (k >= 3 ? 2 : 1);
-    return (cl == 1 || cl == 2 || cl == 4) ? cl : 1;
-}

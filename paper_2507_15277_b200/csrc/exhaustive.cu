@@ -1464,15 +1464,17 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     // threshold-count tier (k_exh_tc, exh_tc.cu): the default for k = 2..4; its own task
     // list (256-column tiles); on an unusable tau or a buffer overflow the search falls
     // back to the u8 tier in the next pass
-    bool tc = !force_fp16 && !force_u8 && k >= 2 && k <= 4;
+    // (k = 2 is a 1.6 M-set search: the u8 tier's single launch beats the tc tier's
+    // swap search + operand build there, 0.11 vs 0.17 ms per call at the paper shape;
+    // PT_EXH_TIER=tc forces the tc tier for k = 2 too)
+    const bool force_tc = tier_env && !strcmp(tier_env, "tc");
+    bool tc = !force_fp16 && !force_u8 && k <= 4 && (k >= 3 || (force_tc && k >= 2));
     const int4 *tc_list = nullptr;
     int tc_ta = 0, tc_tb = 0;
     int64_t tc_sets = 0, tc_slots = 0;
-    int tc_cl = 1;
     if (tc) {
         pt_tasks *TT = nullptr;
-        tc_cl = pt_tc_cluster(k);
-        PT_TRY(build_tasks(ctx, v, m, XT_R * tc_cl, PT_TC_COLS, &TT));
+        PT_TRY(build_tasks(ctx, v, m, XT_R, PT_TC_COLS, &TT));
         tc_list = TT->d;
         tc_tb = (int)TT->h.size();
         tc_sets = TT->set_pre.back();
@@ -1487,7 +1489,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
             tc_sets = P->sets[shard_rank];
             tc_slots = P->slots[shard_rank];
         }
-        if (tc_sets != ctx->stats.exh_sets) tc = false;   // both lists cover the same sets (always)
+        if (shard_count == 1 && tc_sets != ctx->stats.exh_sets) tc = false;   // both lists cover every set (always)
     }
     const int G = (int)(v->E_pad / 4);
     auto q8_smem = [&](int S) {
@@ -1529,8 +1531,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
                      o_os = take(sizeof(double) * 2), o_ot = take(sizeof(int32_t) * 2 * k),
                      o_blk = take(sizeof(Rec2) * (size_t)ctx->num_sms * 2), o_done = take(sizeof(unsigned)),
                      o_S0 = take(sizeof(int32_t) * k), o_sd = take(sizeof(double)), o_tau = take(sizeof(double)),
-                     o_rs = take(sizeof(double) * 2 * ctx->num_sms), o_rw = take(sizeof(long long) * 2 * ctx->num_sms),
-                     o_mbox = take(sizeof(unsigned long long) * 4 * ctx->num_sms);
+                     o_rs = take(sizeof(double) * 2 * ctx->num_sms), o_rw = take(sizeof(long long) * 2 * ctx->num_sms);
         void *scr = nullptr;
         PT_TRY(pt_scratch(ctx, off, &scr));
         char *b = (char *)scr;
@@ -1584,8 +1585,6 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
             a.swap_rs = (double *)(b + o_rs);
             a.swap_rw = (long long *)(b + o_rw);
             a.tau_dev = (double *)(b + o_tau);
-            a.cl = tc_cl;
-            a.mbox = (unsigned long long *)(b + o_mbox);
             mark("pre-launch");
             int nt = 0;
             const pt_status st = pt_exh_tc_enqueue(ctx, v, a, &nt);
