@@ -445,8 +445,9 @@ def main():
     # with N ranks the exhaustive searches are sharded; the two unsharded parts
     # (greedy k=24 and the batched holdout) run once per job, on ranks 0 and 1, and
     # those ranks take a correspondingly smaller share of the k=3 task list
-    # (pt_set_shard_weights; extra work from DESIGN.md 6.4/6.8: ~0.24 and ~0.16 ms
-    # against a k=3 search of ~12 ms on one GPU)
+    # (pt_set_shard_weights; extra work per_config-measured on one B200: greedy k=24
+    # ~0.21 ms, the batched holdout ~0.16 ms, k=2 ~0.11 ms, against a k=3 search of
+    # ~1.0 ms on one GPU on the tc tier)
     # exhaustive k=2 is latency-bound (1.6 M pairs = 13 us of ALU work on one GPU, one
     # 32 us wave of 128x64 tiles): sharding it would cost every rank a full call for
     # ~2 us of work each, so with N > 1 it runs unsharded on rank 2 (mod N); only the
@@ -457,10 +458,10 @@ def main():
     shard_w = None
     if world > 1:
         extra = [0.0] * world
-        extra[0] += 0.24
+        extra[0] += 0.21
         extra[1 % world] += 0.16
-        extra[2 % world] += 0.12
-        shard_w = [max(0.2, 1.0 - x * world / 12.0) for x in extra]
+        extra[2 % world] += 0.11
+        shard_w = [max(0.05, 1.0 - x * world / 1.0) for x in extra]
 
     def step(src):
         """One pass of the whole hot path; returns (results, d2h bytes)."""

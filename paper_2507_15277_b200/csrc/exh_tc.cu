@@ -70,15 +70,17 @@ __device__ __forceinline__ void bar_expect_tx(uint64_t *b, uint32_t bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
+// try_wait without a suspend-time hint: with one, the wait compiles to a NANOSLEEP.SYNCS
+// loop whose wake-up added ~1.5 us to every ring round trip (the single MMA thread and
+// the producer ping-pong once per 64-byte K stage)
 __device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity)
 {
     uint32_t ok = 0;
     while (!ok)
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok)
-            : "r"(su32(b)), "r"(parity), "r"(1000000u)
-            : "memory");
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(su32(b)), "r"(parity)
+                     : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
 {
@@ -333,6 +335,26 @@ __device__ __forceinline__ uint32_t expand4(uint32_t nib)
 {
     return ((nib * 0x00204081u) & 0x01010101u) * 0x38u;
 }
+// colex unranking for the builders (pt_unrank_colex's answer; its binary searches cost
+// ~7 K cycles per 256-row task on the critical path of short tasks): the largest c with
+// C(c, u+1) <= r from a float estimate (sqrt / cbrt), corrected exactly in int64
+__device__ __forceinline__ void unrank_fast(int64_t R, int m, int64_t n, int32_t *out)
+{
+    int64_t r = R;
+    for (int u = m - 1; u >= 0; u--) {
+        int64_t c;
+        if (u == 0) c = r;
+        else if (u == 1) c = (int64_t)((1.0f + sqrtf(1.0f + 8.0f * (float)r)) * 0.5f);
+        else if (u == 2) c = (int64_t)cbrtf(6.0f * (float)r) + 1;
+        else c = n - 1;
+        c = min(max(c, (int64_t)u), n - 1);
+        while (c > u && pt_binom(c, u + 1) > r) c--;
+        while (c + 1 <= n - 1 && pt_binom(c + 1, u + 1) <= r) c++;
+        out[u] = (int32_t)c;
+        r -= pt_binom(c, u + 1);
+    }
+}
+
 __device__ __forceinline__ uint4 expand16(uint32_t bits16)
 {
     return make_uint4(expand4(bits16 & 15u), expand4((bits16 >> 4) & 15u), expand4((bits16 >> 8) & 15u),
@@ -352,36 +374,47 @@ struct TcParams {
     float *cand_s;
     unsigned long long *cand_n;
     unsigned cap;
-    int dbg;   // development knob PT_TC_DBG (bit 0: the epilogue skips its TMEM reads, bit 1: no MMAs)
+    int dbg;   // development knob PT_TC_DBG (bit 0: the epilogue skips its TMEM reads, 1: no MMAs,
+               // 3: the builders skip their shared-memory stores, 4: no B copies)
 };
 
 // warp roles (TC_THREADS = 18 warps)
-#define TC_EPI_WARPS 8      // 0-7: epilogue (lane quarter w & 3, column half w >> 2)
-#define TC_BLD_WARPS 8      // 8-15: A builders (2 threads per row)
+#define TC_EPI_WARPS 8      // 0-7: epilogue
+#define TC_BLD_WARPS 8      // 8-15: A builders
 #define TC_PROD_WARP 16
 #define TC_MMA_WARP 17
 
-// One CTA per SM (persistent, dynamic task queue).  A task = 128 rows x its column
-// tiles; the A operand is ONE buffer cut into K-chunks of 64 bytes (8 KB each): chunk kc
-// of task t+1 is built as soon as the last tile of task t has consumed chunk kc, so the
-// next task's A streams in behind the current task's last tile and the rest of shared
-// memory goes to a deep B ring (9 stages at K = 640) -- the ring depth is what hides the
-// latency of the bulk copies (a 4-stage ring with two whole A buffers kept the tensor
-// pipe ~30 % busy).  The last tile of a task is trimmed to N = round_up(columns, 16).
+// One CTA per SM (persistent, dynamic task queue).  H = row halves per task: a task is
+// 128 H rows x its column tiles of N = 256 / H columns; every B stage (N columns x 64 K
+// bytes) feeds H MMAs of 128 x N x 32 per 32 K bytes, one per row half, so the B bytes
+// streamed per MMA flop shrink by H (H = 2 is the default: the bulk-copy stream of B,
+// not the tensor core, bounds H = 1).  Tensor memory: two accumulator buffers x H halves
+// x N columns = 512 columns.  The A operand is ONE buffer (128 H rows x K) cut into
+// K-chunks of 64 bytes: chunk kc of task t+1 is built as soon as the last tile of task t
+// has consumed chunk kc, so the next task's A streams in behind the current task's last
+// tile and the rest of shared memory goes to a deep B ring.  The last tile of a task is
+// trimmed to N = round_up(columns, 16).
+template <int H>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 {
+    constexpr int N = TC_N / H;                 // columns per tile
+    constexpr int ROWS = TC_R * H;              // rows per task
+    constexpr int BSUB = N * TC_KC;             // one 64-byte K chunk of a B tile
+    constexpr int BST = BSUB;                   // one B stage
+    constexpr int ACH = ROWS * TC_KC;           // one A chunk (all rows, 64 K bytes)
+    constexpr int WPT = 256 / ROWS;             // builder threads per row (2 or 1)
     extern __shared__ __align__(128) uint8_t smem[];
     const int K = p.K, S = p.S, nkc = K / TC_KC;
-    uint8_t *Abuf = smem;                                           // [nkc][8 KB]
-    uint8_t *Bbuf = smem + (size_t)TC_R * K;                        // [S][256 x 64]
-    int *last = reinterpret_cast<int *>(Bbuf + (size_t)S * TC_N * TC_KC);   // [2][128]
-    int4 *tinfo = reinterpret_cast<int4 *>(last + 2 * TC_R);        // [2] (row tile, u0, u1, lo)
+    uint8_t *Abuf = smem;                                           // A [nkc][ACH]
+    uint8_t *Bbuf = smem + (size_t)nkc * ACH;                       // B ring [S][BST]
+    int *last = reinterpret_cast<int *>(Bbuf + (size_t)S * BST);    // [2][ROWS]
+    int4 *tinfo = reinterpret_cast<int4 *>(last + 2 * ROWS);        // [2] (first row / 128, u0, u1, lo)
     uint64_t *bars = reinterpret_cast<uint64_t *>(tinfo + 2);
     uint64_t *t_full = bars, *t_empty = bars + 2, *acc_full = bars + 4, *acc_empty = bars + 6;
     uint64_t *a_full = bars + 8, *a_empty = a_full + nkc;
     uint64_t *b_full = a_empty + nkc, *b_empty = b_full + S;
     uint32_t *tmem_s = reinterpret_cast<uint32_t *>(b_empty + S);
-    int *bcast = reinterpret_cast<int *>(tmem_s + 1);               // [2]
+    int *bcast = reinterpret_cast<int *>(tmem_s + 1);               // [2] + the prefetched next index
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (!p.cst->ok) return;   // tau unusable (k_tc_const flagged the search as not run)
@@ -413,31 +446,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     const int m = p.m;
 
     if (warp < TC_EPI_WARPS) {
-        // ---------------- epilogue ----------------
-        const int quarter = warp & 3, half = warp >> 2;
-        const int r = 32 * quarter + lane;
+        // ---------------- epilogue: warp = (lane quarter, row half or column half) ----------------
+        const int quarter = warp & 3, sel = warp >> 2;
+        const int h = H == 2 ? sel : 0;                   // row half whose accumulator it reads
+        const int q0 = H == 2 ? 0 : sel * 4;              // first 32-column chunk
+        const int r = 128 * h + 32 * quarter + lane;      // row within the task
         const float pthr = p.cst->pthr, u_dn = p.cst->u_dn, slk = p.cst->slack;
-        const uint32_t lane_base = tmem + ((uint32_t)(32 * quarter) << 16);
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * quarter) << 16) + h * N;
         uint32_t tcnt = 0;
         for (int t = 0;; t++) {
             const int slot = t & 1;
             bar_wait(&t_full[slot], (t >> 1) & 1);
             const int4 ti = tinfo[slot];
-            const int lastr = last[slot * TC_R + r];
+            const int lastr = last[slot * ROWS + r];
             __syncwarp();
             if (lane == 0) bar_arrive(&t_empty[slot]);
             if (ti.x < 0) break;
             const int64_t R = (int64_t)ti.x * TC_R + r;
             for (int u = ti.y; u < ti.z; u++, tcnt++) {
                 const int buf = tcnt & 1;
-                const int64_t col0 = (int64_t)ti.w + (int64_t)u * TC_N;
-                const int ncols = (int)min((int64_t)TC_N, p.C - col0);
+                const int64_t col0 = (int64_t)ti.w + (int64_t)u * N;
+                const int ncols = (int)min((int64_t)N, p.C - col0);
                 bar_wait(&acc_full[buf], (tcnt >> 1) & 1);
                 tc_fence_after();
 #pragma unroll 1
-                for (int q = half * 4; q < half * 4 + 4 && q * 32 < ncols && !(p.dbg & 1); q++) {
+                for (int q = q0; q < q0 + 4 && q * 32 < ncols && !(p.dbg & 1); q++) {
                     uint32_t v[32];
-                    tc_ld32(lane_base + buf * TC_N + q * 32, v);
+                    tc_ld32(lane_base + buf * 256 + q * 32, v);
                     const int64_t cb = col0 + q * 32;
                     float w[16];
                     if (cb > lastr && cb + 31 < p.C) {   // every column valid: a 32-wide min tree
@@ -476,61 +511,94 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
             }
         }
     } else if (warp < TC_EPI_WARPS + TC_BLD_WARPS) {
-        // ---------------- A builders: thread = (row, half of each chunk) ----------------
+        // ---------------- A builders: thread = (row, share of each chunk) ----------------
         const int bt = tid - TC_EPI_WARPS * 32;          // 0..255
-        const int row = bt & (TC_R - 1), part = bt >> 7;  // part: 16-byte pieces 2 part, 2 part + 1
+        const int row = bt % ROWS, part = bt / ROWS;     // H = 1: two threads per row (part 0/1)
+        const bool prof = (p.dbg & 32) && blockIdx.x == 0 && bt == 0;
+        long long bc[6] = {0, 0, 0, 0, 0, 0};   // t_empty, fetch, unrank, loads, a_empty waits, stores
+        long long b0 = clock64();
+        auto blap = [&](int i) {
+            if (prof) {
+                const long long b1 = clock64();
+                bc[i] += b1 - b0;
+                b0 = b1;
+            }
+        };
         for (int t = 0;; t++) {
             const int slot = t & 1;
             bar_wait(&t_empty[slot], ((t >> 1) & 1) ^ 1);
-            if (bt == 0) bcast[slot] = atomicAdd(p.task_ctr, 1);
+            blap(0);
+            if (bt == 0) {   // this task's index was fetched one task ahead (off the critical path)
+                bcast[slot] = t == 0 ? atomicAdd(p.task_ctr, 1) : bcast[2];
+                bcast[2] = atomicAdd(p.task_ctr, 1);
+            }
             named_sync(1, TC_BLD_WARPS * 32);
             const int ti = bcast[slot];
+            blap(1);
             if (ti >= p.task_hi) {
                 if (bt == 0) tinfo[slot] = make_int4(-1, 0, 0, 0);
                 bar_arrive(&t_full[slot]);
+                if (prof)
+                    printf("[k_exh_tc builder 0, CTA 0] %d tasks, cycles: t_empty %lld fetch %lld unrank %lld loads %lld "
+                           "a_empty %lld stores %lld\n", t, bc[0], bc[1], bc[2], bc[3], bc[4], bc[5]);
                 break;
             }
             const int4 tk = p.tasks[ti];
-            const int64_t R0 = (int64_t)tk.x * TC_R;
-            if (bt == 0) {
-                int32_t mem0[PT_MAXK];
-                pt_unrank_colex(R0, m, p.C, mem0);
-                tinfo[slot] = make_int4(tk.x, tk.y, tk.z, (int)tile_lo(mem0[m - 1]));
-            }
+            const int64_t R0 = (int64_t)tk.x * ROWS;
             const int64_t R = R0 + row;
             const bool valid = R < p.n_rows;
             int32_t mem[PT_MAXK];
-            if (valid) pt_unrank_colex(R, m, p.C, mem);
+            if (valid) unrank_fast(R, m, p.C, mem);
             else for (int u = 0; u < m; u++) mem[u] = 0;
-            if (part == 0) last[slot * TC_R + row] = valid ? mem[m - 1] : 0x7fffffff;
+            if (bt == 0) tinfo[slot] = make_int4((int)(R0 / TC_R), tk.y, tk.z, (int)tile_lo(mem[m - 1]));   // row 0 = R0
+            if (part == 0) last[slot * ROWS + row] = valid ? mem[m - 1] : 0x7fffffff;
             bar_arrive(&t_full[slot]);
-            // this thread's 32-element halves of every chunk: words 2 c + part of the
-            // members' packed rows, ANDed (= the bits of the row's minimum), then expanded
+            blap(2);
+            // the row's packed bits: per chunk c, words 2c and 2c+1 (H = 2: this thread both;
+            // H = 1: word 2c + part), ANDed over the members (= the bits of the row's min)
             const int W = K / 32;
-            const uint32_t *r0 = p.A + (int64_t)mem[0] * W + part;
-            const uint32_t *r1 = p.A + (int64_t)mem[m > 1 ? 1 : 0] * W + part;
-            const uint32_t *r2 = p.A + (int64_t)mem[m > 2 ? 2 : 0] * W + part;
-            uint32_t wv[TC_KMAX / TC_KC];
+            const uint32_t *r0 = p.A + (int64_t)mem[0] * W;
+            const uint32_t *r1 = p.A + (int64_t)mem[m > 1 ? 1 : 0] * W;
+            const uint32_t *r2 = p.A + (int64_t)mem[m > 2 ? 2 : 0] * W;
+            constexpr int WPC = 2 / WPT;                 // words of a chunk per thread
+            uint32_t wv[TC_KMAX / TC_KC][WPC];
 #pragma unroll
             for (int c = 0; c < TC_KMAX / TC_KC; c++) {
                 if (c < nkc) {
-                    uint32_t x = __ldg(r0 + 2 * c);
-                    if (m > 1) x &= __ldg(r1 + 2 * c);
-                    if (m > 2) x &= __ldg(r2 + 2 * c);
-                    wv[c] = valid ? x : 0u;
+#pragma unroll
+                    for (int i = 0; i < WPC; i++) {
+                        const int wi = 2 * c + (WPC == 2 ? i : part);
+                        uint32_t x = __ldg(r0 + wi);
+                        if (m > 1) x &= __ldg(r1 + wi);
+                        if (m > 2) x &= __ldg(r2 + wi);
+                        wv[c][i] = valid ? x : 0u;
+                    }
                 }
             }
-            uint8_t *dst = Abuf + (row >> 3) * 128 + (row & 7) * 16;
+            if (prof) {   // force the loads to complete before the lap (profiling only)
+                uint32_t z = 0;
+                for (int c = 0; c < TC_KMAX / TC_KC; c++)
+                    if (c < nkc) z ^= wv[c][0];
+                if (z == 0x12345678u) bcast[slot] = 0;
+            }
+            blap(3);
+            const int hr = row >> 7, rr = row & 127;     // row half, row within it
+            uint8_t *dst = Abuf + (size_t)hr * (TC_R * TC_KC) + (rr >> 3) * 128 + (rr & 7) * 16;
 #pragma unroll
             for (int c = 0; c < TC_KMAX / TC_KC; c++) {
                 if (c >= nkc) break;
-                const uint4 lo = expand16(wv[c] & 0xffffu), hi = expand16(wv[c] >> 16);
-                bar_wait(&a_empty[c], (t & 1) ^ 1);   // the last tile of task t-1 is done with it
-                const int kq = c * (TC_KC / 16) + 2 * part;
-                *reinterpret_cast<uint4 *>(dst + kq * (TC_R * 16)) = lo;
-                *reinterpret_cast<uint4 *>(dst + (kq + 1) * (TC_R * 16)) = hi;
+                bar_wait(&a_empty[c], (t & 1) ^ 1);   // the last tile of task t-1 is done with chunk c
+                blap(4);
+                uint8_t *cd = dst + (size_t)c * ACH;
+#pragma unroll
+                for (int i = 0; i < WPC && !(p.dbg & 8); i++) {
+                    const int piece = 2 * (WPC == 2 ? i : part);   // 16-byte K piece within the chunk
+                    *reinterpret_cast<uint4 *>(cd + piece * (TC_R * 16)) = expand16(wv[c][i] & 0xffffu);
+                    *reinterpret_cast<uint4 *>(cd + (piece + 1) * (TC_R * 16)) = expand16(wv[c][i] >> 16);
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
                 bar_arrive(&a_full[c]);
+                blap(5);
             }
         }
     } else if (warp == TC_PROD_WARP) {
@@ -546,14 +614,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                 bar_arrive(&t_empty[slot]);
                 if (ti.x < 0) break;
                 for (int u = ti.y; u < ti.z; u++) {
-                    const int64_t col0 = (int64_t)ti.w + (int64_t)u * TC_N;
-                    const int n_eff = (int)min((int64_t)TC_N, (p.C - col0 + 15) & ~(int64_t)15);
+                    const int64_t col0 = (int64_t)ti.w + (int64_t)u * N;
+                    const int n_eff = (int)min((int64_t)N, (p.C - col0 + 15) & ~(int64_t)15);
                     const uint32_t bytes = (uint32_t)n_eff * TC_KC;
                     const uint8_t *src = p.B + (col0 >> 3) * (8 * TC_KC);
                     for (int kc = 0; kc < nkc; kc++, src += kstride) {
                         bar_wait(&b_empty[st], ph ^ 1);
-                        bar_expect_tx(&b_full[st], bytes);
-                        bulk_g2s(Bbuf + (size_t)st * TC_N * TC_KC, src, bytes, &b_full[st]);
+                        if (p.dbg & 16) {
+                            bar_arrive(&b_full[st]);
+                        } else {
+                            bar_expect_tx(&b_full[st], bytes);
+                            bulk_g2s(Bbuf + (size_t)st * BST, src, bytes, &b_full[st]);
+                        }
                         if (++st == S) {
                             st = 0;
                             ph ^= 1;
@@ -572,45 +644,69 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
             uint32_t ph = 0, tcnt = 0;
             const uint64_t adesc0 = sdesc(su32(Abuf), TC_R * 16, 128);
             const uint64_t bdesc0 = sdesc(su32(Bbuf), 128, 8 * TC_KC);
-            constexpr uint64_t A_KC = (uint64_t)(TC_KC / 16) * TC_R * 16 >> 4;   // one A chunk (8 KB)
-            constexpr uint64_t A_K32 = (uint64_t)2 * TC_R * 16 >> 4;              // 32 bytes of K in A
-            constexpr uint64_t B_ST = (uint64_t)TC_N * TC_KC >> 4;                // one B stage (16 KB)
-            constexpr uint64_t B_K32 = 256 >> 4;                                  // 32 bytes of K in B
+            constexpr uint64_t A_HALF = (uint64_t)TC_R * TC_KC >> 4;   // the second row half of a chunk
+            constexpr uint64_t A_CH = (uint64_t)ACH >> 4;                // one A chunk
+            constexpr uint64_t A_K32 = (uint64_t)2 * TC_R * 16 >> 4;     // 32 bytes of K in A
+            constexpr uint64_t B_ST = (uint64_t)BST >> 4;                // one B stage
+            constexpr uint64_t B_K32 = 256 >> 4;                         // 32 bytes of K in B
+            const bool prof = (p.dbg & 32) && blockIdx.x == 0;
+            long long cyc[6] = {0, 0, 0, 0, 0, 0};   // t_full, acc_empty, a_full, b_full, mma, commit
+            long long c0 = clock64();
+            auto lap = [&](int i) {
+                if (prof) {
+                    const long long c1 = clock64();
+                    cyc[i] += c1 - c0;
+                    c0 = c1;
+                }
+            };
             for (int t = 0;; t++) {
                 const int slot = t & 1;
                 bar_wait(&t_full[slot], (t >> 1) & 1);
+                lap(0);
                 const int4 ti = tinfo[slot];
                 bar_arrive(&t_empty[slot]);
                 if (ti.x < 0) break;
                 for (int u = ti.y; u < ti.z; u++, tcnt++) {
                     const int buf = tcnt & 1;
-                    const int64_t col0 = (int64_t)ti.w + (int64_t)u * TC_N;
-                    const int n_eff = (int)min((int64_t)TC_N, (p.C - col0 + 15) & ~(int64_t)15);
+                    const int64_t col0 = (int64_t)ti.w + (int64_t)u * N;
+                    const int n_eff = (int)min((int64_t)N, (p.C - col0 + 15) & ~(int64_t)15);
                     const uint32_t idesc = (1u << 4) | ((uint32_t)(n_eff >> 3) << 17) | ((uint32_t)(TC_R >> 4) << 24);
                     const bool first = u == ti.y, lastu = u == ti.z - 1;
                     bar_wait(&acc_empty[buf], ((tcnt >> 1) & 1) ^ 1);
                     tc_fence_after();
-                    const uint32_t d = tmem + buf * TC_N;
+                    lap(1);
+                    const uint32_t d = tmem + buf * 256;
                     uint64_t ad = adesc0;
-                    for (int kc = 0; kc < nkc; kc++, ad += A_KC) {
+                    for (int kc = 0; kc < nkc; kc++, ad += A_CH) {
                         if (first) bar_wait(&a_full[kc], t & 1);
+                        lap(2);
                         bar_wait(&b_full[st], ph);
                         tc_fence_after();
+                        lap(3);
                         const uint64_t bd = bdesc0 + (uint64_t)st * B_ST;
                         if (!(p.dbg & 2)) {
-                            tc_mma(d, ad, bd, idesc, kc ? 1u : 0u);
-                            tc_mma(d, ad + A_K32, bd + B_K32, idesc, 1u);
+#pragma unroll
+                            for (int hh = 0; hh < H; hh++) {
+                                tc_mma(d + hh * N, ad + hh * A_HALF, bd, idesc, kc ? 1u : 0u);
+                                tc_mma(d + hh * N, ad + hh * A_HALF + A_K32, bd + B_K32, idesc, 1u);
+                            }
                         }
+                        lap(4);
                         tc_commit(&b_empty[st]);
                         if (lastu) tc_commit(&a_empty[kc]);   // the task's last use of A chunk kc
+                        lap(5);
                         if (++st == S) {
                             st = 0;
                             ph ^= 1;
                         }
                     }
                     tc_commit(&acc_full[buf]);
+                    lap(5);
                 }
             }
+            if (prof)
+                printf("[k_exh_tc MMA thread, CTA 0] cycles: t_full %lld acc_empty %lld a_full %lld b_full %lld mma %lld commit %lld\n",
+                       cyc[0], cyc[1], cyc[2], cyc[3], cyc[4], cyc[5]);
         }
         __syncwarp();
     }
@@ -623,10 +719,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static size_t tc_smem(int K, int S)
+static size_t tc_smem(int K, int S, int H)
 {
-    return (size_t)TC_R * K + (size_t)S * TC_N * TC_KC + sizeof(int) * 2 * TC_R + sizeof(int4) * 2 +
-           sizeof(uint64_t) * (8 + 2 * (K / TC_KC) + 2 * S) + 16;
+    return (size_t)TC_R * H * K + (size_t)S * (TC_N / H) * TC_KC + sizeof(int) * 2 * TC_R * H + sizeof(int4) * 2 +
+           sizeof(uint64_t) * (8 + 2 * (K / TC_KC) + 2 * S) + 32;
+}
+
+// row halves per task (PT_TC_H = 1 or 2, default 1); the caller's task list has 128 H rows
+// and 256 / H columns per tile
+int pt_tc_halves()
+{
+    const char *e = getenv("PT_TC_H");
+    return (e && atoi(e) == 2) ? 2 : 1;
 }
 
 pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, int *nt_out)
@@ -642,9 +746,11 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     if (nt < 1) return PT_EINVAL;
     const int K = nt * (int)v->E_pad;
     const size_t smem_limit = 227 * 1024 - 1024;   // margin for static shared memory
-    int S = 16;   // as deep a B ring as fits beside the A buffer
-    while (S > 4 && tc_smem(K, S) > smem_limit) S--;
-    if (tc_smem(K, S) > smem_limit) return PT_EINVAL;
+    const int H = a.halves;
+    // B ring: as many 64-byte K stages as fit beside the A buffer (up to 16)
+    int S = 16;
+    while (S > 2 && tc_smem(K, S, H) > smem_limit) S--;
+    if (tc_smem(K, S, H) > smem_limit) return PT_EINVAL;
     // per-call operands (the thresholds follow tau)
     pt_view *mv = const_cast<pt_view *>(v);
     const int64_t n_cfg = pt_round_up(v->C + TC_N + 8, 8);
@@ -670,7 +776,8 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
         auto it = occ_cache.find(key);
         if (it == occ_cache.end()) {
             PT_TRY(pt_smem_optin(ctx, (const void *)k_swap_tau));
-            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc));
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc<1>));
+            PT_TRY(pt_smem_optin(ctx, (const void *)k_exh_tc<2>));
             PT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_swap_tau, 256, sw_smem));
             occ_cache[key] = occ;
         } else {
@@ -720,9 +827,11 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     p.cand_n = a.cand_n;
     p.cap = a.cap;
     p.dbg = getenv("PT_TC_DBG") ? atoi(getenv("PT_TC_DBG")) : 0;
+    const size_t smem = tc_smem(K, S, H);
     const int grid = std::min(ctx->num_sms, a.tb - a.ta);
     PT_CK(cudaEventRecord(ctx->ev0, s));
-    k_exh_tc<<<grid, TC_THREADS, tc_smem(K, S), s>>>(p);
+    if (H == 2) k_exh_tc<2><<<grid, TC_THREADS, smem, s>>>(p);
+    else k_exh_tc<1><<<grid, TC_THREADS, smem, s>>>(p);
     PT_CK(cudaEventRecord(ctx->ev1, s));
     ctx->stats.launches++;
     PT_CK(cudaGetLastError());

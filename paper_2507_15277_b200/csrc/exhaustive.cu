@@ -1472,9 +1472,11 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     const int4 *tc_list = nullptr;
     int tc_ta = 0, tc_tb = 0;
     int64_t tc_sets = 0, tc_slots = 0;
+    int tc_halves = 2;
     if (tc) {
         pt_tasks *TT = nullptr;
-        PT_TRY(build_tasks(ctx, v, m, XT_R, PT_TC_COLS, &TT));
+        tc_halves = pt_tc_halves();
+        PT_TRY(build_tasks(ctx, v, m, XT_R * tc_halves, 256 / tc_halves, &TT));
         tc_list = TT->d;
         tc_tb = (int)TT->h.size();
         tc_sets = TT->set_pre.back();
@@ -1585,6 +1587,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
             a.swap_rs = (double *)(b + o_rs);
             a.swap_rw = (long long *)(b + o_rw);
             a.tau_dev = (double *)(b + o_tau);
+            a.halves = tc_halves;
             mark("pre-launch");
             int nt = 0;
             const pt_status st = pt_exh_tc_enqueue(ctx, v, a, &nt);

@@ -227,9 +227,10 @@ struct pt_tc_args {
     double *swap_rs = nullptr;         // [2 num_sms] scratch
     long long *swap_rw = nullptr;      // [2 num_sms] scratch
     double *tau_dev = nullptr;         // [1] scratch
+    int halves = 2;                    // row halves per task: 128 halves rows x (256 / halves) columns
 };
 pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, int *nt_out);
-#define PT_TC_COLS 256   // the tc tier's column-tile width (its task list)
+int pt_tc_halves();
 // sharded search (dist.cu): pack the local top-2 (device os[2], ot[2k]) into ctx->rec_out
 void pt_pack_record(pt_ctx *ctx, const double *d_os, const int32_t *d_ot, int k);
 // fleet objective (fleet.cu): rates of sets / greedy / exhaustive, env_mask may be NULL
