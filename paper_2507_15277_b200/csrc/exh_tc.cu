@@ -363,7 +363,7 @@ __device__ __forceinline__ uint4 expand16(uint32_t bits16)
 
 struct TcParams {
     int64_t C, n_rows, n_grp;
-    int m, K, S;
+    int m, K, S, AB;   // S = B stages, AB = A buffers (1 or 2)
     const int4 *tasks;
     int task_hi;
     int *task_ctr;
@@ -404,15 +404,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     constexpr int ACH = ROWS * TC_KC;           // one A chunk (all rows, 64 K bytes)
     constexpr int WPT = 256 / ROWS;             // builder threads per row (2 or 1)
     extern __shared__ __align__(128) uint8_t smem[];
-    const int K = p.K, S = p.S, nkc = K / TC_KC;
-    uint8_t *Abuf = smem;                                           // A [nkc][ACH]
-    uint8_t *Bbuf = smem + (size_t)nkc * ACH;                       // B ring [S][BST]
+    const int K = p.K, S = p.S, AB = p.AB, nkc = K / TC_KC;
+    uint8_t *Abuf = smem;                                           // A [AB][nkc][ACH]
+    uint8_t *Bbuf = smem + (size_t)AB * nkc * ACH;                  // B ring [S][BST]
     int *last = reinterpret_cast<int *>(Bbuf + (size_t)S * BST);    // [2][ROWS]
     int4 *tinfo = reinterpret_cast<int4 *>(last + 2 * ROWS);        // [2] (first row / 128, u0, u1, lo)
     uint64_t *bars = reinterpret_cast<uint64_t *>(tinfo + 2);
     uint64_t *t_full = bars, *t_empty = bars + 2, *acc_full = bars + 4, *acc_empty = bars + 6;
-    uint64_t *a_full = bars + 8, *a_empty = a_full + nkc;
-    uint64_t *b_full = a_empty + nkc, *b_empty = b_full + S;
+    uint64_t *a_full = bars + 8, *a_empty = a_full + AB * nkc;     // [AB][nkc] each
+    uint64_t *b_full = a_empty + AB * nkc, *b_empty = b_full + S;
     uint32_t *tmem_s = reinterpret_cast<uint32_t *>(b_empty + S);
     int *bcast = reinterpret_cast<int *>(tmem_s + 1);               // [2] + the prefetched next index
 
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
             bar_init(&acc_full[i], 1);
             bar_init(&acc_empty[i], TC_EPI_WARPS);
         }
-        for (int c = 0; c < nkc; c++) {
+        for (int c = 0; c < AB * nkc; c++) {
             bar_init(&a_full[c], TC_BLD_WARPS * 32);
             bar_init(&a_empty[c], 1);
         }
@@ -584,12 +584,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
             blap(3);
             const int hr = row >> 7, rr = row & 127;     // row half, row within it
             uint8_t *dst = Abuf + (size_t)hr * (TC_R * TC_KC) + (rr >> 3) * 128 + (rr & 7) * 16;
+            // A buffer t % AB: with two, task t+1's A is built while task t's tiles run
+            const int ab = AB == 2 ? (t & 1) : 0;
+            const uint32_t aph = (uint32_t)((AB == 2 ? t >> 1 : t) & 1);   // this buffer's use parity
 #pragma unroll
             for (int c = 0; c < TC_KMAX / TC_KC; c++) {
                 if (c >= nkc) break;
-                bar_wait(&a_empty[c], (t & 1) ^ 1);   // the last tile of task t-1 is done with chunk c
+                bar_wait(&a_empty[ab * nkc + c], aph ^ 1);   // the buffer's previous task is done with chunk c
                 blap(4);
-                uint8_t *cd = dst + (size_t)c * ACH;
+                uint8_t *cd = dst + (size_t)(ab * nkc + c) * ACH;
 #pragma unroll
                 for (int i = 0; i < WPC && !(p.dbg & 8); i++) {
                     const int piece = 2 * (WPC == 2 ? i : part);   // 16-byte K piece within the chunk
@@ -597,7 +600,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                     *reinterpret_cast<uint4 *>(cd + (piece + 1) * (TC_R * 16)) = expand16(wv[c][i] >> 16);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
-                bar_arrive(&a_full[c]);
+                bar_arrive(&a_full[ab * nkc + c]);
                 blap(5);
             }
         }
@@ -676,9 +679,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                     tc_fence_after();
                     lap(1);
                     const uint32_t d = tmem + buf * 256;
-                    uint64_t ad = adesc0;
+                    const int ab = AB == 2 ? (t & 1) : 0;
+                    const uint32_t aph = (uint32_t)((AB == 2 ? t >> 1 : t) & 1);
+                    uint64_t ad = adesc0 + (uint64_t)ab * nkc * A_CH;
                     for (int kc = 0; kc < nkc; kc++, ad += A_CH) {
-                        if (first) bar_wait(&a_full[kc], t & 1);
+                        if (first) bar_wait(&a_full[ab * nkc + kc], aph);
                         lap(2);
                         bar_wait(&b_full[st], ph);
                         tc_fence_after();
@@ -693,7 +698,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                         }
                         lap(4);
                         tc_commit(&b_empty[st]);
-                        if (lastu) tc_commit(&a_empty[kc]);   // the task's last use of A chunk kc
+                        if (lastu) tc_commit(&a_empty[ab * nkc + kc]);   // the task's last use of A chunk kc
                         lap(5);
                         if (++st == S) {
                             st = 0;
@@ -719,10 +724,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static size_t tc_smem(int K, int S, int H)
+static size_t tc_smem(int K, int S, int H, int AB)
 {
-    return (size_t)TC_R * H * K + (size_t)S * (TC_N / H) * TC_KC + sizeof(int) * 2 * TC_R * H + sizeof(int4) * 2 +
-           sizeof(uint64_t) * (8 + 2 * (K / TC_KC) + 2 * S) + 32;
+    return (size_t)AB * TC_R * H * K + (size_t)S * (TC_N / H) * TC_KC + sizeof(int) * 2 * TC_R * H + sizeof(int4) * 2 +
+           sizeof(uint64_t) * (8 + 2 * AB * (K / TC_KC) + 2 * S) + 32;
 }
 
 // row halves per task (PT_TC_H = 1 or 2, default 1); the caller's task list has 128 H rows
@@ -747,10 +752,13 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     const int K = nt * (int)v->E_pad;
     const size_t smem_limit = 227 * 1024 - 1024;   // margin for static shared memory
     const int H = a.halves;
-    // B ring: as many 64-byte K stages as fit beside the A buffer (up to 16)
+    // two A buffers when they fit beside a B ring of >= 4 stages (PT_TC_AB=1 forces one);
+    // then as many 64-byte K stages as fit (up to 16)
+    int AB = (getenv("PT_TC_AB") && atoi(getenv("PT_TC_AB")) == 1) ? 1 : 2;
+    if (AB == 2 && tc_smem(K, 4, H, 2) > smem_limit) AB = 1;
     int S = 16;
-    while (S > 2 && tc_smem(K, S, H) > smem_limit) S--;
-    if (tc_smem(K, S, H) > smem_limit) return PT_EINVAL;
+    while (S > 2 && tc_smem(K, S, H, AB) > smem_limit) S--;
+    if (tc_smem(K, S, H, AB) > smem_limit) return PT_EINVAL;
     // per-call operands (the thresholds follow tau)
     pt_view *mv = const_cast<pt_view *>(v);
     const int64_t n_cfg = pt_round_up(v->C + TC_N + 8, 8);
@@ -816,6 +824,7 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     p.m = m;
     p.K = K;
     p.S = S;
+    p.AB = AB;
     p.tasks = a.tasks;
     p.task_hi = a.tb;
     p.task_ctr = a.ctr;
@@ -827,7 +836,7 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     p.cand_n = a.cand_n;
     p.cap = a.cap;
     p.dbg = getenv("PT_TC_DBG") ? atoi(getenv("PT_TC_DBG")) : 0;
-    const size_t smem = tc_smem(K, S, H);
+    const size_t smem = tc_smem(K, S, H, AB);
     const int grid = std::min(ctx->num_sms, a.tb - a.ta);
     PT_CK(cudaEventRecord(ctx->ev0, s));
     if (H == 2) k_exh_tc<2><<<grid, TC_THREADS, smem, s>>>(p);
