@@ -402,9 +402,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     constexpr int BSUB = N * TC_KC;             // one 64-byte K chunk of a B tile
     constexpr int BST = BSUB;                   // one B stage
     constexpr int ACH = ROWS * TC_KC;           // one A chunk (all rows, 64 K bytes)
-    constexpr int WPT = 256 / ROWS;             // builder threads per row (2 or 1)
     extern __shared__ __align__(128) uint8_t smem[];
     const int K = p.K, S = p.S, AB = p.AB, nkc = K / TC_KC;
+    // builder groups: with H = 1 and two A buffers, two groups of 4 warps build alternate
+    // tasks (group g: tasks t = g mod 2, A buffer g), so each has two tasks' time per task
+    const int G = (H == 1 && AB == 2) ? 2 : 1;
     uint8_t *Abuf = smem;                                           // A [AB][nkc][ACH]
     uint8_t *Bbuf = smem + (size_t)AB * nkc * ACH;                  // B ring [S][BST]
     int *last = reinterpret_cast<int *>(Bbuf + (size_t)S * BST);    // [2][ROWS]
@@ -414,19 +416,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     uint64_t *a_full = bars + 8, *a_empty = a_full + AB * nkc;     // [AB][nkc] each
     uint64_t *b_full = a_empty + AB * nkc, *b_empty = b_full + S;
     uint32_t *tmem_s = reinterpret_cast<uint32_t *>(b_empty + S);
-    int *bcast = reinterpret_cast<int *>(tmem_s + 1);               // [2] + the prefetched next index
+    int *bcast = reinterpret_cast<int *>(tmem_s + 1);               // [2] + each group's prefetched next index
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (!p.cst->ok) return;   // tau unusable (k_tc_const flagged the search as not run)
     if (tid == 0) {
         for (int i = 0; i < 2; i++) {
-            bar_init(&t_full[i], TC_BLD_WARPS * 32);
+            bar_init(&t_full[i], TC_BLD_WARPS * 32 / G);
             bar_init(&t_empty[i], 1 + 1 + TC_EPI_WARPS);   // producer, MMA, epilogue warps
             bar_init(&acc_full[i], 1);
             bar_init(&acc_empty[i], TC_EPI_WARPS);
         }
         for (int c = 0; c < AB * nkc; c++) {
-            bar_init(&a_full[c], TC_BLD_WARPS * 32);
+            bar_init(&a_full[c], TC_BLD_WARPS * 32 / G);
             bar_init(&a_empty[c], 1);
         }
         for (int q = 0; q < S; q++) {
@@ -454,14 +456,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
         const float pthr = p.cst->pthr, u_dn = p.cst->u_dn, slk = p.cst->slack;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * quarter) << 16) + h * N;
         uint32_t tcnt = 0;
+        int done = 0;   // bit g: builder group g posted its last task
         for (int t = 0;; t++) {
             const int slot = t & 1;
+            if (done >> slot & 1) continue;
             bar_wait(&t_full[slot], (t >> 1) & 1);
             const int4 ti = tinfo[slot];
             const int lastr = last[slot * ROWS + r];
             __syncwarp();
             if (lane == 0) bar_arrive(&t_empty[slot]);
-            if (ti.x < 0) break;
+            if (ti.x < 0) {   // this builder group is done (with one group: every group)
+                done |= 1 << slot;
+                if (G == 1 || done == 3) break;
+                continue;
+            }
             const int64_t R = (int64_t)ti.x * TC_R + r;
             for (int u = ti.y; u < ti.z; u++, tcnt++) {
                 const int buf = tcnt & 1;
@@ -512,9 +520,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
         }
     } else if (warp < TC_EPI_WARPS + TC_BLD_WARPS) {
         // ---------------- A builders: thread = (row, share of each chunk) ----------------
-        const int bt = tid - TC_EPI_WARPS * 32;          // 0..255
-        const int row = bt % ROWS, part = bt / ROWS;     // H = 1: two threads per row (part 0/1)
-        const bool prof = (p.dbg & 32) && blockIdx.x == 0 && bt == 0;
+        const int nthr = TC_BLD_WARPS * 32 / G;                   // threads per group
+        const int g = (tid - TC_EPI_WARPS * 32) / nthr;           // this thread's group
+        const int bt = tid - TC_EPI_WARPS * 32 - g * nthr;        // thread within the group
+        const int row = bt % ROWS, part = bt / ROWS;               // part: the thread's share of a row
+        const int wpc = 2 * ROWS / nthr;                           // words of a chunk per thread (1 or 2)
+        const bool prof = (p.dbg & 32) && blockIdx.x == 0 && bt == 0 && g == 0;
         long long bc[6] = {0, 0, 0, 0, 0, 0};   // t_empty, fetch, unrank, loads, a_empty waits, stores
         long long b0 = clock64();
         auto blap = [&](int i) {
@@ -524,15 +535,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                 b0 = b1;
             }
         };
-        for (int t = 0;; t++) {
+        for (int n = 0;; n++) {
+            const int t = n * G + g;
             const int slot = t & 1;
             bar_wait(&t_empty[slot], ((t >> 1) & 1) ^ 1);
             blap(0);
             if (bt == 0) {   // this task's index was fetched one task ahead (off the critical path)
-                bcast[slot] = t == 0 ? atomicAdd(p.task_ctr, 1) : bcast[2];
-                bcast[2] = atomicAdd(p.task_ctr, 1);
+                bcast[slot] = n == 0 ? atomicAdd(p.task_ctr, 1) : bcast[2 + g];
+                bcast[2 + g] = atomicAdd(p.task_ctr, 1);
             }
-            named_sync(1, TC_BLD_WARPS * 32);
+            named_sync(1 + g, nthr);
             const int ti = bcast[slot];
             blap(1);
             if (ti >= p.task_hi) {
@@ -560,14 +572,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
             const uint32_t *r0 = p.A + (int64_t)mem[0] * W;
             const uint32_t *r1 = p.A + (int64_t)mem[m > 1 ? 1 : 0] * W;
             const uint32_t *r2 = p.A + (int64_t)mem[m > 2 ? 2 : 0] * W;
-            constexpr int WPC = 2 / WPT;                 // words of a chunk per thread
-            uint32_t wv[TC_KMAX / TC_KC][WPC];
+            uint32_t wv[TC_KMAX / TC_KC][2];
 #pragma unroll
             for (int c = 0; c < TC_KMAX / TC_KC; c++) {
                 if (c < nkc) {
 #pragma unroll
-                    for (int i = 0; i < WPC; i++) {
-                        const int wi = 2 * c + (WPC == 2 ? i : part);
+                    for (int i = 0; i < 2; i++) {
+                        if (i >= wpc) break;
+                        const int wi = 2 * c + (wpc == 2 ? i : part);
                         uint32_t x = __ldg(r0 + wi);
                         if (m > 1) x &= __ldg(r1 + wi);
                         if (m > 2) x &= __ldg(r2 + wi);
@@ -594,14 +606,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                 blap(4);
                 uint8_t *cd = dst + (size_t)(ab * nkc + c) * ACH;
 #pragma unroll
-                for (int i = 0; i < WPC && !(p.dbg & 8); i++) {
-                    const int piece = 2 * (WPC == 2 ? i : part);   // 16-byte K piece within the chunk
+                for (int i = 0; i < 2; i++) {
+                    if (i >= wpc || (p.dbg & 8)) break;
+                    const int piece = 2 * (wpc == 2 ? i : part);   // 16-byte K piece within the chunk
                     *reinterpret_cast<uint4 *>(cd + piece * (TC_R * 16)) = expand16(wv[c][i] & 0xffffu);
                     *reinterpret_cast<uint4 *>(cd + (piece + 1) * (TC_R * 16)) = expand16(wv[c][i] >> 16);
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
-                bar_arrive(&a_full[ab * nkc + c]);
+                if (AB == 1) {   // single buffer: hand each chunk over as soon as it is written
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+                    bar_arrive(&a_full[ab * nkc + c]);
+                }
                 blap(5);
+            }
+            if (AB == 2) {   // the buffer is built a task ahead: one proxy fence for all chunks
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                for (int c = 0; c < nkc; c++) bar_arrive(&a_full[ab * nkc + c]);
             }
         }
     } else if (warp == TC_PROD_WARP) {
@@ -610,12 +629,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
             int st = 0;
             uint32_t ph = 0;   // ring position and the phase parity of its current lap
             const int64_t kstride = p.n_grp * (8 * TC_KC);
+            int done = 0;   // bit g: builder group g posted its last task
             for (int t = 0;; t++) {
                 const int slot = t & 1;
+                if (done >> slot & 1) continue;
                 bar_wait(&t_full[slot], (t >> 1) & 1);
                 const int4 ti = tinfo[slot];
                 bar_arrive(&t_empty[slot]);
-                if (ti.x < 0) break;
+                if (ti.x < 0) {
+                    done |= 1 << slot;
+                    if (G == 1 || done == 3) break;
+                    continue;
+                }
                 for (int u = ti.y; u < ti.z; u++) {
                     const int64_t col0 = (int64_t)ti.w + (int64_t)u * N;
                     const int n_eff = (int)min((int64_t)N, (p.C - col0 + 15) & ~(int64_t)15);
@@ -662,13 +687,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                     c0 = c1;
                 }
             };
+            int done = 0;   // bit g: builder group g posted its last task
             for (int t = 0;; t++) {
                 const int slot = t & 1;
+                if (done >> slot & 1) continue;
                 bar_wait(&t_full[slot], (t >> 1) & 1);
                 lap(0);
                 const int4 ti = tinfo[slot];
                 bar_arrive(&t_empty[slot]);
-                if (ti.x < 0) break;
+                if (ti.x < 0) {
+                    done |= 1 << slot;
+                    if (G == 1 || done == 3) break;
+                    continue;
+                }
                 for (int u = ti.y; u < ti.z; u++, tcnt++) {
                     const int buf = tcnt & 1;
                     const int64_t col0 = (int64_t)ti.w + (int64_t)u * N;
@@ -727,7 +758,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 static size_t tc_smem(int K, int S, int H, int AB)
 {
     return (size_t)AB * TC_R * H * K + (size_t)S * (TC_N / H) * TC_KC + sizeof(int) * 2 * TC_R * H + sizeof(int4) * 2 +
-           sizeof(uint64_t) * (8 + 2 * AB * (K / TC_KC) + 2 * S) + 32;
+           sizeof(uint64_t) * (8 + 2 * AB * (K / TC_KC) + 2 * S) + 48;
 }
 
 // row halves per task (PT_TC_H = 1 or 2, default 1); the caller's task list has 128 H rows
@@ -837,7 +868,10 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     p.cap = a.cap;
     p.dbg = getenv("PT_TC_DBG") ? atoi(getenv("PT_TC_DBG")) : 0;
     const size_t smem = tc_smem(K, S, H, AB);
-    const int grid = std::min(ctx->num_sms, a.tb - a.ta);
+    // an empty shard still runs (one CTA that finds no task): whether the tc tier answers or
+    // falls back is decided on the device from tau, identically on every rank, and all
+    // ranks must scan the same tier's task list
+    const int grid = std::max(1, std::min(ctx->num_sms, a.tb - a.ta));
     PT_CK(cudaEventRecord(ctx->ev0, s));
     if (H == 2) k_exh_tc<2><<<grid, TC_THREADS, smem, s>>>(p);
     else k_exh_tc<1><<<grid, TC_THREADS, smem, s>>>(p);
