@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(256) k_swap_tau(const double *__restrict__ l64
             if (in) continue;
             const double *mr = M + (int64_t)a * E_pad, *col = l64 + b * E_pad;
             double acc = 0.0;
-            for (int64_t e = lane; e < E_pad; e += 32) acc += fmin(mr[e], col[e]);
+#pragma unroll 8
+            for (int64_t e = lane; e < E_pad; e += 32) acc += fmin(mr[e], __ldg(col + e));   // loads in flight
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (acc < bs) {
                 bs = acc;
@@ -304,29 +305,23 @@ __global__ void k_tc_const(const double *__restrict__ tau_dev, int64_t E, int64_
 
 // the bit operands, k = j E_pad + e, bit = [l[c][e] >= (j+1) u] for real configs and
 // environments (0 elsewhere): tcA[c][k/32] packed bits (the builders AND and expand them),
-// tcB bytes (E4M3 1.0 = 0x38) in the B-stage layout.  Thread = (config, 32-bit word).
+// tcB bytes (E4M3 1.0 = 0x38) in the B-stage layout.  Thread = (config, k): a warp holds 32
+// consecutive k of one threshold (E_pad % 64 == 0), its ballot is the packed word.
 __global__ void __launch_bounds__(256) k_tc_build(const double *__restrict__ l64, int64_t C, int64_t E, int64_t E_pad,
                                                  int K, int64_t n_cfg, const TcConst *__restrict__ cst,
                                                  uint32_t *__restrict__ A, uint8_t *__restrict__ B)
 {
-    const int W = K / 32;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_cfg * W) return;
-    const int64_t c = i / W;
-    const int w = (int)(i - c * W);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // n_cfg K is a multiple of 32
+    const int64_t c = i / K;
+    const int k = (int)(i - c * K);
+    const int j = k / (int)E_pad, e = k - j * (int)E_pad;
+    const bool on = i < n_cfg * K && cst->ok && c < C && e < E && l64[c * E_pad + e] >= (double)(j + 1) * cst->u;
+    const uint32_t word = __ballot_sync(0xffffffffu, on);
+    if (i >= n_cfg * K) return;
+    if ((threadIdx.x & 31) == 0) A[i >> 5] = word;
     const int64_t n_grp = n_cfg / 8;
-    const bool ok = cst->ok && c < C;
-    const double u = cst->u;
-    uint32_t bits = 0;
-    for (int b = 0; b < 32; b++) {
-        const int k = 32 * w + b;
-        const int j = k / (int)E_pad, e = k - j * (int)E_pad;
-        const bool on = ok && e < E && l64[c * E_pad + e] >= (double)(j + 1) * u;
-        bits |= (uint32_t)on << b;
-        const int kc = k / TC_KC, kk = k % TC_KC;
-        B[((int64_t)kc * n_grp + c / 8) * (8 * TC_KC) + (kk / 16) * 128 + (c % 8) * 16 + kk % 16] = on ? 0x38 : 0;
-    }
-    A[i] = bits;
+    const int kc = k / TC_KC, kk = k % TC_KC;
+    B[((int64_t)kc * n_grp + c / 8) * (8 * TC_KC) + (kk / 16) * 128 + (c % 8) * 16 + kk % 16] = on ? 0x38 : 0;
 }
 
 // 8 packed bits -> 8 bytes of E4M3 (1.0 = 0x38 where the bit is set): per nibble, the
@@ -843,7 +838,7 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     const unsigned gmax = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ne + 255) / 256, 4L * ctx->num_sms));
     k_tc_lmax<<<gmax, 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, cst);
     k_tc_const<<<1, 1, 0, s>>>(tau_dev, v->E, v->E_pad, alpha, cst, a.U, a.cand_n);
-    const int64_t nb = n_cfg * (K / 32);
+    const int64_t nb = n_cfg * K;
     k_tc_build<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(v->l64, v->C, v->E, v->E_pad, K, n_cfg, cst,
                                                              (uint32_t *)mv->tcA, mv->tcB);
     ctx->stats.launches += 4;

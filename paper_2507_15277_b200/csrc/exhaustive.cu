@@ -1672,7 +1672,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         PT_CK(cudaGetLastError());
         // refine + top-2 run on the device-side survivor count (no host round trip);
         // one synchronisation returns the count, U and the exact top-2
-        k_exh_refine_top2<<<(unsigned)(ctx->num_sms * 2), 256, 0, s>>>(ckey, cq, cn, cap, tau_pass, U, m, v->C,
+        // (the tc tier leaves a few thousand survivors: fewer blocks, a shorter final merge)
+        k_exh_refine_top2<<<(unsigned)(tc_launched ? 64 : ctx->num_sms * 2), 256, 0, s>>>(ckey, cq, cn, cap, tau_pass, U, m, v->C,
                                                                         v->l64, v->E_pad, blk, done, os, ot);
         ctx->stats.launches++;
         mark("launched");

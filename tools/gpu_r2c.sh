@@ -1,6 +1,6 @@
 # round-2 measurement set after the tc tier: tests, bench, reference arm, launch list,
 # k_exh_tc full capture, MMA-thread phase profile, memcheck of the tc path
-mkdir -p gpurun_out/r02c
+mkdir -p gpurun_out/r02c  # (r02d: same commands, output dir r02d)
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02c/pytest_gpu.txt 2>&1
 timeout 900 python bench.py > gpurun_out/r02c/bench.txt 2>&1
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r02c/bench_reference.txt 2>&1
