@@ -137,13 +137,20 @@ pt_status pt_greedy_select(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int3
  *   out_s          host double[2] or NULL: the exact fp64 log-slowdown sums
  *                  s = -|scope| log G of best and runner-up (+inf if absent) --
  *                  the keys pt_merge_top2 orders by.
- * Method (k = 2..4, scopes <= 768 envs): a filter scores every set -- by default
- * the exact integer score of the matrix quantised to bytes (q = rint(l / Delta),
- * Delta = scope max / 255), else fp16 -- keeps every set whose rigorous lower
- * bound reaches the best two, and re-scores those in fp64; the result is the
- * same as scoring every set in fp64.
+ * Method (k = 2..4, scopes <= 768 envs): a filter scores every set, keeps every
+ * set whose rigorous lower bound reaches the best two, and re-scores those in
+ * fp64; the result is the same as scoring every set in fp64.  Filters: for k = 3, 4
+ * (and k = 2 with environment PT_EXH_TIER=tc) the threshold-count lower bound on
+ * the tcgen05 tensor cores against tau from a device-side swap search (DESIGN.md
+ * 6.2c); for k = 2, and whenever that filter cannot run (tau not usable, more than
+ * 2^20 survivors unsharded, > 1024 padded envs), the exact integer score of the
+ * matrix quantised to bytes (q = rint(l / Delta), Delta = scope max / 255,
+ * DESIGN.md 6.2b); PT_EXH_TIER=u8 / fp16 select those tiers.  Sharded searches
+ * choose the tier identically on every rank (tau is computed from the whole scope)
+ * and rerun a tc pass with a larger buffer rather than fall back, so all ranks
+ * scan the same task list.
  * Errors: PT_EINVAL (k < 1, k > C, bad shard), PT_ECAP (C(n,k) > 1e13, or more
- *         than 2^28 fp16-tier survivors), PT_EEMPTY.
+ *         than 2^28 fp16-tier or tc-shard survivors), PT_EEMPTY.
  */
 pt_status pt_exhaustive_best(pt_ctx *ctx, int32_t k, const uint8_t *env_mask, int32_t objective,
                              int32_t shard_rank, int32_t shard_count,
@@ -362,8 +369,8 @@ typedef struct {
     int64_t exh_candidates;  /* filter-tier candidates re-scored in fp64 */
     int32_t exh_passes;      /* 1; +1 per candidate-buffer overflow rerun or u8 -> fp16 hand-over */
     int32_t exh_kernel;      /* 5 = tiled threshold-count filter on tcgen05 (k_exh_tc, the default
-                                for k = 2..4), 4 = tiled u8 filter (k_exh_q8; PT_EXH_TIER=u8, or
-                                the fall-back of the tc tier), 0 = tiled fp16 filter (k_exh_tiled;
+                                for k = 3, 4), 4 = tiled u8 filter (k_exh_q8; k = 2, PT_EXH_TIER=u8,
+                                or the fall-back of the tc tier), 0 = tiled fp16 filter (k_exh_tiled;
                                 PT_EXH_TIER=fp16, or the u8 tier left more than 2^24 candidates),
                                 1 = generic fp64, 2 = fleet fp64, 3 = fleet tiled fp16 */
     double greedy_ms;        /* CUDA-event time of the last greedy selection */
