@@ -54,6 +54,8 @@ namespace cgt = cooperative_groups;
 #define TC_KC 64        // K bytes per B stage
 #define TC_KMAX 1024    // widest K (nt E_pad): the A buffer (128 K bytes) + a ring of >= 4 B stages
 #define TC_THREADS 576
+#define TC_FAM2 (1 << 30)   // tinfo.w: family-2 task (columns a < b, lo = 0)
+#define TC_LOMASK (TC_FAM2 - 1)
 
 namespace {
 
@@ -359,6 +361,8 @@ __device__ __forceinline__ uint4 expand16(uint32_t bits16)
 struct TcParams {
     int64_t C, n_rows, n_grp;
     int m, K, S, AB;   // S = B stages, AB = A buffers (1 or 2)
+    int split;         // k = 3 two-family task list: task .w = family (1: rows (a,b) b < h, 2: rows (b,c) b >= h)
+    int64_t n_rows2;   // family-2 rows (the family-1 row count is n_rows)
     const int4 *tasks;
     int task_hi;
     int *task_ctr;
@@ -404,8 +408,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
     const int G = (H == 1 && AB == 2) ? 2 : 1;
     uint8_t *Abuf = smem;                                           // A [AB][nkc][ACH]
     uint8_t *Bbuf = smem + (size_t)AB * nkc * ACH;                  // B ring [S][BST]
-    int *last = reinterpret_cast<int *>(Bbuf + (size_t)S * BST);    // [2][ROWS]
-    int4 *tinfo = reinterpret_cast<int4 *>(last + 2 * ROWS);        // [2] (first row / 128, u0, u1, lo)
+    int4 *tinfo = reinterpret_cast<int4 *>(Bbuf + (size_t)S * BST);   // [2] (first row / 128, u0, u1, lo | family)
     uint64_t *bars = reinterpret_cast<uint64_t *>(tinfo + 2);
     uint64_t *t_full = bars, *t_empty = bars + 2, *acc_full = bars + 4, *acc_empty = bars + 6;
     uint64_t *a_full = bars + 8, *a_empty = a_full + AB * nkc;     // [AB][nkc] each
@@ -457,7 +460,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
             if (done >> slot & 1) continue;
             bar_wait(&t_full[slot], (t >> 1) & 1);
             const int4 ti = tinfo[slot];
-            const int lastr = last[slot * ROWS + r];
             __syncwarp();
             if (lane == 0) bar_arrive(&t_empty[slot]);
             if (ti.x < 0) {   // this builder group is done (with one group: every group)
@@ -466,9 +468,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                 continue;
             }
             const int64_t R = (int64_t)ti.x * TC_R + r;
+            // the row's own members (decoded here: no per-row smem table).  Family 1 (and
+            // the single decomposition): columns l in (lastr, C), key (R, l).  Family 2: row
+            // (bb, cc), columns a in [0, bb), key (colex rank of (a, bb), cc).
+            const bool fam2 = (ti.w & TC_FAM2) != 0;
+            int lastr = 0x7fffffff, bb = 0, cc = 0;
+            if (R < (fam2 ? p.n_rows2 : p.n_rows)) {
+                int32_t mem[PT_MAXK];
+                unrank_fast(R, m, p.C, mem);
+                if (fam2) {
+                    bb = (int)(p.C - 1 - mem[1]);
+                    cc = (int)(p.C - 1 - mem[0]);
+                } else {
+                    lastr = mem[m - 1];
+                }
+            }
+            const int64_t cmin = fam2 ? -1 : lastr, cend = fam2 ? bb : p.C;   // valid: cmin < l < cend
             for (int u = ti.y; u < ti.z; u++, tcnt++) {
                 const int buf = tcnt & 1;
-                const int64_t col0 = (int64_t)ti.w + (int64_t)u * N;
+                const int64_t col0 = (int64_t)(ti.w & TC_LOMASK) + (int64_t)u * N;
                 const int ncols = (int)min((int64_t)N, p.C - col0);
                 bar_wait(&acc_full[buf], (tcnt >> 1) & 1);
                 tc_fence_after();
@@ -478,14 +496,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                     tc_ld32(lane_base + buf * 256 + q * 32, v);
                     const int64_t cb = col0 + q * 32;
                     float w[16];
-                    if (cb > lastr && cb + 31 < p.C) {   // every column valid: a 32-wide min tree
+                    if (cb > cmin && cb + 31 < cend) {   // every column valid: a 32-wide min tree
 #pragma unroll
                         for (int j = 0; j < 16; j++) w[j] = fminf(__uint_as_float(v[j]), __uint_as_float(v[j + 16]));
-                    } else {                             // row start / matrix end: mask first
+                    } else {                             // row start / range end: mask first
 #pragma unroll
                         for (int j = 0; j < 16; j++) {
-                            const float a = (cb + j > lastr && cb + j < p.C) ? __uint_as_float(v[j]) : INFINITY;
-                            const float b = (cb + j + 16 > lastr && cb + j + 16 < p.C) ? __uint_as_float(v[j + 16]) : INFINITY;
+                            const float a = (cb + j > cmin && cb + j < cend) ? __uint_as_float(v[j]) : INFINITY;
+                            const float b = (cb + j + 16 > cmin && cb + j + 16 < cend) ? __uint_as_float(v[j + 16]) : INFINITY;
                             w[j] = fminf(a, b);
                         }
                     }
@@ -498,10 +516,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                         for (int j = 0; j < 32; j++) {
                             const float P = __uint_as_float(v[j]);
                             const int64_t l = cb + j;
-                            if (P <= pthr && l > lastr && l < p.C) {
+                            if (P <= pthr && l > cmin && l < cend) {
                                 const unsigned long long idx = atomicAdd(p.cand_n, 1ull);
                                 if (idx < p.cap) {
-                                    p.cand_key[idx] = ((unsigned long long)R << KEY_BITS) | (unsigned long long)l;
+                                    // family 2: the set {l, bb, cc} as (colex rank of (l, bb), cc)
+                                    const unsigned long long rk = fam2 ? (unsigned long long)bb * (bb - 1) / 2 + l
+                                                                       : (unsigned long long)R;
+                                    const unsigned long long col = fam2 ? (unsigned long long)cc : (unsigned long long)l;
+                                    p.cand_key[idx] = (rk << KEY_BITS) | col;
                                     p.cand_s[idx] = __fmaf_rd(P, u_dn, -slk);
                                 }
                             }
@@ -551,14 +573,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                 break;
             }
             const int4 tk = p.tasks[ti];
+            const bool fam2 = p.split && tk.w == 2;
             const int64_t R0 = (int64_t)tk.x * ROWS;
             const int64_t R = R0 + row;
-            const bool valid = R < p.n_rows;
+            const bool valid = R < (fam2 ? p.n_rows2 : p.n_rows);
             int32_t mem[PT_MAXK];
             if (valid) unrank_fast(R, m, p.C, mem);
             else for (int u = 0; u < m; u++) mem[u] = 0;
-            if (bt == 0) tinfo[slot] = make_int4((int)(R0 / TC_R), tk.y, tk.z, (int)tile_lo(mem[m - 1]));   // row 0 = R0
-            if (part == 0) last[slot * ROWS + row] = valid ? mem[m - 1] : 0x7fffffff;
+            if (bt == 0)   // row 0 = R0; family 2 starts at column 0
+                tinfo[slot] = make_int4((int)(R0 / TC_R), tk.y, tk.z, fam2 ? TC_FAM2 : (int)tile_lo(mem[m - 1]));
+            if (fam2 && valid) {   // rows (x, y) stand for the pair (b, c) = (C-1-y, C-1-x)
+                const int32_t x = mem[0];
+                mem[0] = (int32_t)(p.C - 1 - mem[1]);
+                mem[1] = (int32_t)(p.C - 1 - x);
+            }
             bar_arrive(&t_full[slot]);
             blap(2);
             // the row's packed bits: per chunk c, words 2c and 2c+1 (H = 2: this thread both;
@@ -637,7 +665,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                     continue;
                 }
                 for (int u = ti.y; u < ti.z; u++) {
-                    const int64_t col0 = (int64_t)ti.w + (int64_t)u * N;
+                    const int64_t col0 = (int64_t)(ti.w & TC_LOMASK) + (int64_t)u * N;
                     const int n_eff = (int)min((int64_t)N, (p.C - col0 + 15) & ~(int64_t)15);
                     const uint32_t bytes = (uint32_t)n_eff * TC_KC;
                     const uint8_t *src = p.B + (col0 >> 3) * (8 * TC_KC);
@@ -697,7 +725,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                 }
                 for (int u = ti.y; u < ti.z; u++, tcnt++) {
                     const int buf = tcnt & 1;
-                    const int64_t col0 = (int64_t)ti.w + (int64_t)u * N;
+                    const int64_t col0 = (int64_t)(ti.w & TC_LOMASK) + (int64_t)u * N;
                     const int n_eff = (int)min((int64_t)N, (p.C - col0 + 15) & ~(int64_t)15);
                     const uint32_t idesc = (1u << 4) | ((uint32_t)(n_eff >> 3) << 17) | ((uint32_t)(TC_R >> 4) << 24);
                     const bool first = u == ti.y, lastu = u == ti.z - 1;
@@ -752,7 +780,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
 // ---------------------------------------------------------------------------
 static size_t tc_smem(int K, int S, int H, int AB)
 {
-    return (size_t)AB * TC_R * H * K + (size_t)S * (TC_N / H) * TC_KC + sizeof(int) * 2 * TC_R * H + sizeof(int4) * 2 +
+    return (size_t)AB * TC_R * H * K + (size_t)S * (TC_N / H) * TC_KC + sizeof(int4) * 2 +
            sizeof(uint64_t) * (8 + 2 * AB * (K / TC_KC) + 2 * S) + 48;
 }
 
@@ -845,12 +873,14 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     PT_CK(cudaGetLastError());
     TcParams p;
     p.C = v->C;
-    p.n_rows = pt_binom(v->C, m);
+    p.n_rows = a.split ? pt_binom(v->C / 2, 2) : pt_binom(v->C, m);   // (split: the family-1 rows)
     p.n_grp = n_cfg / 8;
     p.m = m;
     p.K = K;
     p.S = S;
     p.AB = AB;
+    p.split = a.split ? 1 : 0;
+    p.n_rows2 = a.split ? pt_binom(v->C - v->C / 2, 2) : 0;
     p.tasks = a.tasks;
     p.task_hi = a.tb;
     p.task_ctr = a.ctr;

@@ -228,6 +228,83 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, int
     return PT_OK;
 }
 
+// The tc tier's k = 3 list, split by the middle member b at h = C / 2 so that every task
+// has many columns (its A operand -- 128 rows x K -- is then amortised over >= C/2
+// columns; with one decomposition half of the tasks had one or two 256-column tiles and
+// the tensor core waited for their A hand-overs):
+//   family 1: rows (a, b) with b < h in colex order, columns c > b      (as build_tasks)
+//   family 2: rows (b, c) with b >= h, columns a < b; rows enumerated as the colex pairs
+//             (x, y) = (C-1-c, C-1-b) with y < C - h (b descending, c descending)
+// Every 3-set is in exactly one family.  int4 = (row tile, 0, n_ct, family), the tasks
+// sorted by decreasing size (stable: row-tile order among equals).
+static pt_status build_tasks_split3(pt_ctx *ctx, const pt_view *v, int rows, int cols, pt_tasks **out)
+{
+    static std::mutex mu;
+    static std::map<std::tuple<int, int64_t, int, int>, pt_tasks *> cache;
+    std::lock_guard<std::mutex> g(mu);
+    const auto key = std::make_tuple(ctx->dev, v->C, rows, cols);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return PT_OK;
+    }
+    const int64_t C = v->C, h = C / 2;
+    struct Tk { int4 t; int64_t slots, sets; };
+    std::vector<Tk> all;
+    // family 1
+    const int64_t n1 = pt_binom(h, 2);
+    for (int64_t t = 0; t * rows < n1; t++) {
+        const int64_t R0 = t * rows, R1 = std::min(n1, R0 + rows);
+        int32_t mem[2];
+        pt_unrank_colex(R0, 2, C, mem);
+        const int64_t lo = tile_lo(mem[1]);
+        const int64_t n_ct = (C - lo + cols - 1) / cols;
+        int64_t useful = 0;
+        for (int64_t R = R0; R < R1; R++) {
+            pt_unrank_colex(R, 2, C, mem);
+            useful += C - 1 - mem[1];
+        }
+        all.push_back({make_int4((int)t, 0, (int)n_ct, 1), n_ct * rows * cols, useful});
+    }
+    // family 2
+    const int64_t n2 = pt_binom(C - h, 2);
+    for (int64_t t = 0; t * rows < n2; t++) {
+        const int64_t R0 = t * rows, R1 = std::min(n2, R0 + rows);
+        int32_t mem[2];
+        pt_unrank_colex(R0, 2, C, mem);
+        const int64_t bmax = C - 1 - mem[1];      // the first row has the smallest y: the largest b
+        const int64_t n_ct = (bmax + cols - 1) / cols;
+        int64_t useful = 0;
+        for (int64_t R = R0; R < R1; R++) {
+            pt_unrank_colex(R, 2, C, mem);
+            useful += C - 1 - mem[1];            // b = C-1-y columns a < b
+        }
+        all.push_back({make_int4((int)t, 0, (int)n_ct, 2), n_ct * rows * cols, useful});
+    }
+    std::stable_sort(all.begin(), all.end(), [](const Tk &x, const Tk &y) { return x.t.z > y.t.z; });
+    pt_tasks *T = new pt_tasks();
+    T->m = 2;
+    T->C = C;
+    T->slot_pre.push_back(0);
+    T->set_pre.push_back(0);
+    for (const Tk &x : all) {
+        T->h.push_back(x.t);
+        T->slot_pre.push_back(T->slot_pre.back() + x.slots);
+        T->set_pre.push_back(T->set_pre.back() + x.sets);
+    }
+    if (!T->h.empty()) {
+        if (cudaMalloc(&T->d, sizeof(int4) * T->h.size()) != cudaSuccess) {
+            cudaGetLastError();
+            delete T;
+            return pt_fail(PT_ENOMEM, "task list allocation failed");
+        }
+        cudaMemcpy(T->d, T->h.data(), sizeof(int4) * T->h.size(), cudaMemcpyHostToDevice);
+    }
+    cache[key] = T;
+    *out = T;
+    return PT_OK;
+}
+
 // ---------------------------------------------------------------------------
 // PTX helpers: mbarrier + TMA
 // ---------------------------------------------------------------------------
@@ -1473,10 +1550,15 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
     int tc_ta = 0, tc_tb = 0;
     int64_t tc_sets = 0, tc_slots = 0;
     int tc_halves = 2;
+    bool tc_split = false;
     if (tc) {
         pt_tasks *TT = nullptr;
         tc_halves = pt_tc_halves();
-        PT_TRY(build_tasks(ctx, v, m, XT_R * tc_halves, 256 / tc_halves, &TT));
+        // k = 3 (H = 1): the two-family list (PT_TC_SPLIT=0 keeps the single decomposition)
+        tc_split = m == 2 && tc_halves == 1 && v->C >= 4 &&
+                   !(getenv("PT_TC_SPLIT") && !strcmp(getenv("PT_TC_SPLIT"), "0"));
+        if (tc_split) PT_TRY(build_tasks_split3(ctx, v, XT_R, 256, &TT));
+        else PT_TRY(build_tasks(ctx, v, m, XT_R * tc_halves, 256 / tc_halves, &TT));
         tc_list = TT->d;
         tc_tb = (int)TT->h.size();
         tc_sets = TT->set_pre.back();
@@ -1588,6 +1670,7 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
             a.swap_rw = (long long *)(b + o_rw);
             a.tau_dev = (double *)(b + o_tau);
             a.halves = tc_halves;
+            a.split = tc_split;
             mark("pre-launch");
             int nt = 0;
             const pt_status st = pt_exh_tc_enqueue(ctx, v, a, &nt);

@@ -228,6 +228,7 @@ struct pt_tc_args {
     long long *swap_rw = nullptr;      // [2 num_sms] scratch
     double *tau_dev = nullptr;         // [1] scratch
     int halves = 2;                    // row halves per task: 128 halves rows x (256 / halves) columns
+    bool split = false;                // k = 3 two-family task list (exhaustive.cu build_tasks_split3)
 };
 pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, int *nt_out);
 int pt_tc_halves();
