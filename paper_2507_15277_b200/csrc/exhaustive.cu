@@ -1555,9 +1555,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         pt_tasks *TT = nullptr;
         tc_halves = pt_tc_halves();
         // k = 3 (H = 1): the two-family list (PT_TC_SPLIT=0 keeps the single decomposition)
-        tc_split = m == 2 && tc_halves == 1 && v->C >= 4 &&
-                   !(getenv("PT_TC_SPLIT") && !strcmp(getenv("PT_TC_SPLIT"), "0"));
-        if (tc_split) PT_TRY(build_tasks_split3(ctx, v, XT_R, 256, &TT));
+        tc_split = m == 2 && v->C >= 4 && !(getenv("PT_TC_SPLIT") && !strcmp(getenv("PT_TC_SPLIT"), "0"));
+        if (tc_split) PT_TRY(build_tasks_split3(ctx, v, XT_R * tc_halves, 256 / tc_halves, &TT));
         else PT_TRY(build_tasks(ctx, v, m, XT_R * tc_halves, 256 / tc_halves, &TT));
         tc_list = TT->d;
         tc_tb = (int)TT->h.size();
