@@ -854,7 +854,7 @@ pt_status pt_exh_tc_enqueue(pt_ctx *ctx, const pt_view *v, const pt_tc_args &a, 
     {
         const double *l64 = v->l64;
         int64_t CC = v->C, EE = v->E_pad;
-        int kk = a.k, iters = 16;
+        int kk = a.k, iters = getenv("PT_TC_SWAP_ITERS") ? std::max(1, atoi(getenv("PT_TC_SWAP_ITERS"))) : 16;
         const int32_t *S0 = a.d_S0;
         const double *seed = a.d_seed_s2;
         void *args[] = {(void *)&l64, (void *)&CC, (void *)&EE, (void *)&kk, (void *)&S0, (void *)&seed,
