@@ -373,8 +373,10 @@ struct TcParams {
     float *cand_s;
     unsigned long long *cand_n;
     unsigned cap;
-    int dbg;   // development knob PT_TC_DBG (bit 0: the epilogue skips its TMEM reads, 1: no MMAs,
-               // 3: the builders skip their shared-memory stores, 4: no B copies)
+    int dbg;   // development knob PT_TC_DBG, diagnostics only -- results may be wrong with bits
+               // 0-4, 6 set (bit 0: the epilogue skips its TMEM reads, 1: no MMAs, 2: the MMA
+               // thread does not wait for A, 3: the builders skip their stores, 4: no B copies,
+               // 5: clock64 phase profile of CTA 0, 6: no tcgen05 fence after the B wait)
 };
 
 // warp roles (TC_THREADS = 18 warps)
@@ -737,10 +739,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                     const uint32_t aph = (uint32_t)((AB == 2 ? t >> 1 : t) & 1);
                     uint64_t ad = adesc0 + (uint64_t)ab * nkc * A_CH;
                     for (int kc = 0; kc < nkc; kc++, ad += A_CH) {
-                        if (first) bar_wait(&a_full[ab * nkc + kc], aph);
+                        if (first && !(p.dbg & 4)) bar_wait(&a_full[ab * nkc + kc], aph);   // (bit 2: diagnostics only)
                         lap(2);
                         bar_wait(&b_full[st], ph);
-                        tc_fence_after();
+                        if (!(p.dbg & 64)) tc_fence_after();   // (bit 6: diagnostics only)
                         lap(3);
                         const uint64_t bd = bdesc0 + (uint64_t)st * B_ST;
                         if (!(p.dbg & 2)) {
