@@ -237,12 +237,15 @@ static pt_status build_tasks(pt_ctx *ctx, const pt_view *v, int m, int rows, int
 //             (x, y) = (C-1-c, C-1-b) with y < C - h (b descending, c descending)
 // Every 3-set is in exactly one family.  int4 = (row tile, 0, n_ct, family), the tasks
 // sorted by decreasing size (stable: row-tile order among equals).
-static pt_status build_tasks_split3(pt_ctx *ctx, const pt_view *v, int rows, int cols, pt_tasks **out)
+// pieces > 1 (sharded searches): every task's column tiles are cut into up to `pieces`
+// runs of consecutive tiles (each run rebuilds the row tile's A), so a shard's dynamic
+// queue ends on short runs instead of whole 4-7-tile tasks
+static pt_status build_tasks_split3(pt_ctx *ctx, const pt_view *v, int rows, int cols, int pieces, pt_tasks **out)
 {
     static std::mutex mu;
-    static std::map<std::tuple<int, int64_t, int, int>, pt_tasks *> cache;
+    static std::map<std::tuple<int, int64_t, int, int, int>, pt_tasks *> cache;
     std::lock_guard<std::mutex> g(mu);
-    const auto key = std::make_tuple(ctx->dev, v->C, rows, cols);
+    const auto key = std::make_tuple(ctx->dev, v->C, rows, cols, pieces);
     auto it = cache.find(key);
     if (it != cache.end()) {
         *out = it->second;
@@ -281,7 +284,23 @@ static pt_status build_tasks_split3(pt_ctx *ctx, const pt_view *v, int rows, int
         }
         all.push_back({make_int4((int)t, 0, (int)n_ct, 2), n_ct * rows * cols, useful});
     }
-    std::stable_sort(all.begin(), all.end(), [](const Tk &x, const Tk &y) { return x.t.z > y.t.z; });
+    if (pieces > 1) {   // cut each task's column tiles into runs; useful sets pro rata by slots
+        std::vector<Tk> cut;
+        for (const Tk &x : all) {
+            const int n = x.t.z, np = std::min(pieces, n);
+            int64_t sets_left = x.sets;
+            for (int q = 0, u0 = 0; q < np; q++) {
+                const int u1 = (int)((int64_t)n * (q + 1) / np);
+                const int64_t se = q == np - 1 ? sets_left : x.sets * (u1 - u0) / n;
+                sets_left -= se;
+                cut.push_back({make_int4(x.t.x, u0, u1, x.t.w), (int64_t)(u1 - u0) * rows * cols, se});
+                u0 = u1;
+            }
+        }
+        all.swap(cut);
+    }
+    std::stable_sort(all.begin(), all.end(),
+                     [](const Tk &x, const Tk &y) { return x.t.z - x.t.y > y.t.z - y.t.y; });
     pt_tasks *T = new pt_tasks();
     T->m = 2;
     T->C = C;
@@ -1556,7 +1575,8 @@ static pt_status run_tiled(pt_ctx *ctx, const pt_view *v, int k, int32_t shard_r
         tc_halves = pt_tc_halves();
         // k = 3 (H = 1): the two-family list (PT_TC_SPLIT=0 keeps the single decomposition)
         tc_split = m == 2 && v->C >= 4 && !(getenv("PT_TC_SPLIT") && !strcmp(getenv("PT_TC_SPLIT"), "0"));
-        if (tc_split) PT_TRY(build_tasks_split3(ctx, v, XT_R * tc_halves, 256 / tc_halves, &TT));
+        if (tc_split)
+            PT_TRY(build_tasks_split3(ctx, v, XT_R * tc_halves, 256 / tc_halves, shard_count >= 4 ? 2 : 1, &TT));
         else PT_TRY(build_tasks(ctx, v, m, XT_R * tc_halves, 256 / tc_halves, &TT));
         tc_list = TT->d;
         tc_tb = (int)TT->h.size();
