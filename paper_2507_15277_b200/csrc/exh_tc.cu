@@ -54,6 +54,12 @@ namespace cgt = cooperative_groups;
 #define TC_KC 64        // K bytes per B stage
 #define TC_KMAX 1024    // widest K (nt E_pad): the A buffer (128 K bytes) + a ring of >= 4 B stages
 #define TC_THREADS 576
+// TC_DIAG=1 (build flag) compiles the PT_TC_DBG ablations and the clock64 phase profile
+// into the MMA thread's loop; without it that loop carries none of their branches (the
+// single issuing thread is latency-bound: two extra branches per K chunk cost 4 %)
+#ifndef TC_DIAG
+#define TC_DIAG 0
+#endif
 #define TC_FAM2 (1 << 30)   // tinfo.w: family-2 task (columns a < b, lo = 0)
 #define TC_LOMASK (TC_FAM2 - 1)
 
@@ -702,7 +708,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
             constexpr uint64_t A_K32 = (uint64_t)2 * TC_R * 16 >> 4;     // 32 bytes of K in A
             constexpr uint64_t B_ST = (uint64_t)BST >> 4;                // one B stage
             constexpr uint64_t B_K32 = 256 >> 4;                         // 32 bytes of K in B
-            const bool prof = (p.dbg & 32) && blockIdx.x == 0;
+            const bool prof = TC_DIAG && (p.dbg & 32) && blockIdx.x == 0;
+            const int dbg = TC_DIAG ? p.dbg : 0;
             long long cyc[6] = {0, 0, 0, 0, 0, 0};   // t_full, acc_empty, a_full, b_full, mma, commit
             long long c0 = clock64();
             auto lap = [&](int i) {
@@ -739,13 +746,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                     const uint32_t aph = (uint32_t)((AB == 2 ? t >> 1 : t) & 1);
                     uint64_t ad = adesc0 + (uint64_t)ab * nkc * A_CH;
                     for (int kc = 0; kc < nkc; kc++, ad += A_CH) {
-                        if (first && !(p.dbg & 4)) bar_wait(&a_full[ab * nkc + kc], aph);   // (bit 2: diagnostics only)
+                        if (first && !(dbg & 4)) bar_wait(&a_full[ab * nkc + kc], aph);   // (bit 2: diagnostics only)
                         lap(2);
                         bar_wait(&b_full[st], ph);
-                        if (!(p.dbg & 64)) tc_fence_after();   // (bit 6: diagnostics only)
+                        if (!(dbg & 64)) tc_fence_after();   // (bit 6: diagnostics only)
                         lap(3);
                         const uint64_t bd = bdesc0 + (uint64_t)st * B_ST;
-                        if (!(p.dbg & 2)) {
+                        if (!(dbg & 2)) {
 #pragma unroll
                             for (int hh = 0; hh < H; hh++) {
                                 tc_mma(d + hh * N, ad + hh * A_HALF, bd, idesc, kc ? 1u : 0u);
