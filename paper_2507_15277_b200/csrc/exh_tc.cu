@@ -42,6 +42,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -744,30 +745,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_exh_tc(const TcParams p)
                     const uint32_t d = tmem + buf * 256;
                     const int ab = AB == 2 ? (t & 1) : 0;
                     const uint32_t aph = (uint32_t)((AB == 2 ? t >> 1 : t) & 1);
-                    uint64_t ad = adesc0 + (uint64_t)ab * nkc * A_CH;
-                    for (int kc = 0; kc < nkc; kc++, ad += A_CH) {
-                        if (first && !(dbg & 4)) bar_wait(&a_full[ab * nkc + kc], aph);   // (bit 2: diagnostics only)
-                        lap(2);
-                        bar_wait(&b_full[st], ph);
-                        if (!(dbg & 64)) tc_fence_after();   // (bit 6: diagnostics only)
-                        lap(3);
-                        const uint64_t bd = bdesc0 + (uint64_t)st * B_ST;
-                        if (!(dbg & 2)) {
+                    // the K loop, specialised on (first tile of the task, last tile of the task):
+                    // the single issuing thread is latency-bound, so no per-chunk branches on them
+                    auto kloop = [&](auto FIRST, auto LAST) {
+                        uint64_t ad = adesc0 + (uint64_t)ab * nkc * A_CH;
+                        uint64_t bd = bdesc0 + (uint64_t)st * B_ST;
+                        for (int kc = 0; kc < nkc; kc++, ad += A_CH) {
+                            if (decltype(FIRST)::value && !(dbg & 4)) bar_wait(&a_full[ab * nkc + kc], aph);
+                            lap(2);
+                            bar_wait(&b_full[st], ph);
+                            if (!(dbg & 64)) tc_fence_after();   // (bit 6: diagnostics only)
+                            lap(3);
+                            if (!(dbg & 2)) {
 #pragma unroll
-                            for (int hh = 0; hh < H; hh++) {
-                                tc_mma(d + hh * N, ad + hh * A_HALF, bd, idesc, kc ? 1u : 0u);
-                                tc_mma(d + hh * N, ad + hh * A_HALF + A_K32, bd + B_K32, idesc, 1u);
+                                for (int hh = 0; hh < H; hh++) {
+                                    tc_mma(d + hh * N, ad + hh * A_HALF, bd, idesc, kc ? 1u : 0u);
+                                    tc_mma(d + hh * N, ad + hh * A_HALF + A_K32, bd + B_K32, idesc, 1u);
+                                }
+                            }
+                            lap(4);
+                            tc_commit(&b_empty[st]);
+                            if (decltype(LAST)::value) tc_commit(&a_empty[ab * nkc + kc]);   // the task's last use of chunk kc
+                            lap(5);
+                            if (++st == S) {
+                                st = 0;
+                                ph ^= 1;
+                                bd = bdesc0;
+                            } else {
+                                bd += B_ST;
                             }
                         }
-                        lap(4);
-                        tc_commit(&b_empty[st]);
-                        if (lastu) tc_commit(&a_empty[ab * nkc + kc]);   // the task's last use of A chunk kc
-                        lap(5);
-                        if (++st == S) {
-                            st = 0;
-                            ph ^= 1;
-                        }
-                    }
+                    };
+                    if (first && lastu) kloop(std::true_type(), std::true_type());
+                    else if (first) kloop(std::true_type(), std::false_type());
+                    else if (lastu) kloop(std::false_type(), std::true_type());
+                    else kloop(std::false_type(), std::false_type());
                     tc_commit(&acc_full[buf]);
                     lap(5);
                 }
